@@ -1,0 +1,169 @@
+/* coserve_cuda.h -- C ABI of libcoserve_cuda.so, the B200 (sm_100a) drop-in for the
+ * co-serving iteration of FlexLLM (arXiv 2402.18789).
+ *
+ * The reference (/root/reference/proj) is a header-only C++20 library with no FFI; the
+ * entry points below are what a binding of its hot path needs:
+ *
+ *   cs_engine_create / cs_engine_set_weight  <- TinyModel::init (tiny_model.hpp:44-67):
+ *                                               model config + frozen weights + LoRA A,B
+ *   cs_step (FT forward window)              <- forward_full (tiny_model.hpp:181-221) executed
+ *                                               as forward_window fused with
+ *                                               inference prefill/decode rows
+ *   cs_step (FT backward window)             <- backward_full (tiny_model.hpp:259-327) executed
+ *                                               as backward_window
+ *   cs_step_result.ft_loss_sum               <- generative_loss
+ *   cs_read_lora_grads                       <- LoraGrads (tiny_model.hpp:71-83)
+ *   cs_read_kvgrad                           <- OracleLayerGrads dk/dv (tiny_model.hpp:248-251)
+ *   cs_adam_step                             <- Adam once per mini-batch
+ *   cs_sched_*                               <- latency / max_finetune_tokens / try_admit /
+ *                                               plan_iteration / advance_finetune
+ *
+ * Conventions (mirroring the reference's):
+ *   - every call returns CS_OK (0) or a negative status; the message is in cs_last_error()
+ *     (thread-local).  CS_ERR_INVALID_ARGUMENT <-> std::invalid_argument,
+ *     CS_ERR_RUNTIME <-> std::runtime_error, CS_ERR_CACHE_DESYNC / CS_ERR_ORDERING are the
+ *     spec's cache-desync / ordering-violation errors.
+ *   - host buffers passed in are copied; the caller keeps ownership.  The engine owns all
+ *     device memory.  One host thread per engine; stream-ordered; not thread-safe.
+ *   - weights use the reference layout: row-major [in, out] (x . W convention).
+ */
+#ifndef COSERVE_CUDA_H
+#define COSERVE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+#define CS_OK 0
+#define CS_ERR_INVALID_ARGUMENT (-1)
+#define CS_ERR_RUNTIME (-2)
+#define CS_ERR_CUDA (-3)
+#define CS_ERR_CACHE_DESYNC (-4)
+#define CS_ERR_ORDERING (-5)
+#define CS_ERR_OOM (-6)
+#define CS_ERR_NCCL (-7)
+
+const char* cs_last_error(void);
+int cs_version(void);
+
+/* ---------------------------------------------------------------- primitives (device ptrs) */
+/* C[M,N] (op)= A[M,K] . B[N,K]^T, bf16 operands (K contiguous), fp32 accumulate on
+ * tcgen05/TMEM.  epi: 0 bf16 store (+bias), 1 fp32 store, 2 fp32 +=, 3 fp32 atomic +=.
+ * bn in {0(auto),16,32,64,128,256}; splits 0 = auto (fp32 epilogues only). */
+int cs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                 int64_t M, int64_t N, int64_t K, int epi, const float* bias, int bn, int splits,
+                 void* stream);
+
+/* ---------------------------------------------------------------- engine */
+typedef struct cs_model_config {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, lora_rank;
+  int32_t norm;     /* 0 = none (reference TinyModel), 1 = RMSNorm                  */
+  int32_t act;      /* 0 = ReLU on up (reference),      1 = SwiGLU (gate || up)      */
+  int32_t rope;     /* 0 = none (reference),            1 = rotate-half RoPE         */
+  int32_t qkv_bias; /* Qwen-style QKV bias                                          */
+  float rope_theta;
+  float rms_eps;
+  int32_t page_size;  /* tokens per KV page                                         */
+  int32_t n_pages;    /* KV pool pages (every layer has its own pool of n_pages)    */
+  int32_t max_tokens; /* max tokens in one iteration (inference + FT forward rows)  */
+  int32_t max_ft_len; /* max finetuning sequence length L                           */
+  int32_t max_segments;
+} cs_model_config;
+
+typedef struct cs_engine cs_engine;
+
+int cs_engine_create(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                     const void* nccl_unique_id, cs_engine** out);
+int cs_engine_destroy(cs_engine* e);
+/* dtype: 0 = f64, 1 = f32.  name in {embed, unembed, final_norm, wq, wk, wv, wo, w_gate, w_up,
+ * w_down, lora_a, lora_b, bq, bk, bv, norm1, norm2}; shapes in the reference layout. */
+int cs_engine_set_weight(cs_engine* e, const char* name, int layer, const void* host, int dtype,
+                         int64_t rows, int64_t cols);
+/* LoRA A/B master weights (fp32) read back as f64 (e.g. after cs_adam_step). */
+int cs_engine_get_lora(cs_engine* e, int layer, double* a_out, double* b_out);
+/* Device-side random init with the reference's scales (tiny_model.hpp:51-63) for the
+ * performance configs (no parity claim; counter-based RNG). */
+int cs_engine_init_random(cs_engine* e, uint64_t seed);
+
+#define CS_SEG_DECODE 0
+#define CS_SEG_PREFILL 1
+#define CS_SEG_FT_FWD 2
+
+typedef struct cs_segment {
+  int32_t kind;      /* CS_SEG_*                                                    */
+  int32_t q_start;   /* first row of this segment inside the token batch           */
+  int32_t q_len;     /* rows                                                       */
+  int32_t ctx_start; /* position of the first row (= tokens already in its cache)  */
+  int32_t page_off;  /* offset of its page table inside plan->page_table           */
+  int32_t n_pages;   /* pages covering positions [0, ctx_start + q_len)            */
+  int32_t sample;    /* 1: return argmax next token of the last row                */
+  int32_t adapter;   /* 1: rows pass through the LoRA bypass                        */
+} cs_segment;
+
+#define CS_FT_NONE 0
+#define CS_FT_FORWARD 1
+#define CS_FT_BACKWARD 2
+
+typedef struct cs_ft_window {
+  int32_t phase;           /* CS_FT_*                                                */
+  int32_t seq_len;         /* L of the finetuning sequence                           */
+  int32_t l;               /* forward: l_i (window start); backward: l_j (window end) */
+  int32_t s;               /* window tokens                                          */
+  int32_t layer;           /* backward: layer n                                      */
+  const int32_t* targets;  /* forward: next-token ids of the s rows (-1 = none)      */
+  int32_t page_off;        /* FT sequence page table inside plan->page_table         */
+  int32_t n_pages;
+} cs_ft_window;
+
+typedef struct cs_iteration_plan {
+  int32_t n_tokens;
+  const int32_t* tokens; /* [n_tokens]; FT forward rows (if any) are the last segment */
+  int32_t n_segments;
+  const cs_segment* segments;
+  const int32_t* page_table;
+  int32_t page_table_len;
+  cs_ft_window ft;
+} cs_iteration_plan;
+
+typedef struct cs_step_result {
+  int32_t* next_tokens;  /* [n_segments] or NULL; -1 for unsampled segments           */
+  float* logits;         /* [n_sampled, vocab] or NULL                                */
+  double ft_loss_sum;    /* summed next-token CE of this forward window               */
+  float iteration_ms;    /* device time of the step (CUDA events)                     */
+} cs_step_result;
+
+int cs_step(cs_engine* e, const cs_iteration_plan* plan, cs_step_result* result);
+/* Asynchronous variant: enqueue only (no host sync, no read-back); pair with cs_sync. */
+int cs_step_async(cs_engine* e, const cs_iteration_plan* plan);
+int cs_sync(cs_engine* e, cs_step_result* result);
+
+int cs_adam_step(cs_engine* e, float lr, float beta1, float beta2, float eps);
+int cs_zero_lora_grads(cs_engine* e);
+int cs_read_lora_grads(cs_engine* e, int layer, double* grad_a, double* grad_b);
+/* dK, dV accumulated (ΔKVAccum) for the layer currently being back-propagated, rows [0, L). */
+int cs_read_kvgrad(cs_engine* e, int32_t L, double* dk_out, double* dv_out);
+/* K/V of one sequence (by page table) at one layer, positions [0, len): [len, kv_dim]. */
+int cs_read_kv(cs_engine* e, int layer, const int32_t* pages, int32_t len, double* k_out,
+               double* v_out);
+/* dLoss/d(input of layer) rows [0, L) produced by the last backward windows. */
+int cs_read_dy(cs_engine* e, int32_t L, double* out);
+
+/* ---------------------------------------------------------------- host scheduler (no GPU) */
+typedef struct cs_latency_profile {
+  double t0_ms;
+  double slope_ms_per_token;
+  double knee_tokens; /* <= 0 -> infinite knee */
+} cs_latency_profile;
+
+double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);
+int64_t cs_sched_max_finetune_tokens(const cs_latency_profile* p, int64_t c, double slo_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COSERVE_CUDA_H */

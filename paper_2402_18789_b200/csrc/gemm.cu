@@ -1,0 +1,408 @@
+// gemm.cu -- K1/K3/K10: the base-model GEMMs of the co-serving step on sm_100a.
+//
+//   C[M,N] (op)= A[M,K] . B[N,K]^T      A, B bf16 K-major (row-major with K contiguous),
+//                                        fp32 accumulation in TMEM.
+// Replaces the reference's naive f64 `matmul` / `matmul_nt` (matrix.hpp:69-105) on every
+// projection of tiny_model.hpp:196-211 (forward, B = W^T stored [out,in]) and :283-319
+// (token-level backward dX = dY.W^T, B = W in the reference's own [in,out] layout).
+//
+// Design (one CTA per SM, persistent over a static tile list):
+//   warp 0      : TMA producer  (cp.async.bulk.tensor 2D, SWIZZLE_128B, mbarrier complete_tx)
+//   warp 1      : MMA issuer    (one thread issues tcgen05.mma.cta_group::1.kind::f16,
+//                                M=128, N=BN, K=16 per instruction; commits to mbarriers)
+//   warp 2      : TMEM allocator (2*BN columns: double-buffered accumulator)
+//   warps 4..7  : epilogue      (tcgen05.ld 32x32b -> registers -> bias/residual -> global)
+// Work unit = (m block, n block, k split).  Split-K partial sums are combined with fp32
+// vector atomics (only for fp32 outputs).  Rows >= M / cols >= N are masked in the
+// epilogue, so A/B tensor maps can describe whole (capacity-sized) buffers.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cs {
+
+struct GemmArgs {
+  int M, N, K;
+  int kb_total;  // ceil(K / 64)
+  int splits;
+  int num_m, num_n;
+  int epi;
+  void* C;
+  long ldc;
+  const float* bias;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128;
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int CHUNK = BN >= 32 ? 32 : 16;
+};
+
+__device__ __forceinline__ void decode_work(int w, const GemmArgs& a, int& m_blk, int& n_blk,
+                                            int& kb0, int& kb1) {
+  int m = w % a.num_m;
+  int rest = w / a.num_m;
+  int ks = rest % a.splits;
+  int n = rest / a.splits;
+  m_blk = m;
+  n_blk = n;
+  kb0 = (int)(((long)ks * a.kb_total) / a.splits);
+  kb1 = (int)(((long)(ks + 1) * a.kb_total) / a.splits);
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_store(const GemmArgs& a, int row, int col0,
+                                               const uint32_t* r, int cnt) {
+  // r: cnt fp32 values (as bits) for columns col0 .. col0+cnt-1 of `row`
+  if (row >= a.M) return;
+  const bool full = (col0 + cnt) <= a.N;
+  if (a.epi == EPI_BF16) {
+    __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(a.C) + (long)row * a.ldc + col0;
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < cnt) v[i] = __uint_as_float(r[i]) + (a.bias ? a.bias[min(col0 + i, a.N - 1)] : 0.f);
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        if (i < cnt) {
+          uint4 p;
+          p.x = pack_bf16(v[i], v[i + 1]);
+          p.y = pack_bf16(v[i + 2], v[i + 3]);
+          p.z = pack_bf16(v[i + 4], v[i + 5]);
+          p.w = pack_bf16(v[i + 6], v[i + 7]);
+          *reinterpret_cast<uint4*>(C + i) = p;
+        }
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i)
+        if (col0 + i < a.N) C[i] = __float2bfloat16(v[i]);
+    }
+  } else {
+    float* C = reinterpret_cast<float*>(a.C) + (long)row * a.ldc + col0;
+    const bool atomic = a.splits > 1 || a.epi == EPI_F32_ATOMIC;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        if (i < cnt) {
+          float4 v = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                 __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          float4* p = reinterpret_cast<float4*>(C + i);
+          if (atomic) {
+            atomicAdd(p, v);
+          } else if (a.epi == EPI_F32_ADD) {
+            float4 o = *p;
+            o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w;
+            *p = o;
+          } else {
+            *p = v;
+          }
+        }
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) {
+        if (col0 + i >= a.N) break;
+        float v = __uint_as_float(r[i]);
+        if (atomic) atomicAdd(C + i, v);
+        else if (a.epi == EPI_F32_ADD) C[i] += v;
+        else C[i] = v;
+      }
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total = args.num_m * args.num_n * args.splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int mb, nb, kb0, kb1;
+        decode_work(w, args, mb, nb, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * Cfg::BM);
+          tma_load_2d(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int mb, nb, kb0, kb1;
+        decode_work(w, args, mb, nb, kb0, kb1);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+          const uint64_t ad = umma_desc_sw128(sa);
+          const uint64_t bd = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < Cfg::BK / 16; ++k) {
+            // +32 bytes per K=16 step inside the 128B swizzle atom (16-byte units)
+            mma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                     (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;  // == warp % 4 -> TMEM lanes [32*ew, 32*ew+32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int mb, nb, kb0, kb1;
+      decode_work(w, args, mb, nb, kb0, kb1);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * Cfg::BM + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += Cfg::CHUNK) {
+        const int col0 = nb * BN + c0;
+        uint32_t r[32];
+        if constexpr (Cfg::CHUNK == 32) {
+          tmem_ld_32x32b_x32(tbase + c0, r);
+        } else {
+          uint32_t r16[16];
+          tmem_ld_32x32b_x16(tbase + c0, r16);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = r16[i];
+        }
+        tmem_ld_wait();
+        if (col0 < args.N) epilogue_store<BN>(args, row, col0, r, Cfg::CHUNK);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  long rows, cols, ld;
+  int box_rows;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld &&
+           box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.ptr);
+    h ^= (size_t)k.rows * 0x9E3779B97F4A7C15ull + (size_t)k.cols * 31 + (size_t)k.ld * 131 +
+         (size_t)k.box_rows * 7;
+    return h;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, int box_rows) {
+  MapKey key{ptr, rows, cols, ld, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return 0;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -2;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = *out;
+  return 0;
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
+                      int grid, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  gemm_tn_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_pick_bn(long M, long N) {
+  const long mt = (M + 127) / 128;
+  if (N <= 16) return 16;
+  if (N <= 32) return 32;
+  // largest BN that still gives ~a full wave of tiles
+  for (int bn : {256, 128}) {
+    if (mt * ((N + bn - 1) / bn) >= 120) return bn;
+  }
+  return 64;
+}
+
+cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
+  if (d.M <= 0 || d.N <= 0) return cudaSuccess;
+  if (d.K <= 0 || (d.K % 8) != 0 || (d.lda % 8) != 0 || (d.ldb % 8) != 0)
+    return cudaErrorInvalidValue;
+  int bn = d.bn > 0 ? d.bn : gemm_pick_bn(d.M, d.N);
+  GemmArgs a;
+  a.M = (int)d.M;
+  a.N = (int)d.N;
+  a.K = (int)d.K;
+  a.kb_total = (int)((d.K + 63) / 64);
+  a.num_m = (int)((d.M + 127) / 128);
+  a.num_n = (int)((d.N + bn - 1) / bn);
+  a.epi = d.epi;
+  a.C = d.C;
+  a.ldc = d.ldc;
+  a.bias = d.bias;
+  int splits = d.splits;
+  const long tiles = (long)a.num_m * a.num_n;
+  if (splits <= 0) {
+    splits = 1;
+    if (d.epi != EPI_BF16 && tiles < kNumSMs) {
+      splits = (int)((kNumSMs + tiles - 1) / tiles);
+      splits = std::min(splits, std::max(1, a.kb_total / 4));
+    }
+  }
+  if (d.epi == EPI_BF16) splits = 1;
+  splits = std::max(1, std::min(splits, a.kb_total));
+  a.splits = splits;
+  if (d.epi == EPI_F32 && splits > 1) {
+    cudaError_t e = cudaMemset2DAsync(d.C, d.ldc * sizeof(float), 0, d.N * sizeof(float), d.M, st);
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap ma, mb;
+  const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
+  const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
+  if (make_map(&ma, d.A, a_rows, d.K, d.lda, 128) != 0) return cudaErrorInvalidValue;
+  if (make_map(&mb, d.B, b_rows, d.K, d.ldb, bn) != 0) return cudaErrorInvalidValue;
+  const long work = tiles * splits;
+  const int grid = (int)std::min<long>(work, d.max_ctas > 0 ? d.max_ctas : kNumSMs);
+  switch (bn) {
+    case 16: return launch_bn<16>(ma, mb, a, grid, st);
+    case 32: return launch_bn<32>(ma, mb, a, grid, st);
+    case 64: return launch_bn<64>(ma, mb, a, grid, st);
+    case 128: return launch_bn<128>(ma, mb, a, grid, st);
+    case 256: return launch_bn<256>(ma, mb, a, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace cs

@@ -1,0 +1,37 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal to libcoserve_cuda.so).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cs {
+
+// ------------------------------------------------------------------ GEMM (gemm.cu)
+enum GemmEpi : int {
+  EPI_BF16 = 0,        // C_bf16 = acc (+ bias)
+  EPI_F32 = 1,         // C_f32  = acc
+  EPI_F32_ADD = 2,     // C_f32 += acc   (residual stream; split-K via atomics)
+  EPI_F32_ATOMIC = 3,  // C_f32 += acc with atomics (caller-initialised C)
+};
+
+struct GemmDesc {
+  const void* A = nullptr;  // bf16 [M, K] row-major, leading dim lda (elements)
+  long lda = 0;
+  long a_rows = 0;          // rows described by the TMA map (>= M; 0 -> M)
+  const void* B = nullptr;  // bf16 [N, K] row-major, leading dim ldb
+  long ldb = 0;
+  long b_rows = 0;          // (>= N; 0 -> N)
+  void* C = nullptr;
+  long ldc = 0;
+  long M = 0, N = 0, K = 0;
+  int epi = EPI_BF16;
+  const float* bias = nullptr;  // [N] (EPI_BF16 only)
+  int bn = 0;                   // 0 = heuristic
+  int splits = 0;               // 0 = heuristic (fp32 epilogues only)
+  int max_ctas = 0;             // 0 = #SMs
+};
+
+cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);
+int gemm_pick_bn(long M, long N);
+
+}  // namespace cs

@@ -1,0 +1,67 @@
+"""K1: tcgen05/TMA GEMM parity vs a torch fp32 reference of the same op (bf16 inputs)."""
+import ctypes
+
+import pytest
+import torch
+
+from paper_2402_18789_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, C, epi, bias=None, bn=0, splits=0, M=None):
+    L = _lib.lib()
+    M = A.shape[0] if M is None else M
+    N, K = B.shape
+    rc = L.cs_gemm_bf16(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(),
+                        C.stride(0), M, N, K, epi,
+                        None if bias is None else bias.data_ptr(), bn, splits,
+                        torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "cs_gemm_bf16")
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (128, 128, 128, 128), (300, 200, 320, 64),
+                                      (77, 96, 256, 32), (1000, 1536, 512, 0), (5, 16, 1088, 16),
+                                      (4096, 4096, 4096, 0), (64, 6144, 4096, 0)])
+def test_gemm_bf16_out(cuda, M, N, K, bn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    C = torch.zeros(M, N, device=cuda, dtype=torch.bfloat16)
+    _gemm(A, B, C, 0, bn=bn)
+    ref = A.float() @ B.float().T
+    torch.cuda.synchronize()
+    err = (C.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(128, 256, 1024, 1), (64, 4096, 4096, 0), (256, 512, 2048, 4),
+                                          (16, 4096, 14400, 0)])
+def test_gemm_f32_add_splitk(cuda, M, N, K, splits):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    R = torch.randn(M, N, device=cuda, generator=g)
+    C = R.clone()
+    _gemm(A, B, C, 2, splits=splits)
+    ref = R + A.float() @ B.float().T
+    torch.cuda.synchronize()
+    err = (C - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-4, err
+
+
+def test_gemm_f32_store_bias(cuda):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    M, N, K = 200, 96, 256
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g)
+    C = torch.zeros(M, N, device=cuda, dtype=torch.bfloat16)
+    _gemm(A, B, C, 0, bias=bias)
+    ref = A.float() @ B.float().T + bias
+    C2 = torch.full((M, N), 7.0, device=cuda)
+    _gemm(A, B, C2, 1, splits=2)
+    torch.cuda.synchronize()
+    assert (C.float() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
+    ref2 = A.float() @ B.float().T
+    assert (C2 - ref2).abs().max().item() / ref2.abs().max().item() < 1e-4
