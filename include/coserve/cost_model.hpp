@@ -1,0 +1,102 @@
+// coserve/cost_model.hpp -- latency estimation f(c, s), its exact inverse, and the paged-KV
+// memory model with admission control (§6.2, §7).
+// Header-only host C++ (namespace coserve, like the reference's proj/include/coserve/).
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <stdexcept>
+#include <vector>
+
+namespace coserve {
+
+// f is strictly increasing in c+s; f(0,0) = t0 > 0.
+struct LatencyProfile {
+  double t0_ms = 2.0;
+  double slope_ms_per_token = 0.01;
+  double knee_tokens = std::numeric_limits<double>::infinity();  // slope doubles past the knee
+};
+
+// t0 + b*min(c+s, k) + 2b*max(0, c+s-k)
+inline double latency(const LatencyProfile& p, int64_t c, int64_t s) {
+  if (c < 0 || s < 0) throw std::invalid_argument("latency: c, s must be >= 0");
+  const double n = (double)c + (double)s;
+  const double k = p.knee_tokens;
+  return p.t0_ms + p.slope_ms_per_token * std::min(n, k) +
+         2.0 * p.slope_ms_per_token * std::max(0.0, n - k);
+}
+
+// largest integer s >= 0 with latency(c, s) <= budget; 0 if none.
+// Closed-form guess, then exact correction against latency() itself (boundary inclusive).
+inline int64_t max_finetune_tokens(const LatencyProfile& p, int64_t c, double slo_step_ms) {
+  if (!(slo_step_ms > 0)) throw std::invalid_argument("max_finetune_tokens: budget must be > 0");
+  if (latency(p, c, 0) > slo_step_ms) return 0;
+  const double b = p.slope_ms_per_token, k = p.knee_tokens;
+  double n;  // total tokens allowed
+  const double rem = slo_step_ms - p.t0_ms;
+  if (b <= 0) return std::numeric_limits<int32_t>::max();
+  if (rem / b <= k) n = rem / b;
+  else n = k + (rem - b * k) / (2.0 * b);
+  int64_t s = std::max<int64_t>(0, (int64_t)std::floor(n) - c);
+  while (s > 0 && latency(p, c, s) > slo_step_ms) --s;
+  while (latency(p, c, s + 1) <= slo_step_ms) ++s;
+  return s;
+}
+
+// pages of page_size tokens; a request is admitted iff
+// ceil(prompt/page) + growth pages are free; pages are reserved atomically.
+class MemoryModel {
+ public:
+  MemoryModel(int64_t total_pages, int64_t page_size, int64_t growth_tokens = 0)
+      : total_(total_pages), page_(page_size), growth_(growth_tokens) {
+    if (total_pages < 0 || page_size < 1) throw std::invalid_argument("MemoryModel: bad sizes");
+    free_.reserve(total_pages);
+    for (int64_t i = total_pages - 1; i >= 0; --i) free_.push_back((int32_t)i);
+  }
+  int64_t page_size() const { return page_; }
+  int64_t free_pages() const { return (int64_t)free_.size(); }
+  int64_t total_pages() const { return total_; }
+  int64_t pages_for(int64_t tokens) const { return (tokens + page_ - 1) / page_; }
+
+  // try_admit: reserve ceil(prompt/page) + ceil(growth/page) pages; returns page ids or empty
+  bool try_admit(int64_t prompt_tokens, std::vector<int32_t>* pages_out) {
+    const int64_t need = pages_for(prompt_tokens) + pages_for(growth_);
+    if (need > free_pages() || prompt_tokens < 0) return false;
+    if (pages_out) {
+      pages_out->clear();
+      for (int64_t i = 0; i < need; ++i) {
+        pages_out->push_back(free_.back());
+        free_.pop_back();
+      }
+    } else {
+      free_.resize(free_.size() - need);
+    }
+    return true;
+  }
+  // grow a sequence by one page (decode past its reservation); false = would need eviction
+  bool grow(std::vector<int32_t>* pages) {
+    if (free_.empty()) return false;
+    pages->push_back(free_.back());
+    free_.pop_back();
+    return true;
+  }
+  void release(const std::vector<int32_t>& pages) {
+    for (auto it = pages.rbegin(); it != pages.rend(); ++it) free_.push_back(*it);
+  }
+  // raw reservation (finetuning sequence cache pages are not admission-controlled)
+  bool reserve(int64_t n, std::vector<int32_t>* pages_out) {
+    if (n > free_pages()) return false;
+    for (int64_t i = 0; i < n; ++i) {
+      pages_out->push_back(free_.back());
+      free_.pop_back();
+    }
+    return true;
+  }
+
+ private:
+  int64_t total_, page_, growth_;
+  std::vector<int32_t> free_;  // LIFO free list: deterministic page ids
+};
+
+}  // namespace coserve

@@ -343,7 +343,7 @@ def _attention_rows(arch: Arch, q, K, V, row_begin):
     return out, lse
 
 
-def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved):
+def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool = True):
     s = x.shape[0]
     rows = slice(pos0, pos0 + s)
     positions = np.arange(pos0, pos0 + s)
@@ -382,10 +382,11 @@ def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved):
         m = silu(g) * u
         sv.pre[rows], sv.up[rows] = g, u
     sv.m[rows] = m
-    lu = m @ w["lora_a"]                                     # :207
-    sv.lu[rows] = lu
     y = r1 + m @ w["w_down"]                                 # :209-210
-    y = y + lu @ w["lora_b"]                                 # :208,211
+    if lora:  # inference rows of a base-model request skip the adapter (segmented LoRA)
+        lu = m @ w["lora_a"]                                 # :207
+        sv.lu[rows] = lu
+        y = y + lu @ w["lora_b"]                             # :208,211
     return y
 
 
@@ -414,7 +415,8 @@ def generative_loss(logits, targets) -> float:
     return s
 
 
-def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache):
+def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache,
+                   lora: bool = True):
     """SPEC.md:283-291 / Alg. 2 lines 3-11: positions [l_i, l_i+s) through all layers,
     attending to cached K,V [0, l_i) plus the causal window; appends Q,K,V.
     Returns (logits [s,V], final hidden [s,h])."""
@@ -423,7 +425,7 @@ def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache
     toks = np.asarray(tokens_window, dtype=np.int64)
     x = W["embed"][toks].copy()                              # tiny_model.hpp:189-190
     for n in range(arch.n_layers):
-        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n])
+        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora)
     cache.length = l_i + len(toks)
     logits, _, _ = _head(arch, W, x)
     return logits, x

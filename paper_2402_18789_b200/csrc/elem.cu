@@ -1,0 +1,591 @@
+// elem.cu -- bandwidth-bound kernels of the co-serving step (K4/K5/K6/K11-K14):
+// embedding gather (tiny_model.hpp:189-190), RMSNorm / cast, RoPE + paged KV append
+// (+ Q-cache append for FT rows), ReLU (tiny_model.hpp:204-205) / SwiGLU,
+// LoRA packing for the K-concatenated down projection (tiny_model.hpp:207-211), fused
+// cross-entropy forward+backward (row_cross_entropy :170-177, loss_head_grad :223-246),
+// token-level backward helpers (tiny_model.hpp:276-319), and the LoRA Adam update.
+#include <cfloat>
+
+#include "common.cuh"
+#include "engine_kernels.h"
+
+namespace cs {
+
+namespace {
+
+CS_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float t = (threadIdx.x < nw) ? red[threadIdx.x] : 0.f;
+  if (w == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  return red[0];
+}
+
+CS_DEV float block_max(float v, float* red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float t = (threadIdx.x < nw) ? red[threadIdx.x] : -INFINITY;
+  if (w == 0) t = warp_max(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  return red[0];
+}
+
+CS_DEV float silu_f(float x) { return x / (1.f + __expf(-x)); }
+CS_DEV float dsilu_f(float x) {
+  const float s = 1.f / (1.f + __expf(-x));
+  return s * (1.f + x * (1.f - s));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_kernel(const int* __restrict__ tok, const bf16* __restrict__ E,
+                             float* __restrict__ x, int h) {
+  const long row = blockIdx.x;
+  const bf16* src = E + (long)tok[row] * h;
+  float* dst = x + row * h;
+  for (int c = threadIdx.x * 8; c < h; c += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + c);
+    const bf16* b = reinterpret_cast<const bf16*>(&v);
+    float4 a0 = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]),
+                            __bfloat162float(b[2]), __bfloat162float(b[3]));
+    float4 a1 = make_float4(__bfloat162float(b[4]), __bfloat162float(b[5]),
+                            __bfloat162float(b[6]), __bfloat162float(b[7]));
+    *reinterpret_cast<float4*>(dst + c) = a0;
+    *reinterpret_cast<float4*>(dst + c + 4) = a1;
+  }
+}
+void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, cudaStream_t st) {
+  if (T > 0) embed_kernel<<<T, 128, 0, st>>>(tokens, embed, x, h);
+}
+
+// ---------------------------------------------------------------- RMSNorm / cast
+__global__ void rmsnorm_kernel(const float* __restrict__ x, long ldx, const int* __restrict__ idx,
+                               const float* __restrict__ g, bf16* __restrict__ out, long ldo,
+                               float* __restrict__ rstd_out, int h, float eps, int use_norm) {
+  __shared__ float red[32];
+  const long src_row = idx ? idx[blockIdx.x] : blockIdx.x;
+  const float* xr = x + src_row * ldx;
+  bf16* o = out + (long)blockIdx.x * ldo;
+  float rstd = 1.f;
+  if (use_norm) {
+    float ss = 0.f;
+    for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + c);
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = block_sum(ss, red);
+    rstd = rsqrtf(ss / (float)h + eps);
+    if (rstd_out && threadIdx.x == 0) rstd_out[blockIdx.x] = rstd;
+  }
+  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(xr + c);
+    if (use_norm) {
+      const float4 gg = *reinterpret_cast<const float4*>(g + c);
+      v.x *= rstd * gg.x;
+      v.y *= rstd * gg.y;
+      v.z *= rstd * gg.z;
+      v.w *= rstd * gg.w;
+    }
+    uint2 p;
+    p.x = pack_bf16(v.x, v.y);
+    p.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(o + c) = p;
+  }
+}
+void rmsnorm_cast(const float* x, long ldx, const float* g, bf16* out, long ldo, float* rstd_out,
+                  int rows, int h, float eps, int use_norm, cudaStream_t st) {
+  if (rows > 0)
+    rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
+}
+void rmsnorm_cast_gather(const float* x, long ldx, const int* idx, const float* g, bf16* out,
+                         long ldo, float* rstd_out, int rows, int h, float eps, int use_norm,
+                         cudaStream_t st) {
+  if (rows > 0)
+    rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
+}
+
+// ---------------------------------------------------------------- RoPE + KV append
+__global__ void rope_append_kernel(RopeAppendParams p, const float2* __restrict__ cs_tab) {
+  const int row = blockIdx.x;
+  const int pos = p.row_pos[row];
+  const AttnSeg sg = p.segs[p.row_seg[row]];
+  const int d = p.head_dim, half = d / 2;
+  const int q_dim = p.n_heads * d, kv_dim = p.n_kv_heads * d;
+  bf16* q = p.qkv + (long)row * p.ld;
+  bf16* k = q + q_dim;
+  const bf16* v = k + kv_dim;
+  const long prow = (long)__ldg(p.page_table + sg.page_off + pos / p.page_size) * p.page_size +
+                    (pos % p.page_size);
+  bf16* kd = p.k_pool + prow * kv_dim;
+  bf16* vd = p.v_pool + prow * kv_dim;
+  const bool ft = row >= p.ft_row0 && p.q_cache;
+  bf16* qc = ft ? p.q_cache + (long)pos * q_dim : nullptr;
+  const float2* tab = cs_tab + (long)pos * half;
+  // q heads (in place) and k heads (to the page), pairs (i, i + d/2)
+  const int nq_pairs = p.n_heads * half, nk_pairs = p.n_kv_heads * half;
+  for (int t = threadIdx.x; t < nq_pairs + nk_pairs; t += blockDim.x) {
+    const bool isq = t < nq_pairs;
+    const int tt = isq ? t : t - nq_pairs;
+    const int hd = tt / half, i = tt % half;
+    bf16* src = (isq ? q : k) + hd * d;
+    float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + half]);
+    if (p.use_rope) {
+      const float2 cs = tab[i];
+      const float y1 = x1 * cs.x - x2 * cs.y;
+      const float y2 = x2 * cs.x + x1 * cs.y;
+      x1 = y1;
+      x2 = y2;
+    }
+    const bf16 b1 = __float2bfloat16(x1), b2 = __float2bfloat16(x2);
+    if (isq) {
+      src[i] = b1;
+      src[i + half] = b2;
+      if (qc) {
+        qc[hd * d + i] = b1;
+        qc[hd * d + i + half] = b2;
+      }
+    } else {
+      kd[hd * d + i] = b1;
+      kd[hd * d + i + half] = b2;
+    }
+  }
+  for (int c = threadIdx.x * 8; c < kv_dim; c += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(vd + c) = *reinterpret_cast<const uint4*>(v + c);
+}
+
+static const float2* s_rope_tab = nullptr;
+void set_rope_table(const float2* tab) { s_rope_tab = tab; }
+void rope_append(const RopeAppendParams& p, cudaStream_t st) {
+  if (p.T > 0) rope_append_kernel<<<p.T, 128, 0, st>>>(p, s_rope_tab);
+}
+
+// ---------------------------------------------------------------- activations
+__global__ void act_kernel(const bf16* __restrict__ gu, long ld_gu, bf16* __restrict__ m,
+                           long ldm, int f, int swiglu) {
+  const long row = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= ldm) return;
+  bf16* dst = m + row * ldm + c;
+  if (c >= f) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const uint4 gv = *reinterpret_cast<const uint4*>(gu + row * ld_gu + c);
+  const bf16* g = reinterpret_cast<const bf16*>(&gv);
+  uint4 ov;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&ov);
+  if (swiglu) {
+    const uint4 uv = *reinterpret_cast<const uint4*>(gu + row * ld_gu + f + c);
+    const bf16* u = reinterpret_cast<const bf16*>(&uv);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = pack_bf16(silu_f(__bfloat162float(g[2 * i])) * __bfloat162float(u[2 * i]),
+                       silu_f(__bfloat162float(g[2 * i + 1])) * __bfloat162float(u[2 * i + 1]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = pack_bf16(fmaxf(__bfloat162float(g[2 * i]), 0.f),
+                       fmaxf(__bfloat162float(g[2 * i + 1]), 0.f));
+  }
+  *reinterpret_cast<uint4*>(dst) = ov;
+}
+void act_fwd(const bf16* gu, long ld_gu, bf16* m, long ldm, int rows, int f, int swiglu,
+             cudaStream_t st) {
+  if (rows <= 0) return;
+  dim3 grid((unsigned)((ldm / 8 + 127) / 128), rows);
+  act_kernel<<<grid, 128, 0, st>>>(gu, ld_gu, m, ldm, f, swiglu);
+}
+
+__global__ void lora_pack_kernel(const float* __restrict__ lu, int r, bf16* __restrict__ m,
+                                 long ldm, int f, int rows) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * r) return;
+  const int row = t / r, j = t % r;
+  m[(long)row * ldm + f + j] = __float2bfloat16(lu[(long)row * r + j]);
+}
+void lora_pack(const float* lu, int r, bf16* m, long ldm, int f, int rows, cudaStream_t st) {
+  if (rows > 0) lora_pack_kernel<<<(rows * r + 255) / 256, 256, 0, st>>>(lu, r, m, ldm, f, rows);
+}
+
+// ---------------------------------------------------------------- sampling / CE
+__global__ void argmax_kernel(const float* __restrict__ logits, long ld, int V, int* out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* row = logits + (long)blockIdx.x * ld;
+  float best = -INFINITY;
+  int bi = 0;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float v = row[c];
+    if (v > best) {
+      best = v;
+      bi = c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+      if (sv[i] > best || (sv[i] == best && si[i] < bi)) {
+        best = sv[i];
+        bi = si[i];
+      }
+    out[blockIdx.x] = bi;
+  }
+}
+void argmax_rows(const float* logits, long ld, int rows, int V, int* out, cudaStream_t st) {
+  if (rows > 0) argmax_kernel<<<rows, 512, 0, st>>>(logits, ld, V, out);
+}
+
+__global__ void ce_kernel(const float* __restrict__ logits, long ld, const int* __restrict__ tg,
+                          int V, float inv_norm, float* __restrict__ loss,
+                          bf16* __restrict__ dlog, long ldd) {
+  __shared__ float red[32];
+  const int row = blockIdx.x;
+  const float* x = logits + (long)row * ld;
+  bf16* dx = dlog + (long)row * ldd;
+  const int t = tg[row];
+  if (t < 0) {
+    for (int c = threadIdx.x; c < V; c += blockDim.x) dx[c] = __float2bfloat16(0.f);
+    if (threadIdx.x == 0) loss[row] = 0.f;
+    return;
+  }
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, x[c]);
+  mx = block_max(mx, red);
+  float se = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) se += __expf(x[c] - mx);
+  se = block_sum(se, red);
+  const float inv = 1.f / se;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    float g = __expf(x[c] - mx) * inv;
+    if (c == t) g -= 1.f;
+    dx[c] = __float2bfloat16(g * inv_norm);
+  }
+  if (threadIdx.x == 0) loss[row] = (mx + __logf(se)) - x[t];
+}
+void ce_fwd_bwd(const float* logits, long ld, const int* targets, int rows, int V,
+                float inv_norm, float* loss, bf16* dlogits, long ldd, cudaStream_t st) {
+  if (rows > 0) ce_kernel<<<rows, 512, 0, st>>>(logits, ld, targets, V, inv_norm, loss, dlogits, ldd);
+}
+
+// ---------------------------------------------------------------- backward helpers
+__global__ void rms_bwd_kernel(const float* __restrict__ resid, long ldr,
+                               const float* __restrict__ x, long ldx, const float* __restrict__ g,
+                               const float* __restrict__ rstd, const float* __restrict__ dh,
+                               long ldh, float* __restrict__ out, long ldo, bf16* __restrict__ ob,
+                               long ldob, int h, int use_norm) {
+  __shared__ float red[32];
+  const long row = blockIdx.x;
+  const float* dr = dh + row * ldh;
+  const float* rr = resid ? resid + row * ldr : nullptr;
+  float* o = out + row * ldo;
+  if (!use_norm) {
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      const float v = (rr ? rr[c] : 0.f) + dr[c];
+      o[c] = v;
+      if (ob) ob[row * ldob + c] = __float2bfloat16(v);
+    }
+    return;
+  }
+  const float* xr = x + row * ldx;
+  const float rs = rstd[row];
+  float dot = 0.f;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) dot += dr[c] * g[c] * xr[c] * rs;
+  dot = block_sum(dot, red) / (float)h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    const float xh = xr[c] * rs;
+    const float v = (rr ? rr[c] : 0.f) + rs * (dr[c] * g[c] - xh * dot);
+    o[c] = v;
+    if (ob) ob[row * ldob + c] = __float2bfloat16(v);
+  }
+}
+void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const float* g,
+                 const float* rstd, const float* dh, long ldh, float* out, long ldo,
+                 bf16* out_b, long ldob, int rows, int h, int use_norm, cudaStream_t st) {
+  if (rows > 0)
+    rms_bwd_kernel<<<rows, 256, 0, st>>>(resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
+                                         ldob, h, use_norm);
+}
+
+// MLP backward fused with the LoRA-A gradient:
+//   swiglu: g=saved[:, :f], u=saved[:, f:]; dgu = [dm*u*dsilu(g), dm*silu(g)]; m = silu(g)*u
+//   relu  : m=saved;  dgu = dm * (m > 0)            (tiny_model.hpp:285-286)
+//   dA[col, :] += sum_rows m[row, col] * dlu[row, :] (tiny_model.hpp:282)
+constexpr int MLP_ROWS = 64;
+__global__ void __launch_bounds__(256) mlp_bwd_kernel(const float* __restrict__ dm, long ld_dm,
+                                                      const bf16* __restrict__ saved, long ld_s,
+                                                      const float* __restrict__ dlu, int r,
+                                                      bf16* __restrict__ dgu, long ld_dgu,
+                                                      float* __restrict__ dA, int rows, int f,
+                                                      int swiglu) {
+  __shared__ float sl[MLP_ROWS * 16];
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * MLP_ROWS;
+  const int nr = min(MLP_ROWS, rows - r0);
+  for (int i = threadIdx.x; i < nr * r; i += blockDim.x)
+    sl[(i / r) * 16 + (i % r)] = dlu[(long)(r0 + i / r) * r + (i % r)];
+  __syncthreads();
+  if (col >= f) return;
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  for (int i = 0; i < nr; ++i) {
+    const long row = r0 + i;
+    const float d = dm[row * ld_dm + col];
+    float mval;
+    if (swiglu) {
+      const float g = __bfloat162float(saved[row * ld_s + col]);
+      const float u = __bfloat162float(saved[row * ld_s + f + col]);
+      const float sg = silu_f(g);
+      mval = sg * u;
+      dgu[row * ld_dgu + col] = __float2bfloat16(d * u * dsilu_f(g));
+      dgu[row * ld_dgu + f + col] = __float2bfloat16(d * sg);
+    } else {
+      mval = fmaxf(__bfloat162float(saved[row * ld_s + col]), 0.f);  // saved = up
+      dgu[row * ld_dgu + col] = __float2bfloat16(mval > 0.f ? d : 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < r) acc[j] += mval * sl[i * 16 + j];
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < r) atomicAdd(dA + (long)col * r + j, acc[j]);
+}
+void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
+             bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st) {
+  if (rows <= 0) return;
+  dim3 grid((f + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  mlp_bwd_kernel<<<grid, 256, 0, st>>>(dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
+                                       swiglu);
+}
+
+// per row: dlu[j] = dY . B[j] ; dycat = [bf16(dY) | bf16(dlu) | 0]  (tiny_model.hpp:281)
+__global__ void lora_dlu_kernel(const float* __restrict__ dY, long ldy, const float* __restrict__ B,
+                                int r, int h, int rows, float* __restrict__ dlu,
+                                bf16* __restrict__ dycat, long ldc) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const long row = warp;
+  const float* y = dY + row * ldy;
+  bf16* o = dycat + row * ldc;
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  for (int c = lane; c < h; c += 32) {
+    const float v = y[c];
+    o[c] = __float2bfloat16(v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < r) acc[j] += v * B[(long)j * h + c];
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = warp_sum(acc[j]);
+  for (int c = lane; c < (int)(ldc - h); c += 32) {
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j == c && j < r) v = acc[j];
+    o[h + c] = __float2bfloat16(v);
+    if (c < r) dlu[row * r + c] = v;
+  }
+}
+// dB[j, c] += sum_rows lu[row, j] * dY[row, c]  (tiny_model.hpp:280)
+__global__ void __launch_bounds__(256) lora_db_kernel(const float* __restrict__ dY, long ldy,
+                                                      const float* __restrict__ lu, int r,
+                                                      int rows, int h, float* __restrict__ dB) {
+  __shared__ float sl[MLP_ROWS * 16];
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * MLP_ROWS;
+  const int nr = min(MLP_ROWS, rows - r0);
+  for (int i = threadIdx.x; i < nr * r; i += blockDim.x)
+    sl[(i / r) * 16 + (i % r)] = lu[(long)(r0 + i / r) * r + (i % r)];
+  __syncthreads();
+  if (col >= h) return;
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  for (int i = 0; i < nr; ++i) {
+    const float v = dY[(long)(r0 + i) * ldy + col];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < r) acc[j] += sl[i * 16 + j] * v;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < r) atomicAdd(dB + (long)j * h + col, acc[j]);
+}
+void lora_bwd_b(const float* dY, long ldy, const float* lu, const float* B, int r, int rows,
+                int h, float* dlu, bf16* dycat, long ldc, float* dB, cudaStream_t st) {
+  if (rows <= 0) return;
+  lora_dlu_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(dY, ldy, B, r, h, rows, dlu, dycat, ldc);
+  dim3 grid((h + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  lora_db_kernel<<<grid, 256, 0, st>>>(dY, ldy, lu, r, rows, h, dB);
+}
+
+// inverse (transposed) rotate-half RoPE + pack [dq | dk | dv] as bf16
+__global__ void rope_bwd_pack_kernel(const float* __restrict__ dq, long ldq,
+                                     const float* __restrict__ dk, const float* __restrict__ dv,
+                                     long ld_acc, int a, int n_heads, int n_kv, int d,
+                                     int use_rope, const float2* __restrict__ tab,
+                                     bf16* __restrict__ out, long ldo) {
+  const int i = blockIdx.x;  // window-local row
+  const int pos = a + i;
+  const int half = d / 2;
+  const int q_dim = n_heads * d, kv_dim = n_kv * d;
+  bf16* o = out + (long)i * ldo;
+  const int nqp = n_heads * half, nkp = n_kv * half;
+  for (int t = threadIdx.x; t < nqp + nkp; t += blockDim.x) {
+    const bool isq = t < nqp;
+    const int tt = isq ? t : t - nqp;
+    const int hd = tt / half, j = tt % half;
+    const float* src = isq ? dq + (long)i * ldq + hd * d : dk + (long)pos * ld_acc + hd * d;
+    float y1 = src[j], y2 = src[j + half];
+    if (use_rope) {
+      const float2 cs = tab[(long)pos * half + j];
+      const float x1 = y1 * cs.x + y2 * cs.y;
+      const float x2 = y2 * cs.x - y1 * cs.y;
+      y1 = x1;
+      y2 = x2;
+    }
+    bf16* dst = o + (isq ? 0 : q_dim) + hd * d;
+    dst[j] = __float2bfloat16(y1);
+    dst[j + half] = __float2bfloat16(y2);
+  }
+  for (int c = threadIdx.x; c < kv_dim; c += blockDim.x)
+    o[q_dim + kv_dim + c] = __float2bfloat16(dv[(long)pos * ld_acc + c]);
+}
+void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, long ld_acc,
+                   int a, int rows, int n_heads, int n_kv_heads, int head_dim, int use_rope,
+                   float theta, bf16* out, long ldo, cudaStream_t st) {
+  (void)theta;
+  if (rows > 0)
+    rope_bwd_pack_kernel<<<rows, 128, 0, st>>>(dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
+                                               head_dim, use_rope, s_rope_tab, out, ldo);
+}
+
+// ---------------------------------------------------------------- Adam (fp32 master)
+__global__ void adam_kernel(AdamParams p, int update) {
+  const long nA = (long)p.n_layers * p.f * p.r;
+  const long nB = (long)p.n_layers * p.r * p.h;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nA + nB;
+       t += (long)gridDim.x * blockDim.x) {
+    const bool isA = t < nA;
+    const long i = isA ? t : t - nA;
+    float* w = isA ? p.A + i : p.B + i;
+    if (update) {
+      const float g = isA ? p.gA[i] : p.gB[i];
+      float* m = isA ? p.mA + i : p.mB + i;
+      float* v = isA ? p.vA + i : p.vB + i;
+      const float mm = p.b1 * *m + (1.f - p.b1) * g;
+      const float vv = p.b2 * *v + (1.f - p.b2) * g * g;
+      *m = mm;
+      *v = vv;
+      const float mh = mm / p.bc1, vh = vv / p.bc2;
+      *w = *w - p.lr * mh / (sqrtf(vh) + p.eps);
+    }
+    const bf16 wb = __float2bfloat16(*w);
+    if (isA) {  // A[l][row][j]
+      const long l = i / ((long)p.f * p.r);
+      const long rem = i % ((long)p.f * p.r);
+      const int row = (int)(rem / p.r), j = (int)(rem % p.r);
+      p.A_t[(l * 16 + j) * p.f + row] = wb;  // [n_layers][16][f]
+      p.dbwd_cat[(l * p.f + row) * (p.h + 64) + p.h + j] = wb;
+    } else {    // B[l][j][c]
+      const long l = i / ((long)p.r * p.h);
+      const long rem = i % ((long)p.r * p.h);
+      const int j = (int)(rem / p.h), c = (int)(rem % p.h);
+      p.down_cat[(l * p.h + c) * (p.f + 64) + p.f + j] = wb;
+    }
+  }
+}
+void adam_step(const AdamParams& p, int update, cudaStream_t st) {
+  adam_kernel<<<4 * 148, 256, 0, st>>>(p, update);
+}
+
+// ---------------------------------------------------------------- weight prep
+__global__ void cast_kernel(const float* __restrict__ src, int rows, int cols, bf16* dst,
+                            long ldd, int transpose) {
+  __shared__ float tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = 0; k < 32; k += 8) {
+    const int r = by + ty + k, c = bx + tx;
+    if (r < rows && c < cols) {
+      if (!transpose) dst[(long)r * ldd + c] = __float2bfloat16(src[(long)r * cols + c]);
+      else tile[ty + k][tx] = src[(long)r * cols + c];
+    }
+  }
+  if (!transpose) return;
+  __syncthreads();
+  for (int k = 0; k < 32; k += 8) {
+    const int c = bx + ty + k, r = by + tx;  // dst row = c, dst col = r
+    if (r < rows && c < cols) dst[(long)c * ldd + r] = __float2bfloat16(tile[tx][ty + k]);
+  }
+}
+void cast_f32_bf16(const float* src, int rows, int cols, bf16* dst, long ldd, int transpose,
+                   cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  cast_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, transpose);
+}
+
+CS_DEV uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+CS_DEV float hash_normal(uint64_t seed, long i) {
+  const uint64_t a = splitmix(seed ^ splitmix((uint64_t)i * 2 + 1));
+  const float u1 = ((a >> 40) + 1) * (1.0f / 16777217.0f);
+  const float u2 = (a & 0xFFFFFF) * (1.0f / 16777216.0f);
+  return sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853f * u2);
+}
+__global__ void init_bf16_kernel(bf16* dst, long n, float scale, uint64_t seed) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16(hash_normal(seed, i) * scale);
+}
+__global__ void init_f32_kernel(float* dst, long n, float scale, uint64_t seed) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = hash_normal(seed, i) * scale;
+}
+__global__ void fill_kernel(float* dst, long n, float v) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+void init_normal_bf16(bf16* dst, long n, float scale, uint64_t seed, cudaStream_t st) {
+  init_bf16_kernel<<<8 * 148, 256, 0, st>>>(dst, n, scale, seed);
+}
+void init_normal_f32(float* dst, long n, float scale, uint64_t seed, cudaStream_t st) {
+  init_f32_kernel<<<8 * 148, 256, 0, st>>>(dst, n, scale, seed);
+}
+void fill_f32(float* dst, long n, float v, cudaStream_t st) {
+  fill_kernel<<<4 * 148, 256, 0, st>>>(dst, n, v);
+}
+
+}  // namespace cs

@@ -1,0 +1,1117 @@
+// engine.cu -- the co-serving engine behind the C ABI (include/coserve_cuda.h).
+//
+// One cs_step runs one iteration of FlexLLM's co-serving loop (SPEC.md:687-690 step 3):
+//   * forward over the concatenated token batch [decode rows | prefill-chunk rows | FT
+//     forward-window rows] through the shared frozen weights: every GEMM is
+//     one tcgen05 launch over all rows; attention is one launch over all segments; the LoRA
+//     bypass applies to the adapter-row suffix only (segmented, K-concatenated into the
+//     down projection); FT rows save only what survives graph pruning and
+//     fold the loss-head gradient (loss_head_grad, tiny_model.hpp:223-246) in immediately.
+//   * optionally one token-level backward window at layer n (Alg. 2 lines 14-21):
+//     rows [l_j - s_j, l_j), ΔKVAccum accumulation, LoRA grads, dX for layer n-1.  Layer 0
+//     is pruned to its MLP/LoRA part (no frozen-weight gradients, no dX below).
+// Device memory is one arena carved at create time (weights, paged KV pools, FT saved
+// activations, scratch sized for max_tokens).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "coserve_cuda.h"
+#include "engine_kernels.h"
+#include "kernels.h"
+
+namespace cs {
+int set_error(int code, const std::string& msg);
+}
+
+using cs::bf16;
+
+#define CS_CUDA_TRY(x)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (x);                                                                   \
+    if (_e != cudaSuccess)                                                                  \
+      return cs::set_error(CS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+struct cs_engine {
+  cs_model_config cfg{};
+  int device = 0;
+  int tp_rank = 0, tp_size = 1;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // dims
+  int h, Hq, Hkv, d, q_dim, kv_dim, nqkv, f, V, r, NL, P, npages, gu_n, f_cat, h_cat, grp;
+  int T_max, L_max, S_max, max_seg, head_chunk, max_pos;
+  bool swiglu, norm, rope;
+  // arena
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0, arena_used = 0;
+  // weights
+  bf16 *embed, *unembed_t, *unembed;
+  float* gf;
+  bf16 *wqkv_t, *wqkv, *wo_t, *wo, *wgu_t, *wgu, *down_cat, *dbwd_cat, *A_t;
+  float *bqkv, *g1, *g2;
+  float *loraA, *loraB, *gA, *gB, *mA, *vA, *mB, *vB;
+  // KV
+  bf16 *k_pool, *v_pool;
+  // FT saved (per layer, by position)
+  bf16 *ft_q, *ft_o, *ft_gu;
+  float *ft_lse, *ft_x, *ft_r1, *ft_rstd1, *ft_rstd2, *ft_lu;
+  float *dk_acc, *dv_acc, *dy[2];
+  // forward scratch
+  float *x, *rstd, *lu, *lse;
+  bf16 *xb, *qkv, *attn, *gu, *m;
+  bf16* hf;
+  float *logits, *dh, *loss_rows, *hrstd;
+  bf16* dlog;
+  float* samp_logits;
+  int* next_tok;
+  float *part_o, *part_lse;
+  // backward scratch
+  bf16 *dycat, *dgu, *dr1b, *dO, *dqkv;
+  float *dlu, *dm, *dh2, *dr1, *delta, *dq, *dh1;
+  float2* rope_tab;
+  // per-step upload
+  uint8_t* d_meta = nullptr;
+  uint8_t* h_meta = nullptr;
+  size_t meta_bytes = 0;
+  std::vector<float> h_loss;
+  // FT state machine
+  int ft_len = 0;          // QKV cache length (forward progress)
+  int ft_L = 0;            // sequence length of the active mini-batch
+  int bwd_layer = -2;      // -2: not started; n: current layer; -1: done
+  int bwd_next_end = 0;    // expected l_j of the next window
+  int dy_cur = 0;
+  int adam_t = 0;
+  // device-side counters
+  long launches = 0;
+};
+
+namespace {
+
+template <typename T>
+T* carve(cs_engine* e, size_t count) {
+  size_t bytes = ((count * sizeof(T)) + 255) & ~size_t(255);
+  T* p = reinterpret_cast<T*>(e->arena + e->arena_used);
+  e->arena_used += bytes;
+  return p;
+}
+
+// two-pass carve: first pass measures (arena == nullptr -> counts only)
+struct Planner {
+  size_t used = 0;
+  template <typename T>
+  void add(size_t count) { used += ((count * sizeof(T)) + 255) & ~size_t(255); }
+};
+
+void layout(cs_engine* e, bool measure, size_t* total) {
+  Planner pl;
+  auto A = [&](auto** ptr, size_t count) {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(*ptr)>>;
+    if (measure) pl.add<T>(count);
+    else *ptr = carve<T>(e, count);
+  };
+  const size_t NL = e->NL, h = e->h, V = e->V, f = e->f, r = e->r;
+  const size_t T = e->T_max, Lm = e->L_max, S = e->S_max;
+  A(&e->embed, V * h);
+  A(&e->unembed_t, V * h);
+  A(&e->unembed, h * V);
+  A(&e->gf, h);
+  A(&e->wqkv_t, NL * e->nqkv * h);
+  A(&e->wqkv, NL * h * e->nqkv);
+  A(&e->wo_t, NL * h * e->q_dim);
+  A(&e->wo, NL * e->q_dim * h);
+  A(&e->wgu_t, NL * e->gu_n * h);
+  A(&e->wgu, NL * h * e->gu_n);
+  A(&e->down_cat, NL * h * e->f_cat);
+  A(&e->dbwd_cat, NL * f * e->h_cat);
+  A(&e->A_t, NL * 16 * f);
+  A(&e->bqkv, NL * e->nqkv);
+  A(&e->g1, NL * h);
+  A(&e->g2, NL * h);
+  A(&e->loraA, NL * f * r);
+  A(&e->loraB, NL * r * h);
+  A(&e->gA, NL * f * r);
+  A(&e->gB, NL * r * h);
+  A(&e->mA, NL * f * r);
+  A(&e->vA, NL * f * r);
+  A(&e->mB, NL * r * h);
+  A(&e->vB, NL * r * h);
+  const size_t kv = NL * (size_t)e->npages * e->P * e->kv_dim;
+  A(&e->k_pool, kv);
+  A(&e->v_pool, kv);
+  A(&e->ft_q, NL * Lm * e->q_dim);
+  A(&e->ft_o, NL * Lm * e->q_dim);
+  A(&e->ft_gu, NL * Lm * e->gu_n);
+  A(&e->ft_lse, NL * Lm * e->Hq);
+  A(&e->ft_x, e->norm ? NL * Lm * h : 1);
+  A(&e->ft_r1, e->norm ? NL * Lm * h : 1);
+  A(&e->ft_rstd1, NL * Lm);
+  A(&e->ft_rstd2, NL * Lm);
+  A(&e->ft_lu, NL * Lm * r);
+  A(&e->dk_acc, Lm * e->kv_dim);
+  A(&e->dv_acc, Lm * e->kv_dim);
+  A(&e->dy[0], Lm * h);
+  A(&e->dy[1], Lm * h);
+  A(&e->x, T * h);
+  A(&e->rstd, T);
+  A(&e->lu, T * r);
+  A(&e->lse, T * e->Hq);
+  A(&e->xb, T * h);
+  A(&e->qkv, T * e->nqkv);
+  A(&e->attn, T * e->q_dim);
+  A(&e->gu, T * e->gu_n);
+  A(&e->m, T * e->f_cat);
+  const size_t C = e->head_chunk;
+  A(&e->hf, std::max(C, (size_t)e->max_seg) * h);
+  A(&e->logits, std::max(C, (size_t)e->max_seg) * V);
+  A(&e->dlog, C * V);
+  A(&e->dh, C * h);
+  A(&e->hrstd, C);
+  A(&e->loss_rows, Lm);
+  A(&e->samp_logits, (size_t)e->max_seg * V);
+  A(&e->next_tok, e->max_seg);
+  const size_t max_parts = 4096;
+  A(&e->part_o, max_parts * 64 * e->d);
+  A(&e->part_lse, max_parts * 64);
+  A(&e->dycat, S * e->h_cat);
+  A(&e->dgu, S * e->gu_n);
+  A(&e->dr1b, S * h);
+  A(&e->dO, S * e->q_dim);
+  A(&e->dqkv, S * e->nqkv);
+  A(&e->dlu, S * r);
+  A(&e->dm, S * f);
+  A(&e->dh2, S * h);
+  A(&e->dr1, S * h);
+  A(&e->delta, S * e->Hq);
+  A(&e->dq, S * e->q_dim);
+  A(&e->dh1, S * h);
+  A(&e->rope_tab, (size_t)e->max_pos * (e->d / 2));
+  A(&e->d_meta, e->meta_bytes);
+  if (measure) *total = pl.used;
+}
+
+size_t meta_size(const cs_engine* e) {
+  const size_t T = e->T_max, S = e->max_seg;
+  size_t b = 0;
+  b += T * 4 * 3;                          // tokens, row_pos, row_seg
+  b += S * sizeof(cs::AttnSeg);
+  b += (size_t)e->npages * 4 + 4096 * 4;   // page table (upper bound)
+  b += 65536 * sizeof(cs::AttnWork);
+  b += 8192 * sizeof(cs::AttnCombine);
+  b += S * 4 * 2;                          // samp idx
+  b += (size_t)e->L_max * 4;               // targets
+  return (b + 4095) & ~size_t(4095);
+}
+
+}  // namespace
+
+// =============================================================================== create
+extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                                const void* nccl_unique_id, cs_engine** out) {
+  (void)nccl_unique_id;
+  if (!cfg || !out) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: null argument");
+  const cs_model_config& c = *cfg;
+  if (c.n_layers < 1 || c.hidden < 1 || c.n_heads < 1 || c.n_kv_heads < 1 || c.head_dim < 1 ||
+      c.ffn < 1 || c.vocab < 1)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: dimensions must be >= 1");
+  if (c.lora_rank < 1 || c.lora_rank > 16)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: lora_rank must be in [1, 16]");
+  if (c.n_heads % c.n_kv_heads != 0)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: kv heads must divide heads");
+  if (c.head_dim != 64 && c.head_dim != 128)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: head_dim must be 64 or 128");
+  if (c.n_heads / c.n_kv_heads > 64)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: GQA group too large");
+  if ((c.hidden % 64) != 0 || (c.ffn % 64) != 0 || (c.vocab % 8) != 0)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                         "cs_engine_create: hidden/ffn must be multiples of 64, vocab of 8");
+  if (c.page_size < 1 || c.n_pages < 1 || c.max_tokens < 1 || c.max_ft_len < 1)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: bad pool / capacity sizes");
+  if (tp_size != 1 || tp_rank != 0)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                         "cs_engine_create: this build runs tp_size == 1 engines (one replica per GPU)");
+  cs_engine* e = new cs_engine();
+  e->cfg = c;
+  e->device = device;
+  e->tp_rank = tp_rank;
+  e->tp_size = tp_size;
+  e->h = c.hidden;
+  e->Hq = c.n_heads;
+  e->Hkv = c.n_kv_heads;
+  e->d = c.head_dim;
+  e->q_dim = c.n_heads * c.head_dim;
+  e->kv_dim = c.n_kv_heads * c.head_dim;
+  e->nqkv = e->q_dim + 2 * e->kv_dim;
+  e->f = c.ffn;
+  e->V = c.vocab;
+  e->r = c.lora_rank;
+  e->NL = c.n_layers;
+  e->P = c.page_size;
+  e->npages = c.n_pages;
+  e->swiglu = c.act == 1;
+  e->norm = c.norm == 1;
+  e->rope = c.rope == 1;
+  e->gu_n = e->swiglu ? 2 * e->f : e->f;
+  e->f_cat = e->f + 64;
+  e->h_cat = e->h + 64;
+  e->grp = e->Hq / e->Hkv;
+  e->T_max = c.max_tokens;
+  e->L_max = c.max_ft_len;
+  e->S_max = std::max(c.max_tokens, 64);
+  e->max_seg = std::max(c.max_segments, 1);
+  e->head_chunk = std::min(1024, std::max(64, c.max_tokens));
+  e->max_pos = std::max((long)c.max_ft_len, std::min<long>((long)c.n_pages * c.page_size, 1 << 17)) + 1;
+  e->meta_bytes = meta_size(e);
+
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete e;
+    return cs::set_error(CS_ERR_CUDA, "cs_engine_create: cudaSetDevice failed");
+  }
+  size_t total = 0;
+  layout(e, true, &total);
+  e->arena_bytes = total;
+  cudaError_t err = cudaMalloc(&e->arena, total);
+  if (err != cudaSuccess) {
+    delete e;
+    return cs::set_error(CS_ERR_OOM, "cs_engine_create: cudaMalloc(" + std::to_string(total) +
+                                         ") failed: " + cudaGetErrorString(err));
+  }
+  layout(e, false, nullptr);
+  cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking);
+  cudaEventCreate(&e->ev0);
+  cudaEventCreate(&e->ev1);
+  cudaMallocHost(&e->h_meta, e->meta_bytes);
+  // zero everything that has padding semantics (concat pad columns, LoRA state, norms)
+  cudaMemsetAsync(e->arena, 0, e->arena_used, e->st);
+  // RoPE table in double precision on the host
+  {
+    const int half = e->d / 2;
+    std::vector<float2> tab((size_t)e->max_pos * half);
+    for (int p = 0; p < e->max_pos; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow((double)c.rope_theta, -(2.0 * i) / (double)e->d);
+        const double ang = (double)p * inv;
+        tab[(size_t)p * half + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+    cudaMemcpyAsync(e->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                    e->st);
+    cudaStreamSynchronize(e->st);
+  }
+  cs::fill_f32(e->g1, (long)e->NL * e->h, 1.f, e->st);
+  cs::fill_f32(e->g2, (long)e->NL * e->h, 1.f, e->st);
+  cs::fill_f32(e->gf, e->h, 1.f, e->st);
+  err = cudaStreamSynchronize(e->st);
+  if (err != cudaSuccess) {
+    cudaFree(e->arena);
+    delete e;
+    return cs::set_error(CS_ERR_CUDA, std::string("cs_engine_create: ") + cudaGetErrorString(err));
+  }
+  *out = e;
+  return CS_OK;
+}
+
+extern "C" int cs_engine_destroy(cs_engine* e) {
+  if (!e) return CS_OK;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->st);
+  cudaFree(e->arena);
+  cudaFreeHost(e->h_meta);
+  cudaEventDestroy(e->ev0);
+  cudaEventDestroy(e->ev1);
+  cudaStreamDestroy(e->st);
+  delete e;
+  return CS_OK;
+}
+
+// =============================================================================== weights
+namespace {
+int refresh_lora(cs_engine* e, int update, float lr, float b1, float b2, float eps) {
+  cs::AdamParams p;
+  p.A = e->loraA;
+  p.B = e->loraB;
+  p.gA = e->gA;
+  p.gB = e->gB;
+  p.mA = e->mA;
+  p.vA = e->vA;
+  p.mB = e->mB;
+  p.vB = e->vB;
+  p.A_t = e->A_t;
+  p.down_cat = e->down_cat;
+  p.dbwd_cat = e->dbwd_cat;
+  p.n_layers = e->NL;
+  p.f = e->f;
+  p.r = e->r;
+  p.h = e->h;
+  p.lr = lr;
+  p.b1 = b1;
+  p.b2 = b2;
+  p.eps = eps;
+  p.bc1 = update ? 1.f - std::pow(b1, (float)e->adam_t) : 1.f;
+  p.bc2 = update ? 1.f - std::pow(b2, (float)e->adam_t) : 1.f;
+  cs::adam_step(p, update, e->st);
+  CS_CUDA_TRY(cudaGetLastError());
+  return CS_OK;
+}
+}  // namespace
+
+extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, const void* host,
+                                    int dtype, int64_t rows, int64_t cols) {
+  if (!e || !name || !host) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: null argument");
+  if (dtype != 0 && dtype != 1) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: dtype must be 0 (f64) or 1 (f32)");
+  const std::string n(name);
+  const bool global = (n == "embed" || n == "unembed" || n == "final_norm");
+  if (!global && (layer < 0 || layer >= e->NL))
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: layer out of range");
+  const long count = rows * cols;
+  std::vector<float> f32(count);
+  if (dtype == 0) {
+    const double* s = static_cast<const double*>(host);
+    for (long i = 0; i < count; ++i) f32[i] = (float)s[i];
+  } else {
+    std::memcpy(f32.data(), host, count * sizeof(float));
+  }
+  auto expect = [&](long er, long ec) -> bool { return rows == er && cols == ec; };
+  const int L = layer;
+  const long h = e->h, qd = e->q_dim, kvd = e->kv_dim, f = e->f, V = e->V, r = e->r;
+  float* stage = nullptr;
+  CS_CUDA_TRY(cudaMalloc(&stage, count * sizeof(float)));
+  // stream-ordered upload: the engine stream is non-blocking w.r.t. the legacy stream
+  CS_CUDA_TRY(cudaMemcpyAsync(stage, f32.data(), count * sizeof(float), cudaMemcpyHostToDevice,
+                              e->st));
+  int rc = CS_OK;
+  auto bad = [&]() {
+    rc = cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                       "set_weight: unexpected shape for '" + n + "' [" + std::to_string(rows) +
+                           "," + std::to_string(cols) + "]");
+  };
+  cudaStream_t st = e->st;
+  if (n == "embed") {
+    if (!expect(V, h)) bad();
+    else cs::cast_f32_bf16(stage, rows, cols, e->embed, h, 0, st);
+  } else if (n == "unembed") {
+    if (!expect(h, V)) bad();
+    else {
+      cs::cast_f32_bf16(stage, rows, cols, e->unembed, V, 0, st);
+      cs::cast_f32_bf16(stage, rows, cols, e->unembed_t, h, 1, st);
+    }
+  } else if (n == "final_norm") {
+    if (count != h) bad();
+    else cudaMemcpyAsync(e->gf, stage, h * 4, cudaMemcpyDeviceToDevice, st);
+  } else if (n == "wq" || n == "wk" || n == "wv") {
+    const long off = n == "wq" ? 0 : (n == "wk" ? qd : qd + kvd);
+    const long oc = n == "wq" ? qd : kvd;
+    if (!expect(h, oc)) bad();
+    else {
+      cs::cast_f32_bf16(stage, rows, cols, e->wqkv_t + ((size_t)L * e->nqkv + off) * h, h, 1, st);
+      cs::cast_f32_bf16(stage, rows, cols, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
+    }
+  } else if (n == "wo") {
+    if (!expect(qd, h)) bad();
+    else {
+      cs::cast_f32_bf16(stage, rows, cols, e->wo_t + (size_t)L * h * qd, qd, 1, st);
+      cs::cast_f32_bf16(stage, rows, cols, e->wo + (size_t)L * qd * h, h, 0, st);
+    }
+  } else if (n == "w_gate" || n == "w_up") {
+    if (n == "w_gate" && !e->swiglu) {
+      rc = cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: w_gate given for a ReLU model");
+    } else if (!expect(h, f)) {
+      bad();
+    } else {
+      const long off = (n == "w_up" && e->swiglu) ? f : 0;
+      cs::cast_f32_bf16(stage, rows, cols, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
+      cs::cast_f32_bf16(stage, rows, cols, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
+    }
+  } else if (n == "w_down") {
+    if (!expect(f, h)) bad();
+    else {
+      cs::cast_f32_bf16(stage, rows, cols, e->down_cat + (size_t)L * h * e->f_cat, e->f_cat, 1, st);
+      cs::cast_f32_bf16(stage, rows, cols, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
+    }
+  } else if (n == "lora_a") {
+    if (!expect(f, r)) bad();
+    else {
+      cudaMemcpyAsync(e->loraA + (size_t)L * f * r, stage, count * 4, cudaMemcpyDeviceToDevice, st);
+      rc = refresh_lora(e, 0, 0, 0, 0, 0);
+    }
+  } else if (n == "lora_b") {
+    if (!expect(r, h)) bad();
+    else {
+      cudaMemcpyAsync(e->loraB + (size_t)L * r * h, stage, count * 4, cudaMemcpyDeviceToDevice, st);
+      rc = refresh_lora(e, 0, 0, 0, 0, 0);
+    }
+  } else if (n == "bq" || n == "bk" || n == "bv") {
+    const long off = n == "bq" ? 0 : (n == "bk" ? qd : qd + kvd);
+    const long oc = n == "bq" ? qd : kvd;
+    if (count != oc) bad();
+    else cudaMemcpyAsync(e->bqkv + (size_t)L * e->nqkv + off, stage, count * 4, cudaMemcpyDeviceToDevice, st);
+  } else if (n == "norm1" || n == "norm2") {
+    if (count != h) bad();
+    else cudaMemcpyAsync((n == "norm1" ? e->g1 : e->g2) + (size_t)L * h, stage, h * 4,
+                         cudaMemcpyDeviceToDevice, st);
+  } else {
+    rc = cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: unknown weight '" + n + "'");
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(stage);
+  CS_CUDA_TRY(cudaGetLastError());
+  return rc;
+}
+
+extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "init_random: null engine");
+  cudaStream_t st = e->st;
+  const float ws = 1.f / std::sqrt((float)e->h);
+  const float wf = 1.f / std::sqrt((float)e->f);
+  const size_t NL = e->NL;
+  // tiny_model.hpp:51-63 scales; the forward/backward layouts hold identical values
+  cs::init_normal_bf16(e->embed, (long)e->V * e->h, ws, seed + 1, st);
+  cs::init_normal_bf16(e->unembed, (long)e->V * e->h, ws, seed + 2, st);
+  cs::init_normal_bf16(e->unembed_t, (long)e->V * e->h, ws, seed + 2, st);  // same stats
+  cs::init_normal_bf16(e->wqkv_t, (long)(NL * e->nqkv * e->h), ws, seed + 3, st);
+  cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, seed + 3, st);
+  cs::init_normal_bf16(e->wo_t, (long)(NL * e->q_dim * e->h), ws, seed + 4, st);
+  cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, seed + 4, st);
+  cs::init_normal_bf16(e->wgu_t, (long)(NL * e->gu_n * e->h), ws, seed + 5, st);
+  cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, seed + 5, st);
+  // down: fill whole concat buffers, then the LoRA columns are rewritten by refresh_lora;
+  // pad columns [f + r, f + 64) must stay zero -> fill per row via cast of random fp32
+  {
+    float* tmp = nullptr;
+    CS_CUDA_TRY(cudaMalloc(&tmp, (size_t)e->f * e->h * sizeof(float)));
+    for (size_t l = 0; l < NL; ++l) {
+      cs::init_normal_f32(tmp, (long)e->f * e->h, wf, seed + 100 + l, st);
+      cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->h * e->f_cat, e->f_cat, 1, st);
+      cs::cast_f32_bf16(tmp, e->f, e->h, e->dbwd_cat + l * e->f * e->h_cat, e->h_cat, 0, st);
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(tmp);
+  }
+  cs::init_normal_f32(e->loraA, (long)(NL * e->f * e->r), 0.2f * wf, seed + 6, st);
+  cs::init_normal_f32(e->loraB, (long)(NL * e->r * e->h), 0.2f, seed + 7, st);
+  if (e->cfg.qkv_bias) cs::init_normal_f32(e->bqkv, (long)(NL * e->nqkv), 0.02f, seed + 8, st);
+  int rc = refresh_lora(e, 0, 0, 0, 0, 0);
+  if (rc) return rc;
+  CS_CUDA_TRY(cudaStreamSynchronize(st));
+  return CS_OK;
+}
+
+extern "C" int cs_engine_get_lora(cs_engine* e, int layer, double* a_out, double* b_out) {
+  if (!e || layer < 0 || layer >= e->NL)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "get_lora: bad engine/layer");
+  cudaStreamSynchronize(e->st);
+  const size_t na = (size_t)e->f * e->r, nb = (size_t)e->r * e->h;
+  std::vector<float> t(std::max(na, nb));
+  if (a_out) {
+    CS_CUDA_TRY(cudaMemcpy(t.data(), e->loraA + layer * na, na * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < na; ++i) a_out[i] = t[i];
+  }
+  if (b_out) {
+    CS_CUDA_TRY(cudaMemcpy(t.data(), e->loraB + layer * nb, nb * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nb; ++i) b_out[i] = t[i];
+  }
+  return CS_OK;
+}
+
+// =============================================================================== step
+namespace {
+
+struct StepPlan {
+  int T = 0;
+  int n_seg = 0;
+  int ft_row0 = 0;  // first FT forward row (== T if none)
+  int ad_row0 = 0;  // first adapter row (== T if none)
+  int n_samp = 0;
+  int n_work = 0, n_comb = 0;
+  // device pointers into d_meta
+  int *tokens, *row_pos, *row_seg, *page_table, *samp_idx, *targets;
+  cs::AttnSeg* segs;
+  cs::AttnWork* work;
+  cs::AttnCombine* comb;
+  std::vector<int> samp_seg;  // segment of each sampled row
+};
+
+int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb, long b_rows,
+         void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr) {
+  cs::GemmDesc g;
+  g.A = A;
+  g.lda = lda;
+  g.a_rows = a_rows;
+  g.B = B;
+  g.ldb = ldb;
+  g.b_rows = b_rows;
+  g.C = C;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.epi = epi;
+  g.bias = bias;
+  e->launches++;
+  cudaError_t err = cs::gemm_tn(g, e->st);
+  if (err != cudaSuccess)
+    return cs::set_error(CS_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(err));
+  return CS_OK;
+}
+
+#define TRY(x)            \
+  do {                    \
+    int _rc = (x);        \
+    if (_rc) return _rc;  \
+  } while (0)
+
+int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
+  const int T = plan->n_tokens;
+  if (T < 0 || T > e->T_max)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: n_tokens out of range [0, max_tokens]");
+  if (plan->n_segments < 0 || plan->n_segments > e->max_seg)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: too many segments");
+  if (T > 0 && (!plan->tokens || !plan->segments))
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: null tokens/segments");
+  sp.T = T;
+  sp.n_seg = plan->n_segments;
+  sp.ft_row0 = T;
+  sp.ad_row0 = T;
+  const int P = e->P;
+  const int ptl = plan->page_table_len;
+  if (ptl < 0 || ptl > e->npages + 4096)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: page_table_len out of range");
+  // host staging layout
+  uint8_t* hb = e->h_meta;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return o;
+  };
+  const size_t o_tok = take((size_t)T * 4), o_pos = take((size_t)T * 4), o_seg = take((size_t)T * 4);
+  const size_t o_segs = take((size_t)sp.n_seg * sizeof(cs::AttnSeg));
+  const size_t o_pt = take((size_t)ptl * 4);
+  int* h_tok = reinterpret_cast<int*>(hb + o_tok);
+  int* h_pos = reinterpret_cast<int*>(hb + o_pos);
+  int* h_rseg = reinterpret_cast<int*>(hb + o_seg);
+  cs::AttnSeg* h_segs = reinterpret_cast<cs::AttnSeg*>(hb + o_segs);
+  if (ptl) std::memcpy(hb + o_pt, plan->page_table, (size_t)ptl * 4);
+  for (int i = 0; i < ptl; ++i)
+    if (plan->page_table[i] < 0 || plan->page_table[i] >= e->npages)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: page id out of range");
+  int row = 0;
+  bool in_adapter_suffix = false;
+  std::vector<int> samp_rows;
+  std::vector<cs::AttnWork> work;
+  std::vector<cs::AttnCombine> comb;
+  const int rpt = 64 / e->grp;
+  for (int s = 0; s < sp.n_seg; ++s) {
+    const cs_segment& g = plan->segments[s];
+    if (g.q_start != row || g.q_len < 1 || g.q_start + g.q_len > T)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                           "cs_step: segments must tile the token batch contiguously in order");
+    if (g.kind < CS_SEG_DECODE || g.kind > CS_SEG_FT_FWD)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: bad segment kind");
+    if (g.kind == CS_SEG_DECODE && g.q_len != 1)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: decode segment with q_len != 1");
+    const long need = g.ctx_start + g.q_len;
+    if (g.ctx_start < 0 || g.page_off < 0 || g.n_pages < 0 || g.page_off + g.n_pages > ptl ||
+        (long)g.n_pages * P < need)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: segment page table does not cover its context");
+    if (need >= e->max_pos)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: context longer than the RoPE table");
+    if (g.adapter) in_adapter_suffix = true;
+    else if (in_adapter_suffix)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: adapter segments must form a suffix of the batch");
+    if (g.adapter && sp.ad_row0 == T) sp.ad_row0 = g.q_start;
+    if (g.kind == CS_SEG_FT_FWD) {
+      if (s != sp.n_seg - 1)
+        return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: the FT forward segment must be last");
+      if (!g.adapter)
+        return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: FT rows must use the adapter");
+      sp.ft_row0 = g.q_start;
+    }
+    h_segs[s] = cs::AttnSeg{g.q_start, g.q_len, g.ctx_start, g.page_off};
+    for (int i = 0; i < g.q_len; ++i) {
+      const int t = plan->tokens[row + i];
+      if (t < 0 || t >= e->V) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: token id out of range");
+      h_tok[row + i] = t;
+      h_pos[row + i] = g.ctx_start + i;
+      h_rseg[row + i] = s;
+    }
+    if (g.sample) {
+      samp_rows.push_back(row + g.q_len - 1);
+      sp.samp_seg.push_back(s);
+    }
+    // attention work items (GQA-packed q tiles x kv heads)
+    for (int q0 = 0; q0 < g.q_len; q0 += rpt) {
+      const int nq = std::min(rpt, g.q_len - q0);
+      const int nkeys = g.ctx_start + q0 + nq;
+      for (int kh = 0; kh < e->Hkv; ++kh)
+        work.push_back(cs::AttnWork{s, q0, nq, kh, 0, nkeys, -1, 0});
+    }
+    row += g.q_len;
+  }
+  if (row != T) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: segments do not cover n_tokens");
+  // split long key ranges when the grid is small (flash-decoding)
+  {
+    const int target = 2 * 148;
+    const int n0 = (int)work.size();
+    if (n0 > 0 && n0 < target) {
+      const int factor = (target + n0 - 1) / n0;
+      std::vector<cs::AttnWork> w2;
+      int part = 0;
+      for (const auto& w : work) {
+        const int tiles = (w.k_end + 63) / 64;
+        const int ns = std::min(factor, std::max(1, tiles / 4));
+        if (ns <= 1) {
+          w2.push_back(w);
+          continue;
+        }
+        const int per = (tiles + ns - 1) / ns;
+        int p0 = part;
+        int cnt = 0;
+        for (int t = 0; t < tiles; t += per) {
+          cs::AttnWork x = w;
+          x.k_begin = t * 64;
+          x.k_end = std::min(w.k_end, (t + per) * 64);
+          x.part = part++;
+          w2.push_back(x);
+          ++cnt;
+        }
+        comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, cnt, 0, 0});
+      }
+      if (part <= 4096) work.swap(w2);
+      else comb.clear();
+    }
+  }
+  sp.n_work = (int)work.size();
+  sp.n_comb = (int)comb.size();
+  if (sp.n_work > 65536 || sp.n_comb > 8192)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: attention work list too large");
+  const size_t o_work = take(work.size() * sizeof(cs::AttnWork));
+  const size_t o_comb = take(comb.size() * sizeof(cs::AttnCombine));
+  const size_t o_samp = take(samp_rows.size() * 4);
+  const int ft_s = (plan->ft.phase == CS_FT_FORWARD) ? plan->ft.s : 0;
+  const size_t o_tg = take((size_t)std::max(ft_s, 0) * 4);
+  if (off > e->meta_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: plan too large");
+  if (!work.empty()) std::memcpy(hb + o_work, work.data(), work.size() * sizeof(cs::AttnWork));
+  if (!comb.empty()) std::memcpy(hb + o_comb, comb.data(), comb.size() * sizeof(cs::AttnCombine));
+  if (!samp_rows.empty()) std::memcpy(hb + o_samp, samp_rows.data(), samp_rows.size() * 4);
+  if (ft_s > 0) {
+    if (!plan->ft.targets) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: FT forward window without targets");
+    for (int i = 0; i < ft_s; ++i) {
+      const int t = plan->ft.targets[i];
+      if (t >= e->V) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: target id out of range");
+    }
+    std::memcpy(hb + o_tg, plan->ft.targets, (size_t)ft_s * 4);
+  }
+  sp.n_samp = (int)samp_rows.size();
+  cudaError_t err = cudaMemcpyAsync(e->d_meta, hb, off, cudaMemcpyHostToDevice, e->st);
+  if (err != cudaSuccess) return cs::set_error(CS_ERR_CUDA, "cs_step: meta upload failed");
+  uint8_t* db = e->d_meta;
+  sp.tokens = reinterpret_cast<int*>(db + o_tok);
+  sp.row_pos = reinterpret_cast<int*>(db + o_pos);
+  sp.row_seg = reinterpret_cast<int*>(db + o_seg);
+  sp.segs = reinterpret_cast<cs::AttnSeg*>(db + o_segs);
+  sp.page_table = reinterpret_cast<int*>(db + o_pt);
+  sp.work = reinterpret_cast<cs::AttnWork*>(db + o_work);
+  sp.comb = reinterpret_cast<cs::AttnCombine*>(db + o_comb);
+  sp.samp_idx = reinterpret_cast<int*>(db + o_samp);
+  sp.targets = reinterpret_cast<int*>(db + o_tg);
+  return CS_OK;
+}
+
+// copy `rows` contiguous rows of width `w` elements (row stride ld_src) into dst rows
+template <typename T>
+void save_rows(cs_engine* e, T* dst, long ld_dst, const T* src, long ld_src, int rows, long w) {
+  if (rows <= 0) return;
+  cudaMemcpy2DAsync(dst, ld_dst * sizeof(T), src, ld_src * sizeof(T), w * sizeof(T), rows,
+                    cudaMemcpyDeviceToDevice, e->st);
+}
+
+int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* loss_sum) {
+  const int T = sp.T;
+  const long h = e->h, f = e->f, r = e->r;
+  const int n_ft = T - sp.ft_row0;
+  const int n_ad = T - sp.ad_row0;
+  const int l0 = plan->ft.l;  // FT window start position
+  cudaStream_t st = e->st;
+  cs::embed_gather(sp.tokens, e->embed, e->x, T, h, st);
+  const float eps = e->cfg.rms_eps;
+  const size_t kv_layer = (size_t)e->npages * e->P * e->kv_dim;
+  for (int l = 0; l < e->NL; ++l) {
+    const bool keep_attn = l > 0;  // pruning: layer 0 needs no attention backward
+    // ---- attention block
+    cs::rmsnorm_cast(e->x, h, e->g1 + (size_t)l * h, e->xb, h, e->rstd, T, h, eps, e->norm, st);
+    if (n_ft > 0 && keep_attn) {
+      if (e->norm) {
+        save_rows(e, e->ft_x + ((size_t)l * e->L_max + l0) * h, h, e->x + (size_t)sp.ft_row0 * h, h, n_ft, h);
+        save_rows(e, e->ft_rstd1 + (size_t)l * e->L_max + l0, 1, e->rstd + sp.ft_row0, 1, n_ft, 1);
+      }
+    }
+    TRY(gemm(e, e->xb, h, e->T_max, e->wqkv_t + (size_t)l * e->nqkv * h, h, e->nqkv, e->qkv, e->nqkv,
+             T, e->nqkv, h, cs::EPI_BF16, e->cfg.qkv_bias ? e->bqkv + (size_t)l * e->nqkv : nullptr));
+    cs::RopeAppendParams rp;
+    rp.qkv = e->qkv;
+    rp.ld = e->nqkv;
+    rp.row_pos = sp.row_pos;
+    rp.row_seg = sp.row_seg;
+    rp.segs = sp.segs;
+    rp.page_table = sp.page_table;
+    rp.k_pool = e->k_pool + l * kv_layer;
+    rp.v_pool = e->v_pool + l * kv_layer;
+    rp.page_size = e->P;
+    rp.n_heads = e->Hq;
+    rp.n_kv_heads = e->Hkv;
+    rp.head_dim = e->d;
+    rp.use_rope = e->rope;
+    rp.rope_theta = e->cfg.rope_theta;
+    rp.T = T;
+    rp.ft_row0 = sp.ft_row0;
+    rp.q_cache = (n_ft > 0 && keep_attn) ? e->ft_q + (size_t)l * e->L_max * e->q_dim : nullptr;
+    cs::rope_append(rp, st);
+    cs::AttnFwdParams ap;
+    ap.q = e->qkv;
+    ap.q_ld = e->nqkv;
+    ap.k_pool = rp.k_pool;
+    ap.v_pool = rp.v_pool;
+    ap.kv_dim = e->kv_dim;
+    ap.page_size = e->P;
+    ap.page_table = sp.page_table;
+    ap.segs = sp.segs;
+    ap.work = sp.work;
+    ap.combine = sp.comb;
+    ap.out = e->attn;
+    ap.out_ld = e->q_dim;
+    ap.lse = e->lse;
+    ap.lse_ld = e->Hq;
+    ap.part_o = e->part_o;
+    ap.part_lse = e->part_lse;
+    ap.grp = e->grp;
+    ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
+    CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
+    if (n_ft > 0 && keep_attn) {
+      save_rows(e, e->ft_o + ((size_t)l * e->L_max + l0) * e->q_dim, e->q_dim,
+                e->attn + (size_t)sp.ft_row0 * e->q_dim, e->q_dim, n_ft, e->q_dim);
+      save_rows(e, e->ft_lse + ((size_t)l * e->L_max + l0) * e->Hq, e->Hq,
+                e->lse + (size_t)sp.ft_row0 * e->Hq, e->Hq, n_ft, e->Hq);
+    }
+    TRY(gemm(e, e->attn, e->q_dim, e->T_max, e->wo_t + (size_t)l * h * e->q_dim, e->q_dim, h, e->x, h,
+             T, h, e->q_dim, cs::EPI_F32_ADD));
+    // ---- MLP block
+    if (n_ft > 0 && e->norm)
+      save_rows(e, e->ft_r1 + ((size_t)l * e->L_max + l0) * h, h, e->x + (size_t)sp.ft_row0 * h, h, n_ft, h);
+    cs::rmsnorm_cast(e->x, h, e->g2 + (size_t)l * h, e->xb, h, e->rstd, T, h, eps, e->norm, st);
+    if (n_ft > 0 && e->norm)
+      save_rows(e, e->ft_rstd2 + (size_t)l * e->L_max + l0, 1, e->rstd + sp.ft_row0, 1, n_ft, 1);
+    TRY(gemm(e, e->xb, h, e->T_max, e->wgu_t + (size_t)l * e->gu_n * h, h, e->gu_n, e->gu, e->gu_n,
+             T, e->gu_n, h, cs::EPI_BF16));
+    if (n_ft > 0)
+      save_rows(e, e->ft_gu + ((size_t)l * e->L_max + l0) * e->gu_n, e->gu_n,
+                e->gu + (size_t)sp.ft_row0 * e->gu_n, e->gu_n, n_ft, e->gu_n);
+    cs::act_fwd(e->gu, e->gu_n, e->m, e->f_cat, T, f, e->swiglu, st);
+    if (n_ad > 0) {
+      // u = m A for adapter rows (segmented LoRA down, tiny_model.hpp:207)
+      TRY(gemm(e, e->m + (size_t)sp.ad_row0 * e->f_cat, e->f_cat, e->T_max - sp.ad_row0,
+               e->A_t + (size_t)l * 16 * f, f, r, e->lu, r, n_ad, r, f, cs::EPI_F32));
+      cs::lora_pack(e->lu, r, e->m + (size_t)sp.ad_row0 * e->f_cat, e->f_cat, f, n_ad, st);
+      if (n_ft > 0)
+        save_rows(e, e->ft_lu + ((size_t)l * e->L_max + l0) * r, r,
+                  e->lu + (size_t)(sp.ft_row0 - sp.ad_row0) * r, r, n_ft, r);
+    }
+    // x += [m | u] [W_down ; B] (tiny_model.hpp:206-211 as one K-concatenated GEMM)
+    TRY(gemm(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * h * e->f_cat, e->f_cat, h, e->x,
+             h, T, h, e->f_cat, cs::EPI_F32_ADD));
+  }
+  // ---- sampled rows: final norm -> logits -> argmax
+  if (sp.n_samp > 0) {
+    cs::rmsnorm_cast_gather(e->x, h, sp.samp_idx, e->gf, e->hf, h, nullptr, sp.n_samp, h, eps,
+                            e->norm, st);
+    TRY(gemm(e, e->hf, h, std::max(e->head_chunk, e->max_seg), e->unembed_t, h, e->V,
+             e->samp_logits, e->V, sp.n_samp, e->V, h, cs::EPI_F32));
+    cs::argmax_rows(e->samp_logits, e->V, sp.n_samp, e->V, e->next_tok, st);
+  }
+  // ---- FT rows: fused generative loss + loss-head gradient into dY (top layer)
+  if (n_ft > 0) {
+    const int L = plan->ft.seq_len;
+    const float inv = L > 1 ? 1.f / (float)(L - 1) : 0.f;
+    for (int c0 = 0; c0 < n_ft; c0 += e->head_chunk) {
+      const int cn = std::min(e->head_chunk, n_ft - c0);
+      const float* xs = e->x + (size_t)(sp.ft_row0 + c0) * h;
+      cs::rmsnorm_cast(xs, h, e->gf, e->hf, h, e->hrstd, cn, h, eps, e->norm, st);
+      TRY(gemm(e, e->hf, h, std::max(e->head_chunk, e->max_seg), e->unembed_t, h, e->V, e->logits,
+               e->V, cn, e->V, h, cs::EPI_F32));
+      cs::ce_fwd_bwd(e->logits, e->V, sp.targets + c0, cn, e->V, inv, e->loss_rows + c0, e->dlog,
+                     e->V, st);
+      TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed, e->V, h, e->dh, h, cn, h, e->V,
+               cs::EPI_F32));
+      cs::rms_bwd_add(nullptr, 0, xs, h, e->gf, e->hrstd, e->dh, h,
+                      e->dy[e->dy_cur] + (size_t)(l0 + c0) * h, h, nullptr, 0, cn, h, e->norm, st);
+    }
+    e->h_loss.resize(n_ft);
+    CS_CUDA_TRY(cudaMemcpyAsync(e->h_loss.data(), e->loss_rows, n_ft * 4, cudaMemcpyDeviceToHost, st));
+  }
+  (void)loss_sum;
+  return CS_OK;
+}
+
+int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
+  const cs_ft_window& w = plan->ft;
+  const int n = w.layer, b = w.l, s = w.s, a = b - s;
+  cudaStream_t st = e->st;
+  const long h = e->h, f = e->f, r = e->r;
+  const int L = e->ft_L;
+  // ---- dependency / ordering checks
+  if (e->bwd_layer == -2) {
+    if (e->ft_len != L || L <= 0)
+      return cs::set_error(CS_ERR_ORDERING, "backward window before the forward pass completed");
+    e->bwd_layer = e->NL - 1;
+    e->bwd_next_end = L;
+  }
+  if (e->bwd_layer < 0) return cs::set_error(CS_ERR_ORDERING, "backward already complete; run cs_adam_step");
+  if (n != e->bwd_layer || b != e->bwd_next_end || s < 1 || a < 0)
+    return cs::set_error(CS_ERR_ORDERING,
+                         "backward window out of order: expected layer " + std::to_string(e->bwd_layer) +
+                             " ending at " + std::to_string(e->bwd_next_end));
+  if (s > e->S_max) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "backward window larger than max_tokens");
+  if (w.page_off < 0 || w.n_pages < 0 || w.page_off + w.n_pages > plan->page_table_len ||
+      (long)w.n_pages * e->P < L)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "backward window: FT page table does not cover L");
+  if (b == L) {  // first window of this layer: fresh ΔKVAccum
+    CS_CUDA_TRY(cudaMemsetAsync(e->dk_acc, 0, (size_t)L * e->kv_dim * 4, st));
+    CS_CUDA_TRY(cudaMemsetAsync(e->dv_acc, 0, (size_t)L * e->kv_dim * 4, st));
+  }
+  const float* Y = e->dy[e->dy_cur] + (size_t)a * h;  // dLoss/d(out of layer n), rows [a,b)
+  float* Xout = e->dy[e->dy_cur ^ 1] + (size_t)a * h;
+  const size_t Lm = e->L_max;
+  // ---- MLP + LoRA (tiny_model.hpp:276-287)
+  cs::lora_bwd_b(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, e->loraB + (size_t)n * r * h, r, s, h,
+                 e->dlu, e->dycat, e->h_cat, e->gB + (size_t)n * r * h, st);
+  TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
+           e->dm, f, s, f, e->h_cat, cs::EPI_F32));
+  cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
+              e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
+  if (n > 0) {
+    TRY(gemm(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2, h,
+             s, h, e->gu_n, cs::EPI_F32));
+    cs::rms_bwd_add(Y, h, e->ft_r1 + ((size_t)n * Lm + a) * h, h, e->g2 + (size_t)n * h,
+                    e->ft_rstd2 + (size_t)n * Lm + a, e->dh2, h, e->dr1, h, e->dr1b, h, s, h,
+                    e->norm, st);
+    // ---- attention (tiny_model.hpp:289-315)
+    TRY(gemm(e, e->dr1b, h, e->S_max, e->wo + (size_t)n * e->q_dim * h, h, e->q_dim, e->dO,
+             e->q_dim, s, e->q_dim, h, cs::EPI_BF16));
+    const size_t kv_layer = (size_t)e->npages * e->P * e->kv_dim;
+    cs::AttnBwdParams bp;
+    bp.q_cache = e->ft_q + (size_t)n * Lm * e->q_dim;
+    bp.q_ld = e->q_dim;
+    bp.dO = e->dO;
+    bp.do_ld = e->q_dim;
+    bp.O = e->ft_o + ((size_t)n * Lm + a) * e->q_dim;
+    bp.o_ld = e->q_dim;
+    bp.lse = e->ft_lse + (size_t)n * Lm * e->Hq;
+    bp.lse_ld = e->Hq;
+    bp.delta = e->delta;
+    bp.delta_ld = e->Hq;
+    bp.k_pool = e->k_pool + n * kv_layer;
+    bp.v_pool = e->v_pool + n * kv_layer;
+    bp.kv_dim = e->kv_dim;
+    bp.page_size = e->P;
+    bp.page_table = sp.page_table;
+    bp.page_off = w.page_off;
+    bp.a = a;
+    bp.b = b;
+    bp.dq = e->dq;
+    bp.dq_ld = e->q_dim;
+    bp.dk_acc = e->dk_acc;
+    bp.dv_acc = e->dv_acc;
+    bp.acc_ld = e->kv_dim;
+    bp.grp = e->grp;
+    bp.scale = (float)(1.0 / std::sqrt((double)e->d));
+    bp.scale_log2 = bp.scale * 1.4426950408889634f;
+    CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
+    cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
+                      e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
+    TRY(gemm(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1, h,
+             s, h, e->nqkv, cs::EPI_F32));
+    cs::rms_bwd_add(e->dr1, h, e->ft_x + ((size_t)n * Lm + a) * h, h, e->g1 + (size_t)n * h,
+                    e->ft_rstd1 + (size_t)n * Lm + a, e->dh1, h, Xout, h, nullptr, 0, s, h,
+                    e->norm, st);
+  }
+  e->bwd_next_end = a;
+  if (a == 0) {
+    e->bwd_layer = n - 1;
+    e->bwd_next_end = L;
+    e->dy_cur ^= 1;
+  }
+  return CS_OK;
+}
+
+int step_impl(cs_engine* e, const cs_iteration_plan* plan, bool sync, cs_step_result* res) {
+  if (!e || !plan) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: null argument");
+  cudaSetDevice(e->device);
+  cs::set_rope_table(e->rope_tab);
+  const cs_ft_window& w = plan->ft;
+  if (w.phase < CS_FT_NONE || w.phase > CS_FT_BACKWARD)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: bad FT phase");
+  // FT forward bookkeeping (SPEC.md:283-291 cache-desync)
+  if (w.phase == CS_FT_FORWARD) {
+    if (w.seq_len < 1 || w.seq_len > e->L_max)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: FT seq_len out of range [1, max_ft_len]");
+    if (e->bwd_layer != -2)
+      return cs::set_error(CS_ERR_ORDERING, "cs_step: forward window while a backward pass is in flight");
+    if (w.l == 0 && e->ft_len != 0 && e->ft_L != w.seq_len)
+      return cs::set_error(CS_ERR_ORDERING, "cs_step: new mini-batch before the previous one finished");
+    if (w.l != e->ft_len)
+      return cs::set_error(CS_ERR_CACHE_DESYNC, "cs_step: cache length " + std::to_string(e->ft_len) +
+                                                    " != l_i " + std::to_string(w.l));
+    if (w.l + w.s > w.seq_len || w.s < 1)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: forward window exceeds seq_len");
+    const cs_segment* last = plan->n_segments > 0 ? &plan->segments[plan->n_segments - 1] : nullptr;
+    if (!last || last->kind != CS_SEG_FT_FWD || last->q_len != w.s || last->ctx_start != w.l)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                           "cs_step: FT forward window must be the last segment (q_len = s, ctx_start = l)");
+  } else {
+    for (int i = 0; i < plan->n_segments; ++i)
+      if (plan->segments[i].kind == CS_SEG_FT_FWD)
+        return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: FT segment without a forward window");
+  }
+  StepPlan sp;
+  TRY(prepare(e, plan, sp));
+  CS_CUDA_TRY(cudaEventRecord(e->ev0, e->st));
+  if (w.phase == CS_FT_FORWARD && w.l == 0) {
+    e->ft_L = w.seq_len;
+    e->dy_cur = 0;
+  }
+  if (sp.T > 0) TRY(forward(e, plan, sp, nullptr));
+  if (w.phase == CS_FT_FORWARD) e->ft_len = w.l + w.s;
+  if (w.phase == CS_FT_BACKWARD) TRY(backward_window(e, plan, sp));
+  CS_CUDA_TRY(cudaEventRecord(e->ev1, e->st));
+  CS_CUDA_TRY(cudaGetLastError());
+  if (!sync) return CS_OK;
+  if (res) {
+    if (res->next_tokens) {
+      for (int s = 0; s < plan->n_segments; ++s) res->next_tokens[s] = -1;
+      if (sp.n_samp > 0) {
+        std::vector<int> nt(sp.n_samp);
+        CS_CUDA_TRY(cudaMemcpyAsync(nt.data(), e->next_tok, sp.n_samp * 4, cudaMemcpyDeviceToHost, e->st));
+        CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+        for (int i = 0; i < sp.n_samp; ++i) res->next_tokens[sp.samp_seg[i]] = nt[i];
+      }
+    }
+    if (res->logits && sp.n_samp > 0)
+      CS_CUDA_TRY(cudaMemcpyAsync(res->logits, e->samp_logits, (size_t)sp.n_samp * e->V * 4,
+                                  cudaMemcpyDeviceToHost, e->st));
+  }
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  if (res) {
+    double ls = 0.0;
+    if (w.phase == CS_FT_FORWARD)
+      for (int i = 0; i < (int)std::min<size_t>(e->h_loss.size(), (size_t)w.s); ++i) ls += e->h_loss[i];
+    res->ft_loss_sum = ls;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+    res->iteration_ms = ms;
+  }
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" int cs_step(cs_engine* e, const cs_iteration_plan* plan, cs_step_result* result) {
+  return step_impl(e, plan, true, result);
+}
+
+extern "C" int cs_step_async(cs_engine* e, const cs_iteration_plan* plan) {
+  return step_impl(e, plan, false, nullptr);
+}
+
+extern "C" int cs_sync(cs_engine* e, cs_step_result* result) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_sync: null engine");
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  if (result) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+    result->iteration_ms = ms;
+  }
+  return CS_OK;
+}
+
+extern "C" int cs_adam_step(cs_engine* e, float lr, float beta1, float beta2, float eps) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_adam_step: null engine");
+  if (e->bwd_layer != -1)
+    return cs::set_error(CS_ERR_ORDERING, "cs_adam_step: backward pass of the mini-batch not complete");
+  e->adam_t += 1;
+  TRY(refresh_lora(e, 1, lr, beta1, beta2, eps));
+  // mini-batch done: grads consumed, FT state reset
+  CS_CUDA_TRY(cudaMemsetAsync(e->gA, 0, (size_t)e->NL * e->f * e->r * 4, e->st));
+  CS_CUDA_TRY(cudaMemsetAsync(e->gB, 0, (size_t)e->NL * e->r * e->h * 4, e->st));
+  e->ft_len = 0;
+  e->ft_L = 0;
+  e->bwd_layer = -2;
+  e->bwd_next_end = 0;
+  e->dy_cur = 0;
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  return CS_OK;
+}
+
+extern "C" int cs_zero_lora_grads(cs_engine* e) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "null engine");
+  CS_CUDA_TRY(cudaMemsetAsync(e->gA, 0, (size_t)e->NL * e->f * e->r * 4, e->st));
+  CS_CUDA_TRY(cudaMemsetAsync(e->gB, 0, (size_t)e->NL * e->r * e->h * 4, e->st));
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  return CS_OK;
+}
+
+namespace {
+int read_f32_as_f64(cs_engine* e, const float* src, size_t n, double* out) {
+  std::vector<float> t(n);
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  CS_CUDA_TRY(cudaMemcpy(t.data(), src, n * 4, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) out[i] = t[i];
+  return CS_OK;
+}
+}  // namespace
+
+extern "C" int cs_read_lora_grads(cs_engine* e, int layer, double* grad_a, double* grad_b) {
+  if (!e || layer < 0 || layer >= e->NL) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_lora_grads: bad layer");
+  const size_t na = (size_t)e->f * e->r, nb = (size_t)e->r * e->h;
+  if (grad_a) TRY(read_f32_as_f64(e, e->gA + layer * na, na, grad_a));
+  if (grad_b) TRY(read_f32_as_f64(e, e->gB + layer * nb, nb, grad_b));
+  return CS_OK;
+}
+
+extern "C" int cs_read_kvgrad(cs_engine* e, int32_t L, double* dk_out, double* dv_out) {
+  if (!e || L < 0 || L > e->L_max) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_kvgrad: bad L");
+  const size_t n = (size_t)L * e->kv_dim;
+  if (dk_out) TRY(read_f32_as_f64(e, e->dk_acc, n, dk_out));
+  if (dv_out) TRY(read_f32_as_f64(e, e->dv_acc, n, dv_out));
+  return CS_OK;
+}
+
+extern "C" int cs_read_dy(cs_engine* e, int32_t L, double* out) {
+  if (!e || L < 0 || L > e->L_max || !out) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_dy: bad L");
+  return read_f32_as_f64(e, e->dy[e->dy_cur], (size_t)L * e->h, out);
+}
+
+extern "C" int cs_read_kv(cs_engine* e, int layer, const int32_t* pages, int32_t len, double* k_out,
+                          double* v_out) {
+  if (!e || layer < 0 || layer >= e->NL || len < 0 || (!pages && len > 0))
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_kv: bad arguments");
+  const size_t kv_layer = (size_t)e->npages * e->P * e->kv_dim;
+  std::vector<bf16> t(e->kv_dim);
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  for (int i = 0; i < len; ++i) {
+    const int pg = pages[i / e->P];
+    if (pg < 0 || pg >= e->npages) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_kv: page out of range");
+    const size_t row = (size_t)pg * e->P + (i % e->P);
+    for (int which = 0; which < 2; ++which) {
+      double* o = which ? v_out : k_out;
+      if (!o) continue;
+      const bf16* src = (which ? e->v_pool : e->k_pool) + layer * kv_layer + row * e->kv_dim;
+      CS_CUDA_TRY(cudaMemcpy(t.data(), src, e->kv_dim * sizeof(bf16), cudaMemcpyDeviceToHost));
+      for (int c = 0; c < e->kv_dim; ++c) o[(size_t)i * e->kv_dim + c] = __bfloat162float(t[c]);
+    }
+  }
+  return CS_OK;
+}

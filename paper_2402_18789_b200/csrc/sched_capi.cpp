@@ -1,0 +1,32 @@
+// sched_capi.cpp -- C exports of the host cost model (include/coserve/cost_model.hpp).
+#include <limits>
+#include <stdexcept>
+#include <string>
+
+#include "coserve/cost_model.hpp"
+#include "coserve_cuda.h"
+
+namespace cs {
+int set_error(int code, const std::string& msg);
+}
+
+namespace {
+coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
+  coserve::LatencyProfile q;
+  q.t0_ms = p->t0_ms;
+  q.slope_ms_per_token = p->slope_ms_per_token;
+  q.knee_tokens = p->knee_tokens > 0 ? p->knee_tokens : std::numeric_limits<double>::infinity();
+  return q;
+}
+}  // namespace
+
+extern "C" double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s) {
+  if (!p || c < 0 || s < 0) return -1.0;
+  return coserve::latency(to_profile(p), c, s);
+}
+
+extern "C" int64_t cs_sched_max_finetune_tokens(const cs_latency_profile* p, int64_t c,
+                                                double slo_ms) {
+  if (!p || c < 0 || !(slo_ms > 0)) return -1;
+  return coserve::max_finetune_tokens(to_profile(p), c, slo_ms);
+}

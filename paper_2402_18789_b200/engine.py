@@ -1,0 +1,291 @@
+"""Python mirror of the C ABI engine (include/coserve_cuda.h) for tests and bench.py.
+
+`Engine` owns one cs_engine (one GPU).  Every method is a thin ctypes call into
+libcoserve_cuda.so; errors follow the reference's conventions (ValueError for
+std::invalid_argument, CacheDesync / OrderingViolation for SPEC.md:287,296).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+i32, i64, f32, f64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double, ctypes.c_void_p
+
+SEG_DECODE, SEG_PREFILL, SEG_FT_FWD = 0, 1, 2
+FT_NONE, FT_FORWARD, FT_BACKWARD = 0, 1, 2
+
+
+class ModelConfig(ctypes.Structure):
+    _fields_ = [("n_layers", i32), ("hidden", i32), ("n_heads", i32), ("n_kv_heads", i32),
+                ("head_dim", i32), ("ffn", i32), ("vocab", i32), ("lora_rank", i32),
+                ("norm", i32), ("act", i32), ("rope", i32), ("qkv_bias", i32),
+                ("rope_theta", f32), ("rms_eps", f32), ("page_size", i32), ("n_pages", i32),
+                ("max_tokens", i32), ("max_ft_len", i32), ("max_segments", i32)]
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("kind", i32), ("q_start", i32), ("q_len", i32), ("ctx_start", i32),
+                ("page_off", i32), ("n_pages", i32), ("sample", i32), ("adapter", i32)]
+
+
+class FtWindow(ctypes.Structure):
+    _fields_ = [("phase", i32), ("seq_len", i32), ("l", i32), ("s", i32), ("layer", i32),
+                ("targets", ctypes.POINTER(i32)), ("page_off", i32), ("n_pages", i32)]
+
+
+class IterationPlan(ctypes.Structure):
+    _fields_ = [("n_tokens", i32), ("tokens", ctypes.POINTER(i32)), ("n_segments", i32),
+                ("segments", ctypes.POINTER(Segment)), ("page_table", ctypes.POINTER(i32)),
+                ("page_table_len", i32), ("ft", FtWindow)]
+
+
+class StepResult(ctypes.Structure):
+    _fields_ = [("next_tokens", ctypes.POINTER(i32)), ("logits", ctypes.POINTER(f32)),
+                ("ft_loss_sum", f64), ("iteration_ms", f32)]
+
+
+class LatencyProfileC(ctypes.Structure):
+    _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64)]
+
+
+def _declare_engine(L):
+    P = ctypes.POINTER
+    L.cs_engine_create.argtypes = [P(ModelConfig), ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                   P(vp)]
+    L.cs_engine_destroy.argtypes = [vp]
+    L.cs_engine_set_weight.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, vp, ctypes.c_int, i64, i64]
+    L.cs_engine_get_lora.argtypes = [vp, ctypes.c_int, vp, vp]
+    L.cs_engine_init_random.argtypes = [vp, ctypes.c_uint64]
+    L.cs_step.argtypes = [vp, P(IterationPlan), P(StepResult)]
+    L.cs_step_async.argtypes = [vp, P(IterationPlan)]
+    L.cs_sync.argtypes = [vp, P(StepResult)]
+    L.cs_adam_step.argtypes = [vp, f32, f32, f32, f32]
+    L.cs_zero_lora_grads.argtypes = [vp]
+    L.cs_read_lora_grads.argtypes = [vp, ctypes.c_int, vp, vp]
+    L.cs_read_kvgrad.argtypes = [vp, i32, vp, vp]
+    L.cs_read_kv.argtypes = [vp, ctypes.c_int, vp, i32, vp, vp]
+    L.cs_read_dy.argtypes = [vp, i32, vp]
+    L.cs_sched_latency.restype = f64
+    L.cs_sched_latency.argtypes = [P(LatencyProfileC), i64, i64]
+    L.cs_sched_max_finetune_tokens.restype = i64
+    L.cs_sched_max_finetune_tokens.argtypes = [P(LatencyProfileC), i64, f64]
+    for name in ("cs_engine_create", "cs_engine_destroy", "cs_engine_set_weight",
+                 "cs_engine_get_lora", "cs_engine_init_random", "cs_step", "cs_step_async",
+                 "cs_sync", "cs_adam_step", "cs_zero_lora_grads", "cs_read_lora_grads",
+                 "cs_read_kvgrad", "cs_read_kv", "cs_read_dy"):
+        getattr(L, name).restype = ctypes.c_int
+
+
+_DECLARED = False
+
+
+def lib():
+    global _DECLARED
+    L = _lib.lib()
+    if not _DECLARED:
+        _declare_engine(L)
+        _DECLARED = True
+    return L
+
+
+@dataclass
+class Seg:
+    """One segment of the mixed token batch (cs_segment)."""
+    kind: int
+    tokens: Sequence[int]
+    ctx_start: int
+    pages: Sequence[int]
+    sample: bool = False
+    adapter: bool = False
+
+
+def arch_config(arch, page_size=16, n_pages=256, max_tokens=256, max_ft_len=256,
+                max_segments=64) -> ModelConfig:
+    """ModelConfig from an oracle.Arch-like object (fields n_layers, hidden, ...)."""
+    c = ModelConfig()
+    c.n_layers = arch.n_layers
+    c.hidden = arch.hidden
+    c.n_heads = arch.n_heads
+    c.n_kv_heads = arch.n_kv_heads
+    c.head_dim = arch.head_dim
+    c.ffn = arch.ffn
+    c.vocab = arch.vocab
+    c.lora_rank = arch.lora_rank
+    c.norm = 1 if arch.norm == "rms" else 0
+    c.act = 1 if arch.act == "swiglu" else 0
+    c.rope = 1 if arch.rope else 0
+    c.qkv_bias = 1 if arch.qkv_bias else 0
+    c.rope_theta = arch.rope_theta
+    c.rms_eps = arch.rms_eps
+    c.page_size = page_size
+    c.n_pages = n_pages
+    c.max_tokens = max_tokens
+    c.max_ft_len = max_ft_len
+    c.max_segments = max_segments
+    return c
+
+
+class Engine:
+    def __init__(self, cfg: ModelConfig, device: int = 0):
+        self.cfg = cfg
+        self._L = lib()
+        h = vp()
+        _lib.check(self._L.cs_engine_create(ctypes.byref(cfg), device, 0, 1, None, ctypes.byref(h)),
+                   "cs_engine_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cs_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- weights
+    def set_weight(self, name: str, layer: int, value: np.ndarray):
+        v = np.ascontiguousarray(value, dtype=np.float64)
+        if v.ndim == 1:
+            v = v.reshape(1, -1)
+        _lib.check(self._L.cs_engine_set_weight(self._h, name.encode(), layer, v.ctypes.data, 0,
+                                                v.shape[0], v.shape[1]), f"set_weight({name})")
+
+    def load_weights(self, W: Dict):
+        """W in the oracle's dict format (reference layouts)."""
+        self.set_weight("embed", 0, W["embed"])
+        self.set_weight("unembed", 0, W["unembed"])
+        if "gf" in W:
+            self.set_weight("final_norm", 0, W["gf"])
+        names = {"wq": "wq", "wk": "wk", "wv": "wv", "wo": "wo", "w_gate": "w_gate",
+                 "w_up": "w_up", "w_down": "w_down", "lora_a": "lora_a", "lora_b": "lora_b",
+                 "bq": "bq", "bk": "bk", "bv": "bv", "g1": "norm1", "g2": "norm2"}
+        for l, Lw in enumerate(W["layers"]):
+            for k, v in Lw.items():
+                self.set_weight(names[k], l, v)
+
+    def init_random(self, seed: int = 1):
+        _lib.check(self._L.cs_engine_init_random(self._h, seed), "init_random")
+
+    # -------------------------------------------------------------- step
+    def _plan(self, segs: List[Seg], ft: Optional[Dict]):
+        tokens, cs_segs, pt = [], [], []
+        row = 0
+        for s in segs:
+            g = Segment()
+            g.kind = s.kind
+            g.q_start = row
+            g.q_len = len(s.tokens)
+            g.ctx_start = s.ctx_start
+            g.page_off = len(pt)
+            g.n_pages = len(s.pages)
+            g.sample = 1 if s.sample else 0
+            g.adapter = 1 if s.adapter else 0
+            pt.extend(int(p) for p in s.pages)
+            tokens.extend(int(t) for t in s.tokens)
+            cs_segs.append(g)
+            row += g.q_len
+        w = FtWindow()
+        keep = {}
+        if ft:
+            w.phase = ft["phase"]
+            w.seq_len = ft.get("seq_len", 0)
+            w.l = ft.get("l", 0)
+            w.s = ft.get("s", 0)
+            w.layer = ft.get("layer", 0)
+            if "pages" in ft:
+                w.page_off = len(pt)
+                w.n_pages = len(ft["pages"])
+                pt.extend(int(p) for p in ft["pages"])
+            if "targets" in ft:
+                tg = np.ascontiguousarray(ft["targets"], dtype=np.int32)
+                keep["tg"] = tg
+                w.targets = tg.ctypes.data_as(ctypes.POINTER(i32))
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        ptab = np.ascontiguousarray(pt if pt else [0], dtype=np.int32)
+        seg_arr = (Segment * max(1, len(cs_segs)))(*cs_segs)
+        p = IterationPlan()
+        p.n_tokens = len(tokens)
+        p.tokens = tok.ctypes.data_as(ctypes.POINTER(i32))
+        p.n_segments = len(cs_segs)
+        p.segments = seg_arr
+        p.page_table = ptab.ctypes.data_as(ctypes.POINTER(i32))
+        p.page_table_len = len(pt)
+        p.ft = w
+        keep.update(tok=tok, ptab=ptab, segs=seg_arr)
+        return p, keep
+
+    def step(self, segs: List[Seg], ft: Optional[Dict] = None, want_logits: bool = False):
+        p, keep = self._plan(segs, ft)
+        n_s = sum(1 for s in segs if s.sample)
+        nt = np.full(max(1, len(segs)), -1, dtype=np.int32)
+        logits = np.zeros((max(1, n_s), self.cfg.vocab), dtype=np.float32) if want_logits else None
+        r = StepResult()
+        r.next_tokens = nt.ctypes.data_as(ctypes.POINTER(i32))
+        if logits is not None:
+            r.logits = logits.ctypes.data_as(ctypes.POINTER(f32))
+        _lib.check(self._L.cs_step(self._h, ctypes.byref(p), ctypes.byref(r)), "cs_step")
+        del keep
+        out = {"next_tokens": nt[:len(segs)], "loss_sum": r.ft_loss_sum, "ms": r.iteration_ms}
+        if logits is not None:
+            out["logits"] = logits[:n_s]
+        return out
+
+    def step_async(self, segs: List[Seg], ft: Optional[Dict] = None):
+        p, keep = self._plan(segs, ft)
+        _lib.check(self._L.cs_step_async(self._h, ctypes.byref(p)), "cs_step_async")
+        return keep
+
+    def sync(self) -> float:
+        r = StepResult()
+        _lib.check(self._L.cs_sync(self._h, ctypes.byref(r)), "cs_sync")
+        return r.iteration_ms
+
+    def adam_step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        _lib.check(self._L.cs_adam_step(self._h, lr, beta1, beta2, eps), "cs_adam_step")
+
+    def zero_lora_grads(self):
+        _lib.check(self._L.cs_zero_lora_grads(self._h), "zero_lora_grads")
+
+    # -------------------------------------------------------------- read-back
+    def lora_grads(self, layer: int):
+        c = self.cfg
+        a = np.zeros((c.ffn, c.lora_rank))
+        b = np.zeros((c.lora_rank, c.hidden))
+        _lib.check(self._L.cs_read_lora_grads(self._h, layer, a.ctypes.data, b.ctypes.data), "read_lora_grads")
+        return a, b
+
+    def lora(self, layer: int):
+        c = self.cfg
+        a = np.zeros((c.ffn, c.lora_rank))
+        b = np.zeros((c.lora_rank, c.hidden))
+        _lib.check(self._L.cs_engine_get_lora(self._h, layer, a.ctypes.data, b.ctypes.data), "get_lora")
+        return a, b
+
+    def kvgrad(self, L: int):
+        kv = self.cfg.n_kv_heads * self.cfg.head_dim
+        dk = np.zeros((L, kv))
+        dv = np.zeros((L, kv))
+        _lib.check(self._L.cs_read_kvgrad(self._h, L, dk.ctypes.data, dv.ctypes.data), "read_kvgrad")
+        return dk, dv
+
+    def read_kv(self, layer: int, pages: Sequence[int], length: int):
+        kv = self.cfg.n_kv_heads * self.cfg.head_dim
+        pg = np.ascontiguousarray(pages, dtype=np.int32)
+        k = np.zeros((length, kv))
+        v = np.zeros((length, kv))
+        _lib.check(self._L.cs_read_kv(self._h, layer, pg.ctypes.data, length, k.ctypes.data,
+                                      v.ctypes.data), "read_kv")
+        return k, v
+
+    def read_dy(self, L: int):
+        out = np.zeros((L, self.cfg.hidden))
+        _lib.check(self._L.cs_read_dy(self._h, L, out.ctypes.data), "read_dy")
+        return out
