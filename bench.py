@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""bench.py -- FlexLLM co-serving on B200: finetune tokens/s under the inference SLO.
+
+Headline (BASELINE.json metric / configs[1]): LLaMA-3.1-8B-shaped random-init model, LoRA r=16
+on the MLP down projections, co-serving on 1 B200 with synthetic Poisson arrivals at 20 req/s
+(also reported at 4 and 10 req/s), TPOT SLO 50 ms.  A "step" is one co-serving iteration
+(cs_step through the C ABI: mixed decode / chunked-prefill / finetuning-window batch, one fused
+forward over all rows plus the token-level backward window).  The loop itself (scheduler,
+admission, KV paging, Adam per mini-batch) is the C++ runtime in include/coserve/, entered via
+cs_coserve_run.
+
+value   : finetune tokens/s from device time (CUDA events per step)
+e2e     : the same metric on the wall clock of the C-ABI calls with host buffers (plan H2D,
+          next-token/loss D2H inside every step)
+Finetune tokens/s = L / (time of one mini-batch) where the mini-batch time is estimated from
+the measured forward-window rate r_f (tokens/ms over forward-phase iterations) and backward
+rate r_b (layer-tokens/ms): t_mb = L/r_f + N_layers*L/r_b.
+
+Multi-GPU (--gpus N under torchrun): 8B runs as N independent replicas (TP=1 pipelines, as in
+PAPER.md:437-439 for the 8B model), each at the per-replica arrival rate: weak scaling, no
+data-path collective; value = sum of replica throughputs over the max-over-ranks time.
+
+--impl reference: the reference's own CPU path (oracle/_ref: tiny_model.hpp forward_full +
+backward_full compiled unmodified) on an 8B-shaped single layer, all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "finetune tokens/s under inference SLO at N req/s; co-serve iteration ms"
+SLO_MS = 50.0
+
+# LLaMA-3.1-8B shape
+L8B = dict(n_layers=32, hidden=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn=14336,
+           vocab=128256, lora_rank=16)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rate", type=float, default=20.0)
+    ap.add_argument("--rates", default="4,10,20")
+    ap.add_argument("--ft-len", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--log", default="")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+def _ref_worker(args):
+    """One host process: the reference's forward_full + backward_full on an 8B-shaped layer."""
+    L_tok, samples, seed = args
+    sys.path.insert(0, ROOT)
+    from oracle import ref as R  # noqa: E402  (reference CPU path = the measured thing here)
+    m = R.RefTinyModel(depth=1, hidden=4096, heads=32, ffn_mult=4, vocab=64, rank=16, seed=seed)
+    toks = list(range(L_tok))
+    ts = []
+    for _ in range(samples):
+        ts.append(m.time_forward_backward(toks, 1))
+    return ts
+
+
+def reference_rate(L_tok: int, samples: int, procs: int):
+    """FT tokens/s of the reference CPU path: one layer fwd+bwd on L_tok tokens, extrapolated x32
+    layers (the reference cannot express f=14336 / GQA / V=128256: ffn_mult=4, MHA, V=64)."""
+    import multiprocessing as mp
+    if procs <= 1:
+        ts = _ref_worker((L_tok, samples, 1))
+        per = [L_tok / (t * L8B["n_layers"]) for t in ts]
+        return statistics.median(per), ts
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_worker, [(L_tok, samples, 1 + i) for i in range(procs)])
+    # aggregate throughput: each process contributes its own rate
+    rate = sum(statistics.median([L_tok / (t * L8B["n_layers"]) for t in ts]) for ts in res)
+    return rate, [t for ts in res for t in ts]
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    try:
+        from oracle import ref as R
+        if not R.available():
+            raise FileNotFoundError("oracle/_ref/libcoserve_ref.so not built")
+    except Exception as ex:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU build missing: {ex}"}))
+        return 0
+    cores = os.cpu_count() or 1
+    L_tok = 4
+    t0 = time.time()
+    # warmup W and K steps are bounded samples: each step = one fwd+bwd of L_tok tokens through
+    # one 8B-shaped layer in every worker process
+    steps = max(1, min(a.steps, 3))
+    rate, ts = reference_rate(L_tok, steps, cores)
+    wall = time.time() - t0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(rate, 6), "unit": "tokens/s",
+        "n_gpus": world, "steps": steps, "warmup": 0,
+        "ms_per_step": round(1000.0 * statistics.median(ts), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic tokens, reference TinyModel::init weights",
+        "config": {"workload": "LLaMA-3.1-8B-shaped layer (h=4096, 32 heads MHA, ffn 4x, V=64), "
+                               f"{L_tok}-token finetuning window fwd+bwd, x32 layers extrapolated",
+                   "model": "reference tiny_model.hpp (f64)", "rate_rps": a.rate},
+        "cpu_baseline": {"value": round(rate, 6), "unit": "tokens/s", "cores": cores,
+                         "kind": "reference",
+                         "sample": f"{steps} x forward_full+backward_full, depth 1, L={L_tok}, "
+                                   f"per process, {cores} processes"},
+        "e2e": {"value": round(rate, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(wall, 1),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{device}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def make_engine(device: int, ft_len: int):
+    from paper_2402_18789_b200.engine import Engine, ModelConfig
+    c = ModelConfig()
+    for k, v in L8B.items():
+        setattr(c, k, v)
+    c.norm, c.act, c.rope, c.qkv_bias = 1, 1, 1, 0
+    c.rope_theta, c.rms_eps = 500000.0, 1e-5
+    c.page_size = 16
+    c.n_pages = 12288          # 196,608 KV token slots per layer (~24 GiB of KV)
+    c.max_tokens = 8192
+    c.max_ft_len = ft_len
+    c.max_segments = 96
+    eng = Engine(c, device=device)
+    eng.init_random(1234)
+    return eng
+
+
+def offline_profile(eng, ft_len: int):
+    """Fit f(c, s) = t0 + b (c + s) and the backward-token weight on this B200 (SPEC.md:395,
+    PAPER.md §6.2 'derived via offline profiling').  Doubles as warm-up of every kernel."""
+    from paper_2402_18789_b200.engine import (Seg, SEG_DECODE, SEG_FT_FWD, FT_FORWARD,
+                                              FT_BACKWARD)
+    P = 16
+    n_dec, ctx = 32, 512
+    base = 0
+    dec_pages = []
+    for i in range(n_dec):
+        dec_pages.append(list(range(base, base + ctx // P + 2)))
+        base += ctx // P + 2
+    ft_pages = list(range(base, base + (ft_len + P - 1) // P))
+
+    def decs(k=n_dec):
+        return [Seg(SEG_DECODE, [i % 1000], ctx, dec_pages[i], sample=True) for i in range(k)]
+
+    eng.reset_ft()
+    t_dec = []
+    for _ in range(3):
+        t_dec.append(eng.step(decs())["ms"])
+    t0 = min(t_dec)
+    fwd = []
+    win = 1024
+    toks = [(7 * i) % 1000 for i in range(ft_len)]
+    for l in range(0, ft_len, win):
+        s = min(win, ft_len - l)
+        out = eng.step(decs() + [Seg(SEG_FT_FWD, toks[l:l + s], l, ft_pages, adapter=True)],
+                       ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": s,
+                           "targets": toks[l + 1:l + s + 1] + ([-1] if l + s == ft_len else [])})
+        fwd.append((s, out["ms"]))
+    slope = statistics.mean((ms - t0) / s for s, ms in fwd)
+    bwd = []
+    lj = ft_len
+    bw = 2048
+    for n in range(L8B["n_layers"] - 1, -1, -1):
+        lj = ft_len
+        while lj > 0:
+            s = min(bw if n == L8B["n_layers"] - 1 else ft_len, lj)
+            out = eng.step(decs(), ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": lj, "s": s,
+                                       "layer": n, "pages": ft_pages})
+            if n >= 1:
+                bwd.append((s, out["ms"]))
+            lj -= s
+    eng.adam_step(1e-4)
+    w_b = statistics.mean((ms - t0) / s for s, ms in bwd) / slope
+    return {"t0_ms": t0, "slope_ms_per_token": slope, "bwd_token_weight": w_b,
+            "fwd_samples": fwd, "bwd_samples": bwd[:6]}
+
+
+def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False):
+    from paper_2402_18789_b200.engine import CoserveConfig, profile_struct
+    c = CoserveConfig()
+    c.rate_rps = rate
+    c.duration_s = 3600.0
+    c.burst_amplitude = 0.0
+    c.burst_period_s = 60.0
+    c.tpot_slo_ms = SLO_MS
+    c.ttft_slo_ms = 5000.0
+    c.budget_ms = 0.9 * SLO_MS   # planner budget; the adaptive correction tracks measured ms
+    c.max_batch = 64
+    c.chunk_size = 512
+    c.max_tokens = 8192
+    c.max_ft_window = 8192
+    c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
+                               prof["bwd_token_weight"])
+    c.ft_seq_len = ft_len
+    c.growth_tokens = 128
+    c.warmup_iters = warmup
+    c.timed_iters = steps
+    c.prepopulate = 48
+    c.adaptive = 1
+    c.profile_timed = 1 if profile_timed else 0
+    c.seed = seed
+    return c
+
+
+def ft_rate(st, n_layers, key_ms="ft_fwd_ms", bwd_key="ft_bwd_ms"):
+    """tokens/ms of finetuning mini-batch progress."""
+    f, b = st["ft_fwd_tokens"], st["ft_bwd_tokens"]
+    fm, bm = st[key_ms], st[bwd_key]
+    if f > 0 and b > 0 and fm > 0 and bm > 0:
+        r_f, r_b = f / fm, b / bm
+        return 1.0 / (1.0 / r_f + n_layers / r_b)
+    tot = st["timed_device_ms"]
+    return ((f + b / n_layers) / 2.0) / tot if tot > 0 else 0.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def run_ours(a):
+    rank, world, local = dist_env()
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_
+        dist = dist_
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2402_18789_b200 import build as B
+    if not os.path.exists(B.LIB):
+        raise SystemExit("libcoserve_cuda.so missing: run `python -m paper_2402_18789_b200.build`")
+    from paper_2402_18789_b200.engine import coserve_run
+
+    t_setup = time.time()
+    eng = make_engine(local, a.ft_len)
+    prof = offline_profile(eng, a.ft_len)
+    rates = sorted({float(x) for x in a.rates.split(",") if x} | {a.rate})
+    side = {}
+    for r in rates:
+        if r == a.rate:
+            continue
+        st, _ = coserve_run(eng, coserve_config(r, prof, min(a.steps, 60), a.warmup, a.ft_len,
+                                                seed=11 + int(r)))
+        side[str(int(r) if r.is_integer() else r)] = {
+            "value": round(1000.0 * ft_rate(st, L8B["n_layers"]), 1),
+            "iter_p99_ms": round(st["iter_p99_ms"], 2),
+            "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4)}
+    setup_s = time.time() - t_setup
+
+    clk = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    st, log = coserve_run(eng, coserve_config(a.rate, prof, a.steps, a.warmup, a.ft_len,
+                                               seed=7 + rank, profile_timed=True))
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if dist:
+        dist.barrier()
+    gemm = eng.read_profile(0)
+    attn = eng.read_profile(1)
+    attn_b = eng.read_profile(2)
+
+    n_layers = L8B["n_layers"]
+    rate_dev = ft_rate(st, n_layers)                       # tokens/ms on device time
+    wall_factor = st["timed_device_ms"] / st["timed_ms"] if st["timed_ms"] > 0 else 1.0
+    rate_wall = rate_dev * wall_factor                     # same estimator on the wall clock
+    mine = {"dev_ms": st["timed_device_ms"], "wall_ms": st["timed_ms"],
+            "units_dev": rate_dev * st["timed_device_ms"], "units_wall": rate_wall * st["timed_ms"]}
+    if dist:
+        import torch as T
+        t = T.tensor([mine["dev_ms"], mine["wall_ms"]], device="cuda", dtype=T.float64)
+        u = T.tensor([mine["units_dev"], mine["units_wall"]], device="cuda", dtype=T.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        dev_ms, wall_ms = t.tolist()
+        units_dev, units_wall = u.tolist()
+    else:
+        dev_ms, wall_ms = mine["dev_ms"], mine["wall_ms"]
+        units_dev, units_wall = mine["units_dev"], mine["units_wall"]
+    value = 1000.0 * units_dev / dev_ms if dev_ms > 0 else 0.0
+    e2e = 1000.0 * units_wall / wall_ms if wall_ms > 0 else 0.0
+
+    if rank != 0:
+        return 0
+    peaks, peak_kind = load_peaks()
+    peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    gemm_tf = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            from oracle import ref as R
+            if R.available():
+                t1 = time.time()
+                rate_cpu, ts = reference_rate(16, 1, 1)
+                cpu = {"value": round(rate_cpu, 6), "unit": "tokens/s", "cores": 1,
+                       "kind": "reference",
+                       "sample": "forward_full+backward_full of the reference (f64) on one "
+                                 "8B-shaped layer (h=4096, 32 heads, ffn 4x, V=64), L=16 "
+                                 "finetuning tokens, x32 layers extrapolated; "
+                                 f"{time.time() - t1:.1f}s incl. TinyModel::init"}
+        except Exception as ex:
+            cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {ex}"}
+    K = a.steps
+    h2d = st["h2d_bytes"] / max(1, K)
+    d2h = st["d2h_bytes"] / max(1, K)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": a.warmup,
+        "ms_per_step": round(wall_ms / max(1, K), 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: random-init weights (reference init scales), Poisson arrivals, "
+                "lognormal ShareGPT-like lengths, random tokens",
+        "config": {"workload": "LLaMA-3.1-8B-shaped co-serving, LoRA r=16 on down-proj, "
+                               f"{a.rate:g} req/s Poisson arrivals per GPU, TPOT SLO {SLO_MS:g} ms, "
+                               f"finetuning sequences L={a.ft_len}",
+                   "model": "llama-3.1-8b-shaped", "rate_rps_per_gpu": a.rate,
+                   "ft_seq_len": a.ft_len, "parallelism": f"replicas x{world} (TP=1)",
+                   "max_batch": 64, "chunk": 512,
+                   "l2": "working set (16 GB weights streamed per iteration) >> 126 MB L2"},
+        "e2e": {"value": round(e2e, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all projections)",
+                     "achieved": round(gemm_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(gemm_tf / peak_tf, 4) if peak_tf else None,
+                     "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
+                     "launches": gemm["launches"],
+                     "share_of_step": round(gemm["ms"] / dev_ms, 4) if dev_ms else None},
+        "attention": {"fwd_tflops": round(attn["flops"] / (attn["ms"] * 1e-3) / 1e12, 1) if attn["ms"] else None,
+                      "fwd_share": round(attn["ms"] / dev_ms, 4) if dev_ms else None,
+                      "bwd_tflops": round(attn_b["flops"] / (attn_b["ms"] * 1e-3) / 1e12, 1) if attn_b["ms"] else None,
+                      "bwd_share": round(attn_b["ms"] / dev_ms, 4) if dev_ms else None},
+        "cpu_baseline": cpu,
+        "gpu_launches": int(st["gpu_launches"]),
+        "clocks": clocks,
+        "inference": {"iter_p50_ms": round(st["iter_p50_ms"], 2),
+                      "iter_p99_ms": round(st["iter_p99_ms"], 2),
+                      "iter_max_ms": round(st["iter_max_ms"], 2),
+                      "slo_ms": SLO_MS,
+                      "requests_done": st["requests_done"],
+                      "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4),
+                      "tpot_p99_ms": round(st["tpot_p99_ms"], 2),
+                      "ttft_p99_ms": round(st["ttft_p99_ms"], 1),
+                      "gen_tokens_per_s": round(1000.0 * st["gen_tokens"] / max(1e-9, st["timed_ms"]), 1),
+                      "evictions": st["evictions"]},
+        "finetune": {"fwd_tokens": st["ft_fwd_tokens"], "bwd_layer_tokens": st["ft_bwd_tokens"],
+                     "minibatches_done": st["minibatches_done"]},
+        "other_rates": side,
+        "profile": {k: (round(v, 5) if isinstance(v, float) else v) for k, v in prof.items()
+                    if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight")},
+        "context": {"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200},
+        "setup_s": round(setup_s, 1),
+    }
+    print(json.dumps(line), flush=True)
+    if a.log:
+        with open(a.log, "w") as f:
+            json.dump({"line": line, "iters": log}, f)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

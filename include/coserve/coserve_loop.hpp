@@ -1,0 +1,336 @@
+// coserve/coserve_loop.hpp -- the co-serving engine loop (SPEC.md:675-728 sim_engine, run on a
+// real GPU): inject arrivals with time <= now, plan_iteration, execute the step, advance
+// request and finetuning state, Adam at the end of each mini-batch, record metrics.
+//
+// The clock is either the executor's measured iteration time (GPU: wall time of the step,
+// so arrivals, TTFT and TPOT are real) or the scheduler's predicted latency (simulation,
+// SPEC.md:450 "charges the predicted latency") -- the latter makes plans bit-reproducible
+// for parity against the oracle.  Header-only, no CUDA dependency: the GPU enters through
+// the StepExecutor interface (implemented over the C ABI in csrc/coserve_run.cpp).
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <deque>
+#include <vector>
+
+#include "coserve/cost_model.hpp"
+#include "coserve/scheduler.hpp"
+#include "coserve/workload.hpp"
+
+namespace coserve {
+
+struct StepSegment {
+  int kind = 0;  // 0 decode, 1 prefill, 2 finetuning forward window
+  std::vector<int32_t> tokens;
+  int ctx_start = 0;
+  const std::vector<int32_t>* pages = nullptr;
+  bool sample = false;
+  bool adapter = false;
+};
+
+struct StepInput {
+  std::vector<StepSegment> segs;
+  FtPhase ft_phase = FtPhase::Idle;
+  int ft_L = 0, ft_l = 0, ft_s = 0, ft_layer = -1;
+  std::vector<int32_t> ft_targets;
+  const std::vector<int32_t>* ft_pages = nullptr;
+};
+
+struct StepOutput {
+  std::vector<int32_t> next_tokens;  // per segment (-1 unsampled)
+  double ms = 0.0;                   // clock advance
+  double device_ms = 0.0;            // device time of the step
+};
+
+class StepExecutor {
+ public:
+  virtual ~StepExecutor() = default;
+  virtual bool run(const StepInput& in, StepOutput& out) = 0;
+  virtual bool adam() = 0;
+};
+
+struct LoopConfig {
+  SchedulerConfig sched;
+  LatencyProfile prof;
+  double budget_ms = 50.0;      // per-iteration latency budget handed to the planner
+  int n_layers = 2;
+  int vocab = 64;
+  int page_size = 16;
+  int64_t total_pages = 4096;
+  int growth_tokens = 128;      // admission reservation for generation
+  int ft_seq_len = 64;          // finetuning sequence length L (<= 8192)
+  int warmup_iters = 0;
+  int timed_iters = 100;
+  int prepopulate = 0;          // requests already decoding at t=0 (steady-state start)
+  bool adaptive = false;        // correct the profile with measured/predicted ratios
+  uint64_t seed = 0;
+  WorkloadConfig workload;
+};
+
+struct IterLog {
+  double t_ms = 0, pred_ms = 0, ms = 0, device_ms = 0;
+  int c = 0, s = 0, phase = 0, layer = -1, l = 0;
+  int n_decode = 0, n_prefill = 0, n_running = 0, n_queue = 0;
+  bool timed = false;
+};
+
+struct LoopStats {
+  int64_t iters = 0;
+  double timed_ms = 0, timed_device_ms = 0;
+  int64_t ft_fwd_tokens = 0, ft_bwd_tokens = 0;      // timed region
+  double ft_fwd_ms = 0, ft_bwd_ms = 0;                // timed time in fwd / bwd-phase iterations
+  int64_t minibatches_done = 0;                       // timed region
+  int64_t inf_tokens = 0;                             // timed region (decode + prefill)
+  int64_t gen_tokens = 0;
+  int64_t requests_done = 0, requests_slo_ok = 0;
+  int64_t evictions = 0;
+  std::vector<double> ttft_ms, tpot_ms;
+  std::vector<IterLog> log;
+  bool ok = true;
+};
+
+// deterministic synthetic token ids (data: synthetic)
+inline int32_t synth_token(int64_t id, int64_t pos, int vocab) {
+  uint64_t x = (uint64_t)id * 0x9E3779B97F4A7C15ull ^ (uint64_t)(pos + 1) * 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 31;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 29;
+  return (int32_t)(x % (uint64_t)vocab);
+}
+
+inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
+  LoopStats st;
+  MemoryModel mem(cfg.total_pages, cfg.page_size, cfg.growth_tokens);
+  const std::vector<Arrival> trace = generate_trace(cfg.workload, cfg.seed);
+  size_t next_arrival = 0;
+  std::deque<Request> queue;
+  std::vector<Request> running;
+  int64_t next_id = 0;
+  double now = 0.0;
+  // finetuning: one active mini-batch; its cache pages are reserved for the whole run
+  FtState ft;
+  ft.L = cfg.ft_seq_len;
+  ft.n_layers = cfg.n_layers;
+  std::vector<int32_t> ft_pages;
+  std::vector<int32_t> ft_tokens;
+  if (ft.L > 0) {
+    if (!mem.reserve(mem.pages_for(ft.L), &ft_pages)) {
+      st.ok = false;
+      return st;
+    }
+    ft.phase = FtPhase::Forward;
+    ft.minibatch = 0;
+    for (int i = 0; i < ft.L; ++i) ft_tokens.push_back(synth_token(-1, i, cfg.vocab));
+  }
+  // steady-state start: requests already decoding (synthetic KV contents)
+  {
+    TraceRng prng(cfg.seed ^ 0x5EED5EEDull);
+    for (int i = 0; i < cfg.prepopulate && (int)running.size() < cfg.sched.max_batch; ++i) {
+      Request r;
+      r.id = next_id++;
+      r.prompt_len = clip_len(prng.lognormal(cfg.workload.prompt_mu, cfg.workload.prompt_sigma),
+                              cfg.workload.prompt_min, cfg.workload.prompt_max);
+      r.gen_len = clip_len(prng.lognormal(cfg.workload.gen_mu, cfg.workload.gen_sigma),
+                           cfg.workload.gen_min, cfg.workload.gen_max);
+      r.prefilled = r.prompt_len;
+      r.emitted = 1 + (int)prng.uniform_int(0, std::max(0, r.gen_len - 2));
+      r.arrival_ms = -1e18;  // excluded from SLO statistics
+      r.first_token_ms = -1e18;
+      std::vector<int32_t> pages;
+      if (!mem.reserve(mem.pages_for(r.context() + 1 + cfg.growth_tokens), &pages)) break;
+      r.pages = std::move(pages);
+      r.last_token = synth_token(r.id, r.context(), cfg.vocab);
+      running.push_back(std::move(r));
+    }
+  }
+  double corr = 1.0;  // adaptive: measured / predicted
+  const int total_iters = cfg.warmup_iters + cfg.timed_iters;
+  for (int it = 0; it < total_iters; ++it) {
+    const bool timed = it >= cfg.warmup_iters;
+    while (next_arrival < trace.size() && trace[next_arrival].time_ms <= now) {
+      const Arrival& a = trace[next_arrival++];
+      Request r;
+      r.id = next_id++;
+      r.tenant = a.tenant;
+      r.prompt_len = a.prompt_len;
+      r.gen_len = a.gen_len;
+      r.arrival_ms = a.time_ms;
+      queue.push_back(std::move(r));
+    }
+    // decode growth: make room for each decoding request's next token (eviction if none)
+    for (size_t i = 0; i < running.size();) {
+      Request& r = running[i];
+      if (!r.in_prefill() && !r.done() &&
+          (int64_t)(r.context() + 1) > (int64_t)r.pages.size() * cfg.page_size) {
+        if (!mem.grow(&r.pages)) {
+          mem.release(r.pages);
+          r.pages.clear();
+          r.prefilled = 0;
+          r.emitted = 0;
+          r.evictions += 1;
+          st.evictions += 1;
+          queue.push_front(std::move(r));
+          running.erase(running.begin() + i);
+          continue;
+        }
+      }
+      ++i;
+    }
+    LatencyProfile prof = cfg.prof;
+    if (cfg.adaptive) {
+      prof.t0_ms *= corr;
+      prof.slope_ms_per_token *= corr;
+    }
+    IterationPlan plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
+    if (!enforce_dependencies(plan, ft)) {
+      st.ok = false;
+      return st;
+    }
+    // build the step
+    StepInput in;
+    for (int i : plan.decode) {
+      const Request& r = running[i];
+      StepSegment g;
+      g.kind = 0;
+      g.tokens = {r.last_token};
+      g.ctx_start = r.context();
+      g.pages = &r.pages;
+      g.sample = true;
+      in.segs.push_back(std::move(g));
+    }
+    for (const PrefillChunk& pc : plan.prefill) {
+      const Request& r = running[pc.req];
+      StepSegment g;
+      g.kind = 1;
+      for (int t = 0; t < pc.len; ++t) g.tokens.push_back(synth_token(r.id, pc.start + t, cfg.vocab));
+      g.ctx_start = pc.start;
+      g.pages = &r.pages;
+      g.sample = pc.start + pc.len == r.prompt_len;
+      in.segs.push_back(std::move(g));
+    }
+    const int64_t s = plan.s;
+    if (s > 0) {
+      in.ft_phase = plan.ft_phase;
+      in.ft_L = ft.L;
+      in.ft_s = (int)s;
+      in.ft_pages = &ft_pages;
+      if (plan.ft_phase == FtPhase::Forward) {
+        in.ft_l = ft.l;
+        StepSegment g;
+        g.kind = 2;
+        g.tokens.assign(ft_tokens.begin() + ft.l, ft_tokens.begin() + ft.l + s);
+        g.ctx_start = ft.l;
+        g.pages = &ft_pages;
+        g.adapter = true;
+        in.segs.push_back(std::move(g));
+        for (int64_t i = ft.l; i < ft.l + s; ++i)
+          in.ft_targets.push_back(i + 1 < ft.L ? ft_tokens[i + 1] : -1);
+      } else {
+        in.ft_l = ft.lj;
+        in.ft_layer = ft.layer;
+      }
+    }
+    StepOutput out;
+    if (exec) {
+      if (!exec->run(in, out)) {
+        st.ok = false;
+        return st;
+      }
+    } else {
+      out.ms = plan.predicted_ms;
+      out.device_ms = plan.predicted_ms;
+      out.next_tokens.assign(in.segs.size(), 0);
+    }
+    if (cfg.adaptive && plan.predicted_ms > 0 && out.device_ms > 0)
+      corr = std::max(0.5, std::min(2.0, 0.8 * corr + 0.2 * corr * out.device_ms / plan.predicted_ms));
+    now += out.ms;
+    // advance request state
+    int seg = 0;
+    for (int i : plan.decode) {
+      Request& r = running[i];
+      r.last_token = out.next_tokens[seg++];
+      r.emitted += 1;
+      if (timed) st.gen_tokens += 1;
+      if (r.done()) r.completion_ms = now;
+    }
+    for (const PrefillChunk& pc : plan.prefill) {
+      Request& r = running[pc.req];
+      r.prefilled += pc.len;
+      if (!r.in_prefill()) {
+        r.last_token = out.next_tokens[seg];
+        r.emitted = 1;
+        r.first_token_ms = now;
+        if (timed) st.gen_tokens += 1;
+        if (r.done()) r.completion_ms = now;
+      }
+      ++seg;
+    }
+    // retire finished requests
+    for (size_t i = 0; i < running.size();) {
+      Request& r = running[i];
+      if (r.done()) {
+        if (r.arrival_ms > -1e17) {
+          const double ttft = r.first_token_ms - r.arrival_ms;
+          const double tpot = r.gen_len > 1 ? (r.completion_ms - r.first_token_ms) / (r.gen_len - 1) : 0.0;
+          st.ttft_ms.push_back(ttft);
+          st.tpot_ms.push_back(tpot);
+          st.requests_done += 1;
+          if (tpot <= cfg.sched.tpot_slo_ms && ttft <= cfg.sched.ttft_slo_ms) st.requests_slo_ok += 1;
+        }
+        mem.release(r.pages);
+        running.erase(running.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+    // finetuning progress
+    const FtPhase ph = ft.phase;
+    advance_finetune(ft, s);
+    if (timed) {
+      if (ph == FtPhase::Forward) {
+        st.ft_fwd_tokens += s;
+        st.ft_fwd_ms += out.device_ms;
+      } else if (ph == FtPhase::Backward) {
+        st.ft_bwd_tokens += s;
+        st.ft_bwd_ms += out.device_ms;
+      }
+      st.inf_tokens += plan.c;
+      st.timed_ms += out.ms;
+      st.timed_device_ms += out.device_ms;
+    }
+    if (ft.phase == FtPhase::Done) {
+      if (exec && !exec->adam()) {
+        st.ok = false;
+        return st;
+      }
+      if (timed) st.minibatches_done += 1;
+      ft.phase = FtPhase::Forward;
+      ft.minibatch += 1;
+      ft.l = 0;
+      ft.layer = 0;
+      ft.lj = 0;
+      for (int i = 0; i < ft.L; ++i) ft_tokens[i] = synth_token(-1 - ft.minibatch, i, cfg.vocab);
+    }
+    IterLog lg;
+    lg.t_ms = now;
+    lg.pred_ms = plan.predicted_ms;
+    lg.ms = out.ms;
+    lg.device_ms = out.device_ms;
+    lg.c = (int)plan.c;
+    lg.s = (int)s;
+    lg.phase = (int)plan.ft_phase;
+    lg.layer = plan.ft_layer;
+    lg.l = plan.ft_l;
+    lg.n_decode = (int)plan.decode.size();
+    lg.n_prefill = (int)plan.prefill.size();
+    lg.n_running = (int)running.size();
+    lg.n_queue = (int)queue.size();
+    lg.timed = timed;
+    st.log.push_back(lg);
+    st.iters += 1;
+  }
+  return st;
+}
+
+}  // namespace coserve

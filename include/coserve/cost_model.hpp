@@ -16,6 +16,10 @@ struct LatencyProfile {
   double t0_ms = 2.0;
   double slope_ms_per_token = 0.01;
   double knee_tokens = std::numeric_limits<double>::infinity();  // slope doubles past the knee
+  // Cost of one backward-window token relative to a forward token.  SPEC.md:458 charges both
+  // through the same f (weight 1, the default); a measured B200 profile sets it from the
+  // offline profiler (a backward token touches one layer, a forward token all of them).
+  double bwd_token_weight = 1.0;
 };
 
 // t0 + b*min(c+s, k) + 2b*max(0, c+s-k)

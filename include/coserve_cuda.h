@@ -144,6 +144,8 @@ int cs_sync(cs_engine* e, cs_step_result* result);
 
 int cs_adam_step(cs_engine* e, float lr, float beta1, float beta2, float eps);
 int cs_zero_lora_grads(cs_engine* e);
+/* abandon the active finetuning mini-batch (cache length 0, backward state cleared, grads 0) */
+int cs_engine_reset_ft(cs_engine* e);
 int cs_read_lora_grads(cs_engine* e, int layer, double* grad_a, double* grad_b);
 /* dK, dV accumulated (ΔKVAccum) for the layer currently being back-propagated, rows [0, L). */
 int cs_read_kvgrad(cs_engine* e, int32_t L, double* dk_out, double* dv_out);
@@ -157,11 +159,63 @@ int cs_read_dy(cs_engine* e, int32_t L, double* out);
 typedef struct cs_latency_profile {
   double t0_ms;
   double slope_ms_per_token;
-  double knee_tokens; /* <= 0 -> infinite knee */
+  double knee_tokens;      /* <= 0 -> infinite knee                                   */
+  double bwd_token_weight; /* cost of a backward-window token in forward tokens; <= 0 -> 1 */
 } cs_latency_profile;
 
 double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);
 int64_t cs_sched_max_finetune_tokens(const cs_latency_profile* p, int64_t c, double slo_ms);
+
+/* ---------------------------------------------------------------- co-serving loop */
+/* One run of the co-serving engine loop over synthetic arrivals:
+ * plan_iteration -> cs_step -> advance state -> Adam per mini-batch.  engine == NULL runs the
+ * same loop on a simulated clock (predicted latency): plans are then
+ * bit-reproducible and are what the scheduler parity tests compare against the oracle. */
+typedef struct cs_coserve_config {
+  double rate_rps, duration_s, burst_amplitude, burst_period_s;
+  double tpot_slo_ms, ttft_slo_ms, budget_ms;
+  int32_t max_batch, chunk_size, max_tokens, max_ft_window;
+  cs_latency_profile profile;
+  int32_t ft_seq_len, growth_tokens, warmup_iters, timed_iters, prepopulate, adaptive;
+  int32_t profile_timed; /* switch on cs_engine_set_profiling at the first timed iteration */
+  uint64_t seed;
+  /* simulation-only (engine == NULL): model depth, vocab and KV pool */
+  int32_t n_layers, vocab, page_size;
+  int64_t total_pages;
+} cs_coserve_config;
+
+typedef struct cs_coserve_stats {
+  int64_t iters;
+  double timed_ms, timed_device_ms;
+  int64_t ft_fwd_tokens, ft_bwd_tokens;
+  double ft_fwd_ms, ft_bwd_ms;
+  int64_t minibatches_done;
+  int64_t inf_tokens, gen_tokens, requests_done, requests_slo_ok, evictions;
+  double ttft_p50_ms, ttft_p99_ms, tpot_p50_ms, tpot_p99_ms;
+  double iter_p50_ms, iter_p99_ms, iter_max_ms; /* timed iterations with inference work */
+  int64_t gpu_launches;                        /* kernels launched in the timed region   */
+  int64_t h2d_bytes, d2h_bytes;                /* host<->device bytes in the timed region */
+} cs_coserve_stats;
+
+typedef struct cs_iter_log {
+  double t_ms, pred_ms, ms, device_ms;
+  int32_t c, s, phase, layer, l, n_decode, n_prefill, n_running, n_queue, timed;
+} cs_iter_log;
+
+int cs_coserve_run(cs_engine* e, const cs_coserve_config* cfg, cs_coserve_stats* stats,
+                   cs_iter_log* log, int64_t log_cap, int64_t* log_len);
+/* kernels launched by this library so far (the driver's gpu_launches claim) */
+int64_t cs_engine_launch_count(cs_engine* e);
+/* Live profiling: when on, every GEMM / attention launch is bracketed by CUDA events on the
+ * engine stream; cs_engine_read_profile returns the summed device ms, algorithmic FLOPs and
+ * bytes and launch count per kind (0 = tcgen05 GEMM, 1 = attention fwd, 2 = attention bwd)
+ * since profiling was switched on. */
+int cs_engine_set_profiling(cs_engine* e, int on);
+int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops, double* bytes,
+                           int64_t* launches);
+/* model depth, vocab and KV pool geometry of an engine */
+int cs_engine_pool_info(cs_engine* e, int32_t* n_layers, int32_t* vocab, int32_t* page_size,
+                        int64_t* n_pages);
 
 #ifdef __cplusplus
 }

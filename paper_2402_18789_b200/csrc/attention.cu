@@ -16,8 +16,11 @@
 // XOR-swizzled shared memory with cp.async double buffering.
 #include <cfloat>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "engine_kernels.h"
+#include "kernels.h"
 #include "mma.cuh"
 
 namespace cs {
@@ -632,13 +635,17 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     constexpr int smem = 64 * 128 * 2 * 5;
     static bool once = (set_smem(attn_fwd_kernel<128>, smem), true);
     (void)once;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_fwd_kernel<128><<<n_work, 128, smem, st>>>(p);
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     if (n_combine > 0) attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
   } else if (head_dim == 64) {
     constexpr int smem = 64 * 64 * 2 * 5;
     static bool once = (set_smem(attn_fwd_kernel<64>, smem), true);
     (void)once;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_fwd_kernel<64><<<n_work, 128, smem, st>>>(p);
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     if (n_combine > 0) attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
   } else {
     return cudaErrorInvalidValue;
@@ -651,6 +658,7 @@ cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStre
   if (rows <= 0) return cudaSuccess;
   {
     const int warps = rows * n_heads;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_bwd_delta_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(
         p.dO, p.do_ld, p.O, p.o_ld, rows, n_heads, head_dim, p.delta);
   }
@@ -663,7 +671,9 @@ cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStre
     static bool once = (set_smem(attn_bwd_dq_kernel<128>, sq),
                         set_smem(attn_bwd_dkdv_kernel<128>, sk), true);
     (void)once;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_bwd_dq_kernel<128><<<gq, 128, sq, st>>>(p);
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_bwd_dkdv_kernel<128><<<gk, 128, sk, st>>>(p);
   } else if (head_dim == 64) {
     constexpr int sq = 64 * 64 * 2 * 6;
@@ -671,7 +681,9 @@ cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStre
     static bool once = (set_smem(attn_bwd_dq_kernel<64>, sq),
                         set_smem(attn_bwd_dkdv_kernel<64>, sk), true);
     (void)once;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_bwd_dq_kernel<64><<<gq, 128, sq, st>>>(p);
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     attn_bwd_dkdv_kernel<64><<<gk, 128, sk, st>>>(p);
   } else {
     return cudaErrorInvalidValue;

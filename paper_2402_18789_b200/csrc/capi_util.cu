@@ -5,6 +5,7 @@
 #include "kernels.h"
 
 namespace cs {
+std::atomic<long> g_launches{0};
 thread_local std::string g_last_error;
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;

@@ -6,8 +6,11 @@
 // token-level backward helpers (tiny_model.hpp:276-319), and the LoRA Adam update.
 #include <cfloat>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "engine_kernels.h"
+#include "kernels.h"
 
 namespace cs {
 
@@ -67,6 +70,7 @@ __global__ void embed_kernel(const int* __restrict__ tok, const bf16* __restrict
   }
 }
 void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (T > 0) embed_kernel<<<T, 128, 0, st>>>(tokens, embed, x, h);
 }
 
@@ -107,12 +111,14 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, long ldx, const int*
 void rmsnorm_cast(const float* x, long ldx, const float* g, bf16* out, long ldo, float* rstd_out,
                   int rows, int h, float eps, int use_norm, cudaStream_t st) {
   if (rows > 0)
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 void rmsnorm_cast_gather(const float* x, long ldx, const int* idx, const float* g, bf16* out,
                          long ldo, float* rstd_out, int rows, int h, float eps, int use_norm,
                          cudaStream_t st) {
   if (rows > 0)
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 
@@ -168,6 +174,7 @@ __global__ void rope_append_kernel(RopeAppendParams p, const float2* __restrict_
 static const float2* s_rope_tab = nullptr;
 void set_rope_table(const float2* tab) { s_rope_tab = tab; }
 void rope_append(const RopeAppendParams& p, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (p.T > 0) rope_append_kernel<<<p.T, 128, 0, st>>>(p, s_rope_tab);
 }
 
@@ -205,6 +212,7 @@ void act_fwd(const bf16* gu, long ld_gu, bf16* m, long ldm, int rows, int f, int
              cudaStream_t st) {
   if (rows <= 0) return;
   dim3 grid((unsigned)((ldm / 8 + 127) / 128), rows);
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   act_kernel<<<grid, 128, 0, st>>>(gu, ld_gu, m, ldm, f, swiglu);
 }
 
@@ -216,6 +224,7 @@ __global__ void lora_pack_kernel(const float* __restrict__ lu, int r, bf16* __re
   m[(long)row * ldm + f + j] = __float2bfloat16(lu[(long)row * r + j]);
 }
 void lora_pack(const float* lu, int r, bf16* m, long ldm, int f, int rows, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (rows > 0) lora_pack_kernel<<<(rows * r + 255) / 256, 256, 0, st>>>(lu, r, m, ldm, f, rows);
 }
 
@@ -257,6 +266,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, long ld, int V, 
   }
 }
 void argmax_rows(const float* logits, long ld, int rows, int V, int* out, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (rows > 0) argmax_kernel<<<rows, 512, 0, st>>>(logits, ld, V, out);
 }
 
@@ -289,6 +299,7 @@ __global__ void ce_kernel(const float* __restrict__ logits, long ld, const int* 
 }
 void ce_fwd_bwd(const float* logits, long ld, const int* targets, int rows, int V,
                 float inv_norm, float* loss, bf16* dlogits, long ldd, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (rows > 0) ce_kernel<<<rows, 512, 0, st>>>(logits, ld, targets, V, inv_norm, loss, dlogits, ldd);
 }
 
@@ -327,6 +338,7 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
                  const float* rstd, const float* dh, long ldh, float* out, long ldo,
                  bf16* out_b, long ldob, int rows, int h, int use_norm, cudaStream_t st) {
   if (rows > 0)
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     rms_bwd_kernel<<<rows, 256, 0, st>>>(resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
                                          ldob, h, use_norm);
 }
@@ -380,6 +392,7 @@ void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const fl
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st) {
   if (rows <= 0) return;
   dim3 grid((f + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   mlp_bwd_kernel<<<grid, 256, 0, st>>>(dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
                                        swiglu);
 }
@@ -443,8 +456,10 @@ __global__ void __launch_bounds__(256) lora_db_kernel(const float* __restrict__ 
 void lora_bwd_b(const float* dY, long ldy, const float* lu, const float* B, int r, int rows,
                 int h, float* dlu, bf16* dycat, long ldc, float* dB, cudaStream_t st) {
   if (rows <= 0) return;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   lora_dlu_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(dY, ldy, B, r, h, rows, dlu, dycat, ldc);
   dim3 grid((h + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   lora_db_kernel<<<grid, 256, 0, st>>>(dY, ldy, lu, r, rows, h, dB);
 }
 
@@ -485,6 +500,7 @@ void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, 
                    float theta, bf16* out, long ldo, cudaStream_t st) {
   (void)theta;
   if (rows > 0)
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
     rope_bwd_pack_kernel<<<rows, 128, 0, st>>>(dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
                                                head_dim, use_rope, s_rope_tab, out, ldo);
 }
@@ -525,6 +541,7 @@ __global__ void adam_kernel(AdamParams p, int update) {
   }
 }
 void adam_step(const AdamParams& p, int update, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   adam_kernel<<<4 * 148, 256, 0, st>>>(p, update);
 }
 
@@ -551,6 +568,7 @@ __global__ void cast_kernel(const float* __restrict__ src, int rows, int cols, b
 void cast_f32_bf16(const float* src, int rows, int cols, bf16* dst, long ldd, int transpose,
                    cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   cast_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, transpose);
 }
 
@@ -579,12 +597,15 @@ __global__ void fill_kernel(float* dst, long n, float v) {
     dst[i] = v;
 }
 void init_normal_bf16(bf16* dst, long n, float scale, uint64_t seed, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   init_bf16_kernel<<<8 * 148, 256, 0, st>>>(dst, n, scale, seed);
 }
 void init_normal_f32(float* dst, long n, float scale, uint64_t seed, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   init_f32_kernel<<<8 * 148, 256, 0, st>>>(dst, n, scale, seed);
 }
 void fill_f32(float* dst, long n, float v, cudaStream_t st) {
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   fill_kernel<<<4 * 148, 256, 0, st>>>(dst, n, v);
 }
 

@@ -89,7 +89,52 @@ struct cs_engine {
   int adam_t = 0;
   // device-side counters
   long launches = 0;
+  // live profiling (cs_engine_set_profiling): CUDA events around each GEMM / attention launch
+  bool profiling = false;
+  struct ProfRec {
+    cudaEvent_t a, b;
+    double flops, bytes;
+    int kind;  // 0 gemm, 1 attention fwd, 2 attention bwd
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<ProfRec> recs;
+  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
+  long prof_n[3] = {0, 0, 0};
+  double step_attn_flops = 0, step_attn_bytes = 0;
 };
+
+namespace {
+cudaEvent_t prof_event(cs_engine* e) {
+  if (e->ev_used == e->ev_pool.size()) {
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    e->ev_pool.push_back(ev);
+  }
+  return e->ev_pool[e->ev_used++];
+}
+void prof_begin(cs_engine* e, cs_engine::ProfRec& r) {
+  r.a = prof_event(e);
+  r.b = prof_event(e);
+  cudaEventRecord(r.a, e->st);
+}
+void prof_end(cs_engine* e, cs_engine::ProfRec& r) {
+  cudaEventRecord(r.b, e->st);
+  e->recs.push_back(r);
+}
+void prof_collect(cs_engine* e) {
+  for (auto& r : e->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    e->prof_ms[r.kind] += ms;
+    e->prof_flops[r.kind] += r.flops;
+    e->prof_bytes[r.kind] += r.bytes;
+    e->prof_n[r.kind] += 1;
+  }
+  e->recs.clear();
+  e->ev_used = 0;
+}
+}  // namespace
 
 namespace {
 
@@ -312,6 +357,40 @@ extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_r
     return cs::set_error(CS_ERR_CUDA, std::string("cs_engine_create: ") + cudaGetErrorString(err));
   }
   *out = e;
+  return CS_OK;
+}
+
+extern "C" int cs_engine_set_profiling(cs_engine* e, int on) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_profiling: null engine");
+  cudaStreamSynchronize(e->st);
+  prof_collect(e);
+  e->profiling = on != 0;
+  for (int k = 0; k < 3; ++k) e->prof_ms[k] = e->prof_flops[k] = e->prof_bytes[k] = 0, e->prof_n[k] = 0;
+  return CS_OK;
+}
+
+extern "C" int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops,
+                                      double* bytes, int64_t* launches) {
+  if (!e || kind < 0 || kind > 2) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_profile: bad kind");
+  if (ms) *ms = e->prof_ms[kind];
+  if (flops) *flops = e->prof_flops[kind];
+  if (bytes) *bytes = e->prof_bytes[kind];
+  if (launches) *launches = e->prof_n[kind];
+  return CS_OK;
+}
+
+extern "C" int64_t cs_engine_launch_count(cs_engine* e) {
+  (void)e;
+  return cs::g_launches.load();
+}
+
+extern "C" int cs_engine_pool_info(cs_engine* e, int32_t* n_layers, int32_t* vocab,
+                                   int32_t* page_size, int64_t* n_pages) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "pool_info: null engine");
+  if (n_layers) *n_layers = e->NL;
+  if (vocab) *vocab = e->V;
+  if (page_size) *page_size = e->P;
+  if (n_pages) *n_pages = e->npages;
   return CS_OK;
 }
 
@@ -552,7 +631,15 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
   g.epi = epi;
   g.bias = bias;
   e->launches++;
+  cs_engine::ProfRec pr{};
+  if (e->profiling) {
+    pr.flops = 2.0 * (double)M * (double)N * (double)K;
+    pr.bytes = 2.0 * ((double)M * K + (double)N * K) + (double)M * N * (epi == cs::EPI_BF16 ? 2 : 4);
+    pr.kind = 0;
+    prof_begin(e, pr);
+  }
   cudaError_t err = cs::gemm_tn(g, e->st);
+  if (e->profiling) prof_end(e, pr);
   if (err != cudaSuccess)
     return cs::set_error(CS_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(err));
   return CS_OK;
@@ -605,6 +692,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   std::vector<cs::AttnWork> work;
   std::vector<cs::AttnCombine> comb;
   const int rpt = 64 / e->grp;
+  double attn_flops = 0, attn_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {
     const cs_segment& g = plan->segments[s];
     if (g.q_start != row || g.q_len < 1 || g.q_start + g.q_len > T)
@@ -643,6 +731,11 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       samp_rows.push_back(row + g.q_len - 1);
       sp.samp_seg.push_back(s);
     }
+    {  // algorithmic attention work of this segment per layer
+      const double ql = g.q_len, c0 = g.ctx_start;
+      attn_flops += 4.0 * e->Hq * e->d * (ql * c0 + ql * (ql + 1) / 2.0);
+      attn_bytes += (c0 + ql) * (double)e->kv_dim * 2.0 * 2.0 + ql * e->q_dim * 2.0 * 2.0;
+    }
     // attention work items (GQA-packed q tiles x kv heads)
     for (int q0 = 0; q0 < g.q_len; q0 += rpt) {
       const int nq = std::min(rpt, g.q_len - q0);
@@ -653,6 +746,8 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     row += g.q_len;
   }
   if (row != T) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: segments do not cover n_tokens");
+  e->step_attn_flops = attn_flops;
+  e->step_attn_bytes = attn_bytes;
   // split long key ranges when the grid is small (flash-decoding)
   {
     const int target = 2 * 148;
@@ -790,7 +885,15 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     ap.part_lse = e->part_lse;
     ap.grp = e->grp;
     ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
+    cs_engine::ProfRec apr{};
+    if (e->profiling) {
+      apr.flops = e->step_attn_flops;
+      apr.bytes = e->step_attn_bytes;
+      apr.kind = 1;
+      prof_begin(e, apr);
+    }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
+    if (e->profiling) prof_end(e, apr);
     if (n_ft > 0 && keep_attn) {
       save_rows(e, e->ft_o + ((size_t)l * e->L_max + l0) * e->q_dim, e->q_dim,
                 e->attn + (size_t)sp.ft_row0 * e->q_dim, e->q_dim, n_ft, e->q_dim);
@@ -929,7 +1032,17 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     bp.grp = e->grp;
     bp.scale = (float)(1.0 / std::sqrt((double)e->d));
     bp.scale_log2 = bp.scale * 1.4426950408889634f;
+    cs_engine::ProfRec bpr{};
+    if (e->profiling) {
+      // QK^T recompute twice (dq, dkdv kernels), dP twice, dV, dK, dQ: 7 x 2*d per (q,k,head)
+      const double pairs = (double)s * ((double)a + (s + 1) / 2.0);
+      bpr.flops = 7.0 * 2.0 * e->d * e->Hq * pairs;
+      bpr.bytes = 0;
+      bpr.kind = 2;
+      prof_begin(e, bpr);
+    }
     CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
+    if (e->profiling) prof_end(e, bpr);
     cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
     TRY(gemm(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1, h,
@@ -1004,6 +1117,7 @@ int step_impl(cs_engine* e, const cs_iteration_plan* plan, bool sync, cs_step_re
                                   cudaMemcpyDeviceToHost, e->st));
   }
   CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  if (e->profiling) prof_collect(e);
   if (res) {
     double ls = 0.0;
     if (w.phase == CS_FT_FORWARD)
@@ -1029,6 +1143,7 @@ extern "C" int cs_step_async(cs_engine* e, const cs_iteration_plan* plan) {
 extern "C" int cs_sync(cs_engine* e, cs_step_result* result) {
   if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_sync: null engine");
   CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  if (e->profiling) prof_collect(e);
   if (result) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev0, e->ev1);
@@ -1053,6 +1168,17 @@ extern "C" int cs_adam_step(cs_engine* e, float lr, float beta1, float beta2, fl
   e->dy_cur = 0;
   CS_CUDA_TRY(cudaStreamSynchronize(e->st));
   return CS_OK;
+}
+
+extern "C" int cs_zero_lora_grads(cs_engine* e);
+extern "C" int cs_engine_reset_ft(cs_engine* e) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "reset_ft: null engine");
+  e->ft_len = 0;
+  e->ft_L = 0;
+  e->bwd_layer = -2;
+  e->bwd_next_end = 0;
+  e->dy_cur = 0;
+  return cs_zero_lora_grads(e);
 }
 
 extern "C" int cs_zero_lora_grads(cs_engine* e) {

@@ -22,6 +22,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -339,6 +341,7 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmAr
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   gemm_tn_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, a);
   return cudaGetLastError();
 }

@@ -4,7 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace cs {
+
+extern std::atomic<long> g_launches;  // kernels launched by this library (process-wide)
 
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 enum GemmEpi : int {

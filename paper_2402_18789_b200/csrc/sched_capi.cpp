@@ -16,6 +16,7 @@ coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
   q.t0_ms = p->t0_ms;
   q.slope_ms_per_token = p->slope_ms_per_token;
   q.knee_tokens = p->knee_tokens > 0 ? p->knee_tokens : std::numeric_limits<double>::infinity();
+  q.bwd_token_weight = p->bwd_token_weight > 0 ? p->bwd_token_weight : 1.0;
   return q;
 }
 }  // namespace

@@ -50,7 +50,36 @@ class StepResult(ctypes.Structure):
 
 
 class LatencyProfileC(ctypes.Structure):
-    _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64)]
+    _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64),
+                ("bwd_token_weight", f64)]
+
+
+class CoserveConfig(ctypes.Structure):
+    _fields_ = [("rate_rps", f64), ("duration_s", f64), ("burst_amplitude", f64),
+                ("burst_period_s", f64), ("tpot_slo_ms", f64), ("ttft_slo_ms", f64),
+                ("budget_ms", f64), ("max_batch", i32), ("chunk_size", i32), ("max_tokens", i32),
+                ("max_ft_window", i32), ("profile", LatencyProfileC), ("ft_seq_len", i32),
+                ("growth_tokens", i32), ("warmup_iters", i32), ("timed_iters", i32),
+                ("prepopulate", i32), ("adaptive", i32), ("profile_timed", i32),
+                ("seed", ctypes.c_uint64),
+                ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64)]
+
+
+class CoserveStats(ctypes.Structure):
+    _fields_ = [("iters", i64), ("timed_ms", f64), ("timed_device_ms", f64),
+                ("ft_fwd_tokens", i64), ("ft_bwd_tokens", i64), ("ft_fwd_ms", f64),
+                ("ft_bwd_ms", f64), ("minibatches_done", i64), ("inf_tokens", i64),
+                ("gen_tokens", i64), ("requests_done", i64), ("requests_slo_ok", i64),
+                ("evictions", i64), ("ttft_p50_ms", f64), ("ttft_p99_ms", f64),
+                ("tpot_p50_ms", f64), ("tpot_p99_ms", f64), ("iter_p50_ms", f64),
+                ("iter_p99_ms", f64), ("iter_max_ms", f64), ("gpu_launches", i64),
+                ("h2d_bytes", i64), ("d2h_bytes", i64)]
+
+
+class IterLogC(ctypes.Structure):
+    _fields_ = [("t_ms", f64), ("pred_ms", f64), ("ms", f64), ("device_ms", f64), ("c", i32),
+                ("s", i32), ("phase", i32), ("layer", i32), ("l", i32), ("n_decode", i32),
+                ("n_prefill", i32), ("n_running", i32), ("n_queue", i32), ("timed", i32)]
 
 
 def _declare_engine(L):
@@ -66,10 +95,22 @@ def _declare_engine(L):
     L.cs_sync.argtypes = [vp, P(StepResult)]
     L.cs_adam_step.argtypes = [vp, f32, f32, f32, f32]
     L.cs_zero_lora_grads.argtypes = [vp]
+    L.cs_engine_reset_ft.argtypes = [vp]
+    L.cs_engine_reset_ft.restype = ctypes.c_int
     L.cs_read_lora_grads.argtypes = [vp, ctypes.c_int, vp, vp]
     L.cs_read_kvgrad.argtypes = [vp, i32, vp, vp]
     L.cs_read_kv.argtypes = [vp, ctypes.c_int, vp, i32, vp, vp]
     L.cs_read_dy.argtypes = [vp, i32, vp]
+    L.cs_coserve_run.restype = ctypes.c_int
+    L.cs_coserve_run.argtypes = [vp, P(CoserveConfig), P(CoserveStats), P(IterLogC), i64, P(i64)]
+    L.cs_engine_launch_count.restype = i64
+    L.cs_engine_launch_count.argtypes = [vp]
+    L.cs_engine_set_profiling.restype = ctypes.c_int
+    L.cs_engine_set_profiling.argtypes = [vp, ctypes.c_int]
+    L.cs_engine_read_profile.restype = ctypes.c_int
+    L.cs_engine_read_profile.argtypes = [vp, ctypes.c_int, P(f64), P(f64), P(f64), P(i64)]
+    L.cs_engine_pool_info.restype = ctypes.c_int
+    L.cs_engine_pool_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i64)]
     L.cs_sched_latency.restype = f64
     L.cs_sched_latency.argtypes = [P(LatencyProfileC), i64, i64]
     L.cs_sched_max_finetune_tokens.restype = i64
@@ -251,6 +292,9 @@ class Engine:
     def adam_step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
         _lib.check(self._L.cs_adam_step(self._h, lr, beta1, beta2, eps), "cs_adam_step")
 
+    def reset_ft(self):
+        _lib.check(self._L.cs_engine_reset_ft(self._h), "reset_ft")
+
     def zero_lora_grads(self):
         _lib.check(self._L.cs_zero_lora_grads(self._h), "zero_lora_grads")
 
@@ -285,7 +329,51 @@ class Engine:
                                       v.ctypes.data), "read_kv")
         return k, v
 
+    def set_profiling(self, on: bool):
+        _lib.check(self._L.cs_engine_set_profiling(self._h, 1 if on else 0), "set_profiling")
+
+    def read_profile(self, kind: int) -> Dict:
+        ms, fl, by, n = f64(), f64(), f64(), i64()
+        _lib.check(self._L.cs_engine_read_profile(self._h, kind, ctypes.byref(ms), ctypes.byref(fl),
+                                                  ctypes.byref(by), ctypes.byref(n)), "read_profile")
+        return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": n.value}
+
+    def launch_count(self) -> int:
+        return int(self._L.cs_engine_launch_count(self._h))
+
     def read_dy(self, L: int):
         out = np.zeros((L, self.cfg.hidden))
         _lib.check(self._L.cs_read_dy(self._h, L, out.ctypes.data), "read_dy")
         return out
+
+
+def _struct_dict(st) -> Dict:
+    return {name: getattr(st, name) for name, _ in st._fields_}
+
+
+def coserve_run(engine: Optional["Engine"], cfg: CoserveConfig, log_cap: int = 100000):
+    """cs_coserve_run: the C++ co-serving loop (engine=None -> simulated clock)."""
+    L = lib()
+    stats = CoserveStats()
+    log = (IterLogC * max(1, log_cap))()
+    n = i64(0)
+    rc = L.cs_coserve_run(engine._h if engine is not None else None, ctypes.byref(cfg),
+                          ctypes.byref(stats), log, log_cap, ctypes.byref(n))
+    _lib.check(rc, "cs_coserve_run")
+    return _struct_dict(stats), [_struct_dict(log[i]) for i in range(n.value)]
+
+
+def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0) -> LatencyProfileC:
+    p = LatencyProfileC()
+    p.t0_ms, p.slope_ms_per_token, p.knee_tokens, p.bwd_token_weight = t0_ms, slope, knee, bwd_weight
+    return p
+
+
+def sched_latency(t0_ms, slope, knee, c, s) -> float:
+    p = profile_struct(t0_ms, slope, knee)
+    return lib().cs_sched_latency(ctypes.byref(p), c, s)
+
+
+def sched_max_finetune_tokens(t0_ms, slope, knee, c, slo_ms) -> int:
+    p = profile_struct(t0_ms, slope, knee)
+    return lib().cs_sched_max_finetune_tokens(ctypes.byref(p), c, slo_ms)
