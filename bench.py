@@ -278,17 +278,6 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False)
     return c
 
 
-def ft_rate(st, n_layers, key_ms="ft_fwd_ms", bwd_key="ft_bwd_ms"):
-    """tokens/ms of finetuning mini-batch progress."""
-    f, b = st["ft_fwd_tokens"], st["ft_bwd_tokens"]
-    fm, bm = st[key_ms], st[bwd_key]
-    if f > 0 and b > 0 and fm > 0 and bm > 0:
-        r_f, r_b = f / fm, b / bm
-        return 1.0 / (1.0 / r_f + n_layers / r_b)
-    tot = st["timed_device_ms"]
-    return ((f + b / n_layers) / 2.0) / tot if tot > 0 else 0.0
-
-
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -311,6 +300,7 @@ def run_ours(a):
     if not os.path.exists(B.LIB):
         raise SystemExit("libcoserve_cuda.so missing: run `python -m paper_2402_18789_b200.build`")
     from paper_2402_18789_b200.engine import coserve_run
+    from paper_2402_18789_b200.replicas import ft_rate_per_ms
 
     t_setup = time.time()
     eng = make_engine(local, a.ft_len)
@@ -323,7 +313,7 @@ def run_ours(a):
         st, _ = coserve_run(eng, coserve_config(r, prof, min(a.steps, 60), a.warmup, a.ft_len,
                                                 seed=11 + int(r)))
         side[str(int(r) if r.is_integer() else r)] = {
-            "value": round(1000.0 * ft_rate(st, L8B["n_layers"]), 1),
+            "value": round(1000.0 * ft_rate_per_ms(st, L8B["n_layers"]), 1),
             "iter_p99_ms": round(st["iter_p99_ms"], 2),
             "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4)}
     setup_s = time.time() - t_setup
@@ -344,24 +334,10 @@ def run_ours(a):
     attn_b = eng.read_profile(2)
 
     n_layers = L8B["n_layers"]
-    rate_dev = ft_rate(st, n_layers)                       # tokens/ms on device time
-    wall_factor = st["timed_device_ms"] / st["timed_ms"] if st["timed_ms"] > 0 else 1.0
-    rate_wall = rate_dev * wall_factor                     # same estimator on the wall clock
-    mine = {"dev_ms": st["timed_device_ms"], "wall_ms": st["timed_ms"],
-            "units_dev": rate_dev * st["timed_device_ms"], "units_wall": rate_wall * st["timed_ms"]}
-    if dist:
-        import torch as T
-        t = T.tensor([mine["dev_ms"], mine["wall_ms"]], device="cuda", dtype=T.float64)
-        u = T.tensor([mine["units_dev"], mine["units_wall"]], device="cuda", dtype=T.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)
-        dev_ms, wall_ms = t.tolist()
-        units_dev, units_wall = u.tolist()
-    else:
-        dev_ms, wall_ms = mine["dev_ms"], mine["wall_ms"]
-        units_dev, units_wall = mine["units_dev"], mine["units_wall"]
-    value = 1000.0 * units_dev / dev_ms if dev_ms > 0 else 0.0
-    e2e = 1000.0 * units_wall / wall_ms if wall_ms > 0 else 0.0
+    from paper_2402_18789_b200.replicas import aggregate
+    value, e2e = aggregate(st, n_layers, dist, device="cuda")
+    dev_ms = st["timed_device_ms"]
+    wall_ms = st["timed_ms"]
 
     if rank != 0:
         return 0

@@ -1,0 +1,235 @@
+"""The CPU oracle (oracle/coserve_oracle.py) pinned against the reference.
+
+* golden fixtures generated from the unmodified reference headers (tests/golden/make_golden.py)
+* SURVEY.md Appendix A golden values (reference headers, g++ 13.3)
+* the live reference build (oracle/_ref) when present
+* SPEC.md known answers for the spec-only window functions
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import coserve_oracle as O
+from oracle import ref as R
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+ARCH_A = O.Arch.reference(depth=2, hidden=16, heads=1, vocab=64, rank=2)
+ARCH_B = O.Arch.reference(depth=2, hidden=256, heads=4, vocab=64, rank=8)
+
+
+def test_rng_restatement_bit_exact():
+    r = O.Rng(5)
+    got = []
+    for i in range(1000):
+        k = i % 5
+        got.append([r.uniform, r.normal, lambda: r.lognormal(5.5, 0.8), lambda: r.exponential(4.0),
+                    lambda: float(r.uniform_int(0, 63))][k]())
+    assert np.array_equal(np.array(got), G["rng_mixed_seed5"])
+    assert np.array_equal(O.Rng(42).uniform_int(0, 63, 256), G["rng_uniform_int_seed42"])
+    assert np.array_equal(np.array([O.Rng(7).normal() for _ in range(1)]), G["rng_normal_seed7"][:1])
+    r7 = O.Rng(7)
+    assert np.array_equal(np.array([r7.normal() for _ in range(512)]), G["rng_normal_seed7"])
+
+
+def test_init_matches_reference_weights():
+    W = O.init_tiny(ARCH_A, 1)
+    assert np.array_equal(W["embed"], G["A_embed"])
+    assert np.array_equal(W["layers"][1]["lora_b"], G["A_lora_b1"])
+    assert W["embed"][0, 0] == 0.32821288224639056
+    assert W["layers"][1]["lora_b"][0, 0] == -0.056782015137392186
+    WB = O.init_tiny(ARCH_B, 1)
+    assert WB["embed"][0, 0] == 0.08205322056159764
+    assert WB["layers"][1]["lora_b"][0, 0] == 0.18610438794665335
+    with pytest.raises(ValueError):
+        O.init_tiny(O.Arch(n_layers=1, hidden=10, n_heads=3, n_kv_heads=3, head_dim=3, ffn=40), 1)
+
+
+def test_forward_backward_cfgA_vs_reference_fixture():
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"])
+    assert toks[:8] == [22, 40, 10, 14, 21, 60, 32, 0]
+    tr = O.forward_full(ARCH_A, W, toks)
+    bw = O.backward_full(ARCH_A, W, tr)
+    assert abs(tr["loss"] - 4.2596715437532966) < 1e-12        # Appendix A
+    assert O.rel_err(tr["loss"], float(G["A_loss"][0])) < 1e-13
+    assert O.max_rel_err(tr["logits"], G["A_logits"]) < 1e-12
+    assert abs(tr["logits"].sum() - (-143.45644448706673)) < 1e-9
+    ga = np.stack(bw["grads"]["a"])
+    gb = np.stack(bw["grads"]["b"])
+    assert O.scaled_err(ga, G["A_grad_a"]) < 1e-12
+    assert O.scaled_err(gb, G["A_grad_b"]) < 1e-12
+    assert abs(ga.sum() - (-0.19447850335348221)) < 1e-12
+    assert abs((ga ** 2).sum() - 0.022557606341355153) < 1e-12
+    assert abs(gb.sum() - 0.0064127813365707307) < 1e-12
+    for n in range(2):
+        for k in ("dk", "dv", "dx"):
+            assert O.scaled_err(bw["layers"][n][k], G["A_" + k][n]) < 1e-12
+    assert abs(sum(bw["layers"][n]["dv"].sum() for n in range(2)) - (-0.35241006949771214)) < 1e-12
+    assert abs(sum(bw["layers"][n]["dk"].sum() for n in range(2))) < 1e-15   # softmax rows
+
+
+def test_forward_backward_cfgB_vs_reference_fixture():
+    W = O.init_tiny(ARCH_B, 1)
+    toks = list(O.Rng(42).uniform_int(0, 63, 64))
+    tr = O.forward_full(ARCH_B, W, toks)
+    bw = O.backward_full(ARCH_B, W, tr)
+    assert abs(tr["loss"] - 4.1809416937891104) < 1e-12
+    assert O.max_rel_err(tr["logits"], G["B_logits"]) < 1e-12
+    ga = np.stack(bw["grads"]["a"])
+    assert O.scaled_err(ga, G["B_grad_a"]) < 1e-11
+    assert O.scaled_err(np.stack(bw["grads"]["b"]), G["B_grad_b"]) < 1e-11
+    assert abs(ga.sum() - (-2.7975593190285344)) < 1e-10
+    for n in range(2):
+        assert np.abs(bw["layers"][n]["dk"].sum(axis=1) - G["B_dk_rowsum"][n]).max() < 1e-12
+        assert np.abs(bw["layers"][n]["dv"].sum(axis=1) - G["B_dv_rowsum"][n]).max() < 1e-12
+        assert np.abs(bw["layers"][n]["dx"].sum(axis=1) - G["B_dx_rowsum"][n]).max() < 1e-12
+    assert np.abs(bw["layers"][1]["dx"][0] - G["B_dx_l1_row0"]).max() < 1e-12
+
+
+@pytest.mark.skipif(not R.available(), reason="reference build (oracle/_ref) absent")
+def test_oracle_vs_live_reference_random_configs():
+    rng = np.random.default_rng(0)
+    for depth, hidden, heads, rank, L in [(1, 32, 2, 3, 9), (3, 16, 4, 1, 20), (2, 64, 1, 4, 5)]:
+        arch = O.Arch.reference(depth=depth, hidden=hidden, heads=heads, vocab=64, rank=rank)
+        W = O.init_tiny(arch, 3)
+        toks = list(rng.integers(0, 64, L))
+        m = R.RefTinyModel(depth=depth, hidden=hidden, heads=heads, vocab=64, rank=rank, seed=3)
+        ref = m.forward_backward(toks)
+        tr = O.forward_full(arch, W, toks)
+        bw = O.backward_full(arch, W, tr)
+        assert O.rel_err(tr["loss"], ref["loss"]) < 1e-13
+        assert O.scaled_err(np.stack(bw["grads"]["a"]), ref["grad_a"]) < 1e-12
+        assert O.scaled_err(np.stack([l["dx"] for l in bw["layers"]]), ref["dx"]) < 1e-12
+
+
+# ------------------------------------------------------------------ SPEC.md known answers
+def _full(arch, W, toks):
+    tr = O.forward_full(arch, W, toks)
+    return tr, O.backward_full(arch, W, tr)
+
+
+def test_forward_window_partitions_equal_full():
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"][:4])
+    tr = O.forward_full(ARCH_A, W, toks)
+    cache = O.QkvCache(ARCH_A, 4)
+    l1, _ = O.forward_window(ARCH_A, W, toks[:2], 0, cache)
+    l2, _ = O.forward_window(ARCH_A, W, toks[2:], 2, cache)
+    assert O.max_rel_err(np.concatenate([l1, l2]), tr["logits"]) < 1e-12
+    with pytest.raises(O.CacheDesync):
+        O.forward_window(ARCH_A, W, toks[:2], 2, O.QkvCache(ARCH_A, 4))
+    # window losses sum exactly to the full loss
+    targets = toks[1:] + [-1]
+    s = O.generative_loss(l1, targets[:2]) + O.generative_loss(l2, targets[2:])
+    assert abs(s / 3 - tr["loss"]) < 1e-14
+
+
+def test_backward_window_partitions_L16_acceptance():
+    """Acceptance criterion 1 at L=16: uniform sizes + random partitions."""
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"][:16])
+    tr, ref = _full(ARCH_A, W, toks)
+    rng = np.random.default_rng(1)
+    parts = [[s] * (16 // s) for s in (1, 2, 4, 8, 16)]
+    for _ in range(50):
+        cuts = sorted(rng.choice(np.arange(1, 16), size=rng.integers(1, 6), replace=False))
+        parts.append(list(np.diff([0] + list(cuts) + [16])))
+    for p in parts:
+        bw = O.backward_full(ARCH_A, W, tr, windows=p)
+        assert O.max_grad_rel_err(bw["grads"], ref["grads"]) < 1e-10
+        for n in range(2):
+            assert O.max_rel_err(bw["layers"][n]["dk"], ref["layers"][n]["dk"]) < 1e-10
+            assert O.max_rel_err(bw["layers"][n]["dv"], ref["layers"][n]["dv"]) < 1e-10
+
+
+def test_backward_window_shape_contract():
+    """SPEC.md:298 / acceptance 2: s_j=2, l_j=6, h=16 -> dQ [2,16], dK/dV contributions [6,16]."""
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"][:6])
+    tr = O.forward_full(ARCH_A, W, toks)
+    acc = O.KvGradAccumulator(ARCH_A, 6)
+    dy = np.ones((2, 16))
+    dx, dq, dk, dv = O.backward_window(ARCH_A, W, 1, dy, 6, 2, tr["cache"], acc,
+                                       O.lora_grads_zeros(ARCH_A))
+    assert dq.shape == (2, 16) and dk.shape == (6, 16) and dv.shape == (6, 16) and dx.shape == (2, 16)
+    with pytest.raises(O.OrderingViolation):
+        st = {}
+        O.backward_window(ARCH_A, W, 1, dy, 6, 2, tr["cache"], acc, O.lora_grads_zeros(ARCH_A), st)
+        O.backward_window(ARCH_A, W, 1, dy, 6, 2, tr["cache"], acc, O.lora_grads_zeros(ARCH_A), st)
+
+
+def test_generative_loss_edge_cases():
+    assert O.generative_loss(np.zeros((1, 64)), [-1]) == 0.0
+    assert abs(O.generative_loss(np.zeros((3, 64)), [1, 2, 3]) / 3 - math.log(64)) < 1e-12
+    W = O.init_tiny(ARCH_A, 1)
+    assert O.forward_full(ARCH_A, W, [5])["loss"] == 0.0                      # L=1
+    with pytest.raises(ValueError):
+        O.forward_full(ARCH_A, W, [])
+
+
+def test_finite_differences_reference_arch():
+    """central differences (h=1e-6) on 10 LoRA params agree to <= 1e-6."""
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"][:12])
+    _, bw = _full(ARCH_A, W, toks)
+    rng = np.random.default_rng(4)
+    for _ in range(10):
+        l = int(rng.integers(0, 2))
+        key = "lora_a" if rng.random() < 0.5 else "lora_b"
+        i, j = (int(rng.integers(0, d)) for d in W["layers"][l][key].shape)
+        orig = W["layers"][l][key][i, j]
+        W["layers"][l][key][i, j] = orig + 1e-6
+        lp = O.forward_full(ARCH_A, W, toks)["loss"]
+        W["layers"][l][key][i, j] = orig - 1e-6
+        lm = O.forward_full(ARCH_A, W, toks)["loss"]
+        W["layers"][l][key][i, j] = orig
+        fd = (lp - lm) / 2e-6
+        g = bw["grads"]["a" if key == "lora_a" else "b"][l][i, j]
+        assert abs(fd - g) <= 1e-6 * max(1.0, abs(g)) + 1e-9
+
+
+def test_finite_differences_llama_arch():
+    """The LLaMA/Qwen generalisation (RMSNorm, RoPE, SwiGLU, GQA, bias) has no reference
+    oracle: pin its backward (incl. token-level windows) with central differences."""
+    arch = O.Arch(n_layers=2, hidden=16, n_heads=4, n_kv_heads=2, head_dim=4, ffn=24, vocab=32,
+                  lora_rank=3, norm="rms", act="swiglu", rope=True, qkv_bias=True, rope_theta=100.0)
+    W = O.init_general(arch, 2)
+    toks = list(np.random.default_rng(3).integers(0, 32, 10))
+    tr = O.forward_full(arch, W, toks)
+    bw = O.backward_full(arch, W, tr, windows=[3, 4, 3])
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        l = int(rng.integers(0, 2))
+        key = "lora_a" if rng.random() < 0.5 else "lora_b"
+        i, j = (int(rng.integers(0, d)) for d in W["layers"][l][key].shape)
+        orig = W["layers"][l][key][i, j]
+        W["layers"][l][key][i, j] = orig + 1e-6
+        lp = O.forward_full(arch, W, toks)["loss"]
+        W["layers"][l][key][i, j] = orig - 1e-6
+        lm = O.forward_full(arch, W, toks)["loss"]
+        W["layers"][l][key][i, j] = orig
+        fd = (lp - lm) / 2e-6
+        g = bw["grads"]["a" if key == "lora_a" else "b"][l][i, j]
+        assert abs(fd - g) <= 1e-6 * max(1.0, abs(g)) + 1e-9
+    # dX of the bottom layer via a finite difference on one embedding row
+    tr2 = O.forward_full(arch, W, toks)
+    full = O.backward_full(arch, W, tr2)
+    assert O.max_grad_rel_err(bw["grads"], full["grads"]) < 1e-10
+
+
+def test_causality():
+    W = O.init_tiny(ARCH_A, 1)
+    toks = list(G["A_tokens"][:10])
+    a = O.forward_full(ARCH_A, W, toks)["logits"]
+    b = O.forward_full(ARCH_A, W, toks[:6] + [0, 0, 0, 0])["logits"]
+    assert np.array_equal(a[:6], b[:6])
+
+
+def test_adam_oracle():
+    p = np.array([1.0, -2.0])
+    g = np.array([0.5, -0.1])
+    m, v = np.zeros(2), np.zeros(2)
+    O.adam_step(p, g, m, v, 1, O.AdamConfig(lr=0.1))
+    assert np.allclose(p, [0.9, -1.9], atol=1e-6)                             # step 1: -lr*sign(g)

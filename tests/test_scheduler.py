@@ -1,0 +1,94 @@
+"""Scheduler token selection / page indexing bit-exact: the C++ runtime (cs_coserve_run on the
+simulated clock) against the Python restatement (oracle/scheduler_oracle.py)."""
+import pytest
+
+from oracle import scheduler_oracle as S
+from paper_2402_18789_b200 import engine as E
+
+
+def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth=128,
+         max_batch=64, chunk=512, budget=50.0, amplitude=0.0):
+    c = E.CoserveConfig()
+    c.rate_rps = rate
+    c.duration_s = 600.0
+    c.burst_amplitude = amplitude
+    c.burst_period_s = 20.0
+    c.tpot_slo_ms = 50.0
+    c.ttft_slo_ms = 5000.0
+    c.budget_ms = budget
+    c.max_batch = max_batch
+    c.chunk_size = chunk
+    c.max_tokens = 8192
+    c.max_ft_window = 8192
+    c.profile = E.profile_struct(prof.t0_ms, prof.slope, 0.0 if prof.knee == S.INF else prof.knee,
+                                 prof.bwd_weight)
+    c.ft_seq_len = ft_len
+    c.growth_tokens = growth
+    c.warmup_iters = 0
+    c.timed_iters = iters
+    c.prepopulate = prepop
+    c.adaptive = 0
+    c.seed = seed
+    c.n_layers = n_layers
+    c.vocab = 1000
+    c.page_size = 16
+    c.total_pages = pages
+    return c
+
+
+CASES = [
+    # rate, profile, iters, ft_len, layers, seed, prepop, pages, growth, budget, amplitude
+    (20.0, S.Profile(5.0, 0.01, S.INF, 1.0), 400, 2048, 4, 0, 0, 4096, 128, 50.0, 0.0),
+    (20.0, S.Profile(7.3, 0.03, S.INF, 0.055), 300, 8192, 32, 1, 48, 8192, 128, 45.0, 0.0),
+    (4.0, S.Profile(2.0, 0.01, 4096.0, 1.0), 300, 512, 2, 2, 0, 4096, 64, 50.0, 0.5),
+    (40.0, S.Profile(3.0, 0.02, S.INF, 0.1), 300, 1024, 8, 3, 10, 600, 16, 50.0, 0.9),  # page pressure
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_sim_plans_bit_exact(case):
+    rate, prof, iters, ft_len, nl, seed, prepop, pages, growth, budget, amp = case
+    stats, log = E.coserve_run(None, _cfg(rate, prof, iters, ft_len, nl, seed, prepop, pages,
+                                          growth, budget=budget, amplitude=amp))
+    w = S.Workload(rate=rate, duration_s=600.0, amplitude=amp, period_s=20.0)
+    ref = S.run(prof, w, seed, nl, 16, pages, growth, ft_len, iters, prepopulate=prepop,
+                budget=budget)
+    assert len(log) == len(ref) == iters
+    for i, (a, b) in enumerate(zip(log, ref)):
+        for k in ("c", "s", "phase", "layer", "l", "n_decode", "n_prefill", "n_running", "n_queue"):
+            assert a[k] == b[k], (i, k, a[k], b[k])
+        assert a["t_ms"] == b["t_ms"], i
+        assert a["pred_ms"] == b["pred"], i
+    # SLO safety
+    for a in log:
+        if a["c"] > 0:
+            assert a["pred_ms"] <= budget + 1e-9
+
+
+def test_token_accounting_and_work_conservation():
+    prof = S.Profile(1.0, 0.01, S.INF, 1.0)
+    stats, log = E.coserve_run(None, _cfg(0.0, prof, 200, 64, 3, 0))
+    # no inference: every iteration schedules s = min(max under budget, remaining) > 0
+    assert all(a["s"] > 0 for a in log)
+    assert stats["minibatches_done"] >= 1
+    per_mb = 64 + 3 * 64                         # SPEC.md:707 forward L + N*L backward
+    total = stats["ft_fwd_tokens"] + stats["ft_bwd_tokens"]
+    assert total >= per_mb * stats["minibatches_done"]
+
+
+def test_spec_examples_via_oracle():
+    p = S.Profile(2.0, 0.01, 4096.0)
+    assert S.latency(p, 0, 0) == 2.0
+    assert S.latency(p, 1000, 0) == pytest.approx(12.0)
+    assert S.latency(p, 4196, 0) == pytest.approx(44.96)
+    q = S.Profile(2.0, 0.01)
+    assert S.max_finetune_tokens(q, 1000, 50.0) == 3800
+    assert S.max_finetune_tokens(q, 1000, S.latency(q, 1000, 7)) == 7
+    m = S.MemoryModel(3, 16)
+    assert m.try_admit(60) is None
+    ft = S.FtState(L=8, n_layers=2, phase=S.FWD)
+    trace = []
+    for s in (3, 3, 2):
+        S.advance_finetune(ft, s)
+        trace.append(ft.l)
+    assert trace == [3, 6, 8] and ft.phase == S.BWD
