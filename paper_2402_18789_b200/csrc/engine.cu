@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,6 +48,7 @@ struct cs_engine {
   int h, Hq, Hkv, d, q_dim, kv_dim, nqkv, f, V, r, NL, P, npages, gu_n, f_cat, h_cat, grp;
   int T_max, L_max, S_max, max_seg, head_chunk, max_pos;
   bool swiglu, norm, rope;
+  bool use_tc_attn = true;  // CS_ATTN_TC=0 forces the mma.sync path (A/B testing)
   // arena
   uint8_t* arena = nullptr;
   size_t arena_bytes = 0, arena_used = 0;
@@ -312,6 +314,7 @@ extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_r
   e->head_chunk = std::min(1024, std::max(64, c.max_tokens));
   e->max_pos = std::max((long)c.max_ft_len, std::min<long>((long)c.n_pages * c.page_size, 1 << 17)) + 1;
   e->meta_bytes = meta_size(e);
+  if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -605,11 +608,12 @@ struct StepPlan {
   int ft_row0 = 0;  // first FT forward row (== T if none)
   int ad_row0 = 0;  // first adapter row (== T if none)
   int n_samp = 0;
-  int n_work = 0, n_comb = 0;
+  int n_work = 0, n_comb = 0, n_tc = 0;
   // device pointers into d_meta
   int *tokens, *row_pos, *row_seg, *page_table, *samp_idx, *targets;
   cs::AttnSeg* segs;
   cs::AttnWork* work;
+  cs::AttnWork* work_tc;
   cs::AttnCombine* comb;
   std::vector<int> samp_seg;  // segment of each sampled row
 };
@@ -689,9 +693,11 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   int row = 0;
   bool in_adapter_suffix = false;
   std::vector<int> samp_rows;
-  std::vector<cs::AttnWork> work;
+  std::vector<cs::AttnWork> work, work_tc;
   std::vector<cs::AttnCombine> comb;
   const int rpt = 64 / e->grp;
+  const int rpt_tc = 128 / e->grp;
+  const bool tc_ok = e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn;
   double attn_flops = 0, attn_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {
     const cs_segment& g = plan->segments[s];
@@ -736,12 +742,22 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       attn_flops += 4.0 * e->Hq * e->d * (ql * c0 + ql * (ql + 1) / 2.0);
       attn_bytes += (c0 + ql) * (double)e->kv_dim * 2.0 * 2.0 + ql * e->q_dim * 2.0 * 2.0;
     }
-    // attention work items (GQA-packed q tiles x kv heads)
-    for (int q0 = 0; q0 < g.q_len; q0 += rpt) {
-      const int nq = std::min(rpt, g.q_len - q0);
-      const int nkeys = g.ctx_start + q0 + nq;
-      for (int kh = 0; kh < e->Hkv; ++kh)
-        work.push_back(cs::AttnWork{s, q0, nq, kh, 0, nkeys, -1, 0});
+    // attention work items (GQA-packed q tiles x kv heads): multi-row segments on the
+    // tcgen05 kernel (128 packed rows), decode rows on the bandwidth kernel (64 packed rows)
+    if (tc_ok && g.q_len >= 16) {
+      for (int q0 = 0; q0 < g.q_len; q0 += rpt_tc) {
+        const int nq = std::min(rpt_tc, g.q_len - q0);
+        const int nkeys = g.ctx_start + q0 + nq;
+        for (int kh = 0; kh < e->Hkv; ++kh)
+          work_tc.push_back(cs::AttnWork{s, q0, nq, kh, 0, nkeys, -1, 0});
+      }
+    } else {
+      for (int q0 = 0; q0 < g.q_len; q0 += rpt) {
+        const int nq = std::min(rpt, g.q_len - q0);
+        const int nkeys = g.ctx_start + q0 + nq;
+        for (int kh = 0; kh < e->Hkv; ++kh)
+          work.push_back(cs::AttnWork{s, q0, nq, kh, 0, nkeys, -1, 0});
+      }
     }
     row += g.q_len;
   }
@@ -780,17 +796,23 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       else comb.clear();
     }
   }
+  // longest key ranges first (causal tiles have very different lengths)
+  std::stable_sort(work_tc.begin(), work_tc.end(),
+                   [](const cs::AttnWork& x, const cs::AttnWork& y) { return x.k_end > y.k_end; });
   sp.n_work = (int)work.size();
+  sp.n_tc = (int)work_tc.size();
   sp.n_comb = (int)comb.size();
-  if (sp.n_work > 65536 || sp.n_comb > 8192)
+  if (sp.n_work + sp.n_tc > 65536 || sp.n_comb > 8192)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: attention work list too large");
   const size_t o_work = take(work.size() * sizeof(cs::AttnWork));
+  const size_t o_wtc = take(work_tc.size() * sizeof(cs::AttnWork));
   const size_t o_comb = take(comb.size() * sizeof(cs::AttnCombine));
   const size_t o_samp = take(samp_rows.size() * 4);
   const int ft_s = (plan->ft.phase == CS_FT_FORWARD) ? plan->ft.s : 0;
   const size_t o_tg = take((size_t)std::max(ft_s, 0) * 4);
   if (off > e->meta_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: plan too large");
   if (!work.empty()) std::memcpy(hb + o_work, work.data(), work.size() * sizeof(cs::AttnWork));
+  if (!work_tc.empty()) std::memcpy(hb + o_wtc, work_tc.data(), work_tc.size() * sizeof(cs::AttnWork));
   if (!comb.empty()) std::memcpy(hb + o_comb, comb.data(), comb.size() * sizeof(cs::AttnCombine));
   if (!samp_rows.empty()) std::memcpy(hb + o_samp, samp_rows.data(), samp_rows.size() * 4);
   if (ft_s > 0) {
@@ -812,6 +834,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.page_table = reinterpret_cast<int*>(db + o_pt);
   sp.work = reinterpret_cast<cs::AttnWork*>(db + o_work);
   sp.comb = reinterpret_cast<cs::AttnCombine*>(db + o_comb);
+  sp.work_tc = reinterpret_cast<cs::AttnWork*>(db + o_wtc);
   sp.samp_idx = reinterpret_cast<int*>(db + o_samp);
   sp.targets = reinterpret_cast<int*>(db + o_tg);
   return CS_OK;
@@ -893,6 +916,16 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
       prof_begin(e, apr);
     }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
+    if (sp.n_tc > 0) {
+      CUtensorMap mk, mv;
+      const long pool_rows = (long)e->npages * e->P;
+      if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
+          cs::make_map(&mv, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0)
+        return cs::set_error(CS_ERR_CUDA, "attention: TMA map creation failed");
+      cs::AttnFwdParams tp = ap;
+      tp.work = sp.work_tc;
+      CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, sp.n_tc, st));
+    }
     if (e->profiling) prof_end(e, apr);
     if (n_ft > 0 && keep_attn) {
       save_rows(e, e->ft_o + ((size_t)l * e->L_max + l0) * e->q_dim, e->q_dim,

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cuda.h>
 
 namespace cs {
 
@@ -70,6 +71,9 @@ struct AttnBwdParams {
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
+// tcgen05 forward for prefill / finetuning-window tiles (head_dim 128, 128 packed rows per CTA)
+cudaError_t attn_fwd_tc(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                        int n_work, cudaStream_t st);
 
 // ------------------------------------------------------------------ elementwise (elem.cu)
 void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, cudaStream_t st);

@@ -303,6 +303,8 @@ struct MapKeyHash {
 std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
+}  // namespace
+
 int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, int box_rows) {
   MapKey key{ptr, rows, cols, ld, box_rows};
   {
@@ -329,6 +331,8 @@ int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, i
   g_maps[key] = *out;
   return 0;
 }
+
+namespace {
 
 template <int BN>
 cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cuda.h>
 
 #include <atomic>
 
@@ -36,6 +37,8 @@ struct GemmDesc {
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);
+// cached 2D bf16 TMA map (SWIZZLE_128B, box = 64 columns x box_rows rows); 0 on success
+int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, int box_rows);
 int gemm_pick_bn(long M, long N);
 
 }  // namespace cs

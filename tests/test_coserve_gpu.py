@@ -223,3 +223,33 @@ def test_errors_follow_reference_conventions():
         eng.step([Seg(SEG_PREFILL, [999], 0, [5])])
     with pytest.raises(ValueError):  # page table does not cover the context
         eng.step([Seg(SEG_PREFILL, list(range(20)), 0, [5])])
+
+
+ARCH_D128 = O.Arch(n_layers=2, hidden=512, n_heads=4, n_kv_heads=2, head_dim=128, ffn=512,
+                   vocab=128, lora_rank=8, norm="rms", act="swiglu", rope=True, qkv_bias=False,
+                   rope_theta=10000.0)
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_d128_tcgen05_attention_parity(tc, monkeypatch):
+    """head_dim 128: prefill / FT-window rows run on the tcgen05 attention kernel (CS_ATTN_TC=1)
+    or the mma.sync kernel (0); contexts span several 128-key tiles and a window boundary that
+    is not tile aligned."""
+    monkeypatch.setenv("CS_ATTN_TC", tc)
+    arch = ARCH_D128
+    W = O.init_general(arch, 7)
+    toks = list(np.random.default_rng(9).integers(0, arch.vocab, 300))
+    tr = O.forward_full(arch, W, toks)
+    bw = O.backward_full(arch, W, tr)
+    eng, loss_sum, kvg, dys, dmax = _run_coserve(arch, W, toks, [100, 200], [150, 150], n_inf=5,
+                                                 logit_tol=0.04)
+    assert O.rel_err(loss_sum / 299.0, tr["loss"]) < TOL
+    for l in range(arch.n_layers):
+        ga, gb = eng.lora_grads(l)
+        assert O.max_rel_err(ga, bw["grads"]["a"][l]) < TOL
+        assert O.scaled_err(ga, bw["grads"]["a"][l]) < FLOOR_DEEP, l
+        assert O.scaled_err(gb, bw["grads"]["b"][l]) < FLOOR_DEEP, l
+    dk, dv = kvg[1]
+    assert O.scaled_err(dk, bw["layers"][1]["dk"]) < FLOOR_DEEP
+    assert O.scaled_err(dv, bw["layers"][1]["dv"]) < FLOOR_DEEP
+    assert O.scaled_err(dys[1], bw["layers"][1]["dx"]) < FLOOR_DEEP
