@@ -917,14 +917,16 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
     if (sp.n_tc > 0) {
-      CUtensorMap mk, mv;
+      CUtensorMap mk, mv, mk128, mv128;
       const long pool_rows = (long)e->npages * e->P;
       if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
-          cs::make_map(&mv, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0)
+          cs::make_map(&mv, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
+          cs::make_map(&mk128, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
+          cs::make_map(&mv128, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention: TMA map creation failed");
       cs::AttnFwdParams tp = ap;
       tp.work = sp.work_tc;
-      CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, sp.n_tc, st));
+      CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
     }
     if (e->profiling) prof_end(e, apr);
     if (n_ft > 0 && keep_attn) {

@@ -73,7 +73,8 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
 // tcgen05 forward for prefill / finetuning-window tiles (head_dim 128, 128 packed rows per CTA)
 cudaError_t attn_fwd_tc(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                        int n_work, cudaStream_t st);
+                        const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,
+                        cudaStream_t st);
 
 // ------------------------------------------------------------------ elementwise (elem.cu)
 void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, cudaStream_t st);
