@@ -231,8 +231,7 @@ def offline_profile(eng, ft_len: int):
         out = eng.step(decs() + [Seg(SEG_FT_FWD, toks[l:l + s], l, ft_pages, adapter=True)],
                        ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": s,
                            "targets": toks[l + 1:l + s + 1] + ([-1] if l + s == ft_len else [])})
-        fwd.append((s, out["ms"]))
-    slope = statistics.mean((ms - t0) / s for s, ms in fwd)
+        fwd.append((s, l, out["ms"]))
     bwd = []
     lj = ft_len
     bw = 2048
@@ -243,11 +242,23 @@ def offline_profile(eng, ft_len: int):
             out = eng.step(decs(), ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": lj, "s": s,
                                        "layer": n, "pages": ft_pages})
             if n >= 1:
-                bwd.append((s, out["ms"]))
+                bwd.append((s, lj, out["ms"]))
             lj -= s
     eng.adam_step(1e-4)
-    w_b = statistics.mean((ms - t0) / s for s, ms in bwd) / slope
-    return {"t0_ms": t0, "slope_ms_per_token": slope, "bwd_token_weight": w_b,
+
+    def linfit(xs, ys):
+        mx, my = statistics.mean(xs), statistics.mean(ys)
+        vx = sum((x - mx) ** 2 for x in xs)
+        a = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / vx if vx > 0 else 0.0
+        a = max(a, 0.0)
+        return my - a * mx, a
+
+    # forward window: (ms - t0)/s = b + a_f (l + s/2);  backward: = w_b b + a_b (l_j - s/2)
+    b, a_f = linfit([l + s / 2.0 for s, l, _ in fwd], [(ms - t0) / s for s, _, ms in fwd])
+    wb, a_b = linfit([lj - s / 2.0 for s, lj, _ in bwd], [(ms - t0) / s for s, _, ms in bwd])
+    b = max(b, 1e-6)
+    return {"t0_ms": t0, "slope_ms_per_token": b, "bwd_token_weight": max(wb, 1e-6) / b,
+            "attn_fwd_ms_per_token_ctx": a_f, "attn_bwd_ms_per_token_ctx": a_b,
             "fwd_samples": fwd, "bwd_samples": bwd[:6]}
 
 
@@ -266,7 +277,9 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False)
     c.max_tokens = 8192
     c.max_ft_window = 8192
     c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
-                               prof["bwd_token_weight"])
+                               prof["bwd_token_weight"], prof["attn_fwd_ms_per_token_ctx"],
+                               prof["attn_bwd_ms_per_token_ctx"])
+    c.multi_layer_bwd = 1
     c.ft_seq_len = ft_len
     c.growth_tokens = 128
     c.warmup_iters = warmup
@@ -332,6 +345,7 @@ def run_ours(a):
     gemm = eng.read_profile(0)
     attn = eng.read_profile(1)
     attn_b = eng.read_profile(2)
+    attn_tc = eng.read_profile(3)
 
     n_layers = L8B["n_layers"]
     from paper_2402_18789_b200.replicas import aggregate
@@ -399,8 +413,11 @@ def run_ours(a):
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
                      "launches": gemm["launches"],
                      "share_of_step": round(gemm["ms"] / dev_ms, 4) if dev_ms else None},
-        "attention": {"fwd_tflops": round(attn["flops"] / (attn["ms"] * 1e-3) / 1e12, 1) if attn["ms"] else None,
-                      "fwd_share": round(attn["ms"] / dev_ms, 4) if dev_ms else None,
+        "attention": {"fwd_tc_tflops": round(attn_tc["flops"] / (attn_tc["ms"] * 1e-3) / 1e12, 1) if attn_tc["ms"] else None,
+                      "fwd_tc_share": round(attn_tc["ms"] / dev_ms, 4) if dev_ms else None,
+                      "decode_gbs": round(attn["bytes"] / (attn["ms"] * 1e-3) / 1e9, 1) if attn["ms"] else None,
+                      "decode_hbm_frac": round(attn["bytes"] / (attn["ms"] * 1e-3) / 1e9 / float(load_peaks()[0].get("hbm_gbs", 6650.0)), 4) if attn["ms"] else None,
+                      "decode_share": round(attn["ms"] / dev_ms, 4) if dev_ms else None,
                       "bwd_tflops": round(attn_b["flops"] / (attn_b["ms"] * 1e-3) / 1e12, 1) if attn_b["ms"] else None,
                       "bwd_share": round(attn_b["ms"] / dev_ms, 4) if dev_ms else None},
         "cpu_baseline": cpu,
@@ -420,7 +437,8 @@ def run_ours(a):
                      "minibatches_done": st["minibatches_done"]},
         "other_rates": side,
         "profile": {k: (round(v, 5) if isinstance(v, float) else v) for k, v in prof.items()
-                    if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight")},
+                    if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",
+                             "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx")},
         "context": {"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200},
         "setup_s": round(setup_s, 1),
     }

@@ -35,6 +35,7 @@ struct StepInput {
   int ft_L = 0, ft_l = 0, ft_s = 0, ft_layer = -1;
   std::vector<int32_t> ft_targets;
   const std::vector<int32_t>* ft_pages = nullptr;
+  std::vector<BwdWindow> extra_bwd;  // further backward windows after (ft_layer, ft_l, ft_s)
 };
 
 struct StepOutput {
@@ -144,7 +145,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       running.push_back(std::move(r));
     }
   }
-  double corr = 1.0;  // adaptive: measured / predicted
+  double corr[3] = {1.0, 1.0, 1.0};  // adaptive, per FT phase (none / forward / backward)
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
   for (int it = 0; it < total_iters; ++it) {
     const bool timed = it >= cfg.warmup_iters;
@@ -178,9 +179,12 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       ++i;
     }
     LatencyProfile prof = cfg.prof;
+    const int cph = ft.phase == FtPhase::Forward ? 1 : (ft.phase == FtPhase::Backward ? 2 : 0);
     if (cfg.adaptive) {
-      prof.t0_ms *= corr;
-      prof.slope_ms_per_token *= corr;
+      prof.t0_ms *= corr[cph];
+      prof.slope_ms_per_token *= corr[cph];
+      prof.attn_fwd_ms_per_token_ctx *= corr[cph];
+      prof.attn_bwd_ms_per_token_ctx *= corr[cph];
     }
     IterationPlan plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
     if (!enforce_dependencies(plan, ft)) {
@@ -227,8 +231,10 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
         for (int64_t i = ft.l; i < ft.l + s; ++i)
           in.ft_targets.push_back(i + 1 < ft.L ? ft_tokens[i + 1] : -1);
       } else {
-        in.ft_l = ft.lj;
-        in.ft_layer = ft.layer;
+        in.ft_l = plan.bwd[0].lj;
+        in.ft_layer = plan.bwd[0].layer;
+        in.ft_s = plan.bwd[0].s;
+        in.extra_bwd.assign(plan.bwd.begin() + 1, plan.bwd.end());
       }
     }
     StepOutput out;
@@ -242,8 +248,12 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       out.device_ms = plan.predicted_ms;
       out.next_tokens.assign(in.segs.size(), 0);
     }
-    if (cfg.adaptive && plan.predicted_ms > 0 && out.device_ms > 0)
-      corr = std::max(0.5, std::min(2.0, 0.8 * corr + 0.2 * corr * out.device_ms / plan.predicted_ms));
+    if (cfg.adaptive && plan.predicted_ms > 0 && out.device_ms > 0) {
+      const int ph = plan.ft_phase == FtPhase::Forward ? 1 : (plan.ft_phase == FtPhase::Backward ? 2 : 0);
+      // the step ran with corr[cph]; blend towards the measured ratio of its own phase
+      const double r = corr[cph] * out.device_ms / plan.predicted_ms;
+      corr[ph] = std::max(0.5, std::min(2.0, 0.7 * corr[ph] + 0.3 * r));
+    }
     now += out.ms;
     // advance request state
     int seg = 0;
@@ -286,7 +296,11 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
     // finetuning progress
     const FtPhase ph = ft.phase;
-    advance_finetune(ft, s);
+    if (plan.ft_phase == FtPhase::Backward) {
+      for (const BwdWindow& bw : plan.bwd) advance_finetune(ft, bw.s);
+    } else {
+      advance_finetune(ft, s);
+    }
     if (timed) {
       if (ph == FtPhase::Forward) {
         st.ft_fwd_tokens += s;

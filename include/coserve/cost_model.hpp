@@ -20,6 +20,12 @@ struct LatencyProfile {
   // through the same f (weight 1, the default); a measured B200 profile sets it from the
   // offline profiler (a backward token touches one layer, a forward token all of them).
   double bwd_token_weight = 1.0;
+  // Attention's context dependence (B200 profile; 0 = the spec's f(c, s)): a forward window
+  // of s tokens at position l costs an extra attn_fwd * s * (l + s/2); a backward window ending
+  // at l_j costs an extra attn_bwd * s * (l_j - s/2).
+  double attn_fwd_ms_per_token_ctx = 0.0;
+  double attn_bwd_ms_per_token_ctx = 0.0;
+  bool has_ctx_terms() const { return attn_fwd_ms_per_token_ctx > 0 || attn_bwd_ms_per_token_ctx > 0; }
 };
 
 // t0 + b*min(c+s, k) + 2b*max(0, c+s-k)
@@ -46,6 +52,29 @@ inline int64_t max_finetune_tokens(const LatencyProfile& p, int64_t c, double sl
   while (s > 0 && latency(p, c, s) > slo_step_ms) --s;
   while (latency(p, c, s + 1) <= slo_step_ms) ++s;
   return s;
+}
+
+// Marginal cost of finetuning windows on top of latency(c, 0) (profile with context terms).
+inline double ft_fwd_cost(const LatencyProfile& p, int64_t l, int64_t s) {
+  return p.slope_ms_per_token * (double)s +
+         p.attn_fwd_ms_per_token_ctx * (double)s * ((double)l + 0.5 * (double)s);
+}
+inline double ft_bwd_cost(const LatencyProfile& p, int64_t lj, int64_t s) {
+  const double w = p.bwd_token_weight > 0 ? p.bwd_token_weight : 1.0;
+  return w * p.slope_ms_per_token * (double)s +
+         p.attn_bwd_ms_per_token_ctx * (double)s * ((double)lj - 0.5 * (double)s);
+}
+// largest s in [0, cap] with cost(s) <= room for a cost monotone in s (binary search)
+template <typename F>
+inline int64_t max_tokens_within(F cost, int64_t cap, double room) {
+  if (cap <= 0 || room <= 0 || cost(1) > room) return 0;
+  int64_t lo = 1, hi = cap;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (cost(mid) <= room) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 // pages of page_size tokens; a request is admitted iff

@@ -61,6 +61,16 @@ struct SchedulerConfig {
   double ttft_slo_ms = 5000.0;
   int max_tokens = 8192;       // engine capacity per iteration
   int max_ft_window = 8192;    // cap on s
+  // B200 runtime extension: one iteration may carry consecutive backward windows across
+  // layers (layer n to 0, then n-1 from L) when the budget allows -- Alg. 2 order is kept.
+  // false reproduces SPEC.md:433 (one layer per iteration).
+  bool multi_layer_bwd = false;
+};
+
+struct BwdWindow {
+  int layer = 0;
+  int lj = 0;  // window end
+  int s = 0;
 };
 
 struct PrefillChunk {
@@ -80,6 +90,7 @@ struct IterationPlan {
   int ft_l = 0;                         // forward: l_i ; backward: l_j (window end)
   double predicted_ms = 0.0;
   std::vector<int64_t> admitted;        // request ids admitted this iteration
+  std::vector<BwdWindow> bwd;           // backward windows (first = ft_layer / ft_l / s)
 };
 
 // Tokens the FT state can still take in its current phase (window clipping).
@@ -138,24 +149,70 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
   p.c = c;
   // (3) s = argmax f(c, s) <= budget, clipped to the FT phase and engine capacity
   const double w_b = prof.bwd_token_weight > 0 ? prof.bwd_token_weight : 1.0;
-  if (ft.phase == FtPhase::Forward || ft.phase == FtPhase::Backward) {
-    int64_t s = max_finetune_tokens(prof, c, budget_ms);
-    if (ft.phase == FtPhase::Backward && w_b != 1.0) s = (int64_t)std::floor((double)s / w_b);
-    s = std::min<int64_t>(s, ft_phase_remaining(ft));
-    s = std::min<int64_t>(s, cfg.max_ft_window);
-    if (ft.phase == FtPhase::Forward) s = std::min<int64_t>(s, cfg.max_tokens - c);
-    s = std::max<int64_t>(s, 0);
-    p.s = s;
+  if (!prof.has_ctx_terms() && !cfg.multi_layer_bwd) {
+    // the spec's single-profile form
+    if (ft.phase == FtPhase::Forward || ft.phase == FtPhase::Backward) {
+      int64_t s = max_finetune_tokens(prof, c, budget_ms);
+      if (ft.phase == FtPhase::Backward && w_b != 1.0) s = (int64_t)std::floor((double)s / w_b);
+      s = std::min<int64_t>(s, ft_phase_remaining(ft));
+      s = std::min<int64_t>(s, cfg.max_ft_window);
+      if (ft.phase == FtPhase::Forward) s = std::min<int64_t>(s, cfg.max_tokens - c);
+      s = std::max<int64_t>(s, 0);
+      p.s = s;
+      if (s > 0) {
+        p.ft_phase = ft.phase;
+        p.ft_minibatch = ft.minibatch;
+        p.ft_layer = ft.phase == FtPhase::Backward ? ft.layer : -1;
+        p.ft_l = ft.phase == FtPhase::Forward ? ft.l : ft.lj;
+        if (ft.phase == FtPhase::Backward) p.bwd.push_back(BwdWindow{ft.layer, ft.lj, (int)s});
+      }
+    }
+    const int64_t s_eq = (p.ft_phase == FtPhase::Backward && w_b != 1.0)
+                             ? (int64_t)std::ceil((double)p.s * w_b) : p.s;
+    p.predicted_ms = latency(prof, p.c, s_eq);
+    return p;
+  }
+  // profile with context terms: exact argmax of the window cost within the remaining budget
+  const double base = latency(prof, c, 0);
+  double room = budget_ms - base;
+  double cost = 0.0;
+  if (ft.phase == FtPhase::Forward) {
+    const int64_t cap = std::min<int64_t>({(int64_t)(ft.L - ft.l), (int64_t)cfg.max_ft_window,
+                                           (int64_t)cfg.max_tokens - c});
+    const int64_t l0 = ft.l;
+    const int64_t s = max_tokens_within([&](int64_t x) { return ft_fwd_cost(prof, l0, x); }, cap, room);
     if (s > 0) {
-      p.ft_phase = ft.phase;
+      p.s = s;
+      p.ft_phase = FtPhase::Forward;
       p.ft_minibatch = ft.minibatch;
-      p.ft_layer = ft.phase == FtPhase::Backward ? ft.layer : -1;
-      p.ft_l = ft.phase == FtPhase::Forward ? ft.l : ft.lj;
+      p.ft_l = ft.l;
+      cost = ft_fwd_cost(prof, l0, s);
+    }
+  } else if (ft.phase == FtPhase::Backward) {
+    int layer = ft.layer, lj = ft.lj;
+    while (layer >= 0 && room > 0) {
+      const int64_t cap = std::min<int64_t>({(int64_t)lj, (int64_t)cfg.max_ft_window, (int64_t)cfg.max_tokens});
+      const int64_t lj0 = lj;
+      const int64_t s = max_tokens_within([&](int64_t x) { return ft_bwd_cost(prof, lj0, x); }, cap, room);
+      if (s <= 0) break;
+      const double cw = ft_bwd_cost(prof, lj0, s);
+      p.bwd.push_back(BwdWindow{layer, lj, (int)s});
+      p.s += s;
+      cost += cw;
+      room -= cw;
+      lj -= (int)s;
+      if (lj > 0 || !cfg.multi_layer_bwd) break;
+      layer -= 1;
+      lj = ft.L;
+    }
+    if (!p.bwd.empty()) {
+      p.ft_phase = FtPhase::Backward;
+      p.ft_minibatch = ft.minibatch;
+      p.ft_layer = p.bwd[0].layer;
+      p.ft_l = p.bwd[0].lj;
     }
   }
-  const int64_t s_eq = (p.ft_phase == FtPhase::Backward && w_b != 1.0)
-                           ? (int64_t)std::ceil((double)p.s * w_b) : p.s;
-  p.predicted_ms = latency(prof, p.c, s_eq);
+  p.predicted_ms = base + cost;
   return p;
 }
 

@@ -128,6 +128,10 @@ typedef struct cs_iteration_plan {
   const int32_t* page_table;
   int32_t page_table_len;
   cs_ft_window ft;
+  /* further backward windows run after `ft` in this iteration, in order (each must continue
+   * Alg. 2's descending order; they may cross into the next lower layer) */
+  int32_t n_extra_bwd;
+  const cs_ft_window* extra_bwd;
 } cs_iteration_plan;
 
 typedef struct cs_step_result {
@@ -161,6 +165,8 @@ typedef struct cs_latency_profile {
   double slope_ms_per_token;
   double knee_tokens;      /* <= 0 -> infinite knee                                   */
   double bwd_token_weight; /* cost of a backward-window token in forward tokens; <= 0 -> 1 */
+  double attn_fwd_ms_per_token_ctx; /* forward window extra: a_f * s * (l + s/2)         */
+  double attn_bwd_ms_per_token_ctx; /* backward window extra: a_b * s * (l_j - s/2)      */
 } cs_latency_profile;
 
 double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);
@@ -178,6 +184,7 @@ typedef struct cs_coserve_config {
   cs_latency_profile profile;
   int32_t ft_seq_len, growth_tokens, warmup_iters, timed_iters, prepopulate, adaptive;
   int32_t profile_timed; /* switch on cs_engine_set_profiling at the first timed iteration */
+  int32_t multi_layer_bwd; /* one iteration may carry backward windows of several layers     */
   uint64_t seed;
   /* simulation-only (engine == NULL): model depth, vocab and KV pool */
   int32_t n_layers, vocab, page_size;
@@ -208,7 +215,8 @@ int cs_coserve_run(cs_engine* e, const cs_coserve_config* cfg, cs_coserve_stats*
 int64_t cs_engine_launch_count(cs_engine* e);
 /* Live profiling: when on, every GEMM / attention launch is bracketed by CUDA events on the
  * engine stream; cs_engine_read_profile returns the summed device ms, algorithmic FLOPs and
- * bytes and launch count per kind (0 = tcgen05 GEMM, 1 = attention fwd, 2 = attention bwd)
+ * bytes and launch count per kind (0 = tcgen05 GEMM, 1 = attention fwd bandwidth kernel
+ * (decode rows), 2 = attention bwd, 3 = attention fwd tcgen05 kernel (prefill / FT rows))
  * since profiling was switched on. */
 int cs_engine_set_profiling(cs_engine* e, int on);
 int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops, double* bytes,

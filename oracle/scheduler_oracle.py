@@ -29,6 +29,33 @@ class Profile:
     slope: float = 0.01
     knee: float = INF
     bwd_weight: float = 1.0
+    attn_fwd: float = 0.0   # B200 runtime extension: context term of a forward window
+    attn_bwd: float = 0.0   # ... of a backward window
+
+    def has_ctx(self):
+        return self.attn_fwd > 0 or self.attn_bwd > 0
+
+
+def ft_fwd_cost(p: Profile, l: int, s: int) -> float:
+    return p.slope * float(s) + p.attn_fwd * float(s) * (float(l) + 0.5 * float(s))
+
+
+def ft_bwd_cost(p: Profile, lj: int, s: int) -> float:
+    w = p.bwd_weight if p.bwd_weight > 0 else 1.0
+    return w * p.slope * float(s) + p.attn_bwd * float(s) * (float(lj) - 0.5 * float(s))
+
+
+def max_tokens_within(cost, cap: int, room: float) -> int:
+    if cap <= 0 or room <= 0 or cost(1) > room:
+        return 0
+    lo, hi = 1, cap
+    while lo < hi:
+        mid = lo + (hi - lo + 1) // 2
+        if cost(mid) <= room:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
 
 
 def latency(p: Profile, c: int, s: int) -> float:
@@ -212,7 +239,7 @@ def advance_finetune(ft: FtState, s: int):
 
 def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Profile,
                    max_batch: int, chunk: int, max_tokens: int, max_ft_window: int,
-                   mem: MemoryModel, budget: float):
+                   mem: MemoryModel, budget: float, multi_layer: bool = False):
     """SPEC.md:421-429.  Returns a dict mirroring coserve::IterationPlan."""
     while queue and len(running) < max_batch:
         r = queue[0]
@@ -242,28 +269,64 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
         c += ln
     w_b = prof.bwd_weight if prof.bwd_weight > 0 else 1.0
     s, phase, layer, l = 0, 0, -1, 0
-    if ft.phase in (FWD, BWD):
-        s = max_finetune_tokens(prof, c, budget)
-        if ft.phase == BWD and w_b != 1.0:
-            s = int(math.floor(s / w_b))
-        s = min(s, (ft.L - ft.l) if ft.phase == FWD else ft.lj)
-        s = min(s, max_ft_window)
+    bwd = []
+    if not prof.has_ctx() and not multi_layer:
+        if ft.phase in (FWD, BWD):
+            s = max_finetune_tokens(prof, c, budget)
+            if ft.phase == BWD and w_b != 1.0:
+                s = int(math.floor(s / w_b))
+            s = min(s, (ft.L - ft.l) if ft.phase == FWD else ft.lj)
+            s = min(s, max_ft_window)
+            if ft.phase == FWD:
+                s = min(s, max_tokens - c)
+            s = max(s, 0)
+            if s > 0:
+                phase = ft.phase
+                layer = ft.layer if ft.phase == BWD else -1
+                l = ft.l if ft.phase == FWD else ft.lj
+                if ft.phase == BWD:
+                    bwd.append((ft.layer, ft.lj, s))
+        s_eq = int(math.ceil(s * w_b)) if (phase == BWD and w_b != 1.0) else s
+        pred = latency(prof, c, s_eq)
+    else:
+        base = latency(prof, c, 0)
+        room = budget - base
+        cost = 0.0
         if ft.phase == FWD:
-            s = min(s, max_tokens - c)
-        s = max(s, 0)
-        if s > 0:
-            phase = ft.phase
-            layer = ft.layer if ft.phase == BWD else -1
-            l = ft.l if ft.phase == FWD else ft.lj
-    s_eq = int(math.ceil(s * w_b)) if (phase == BWD and w_b != 1.0) else s
+            cap = min(ft.L - ft.l, max_ft_window, max_tokens - c)
+            l0 = ft.l
+            s = max_tokens_within(lambda x: ft_fwd_cost(prof, l0, x), cap, room)
+            if s > 0:
+                phase, l = FWD, ft.l
+                cost = ft_fwd_cost(prof, l0, s)
+        elif ft.phase == BWD:
+            ly, lj = ft.layer, ft.lj
+            while ly >= 0 and room > 0:
+                cap = min(lj, max_ft_window, max_tokens)
+                sw = max_tokens_within(lambda x, lj0=lj: ft_bwd_cost(prof, lj0, x), cap, room)
+                if sw <= 0:
+                    break
+                cw = ft_bwd_cost(prof, lj, sw)
+                bwd.append((ly, lj, sw))
+                s += sw
+                cost += cw
+                room -= cw
+                lj -= sw
+                if lj > 0 or not multi_layer:
+                    break
+                ly -= 1
+                lj = ft.L
+            if bwd:
+                phase, layer, l = BWD, bwd[0][0], bwd[0][1]
+        pred = base + cost
     return {"decode": decode, "prefill": prefill, "c": c, "s": s, "phase": phase,
-            "layer": layer, "l": l, "pred": latency(prof, c, s_eq)}
+            "layer": layer, "l": l, "pred": pred, "bwd": bwd}
 
 
 def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, total_pages: int,
         growth: int, ft_len: int, iters: int, prepopulate: int = 0, max_batch: int = 64,
         chunk: int = 512, max_tokens: int = 8192, max_ft_window: int = 8192,
-        budget: Optional[float] = None, tpot_slo: float = 50.0):
+        budget: Optional[float] = None, tpot_slo: float = 50.0, multi_layer: bool = False):
     """coserve_loop.hpp run_coserve on the simulated clock.
     Returns the per-iteration log (list of dicts)."""
     budget = tpot_slo if budget is None else budget
@@ -316,10 +379,10 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                     continue
             i += 1
         plan = plan_iteration(queue, running, ft, prof, max_batch, chunk, max_tokens,
-                              max_ft_window, mem, budget)
+                              max_ft_window, mem, budget, multi_layer)
         entry = {"c": plan["c"], "s": plan["s"], "phase": plan["phase"], "layer": plan["layer"],
                  "l": plan["l"], "n_decode": len(plan["decode"]), "n_prefill": len(plan["prefill"]),
-                 "pred": plan["pred"],
+                 "pred": plan["pred"], "bwd": plan["bwd"],
                  "decode_ids": [running[i].id for i in plan["decode"]],
                  "prefill": [(running[i].id, st, ln) for i, st, ln in plan["prefill"]],
                  "pages": {running[i].id: list(running[i].pages) for i in plan["decode"]}}
@@ -344,7 +407,11 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                 running.pop(i)
             else:
                 i += 1
-        advance_finetune(ft, plan["s"])
+        if plan["phase"] == BWD:
+            for (_, _, sw) in plan["bwd"]:
+                advance_finetune(ft, sw)
+        else:
+            advance_finetune(ft, plan["s"])
         if ft.phase == DONE:
             ft.phase, ft.minibatch, ft.l, ft.layer, ft.lj = FWD, ft.minibatch + 1, 0, 0, 0
         entry["t_ms"] = now

@@ -59,6 +59,17 @@ class GpuExecutor : public coserve::StepExecutor {
       w.n_pages = (int)in.ft_pages->size();
       pt_.insert(pt_.end(), in.ft_pages->begin(), in.ft_pages->end());
     }
+    extra_.clear();
+    for (const auto& b : in.extra_bwd) {
+      cs_ft_window x = w;
+      x.l = b.lj;
+      x.s = b.s;
+      x.layer = b.layer;
+      x.targets = nullptr;
+      extra_.push_back(x);
+    }
+    p.n_extra_bwd = (int)extra_.size();
+    p.extra_bwd = extra_.empty() ? nullptr : extra_.data();
     p.page_table = pt_.data();
     p.page_table_len = (int)pt_.size();
     next_.assign(std::max<size_t>(1, segs_.size()), -1);
@@ -87,6 +98,7 @@ class GpuExecutor : public coserve::StepExecutor {
   cs_engine* e_;
   std::vector<int32_t> tokens_, pt_, next_;
   std::vector<cs_segment> segs_;
+  std::vector<cs_ft_window> extra_;
 };
 
 double pct(std::vector<double> v, double q) {
@@ -117,6 +129,9 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.prof.knee_tokens = c->profile.knee_tokens > 0 ? c->profile.knee_tokens
                                                   : std::numeric_limits<double>::infinity();
   L.prof.bwd_token_weight = c->profile.bwd_token_weight > 0 ? c->profile.bwd_token_weight : 1.0;
+  L.prof.attn_fwd_ms_per_token_ctx = c->profile.attn_fwd_ms_per_token_ctx;
+  L.prof.attn_bwd_ms_per_token_ctx = c->profile.attn_bwd_ms_per_token_ctx;
+  L.sched.multi_layer_bwd = c->multi_layer_bwd != 0;
   L.budget_ms = c->budget_ms > 0 ? c->budget_ms : c->tpot_slo_ms;
   L.growth_tokens = c->growth_tokens;
   L.ft_seq_len = c->ft_seq_len;

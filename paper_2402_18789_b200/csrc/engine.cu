@@ -96,14 +96,16 @@ struct cs_engine {
   struct ProfRec {
     cudaEvent_t a, b;
     double flops, bytes;
-    int kind;  // 0 gemm, 1 attention fwd, 2 attention bwd
+    int kind;  // see prof_ms
   };
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<ProfRec> recs;
-  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
-  long prof_n[3] = {0, 0, 0};
-  double step_attn_flops = 0, step_attn_bytes = 0;
+  // kinds: 0 tcgen05 GEMM, 1 attention fwd (bandwidth kernel: decode), 2 attention bwd,
+  //        3 attention fwd (tcgen05 kernel: prefill / FT windows)
+  double prof_ms[4] = {0, 0, 0, 0}, prof_flops[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};
+  long prof_n[4] = {0, 0, 0, 0};
+  double step_attn_flops = 0, step_attn_bytes = 0, step_tc_flops = 0, step_tc_bytes = 0;
 };
 
 namespace {
@@ -368,13 +370,13 @@ extern "C" int cs_engine_set_profiling(cs_engine* e, int on) {
   cudaStreamSynchronize(e->st);
   prof_collect(e);
   e->profiling = on != 0;
-  for (int k = 0; k < 3; ++k) e->prof_ms[k] = e->prof_flops[k] = e->prof_bytes[k] = 0, e->prof_n[k] = 0;
+  for (int k = 0; k < 4; ++k) e->prof_ms[k] = e->prof_flops[k] = e->prof_bytes[k] = 0, e->prof_n[k] = 0;
   return CS_OK;
 }
 
 extern "C" int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops,
                                       double* bytes, int64_t* launches) {
-  if (!e || kind < 0 || kind > 2) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_profile: bad kind");
+  if (!e || kind < 0 || kind > 3) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_profile: bad kind");
   if (ms) *ms = e->prof_ms[kind];
   if (flops) *flops = e->prof_flops[kind];
   if (bytes) *bytes = e->prof_bytes[kind];
@@ -698,7 +700,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   const int rpt = 64 / e->grp;
   const int rpt_tc = 128 / e->grp;
   const bool tc_ok = e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn;
-  double attn_flops = 0, attn_bytes = 0;
+  double attn_flops = 0, attn_bytes = 0, tc_flops = 0, tc_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {
     const cs_segment& g = plan->segments[s];
     if (g.q_start != row || g.q_len < 1 || g.q_start + g.q_len > T)
@@ -739,8 +741,15 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     }
     {  // algorithmic attention work of this segment per layer
       const double ql = g.q_len, c0 = g.ctx_start;
-      attn_flops += 4.0 * e->Hq * e->d * (ql * c0 + ql * (ql + 1) / 2.0);
-      attn_bytes += (c0 + ql) * (double)e->kv_dim * 2.0 * 2.0 + ql * e->q_dim * 2.0 * 2.0;
+      const double fl = 4.0 * e->Hq * e->d * (ql * c0 + ql * (ql + 1) / 2.0);
+      const double by = (c0 + ql) * (double)e->kv_dim * 2.0 * 2.0 + ql * e->q_dim * 2.0 * 2.0;
+      if (tc_ok && g.q_len >= 16) {
+        tc_flops += fl;
+        tc_bytes += by;
+      } else {
+        attn_flops += fl;
+        attn_bytes += by;
+      }
     }
     // attention work items (GQA-packed q tiles x kv heads): multi-row segments on the
     // tcgen05 kernel (128 packed rows), decode rows on the bandwidth kernel (64 packed rows)
@@ -764,6 +773,8 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   if (row != T) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: segments do not cover n_tokens");
   e->step_attn_flops = attn_flops;
   e->step_attn_bytes = attn_bytes;
+  e->step_tc_flops = tc_flops;
+  e->step_tc_bytes = tc_bytes;
   // split long key ranges when the grid is small (flash-decoding)
   {
     const int target = 2 * 148;
@@ -909,13 +920,14 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     ap.grp = e->grp;
     ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
     cs_engine::ProfRec apr{};
-    if (e->profiling) {
+    if (e->profiling && sp.n_work > 0) {
       apr.flops = e->step_attn_flops;
       apr.bytes = e->step_attn_bytes;
       apr.kind = 1;
       prof_begin(e, apr);
     }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
+    if (e->profiling && sp.n_work > 0) prof_end(e, apr);
     if (sp.n_tc > 0) {
       CUtensorMap mk, mv, mk128, mv128;
       const long pool_rows = (long)e->npages * e->P;
@@ -926,9 +938,16 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         return cs::set_error(CS_ERR_CUDA, "attention: TMA map creation failed");
       cs::AttnFwdParams tp = ap;
       tp.work = sp.work_tc;
+      cs_engine::ProfRec tpr{};
+      if (e->profiling) {
+        tpr.flops = e->step_tc_flops;
+        tpr.bytes = e->step_tc_bytes;
+        tpr.kind = 3;
+        prof_begin(e, tpr);
+      }
       CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      if (e->profiling) prof_end(e, tpr);
     }
-    if (e->profiling) prof_end(e, apr);
     if (n_ft > 0 && keep_attn) {
       save_rows(e, e->ft_o + ((size_t)l * e->L_max + l0) * e->q_dim, e->q_dim,
                 e->attn + (size_t)sp.ft_row0 * e->q_dim, e->q_dim, n_ft, e->q_dim);
@@ -1133,7 +1152,19 @@ int step_impl(cs_engine* e, const cs_iteration_plan* plan, bool sync, cs_step_re
   }
   if (sp.T > 0) TRY(forward(e, plan, sp, nullptr));
   if (w.phase == CS_FT_FORWARD) e->ft_len = w.l + w.s;
-  if (w.phase == CS_FT_BACKWARD) TRY(backward_window(e, plan, sp));
+  if (w.phase == CS_FT_BACKWARD) {
+    TRY(backward_window(e, plan, sp));
+    if (plan->n_extra_bwd < 0 || (plan->n_extra_bwd > 0 && !plan->extra_bwd))
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: bad extra backward windows");
+    for (int i = 0; i < plan->n_extra_bwd; ++i) {
+      cs_iteration_plan q = *plan;
+      q.ft = plan->extra_bwd[i];
+      q.ft.phase = CS_FT_BACKWARD;
+      TRY(backward_window(e, &q, sp));
+    }
+  } else if (plan->n_extra_bwd > 0) {
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: extra backward windows without a backward phase");
+  }
   CS_CUDA_TRY(cudaEventRecord(e->ev1, e->st));
   CS_CUDA_TRY(cudaGetLastError());
   if (!sync) return CS_OK;

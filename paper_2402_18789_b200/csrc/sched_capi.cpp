@@ -17,6 +17,8 @@ coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
   q.slope_ms_per_token = p->slope_ms_per_token;
   q.knee_tokens = p->knee_tokens > 0 ? p->knee_tokens : std::numeric_limits<double>::infinity();
   q.bwd_token_weight = p->bwd_token_weight > 0 ? p->bwd_token_weight : 1.0;
+  q.attn_fwd_ms_per_token_ctx = p->attn_fwd_ms_per_token_ctx;
+  q.attn_bwd_ms_per_token_ctx = p->attn_bwd_ms_per_token_ctx;
   return q;
 }
 }  // namespace

@@ -41,7 +41,8 @@ class FtWindow(ctypes.Structure):
 class IterationPlan(ctypes.Structure):
     _fields_ = [("n_tokens", i32), ("tokens", ctypes.POINTER(i32)), ("n_segments", i32),
                 ("segments", ctypes.POINTER(Segment)), ("page_table", ctypes.POINTER(i32)),
-                ("page_table_len", i32), ("ft", FtWindow)]
+                ("page_table_len", i32), ("ft", FtWindow), ("n_extra_bwd", i32),
+                ("extra_bwd", ctypes.POINTER(FtWindow))]
 
 
 class StepResult(ctypes.Structure):
@@ -51,7 +52,8 @@ class StepResult(ctypes.Structure):
 
 class LatencyProfileC(ctypes.Structure):
     _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64),
-                ("bwd_token_weight", f64)]
+                ("bwd_token_weight", f64), ("attn_fwd_ms_per_token_ctx", f64),
+                ("attn_bwd_ms_per_token_ctx", f64)]
 
 
 class CoserveConfig(ctypes.Structure):
@@ -61,6 +63,7 @@ class CoserveConfig(ctypes.Structure):
                 ("max_ft_window", i32), ("profile", LatencyProfileC), ("ft_seq_len", i32),
                 ("growth_tokens", i32), ("warmup_iters", i32), ("timed_iters", i32),
                 ("prepopulate", i32), ("adaptive", i32), ("profile_timed", i32),
+                ("multi_layer_bwd", i32),
                 ("seed", ctypes.c_uint64),
                 ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64)]
 
@@ -249,6 +252,13 @@ class Engine:
                 tg = np.ascontiguousarray(ft["targets"], dtype=np.int32)
                 keep["tg"] = tg
                 w.targets = tg.ctypes.data_as(ctypes.POINTER(i32))
+        extra = []
+        if ft and ft.get("extra"):
+            for x in ft["extra"]:
+                e = FtWindow()
+                e.phase, e.seq_len, e.l, e.s, e.layer = FT_BACKWARD, w.seq_len, x["l"], x["s"], x["layer"]
+                e.page_off, e.n_pages = w.page_off, w.n_pages
+                extra.append(e)
         tok = np.ascontiguousarray(tokens, dtype=np.int32)
         ptab = np.ascontiguousarray(pt if pt else [0], dtype=np.int32)
         seg_arr = (Segment * max(1, len(cs_segs)))(*cs_segs)
@@ -260,6 +270,11 @@ class Engine:
         p.page_table = ptab.ctypes.data_as(ctypes.POINTER(i32))
         p.page_table_len = len(pt)
         p.ft = w
+        if extra:
+            ex_arr = (FtWindow * len(extra))(*extra)
+            p.n_extra_bwd = len(extra)
+            p.extra_bwd = ex_arr
+            keep["extra"] = ex_arr
         keep.update(tok=tok, ptab=ptab, segs=seg_arr)
         return p, keep
 
@@ -363,9 +378,10 @@ def coserve_run(engine: Optional["Engine"], cfg: CoserveConfig, log_cap: int = 1
     return _struct_dict(stats), [_struct_dict(log[i]) for i in range(n.value)]
 
 
-def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0) -> LatencyProfileC:
+def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0, attn_fwd=0.0, attn_bwd=0.0) -> LatencyProfileC:
     p = LatencyProfileC()
     p.t0_ms, p.slope_ms_per_token, p.knee_tokens, p.bwd_token_weight = t0_ms, slope, knee, bwd_weight
+    p.attn_fwd_ms_per_token_ctx, p.attn_bwd_ms_per_token_ctx = attn_fwd, attn_bwd
     return p
 
 

@@ -7,7 +7,7 @@ from paper_2402_18789_b200 import engine as E
 
 
 def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth=128,
-         max_batch=64, chunk=512, budget=50.0, amplitude=0.0):
+         max_batch=64, chunk=512, budget=50.0, amplitude=0.0, multi_layer=False):
     c = E.CoserveConfig()
     c.rate_rps = rate
     c.duration_s = 600.0
@@ -21,7 +21,8 @@ def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth
     c.max_tokens = 8192
     c.max_ft_window = 8192
     c.profile = E.profile_struct(prof.t0_ms, prof.slope, 0.0 if prof.knee == S.INF else prof.knee,
-                                 prof.bwd_weight)
+                                 prof.bwd_weight, prof.attn_fwd, prof.attn_bwd)
+    c.multi_layer_bwd = 1 if multi_layer else 0
     c.ft_seq_len = ft_len
     c.growth_tokens = growth
     c.warmup_iters = 0
@@ -43,6 +44,11 @@ CASES = [
     (4.0, S.Profile(2.0, 0.01, 4096.0, 1.0), 300, 512, 2, 2, 0, 4096, 64, 50.0, 0.5),
     (40.0, S.Profile(3.0, 0.02, S.INF, 0.1), 300, 1024, 8, 3, 10, 600, 16, 50.0, 0.9),  # page pressure
 ]
+# B200 runtime extension: context-aware window costs + multi-layer backward iterations
+CASES_EXT = [
+    (20.0, S.Profile(7.3, 0.018, S.INF, 0.06, 1.1e-6, 8e-8), 400, 8192, 32, 4, 48, 8192, 128, 45.0, 0.0),
+    (10.0, S.Profile(5.0, 0.02, S.INF, 0.1, 2e-6, 1e-7), 300, 2048, 6, 5, 8, 4096, 64, 40.0, 0.5),
+]
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -63,6 +69,26 @@ def test_sim_plans_bit_exact(case):
     for a in log:
         if a["c"] > 0:
             assert a["pred_ms"] <= budget + 1e-9
+
+
+@pytest.mark.parametrize("case", CASES_EXT)
+def test_sim_plans_bit_exact_ctx_multilayer(case):
+    rate, prof, iters, ft_len, nl, seed, prepop, pages, growth, budget, amp = case
+    stats, log = E.coserve_run(None, _cfg(rate, prof, iters, ft_len, nl, seed, prepop, pages,
+                                          growth, budget=budget, amplitude=amp, multi_layer=True))
+    w = S.Workload(rate=rate, duration_s=600.0, amplitude=amp, period_s=20.0)
+    ref = S.run(prof, w, seed, nl, 16, pages, growth, ft_len, iters, prepopulate=prepop,
+                budget=budget, multi_layer=True)
+    multi = 0
+    for i, (a, b) in enumerate(zip(log, ref)):
+        for k in ("c", "s", "phase", "layer", "l", "n_decode", "n_prefill", "n_running", "n_queue"):
+            assert a[k] == b[k], (i, k, a[k], b[k])
+        assert a["t_ms"] == b["t_ms"] and a["pred_ms"] == b["pred"], i
+        multi += len(b["bwd"]) > 1
+        if a["c"] > 0:
+            assert a["pred_ms"] <= budget + 1e-9
+    assert multi > 0  # some iterations carried windows of several layers
+    assert stats["minibatches_done"] >= 1
 
 
 def test_token_accounting_and_work_conservation():
