@@ -218,34 +218,37 @@ def offline_profile(eng, ft_len: int):
     def decs(k=n_dec):
         return [Seg(SEG_DECODE, [i % 1000], ctx, dec_pages[i], sample=True) for i in range(k)]
 
+    def ft_pass(win_f, record_f, record_b):
+        eng.reset_ft()
+        for l in range(0, ft_len, win_f):
+            s = min(win_f, ft_len - l)
+            out = eng.step(decs() + [Seg(SEG_FT_FWD, toks[l:l + s], l, ft_pages, adapter=True)],
+                           ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": s,
+                               "targets": toks[l + 1:l + s + 1] + ([-1] if l + s == ft_len else [])})
+            if record_f is not None:
+                record_f.append((s, l, out["ms"]))
+        for n in range(L8B["n_layers"] - 1, -1, -1):
+            lj = ft_len
+            while lj > 0:
+                s = min(2048 if n == L8B["n_layers"] - 1 else ft_len, lj)
+                out = eng.step(decs(), ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": lj,
+                                           "s": s, "layer": n, "pages": ft_pages})
+                if record_b is not None and n >= 1:
+                    record_b.append((s, lj, out["ms"]))
+                if record_b is not None and n == 0:
+                    layer0.append((s, lj, out["ms"]))
+                lj -= s
+        eng.adam_step(1e-4)
+
+    toks = [(7 * i) % 1000 for i in range(ft_len)]
+    ft_pass(2048, None, None)  # warm-up: first launches, TMA maps, attributes
     eng.reset_ft()
     t_dec = []
     for _ in range(3):
         t_dec.append(eng.step(decs())["ms"])
     t0 = min(t_dec)
-    fwd = []
-    win = 1024
-    toks = [(7 * i) % 1000 for i in range(ft_len)]
-    for l in range(0, ft_len, win):
-        s = min(win, ft_len - l)
-        out = eng.step(decs() + [Seg(SEG_FT_FWD, toks[l:l + s], l, ft_pages, adapter=True)],
-                       ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": s,
-                           "targets": toks[l + 1:l + s + 1] + ([-1] if l + s == ft_len else [])})
-        fwd.append((s, l, out["ms"]))
-    bwd = []
-    lj = ft_len
-    bw = 2048
-    for n in range(L8B["n_layers"] - 1, -1, -1):
-        lj = ft_len
-        while lj > 0:
-            s = min(bw if n == L8B["n_layers"] - 1 else ft_len, lj)
-            out = eng.step(decs(), ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": lj, "s": s,
-                                       "layer": n, "pages": ft_pages})
-            if n >= 1:
-                bwd.append((s, lj, out["ms"]))
-            lj -= s
-    eng.adam_step(1e-4)
-
+    fwd, bwd, layer0 = [], [], []
+    ft_pass(1024, fwd, bwd)
     def linfit(xs, ys):
         mx, my = statistics.mean(xs), statistics.mean(ys)
         vx = sum((x - mx) ** 2 for x in xs)
@@ -257,9 +260,15 @@ def offline_profile(eng, ft_len: int):
     b, a_f = linfit([l + s / 2.0 for s, l, _ in fwd], [(ms - t0) / s for s, _, ms in fwd])
     wb, a_b = linfit([lj - s / 2.0 for s, lj, _ in bwd], [(ms - t0) / s for s, _, ms in bwd])
     b = max(b, 1e-6)
+    w0 = 1.0
+    if layer0:
+        s0, lj0, ms0 = layer0[0]
+        full = wb * s0 + a_b * s0 * (lj0 - s0 / 2.0)
+        w0 = min(1.0, max(0.05, (ms0 - t0) / full)) if full > 0 else 1.0
     return {"t0_ms": t0, "slope_ms_per_token": b, "bwd_token_weight": max(wb, 1e-6) / b,
             "attn_fwd_ms_per_token_ctx": a_f, "attn_bwd_ms_per_token_ctx": a_b,
-            "fwd_samples": fwd, "bwd_samples": bwd[:6]}
+            "bwd_layer0_weight": w0,
+            "fwd_samples": fwd, "bwd_samples": bwd[:8]}
 
 
 def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False):
@@ -278,7 +287,7 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False)
     c.max_ft_window = 8192
     c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
                                prof["bwd_token_weight"], prof["attn_fwd_ms_per_token_ctx"],
-                               prof["attn_bwd_ms_per_token_ctx"])
+                               prof["attn_bwd_ms_per_token_ctx"], prof["bwd_layer0_weight"])
     c.multi_layer_bwd = 1
     c.ft_seq_len = ft_len
     c.growth_tokens = 128
@@ -436,11 +445,14 @@ def run_ours(a):
         "finetune": {"fwd_tokens": st["ft_fwd_tokens"], "bwd_layer_tokens": st["ft_bwd_tokens"],
                      "minibatches_done": st["minibatches_done"]},
         "other_rates": side,
-        "profile": {k: (round(v, 5) if isinstance(v, float) else v) for k, v in prof.items()
+        "profile": {k: (float(f"{v:.4g}") if isinstance(v, float) else v) for k, v in prof.items()
                     if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",
-                             "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx")},
+                             "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx",
+                             "bwd_layer0_weight")},
         "context": {"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200},
         "setup_s": round(setup_s, 1),
+        "profile_samples": {"fwd": [[s_, l_, round(m_, 2)] for s_, l_, m_ in prof["fwd_samples"]],
+                            "bwd": [[s_, l_, round(m_, 2)] for s_, l_, m_ in prof["bwd_samples"]]},
     }
     print(json.dumps(line), flush=True)
     if a.log:

@@ -251,8 +251,8 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     if (cfg.adaptive && plan.predicted_ms > 0 && out.device_ms > 0) {
       const int ph = plan.ft_phase == FtPhase::Forward ? 1 : (plan.ft_phase == FtPhase::Backward ? 2 : 0);
       // the step ran with corr[cph]; blend towards the measured ratio of its own phase
-      const double r = corr[cph] * out.device_ms / plan.predicted_ms;
-      corr[ph] = std::max(0.5, std::min(2.0, 0.7 * corr[ph] + 0.3 * r));
+      const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));
+      corr[ph] = std::max(0.5, std::min(2.0, 0.8 * corr[ph] + 0.2 * r));
     }
     now += out.ms;
     // advance request state

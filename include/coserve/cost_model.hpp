@@ -25,6 +25,9 @@ struct LatencyProfile {
   // at l_j costs an extra attn_bwd * s * (l_j - s/2).
   double attn_fwd_ms_per_token_ctx = 0.0;
   double attn_bwd_ms_per_token_ctx = 0.0;
+  // cost of a layer-0 backward window relative to another layer's (graph pruning leaves only
+  // the MLP/LoRA part there); 1 = no distinction
+  double bwd_layer0_weight = 1.0;
   bool has_ctx_terms() const { return attn_fwd_ms_per_token_ctx > 0 || attn_bwd_ms_per_token_ctx > 0; }
 };
 
@@ -59,10 +62,11 @@ inline double ft_fwd_cost(const LatencyProfile& p, int64_t l, int64_t s) {
   return p.slope_ms_per_token * (double)s +
          p.attn_fwd_ms_per_token_ctx * (double)s * ((double)l + 0.5 * (double)s);
 }
-inline double ft_bwd_cost(const LatencyProfile& p, int64_t lj, int64_t s) {
+inline double ft_bwd_cost(const LatencyProfile& p, int64_t lj, int64_t s, int layer = 1) {
   const double w = p.bwd_token_weight > 0 ? p.bwd_token_weight : 1.0;
-  return w * p.slope_ms_per_token * (double)s +
-         p.attn_bwd_ms_per_token_ctx * (double)s * ((double)lj - 0.5 * (double)s);
+  const double c = w * p.slope_ms_per_token * (double)s +
+                   p.attn_bwd_ms_per_token_ctx * (double)s * ((double)lj - 0.5 * (double)s);
+  return layer == 0 ? p.bwd_layer0_weight * c : c;
 }
 // largest s in [0, cap] with cost(s) <= room for a cost monotone in s (binary search)
 template <typename F>

@@ -193,9 +193,10 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
     while (layer >= 0 && room > 0) {
       const int64_t cap = std::min<int64_t>({(int64_t)lj, (int64_t)cfg.max_ft_window, (int64_t)cfg.max_tokens});
       const int64_t lj0 = lj;
-      const int64_t s = max_tokens_within([&](int64_t x) { return ft_bwd_cost(prof, lj0, x); }, cap, room);
+      const int ly = layer;
+      const int64_t s = max_tokens_within([&](int64_t x) { return ft_bwd_cost(prof, lj0, x, ly); }, cap, room);
       if (s <= 0) break;
-      const double cw = ft_bwd_cost(prof, lj0, s);
+      const double cw = ft_bwd_cost(prof, lj0, s, ly);
       p.bwd.push_back(BwdWindow{layer, lj, (int)s});
       p.s += s;
       cost += cw;

@@ -167,6 +167,7 @@ typedef struct cs_latency_profile {
   double bwd_token_weight; /* cost of a backward-window token in forward tokens; <= 0 -> 1 */
   double attn_fwd_ms_per_token_ctx; /* forward window extra: a_f * s * (l + s/2)         */
   double attn_bwd_ms_per_token_ctx; /* backward window extra: a_b * s * (l_j - s/2)      */
+  double bwd_layer0_weight;  /* layer-0 (pruned) backward window cost factor; <= 0 -> 1     */
 } cs_latency_profile;
 
 double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);

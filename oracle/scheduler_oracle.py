@@ -31,6 +31,7 @@ class Profile:
     bwd_weight: float = 1.0
     attn_fwd: float = 0.0   # B200 runtime extension: context term of a forward window
     attn_bwd: float = 0.0   # ... of a backward window
+    layer0: float = 1.0     # cost factor of a (pruned) layer-0 backward window
 
     def has_ctx(self):
         return self.attn_fwd > 0 or self.attn_bwd > 0
@@ -40,9 +41,10 @@ def ft_fwd_cost(p: Profile, l: int, s: int) -> float:
     return p.slope * float(s) + p.attn_fwd * float(s) * (float(l) + 0.5 * float(s))
 
 
-def ft_bwd_cost(p: Profile, lj: int, s: int) -> float:
+def ft_bwd_cost(p: Profile, lj: int, s: int, layer: int = 1) -> float:
     w = p.bwd_weight if p.bwd_weight > 0 else 1.0
-    return w * p.slope * float(s) + p.attn_bwd * float(s) * (float(lj) - 0.5 * float(s))
+    c = w * p.slope * float(s) + p.attn_bwd * float(s) * (float(lj) - 0.5 * float(s))
+    return p.layer0 * c if layer == 0 else c
 
 
 def max_tokens_within(cost, cap: int, room: float) -> int:
@@ -303,10 +305,11 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
             ly, lj = ft.layer, ft.lj
             while ly >= 0 and room > 0:
                 cap = min(lj, max_ft_window, max_tokens)
-                sw = max_tokens_within(lambda x, lj0=lj: ft_bwd_cost(prof, lj0, x), cap, room)
+                sw = max_tokens_within(lambda x, lj0=lj, ly0=ly: ft_bwd_cost(prof, lj0, x, ly0),
+                                       cap, room)
                 if sw <= 0:
                     break
-                cw = ft_bwd_cost(prof, lj, sw)
+                cw = ft_bwd_cost(prof, lj, sw, ly)
                 bwd.append((ly, lj, sw))
                 s += sw
                 cost += cw

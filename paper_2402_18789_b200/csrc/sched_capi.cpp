@@ -19,6 +19,7 @@ coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
   q.bwd_token_weight = p->bwd_token_weight > 0 ? p->bwd_token_weight : 1.0;
   q.attn_fwd_ms_per_token_ctx = p->attn_fwd_ms_per_token_ctx;
   q.attn_bwd_ms_per_token_ctx = p->attn_bwd_ms_per_token_ctx;
+  q.bwd_layer0_weight = p->bwd_layer0_weight > 0 ? p->bwd_layer0_weight : 1.0;
   return q;
 }
 }  // namespace

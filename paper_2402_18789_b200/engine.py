@@ -53,7 +53,7 @@ class StepResult(ctypes.Structure):
 class LatencyProfileC(ctypes.Structure):
     _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64),
                 ("bwd_token_weight", f64), ("attn_fwd_ms_per_token_ctx", f64),
-                ("attn_bwd_ms_per_token_ctx", f64)]
+                ("attn_bwd_ms_per_token_ctx", f64), ("bwd_layer0_weight", f64)]
 
 
 class CoserveConfig(ctypes.Structure):
@@ -378,10 +378,12 @@ def coserve_run(engine: Optional["Engine"], cfg: CoserveConfig, log_cap: int = 1
     return _struct_dict(stats), [_struct_dict(log[i]) for i in range(n.value)]
 
 
-def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0, attn_fwd=0.0, attn_bwd=0.0) -> LatencyProfileC:
+def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0, attn_fwd=0.0, attn_bwd=0.0,
+                   layer0_weight=1.0) -> LatencyProfileC:
     p = LatencyProfileC()
     p.t0_ms, p.slope_ms_per_token, p.knee_tokens, p.bwd_token_weight = t0_ms, slope, knee, bwd_weight
     p.attn_fwd_ms_per_token_ctx, p.attn_bwd_ms_per_token_ctx = attn_fwd, attn_bwd
+    p.bwd_layer0_weight = layer0_weight
     return p
 
 
