@@ -653,6 +653,12 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
   return cudaGetLastError();
 }
 
+void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st) {
+  const int warps = rows * n_heads;
+  attn_bwd_delta_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(p.dO, p.do_ld, p.O, p.o_ld, rows,
+                                                                n_heads, p.q_ld / n_heads, p.delta);
+}
+
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st) {
   const int rows = p.b - p.a;
   if (rows <= 0) return cudaSuccess;

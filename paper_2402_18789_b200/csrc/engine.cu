@@ -1095,7 +1095,23 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       bpr.kind = 2;
       prof_begin(e, bpr);
     }
-    CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
+    const bool bwd_tc = e->use_tc_attn && e->d == 128 && (e->P % 16) == 0 && (64 % e->grp) == 0;
+    if (bwd_tc) {
+      CUtensorMap mk, mv, mk128, mv128, mq3, mo3;
+      const long pool_rows = (long)e->npages * e->P;
+      if (cs::make_map(&mk, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
+          cs::make_map(&mv, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
+          cs::make_map(&mk128, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
+          cs::make_map(&mv128, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
+          cs::make_map_3d(&mq3, bp.q_cache, 128, e->Hq, e->L_max, 256, (long)e->q_dim * 2, e->grp,
+                          64 / e->grp) != 0 ||
+          cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
+                          64 / e->grp) != 0)
+        return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
+      CS_CUDA_TRY(cs::attn_bwd_tc(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
+    } else {
+      CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
+    }
     if (e->profiling) prof_end(e, bpr);
     cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);

@@ -71,6 +71,12 @@ struct AttnBwdParams {
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
+void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st);
+// tcgen05 backward (dQ and dK/dV kernels); head_dim 128, 64 % grp == 0
+cudaError_t attn_bwd_tc(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                        const CUtensorMap& tmK128, const CUtensorMap& tmV128,
+                        const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
+                        cudaStream_t st);
 // tcgen05 forward for prefill / finetuning-window tiles (head_dim 128, 128 packed rows per CTA)
 cudaError_t attn_fwd_tc(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,

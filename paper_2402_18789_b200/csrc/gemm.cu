@@ -332,6 +332,21 @@ int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, i
   return 0;
 }
 
+// 3D bf16 map (dims innermost first), SWIZZLE_128B, box = {64, box1, box2}; strides in bytes
+int make_map_3d(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
+                long stride2_bytes, int box1, int box2) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)stride1_bytes, (cuuint64_t)stride2_bytes};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, (cuuint32_t)box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 namespace {
 
 template <int BN>
