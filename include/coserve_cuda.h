@@ -77,8 +77,27 @@ typedef struct cs_model_config {
 
 typedef struct cs_engine cs_engine;
 
+/* Tensor parallelism (shard_eval.hpp:111-192 evaluates the same layout):
+ * tp_size > 1 shards the q/kv heads and the ffn columns over the ranks (QKV and gate||up
+ * column-parallel, O and down row-parallel, LoRA A row-sharded with B replicated and its
+ * up-projection folded into the down partial sums); the residual stream is replicated and
+ * all-reduced after O and down (forward) and after the gate||up / QKV input-gradient GEMMs
+ * (backward window); dB is all-reduced once per mini-batch inside cs_adam_step.
+ * Every rank gets the SAME plan.  nccl_unique_id: 128 bytes from cs_nccl_unique_id() on
+ * rank 0, shared by the host (one process per GPU).  Weights are passed whole to every rank
+ * (reference layout); each engine keeps its shard.  Read-backs (lora, grads, kv, kvgrad) are
+ * this rank's shard; grad_b is this rank's partial sum until cs_adam_step. */
 int cs_engine_create(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
                      const void* nccl_unique_id, cs_engine** out);
+int cs_nccl_unique_id(void* out128);
+/* Single-process TP: the ranks are engines of this process (one host thread each, cs_step
+ * called concurrently with the same plan); the all-reduce is a one-shot peer kernel over
+ * the ranks' buffers (NVLink peer access across devices, or one device for testing). */
+typedef struct cs_tp_group cs_tp_group;
+int cs_tp_group_create(int tp_size, cs_tp_group** out);
+int cs_tp_group_destroy(cs_tp_group* g); /* after every engine of the group is destroyed */
+int cs_engine_create_tp_local(const cs_model_config* cfg, int device, int tp_rank,
+                              cs_tp_group* group, cs_engine** out);
 int cs_engine_destroy(cs_engine* e);
 /* dtype: 0 = f64, 1 = f32.  name in {embed, unembed, final_norm, wq, wk, wv, wo, w_gate, w_up,
  * w_down, lora_a, lora_b, bq, bk, bv, norm1, norm2}; shapes in the reference layout. */

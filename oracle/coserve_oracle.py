@@ -343,7 +343,10 @@ def _attention_rows(arch: Arch, q, K, V, row_begin):
     return out, lse
 
 
-def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool = True):
+def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool = True,
+                   ar=None):
+    """ar: tensor-parallel all-reduce of the row-parallel partial sums (oracle/tp_oracle.py);
+    None = one rank, reference op order."""
     s = x.shape[0]
     rows = slice(pos0, pos0 + s)
     positions = np.arange(pos0, pos0 + s)
@@ -365,7 +368,7 @@ def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool
         k = rope_apply(k, positions, arch.n_kv_heads, arch.head_dim, arch.rope_theta)
     sv.q[rows], sv.k[rows], sv.v[rows] = q, k, v
     attn, _ = _attention_rows(arch, q, sv.k, sv.v, pos0)
-    r1 = x + attn @ w["wo"]                                  # tiny_model.hpp:201-202
+    r1 = x + (attn @ w["wo"] if ar is None else ar(attn @ w["wo"]))  # tiny_model.hpp:201-202
     sv.r1[rows] = r1
     if arch.norm == "rms":
         h2, r = rms_fwd(r1, w["g2"], arch.rms_eps)
@@ -382,6 +385,13 @@ def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool
         m = silu(g) * u
         sv.pre[rows], sv.up[rows] = g, u
     sv.m[rows] = m
+    if ar is not None:  # TP: u = m_r A_r partial, its up-projection folded into the down sum
+        delta = m @ w["w_down"]
+        if lora:
+            lu = m @ w["lora_a"]
+            sv.lu[rows] = lu
+            delta = delta + lu @ w["lora_b"]
+        return r1 + ar(delta)
     y = r1 + m @ w["w_down"]                                 # :209-210
     if lora:  # inference rows of a base-model request skip the adapter (segmented LoRA)
         lu = m @ w["lora_a"]                                 # :207
@@ -416,7 +426,7 @@ def generative_loss(logits, targets) -> float:
 
 
 def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache,
-                   lora: bool = True):
+                   lora: bool = True, ar=None):
     """SPEC.md:283-291 / Alg. 2 lines 3-11: positions [l_i, l_i+s) through all layers,
     attending to cached K,V [0, l_i) plus the causal window; appends Q,K,V.
     Returns (logits [s,V], final hidden [s,h])."""
@@ -425,7 +435,7 @@ def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache
     toks = np.asarray(tokens_window, dtype=np.int64)
     x = W["embed"][toks].copy()                              # tiny_model.hpp:189-190
     for n in range(arch.n_layers):
-        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora)
+        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora, ar)
     cache.length = l_i + len(toks)
     logits, _, _ = _head(arch, W, x)
     return logits, x
@@ -454,7 +464,7 @@ def head_grad_rows(arch: Arch, W: Dict, final_hidden, targets, L: int):
 
 def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
                     cache: QkvCache, accum: KvGradAccumulator, grads: Dict,
-                    state: Optional[Dict] = None):
+                    state: Optional[Dict] = None, ar=None):
     """SPEC.md:292-300 / Alg. 2 lines 14-21 at layer n for rows [l_j - s_j, l_j)
     (Slice interpretation SPEC.md:333).  dY_slice is dLoss/d(layer-n output) for those rows.
     Accumulates this window's dK/dV contributions over [0, l_j) into accum (ΔKVAccum);
@@ -487,6 +497,8 @@ def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
         d_g = d_m * u * dsilu(g)
         d_u = d_m * silu(g)
         dh2 = d_g @ w["w_gate"].T + d_u @ w["w_up"].T
+    if ar is not None:
+        dh2 = ar(dh2)
     if arch.norm == "rms":
         dh2 = rms_bwd(sv.r1[rows], w["g2"], sv.rstd2[rows], dh2)
     d_r1 = dY + dh2
@@ -521,6 +533,8 @@ def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
         dq_pre = rope_apply(dq, positions, Hq, d, arch.rope_theta, inverse=True)
         dk_pre = rope_apply(dk_fin, positions, Hkv, d, arch.rope_theta, inverse=True)
     dh1 = dq_pre @ w["wq"].T + dk_pre @ w["wk"].T + dv_fin @ w["wv"].T   # :317-319
+    if ar is not None:
+        dh1 = ar(dh1)
     if arch.norm == "rms":
         dh1 = rms_bwd(sv.x_in[rows], w["g1"], sv.rstd1[rows], dh1)
     dx = d_r1 + dh1                                           # :316
@@ -537,20 +551,20 @@ def lora_grads_zeros(arch: Arch) -> Dict:
 # Full-sequence oracle = a single window (SPEC.md:289,299 degenerate partitions)
 # ---------------------------------------------------------------------------
 
-def forward_full(arch: Arch, W: Dict, tokens):
+def forward_full(arch: Arch, W: Dict, tokens, ar=None):
     """tiny_model.hpp:181-221."""
     L = len(tokens)
     if L < 1:
         raise ValueError("forward_full: empty sequence")     # :183
     cache = QkvCache(arch, L)
-    logits, final = forward_window(arch, W, tokens, 0, cache)
+    logits, final = forward_window(arch, W, tokens, 0, cache, ar=ar)
     targets = np.concatenate([np.asarray(tokens[1:], dtype=np.int64), [-1]])
     loss = generative_loss(logits, targets) / float(L - 1) if L > 1 else 0.0
     return {"tokens": np.asarray(tokens), "cache": cache, "logits": logits,
             "final_hidden": final, "loss": loss}
 
 
-def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None):
+def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None, ar=None):
     """tiny_model.hpp:259-327, optionally executed as token-level backward windows
     (sizes listed in reverse traversal order; default one window per layer)."""
     tokens = tr["tokens"]
@@ -570,13 +584,15 @@ def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None):
             if s <= 0:
                 break
             dxs, dq, _, _ = backward_window(arch, W, n, dy[lj - s:lj], lj, s, tr["cache"],
-                                            accum, grads)
+                                            accum, grads, ar=ar)
             dx[lj - s:lj] = dxs
             dq_all[lj - s:lj] = dq
             lj -= s
         assert lj == 0, "windows must partition [0, L)"
         layers[n] = {"dk": accum.dk[n], "dv": accum.dv[n], "dx": dx, "dq": dq_all}
         dy = dx
+    if ar is not None:  # TP: dB partial sums (folded LoRA), reduced once per mini-batch
+        grads["b"] = [ar(g) for g in grads["b"]]
     return {"loss": tr["loss"], "grads": grads, "layers": layers}
 
 

@@ -630,23 +630,32 @@ cudaError_t set_smem(K kern, int bytes) {
 
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st) {
-  if (n_work <= 0) return cudaSuccess;
+  // the combine also merges the decode kernel's partials (attn_decode runs first)
+  if (n_work <= 0 && n_combine <= 0) return cudaSuccess;
   if (head_dim == 128) {
     constexpr int smem = 64 * 128 * 2 * 5;
     static bool once = (set_smem(attn_fwd_kernel<128>, smem), true);
     (void)once;
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    attn_fwd_kernel<128><<<n_work, 128, smem, st>>>(p);
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (n_combine > 0) attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
+    if (n_work > 0) {
+      cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+      attn_fwd_kernel<128><<<n_work, 128, smem, st>>>(p);
+    }
+    if (n_combine > 0) {
+      cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+      attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
+    }
   } else if (head_dim == 64) {
     constexpr int smem = 64 * 64 * 2 * 5;
     static bool once = (set_smem(attn_fwd_kernel<64>, smem), true);
     (void)once;
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    attn_fwd_kernel<64><<<n_work, 128, smem, st>>>(p);
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (n_combine > 0) attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
+    if (n_work > 0) {
+      cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+      attn_fwd_kernel<64><<<n_work, 128, smem, st>>>(p);
+    }
+    if (n_combine > 0) {
+      cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+      attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
+    }
   } else {
     return cudaErrorInvalidValue;
   }

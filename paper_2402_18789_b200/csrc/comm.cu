@@ -1,0 +1,235 @@
+// comm.cu -- TP all-reduce backends (see comm.h): NCCL, and the local-group one-shot peer
+// all-reduce (reduce-scatter + all-gather in one kernel over peer pointers).
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "comm.h"
+#include "kernels.h"
+
+namespace cs {
+
+// ================================================================================ NCCL
+namespace {
+struct NcclComm final : Comm {
+  ncclComm_t comm = nullptr;
+  int r = 0, n = 1;
+  ~NcclComm() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  int rank() const override { return r; }
+  int size() const override { return n; }
+  int allreduce_f32(float* buf, size_t count, cudaStream_t st, std::string* err) override {
+    ncclResult_t res = ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, comm, st);
+    if (res != ncclSuccess) {
+      if (err) *err = std::string("ncclAllReduce: ") + ncclGetErrorString(res);
+      return -1;
+    }
+    return 0;
+  }
+};
+}  // namespace
+
+int nccl_unique_id(void* out128, std::string* err) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  ncclResult_t res = ncclGetUniqueId(&id);
+  if (res != ncclSuccess) {
+    if (err) *err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(res);
+    return -1;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+Comm* make_nccl_comm(const void* unique_id, int rank, int size, std::string* err) {
+  auto* c = new NcclComm();
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclResult_t res = ncclCommInitRank(&c->comm, size, id, rank);
+  if (res != ncclSuccess) {
+    if (err) *err = std::string("ncclCommInitRank: ") + ncclGetErrorString(res);
+    c->comm = nullptr;
+    delete c;
+    return nullptr;
+  }
+  c->r = rank;
+  c->n = size;
+  return c;
+}
+
+// ========================================================================= local group
+constexpr int kMaxRanks = 8;
+
+struct PeerPtrs {
+  float* p[kMaxRanks];
+};
+
+// rank `me` owns float4 slots [lo, hi) of n4: sum over ranks in rank order (bit-identical on
+// every rank), store the sum into every rank's buffer.  Rank 0 also handles the n % 4 tail.
+__global__ void __launch_bounds__(256) peer_allreduce_kernel(PeerPtrs ptrs, int nranks, int me,
+                                                             size_t n) {
+  const size_t n4 = n / 4;
+  const size_t per = (n4 + nranks - 1) / nranks;
+  const size_t lo = (size_t)me * per, hi = lo + per < n4 ? lo + per : n4;
+  for (size_t i = lo + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(ptrs.p[0])[i];
+    for (int j = 1; j < nranks; ++j) {
+      const float4 v = reinterpret_cast<const float4*>(ptrs.p[j])[i];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    for (int j = 0; j < nranks; ++j) reinterpret_cast<float4*>(ptrs.p[j])[i] = s;
+  }
+  if (me == 0 && blockIdx.x == 0 && threadIdx.x < (int)(n % 4)) {
+    const size_t i = n4 * 4 + threadIdx.x;
+    float s = ptrs.p[0][i];
+    for (int j = 1; j < nranks; ++j) s += ptrs.p[j][i];
+    for (int j = 0; j < nranks; ++j) ptrs.p[j][i] = s;
+  }
+}
+
+struct LocalGroup {
+  int n = 0;
+  // sense-reversing spin barrier (the ranks are host threads of this process)
+  std::atomic<int> arrived{0};
+  std::atomic<int> gen{0};
+  std::atomic<int> attached{0};
+  std::atomic<bool> broken{false};
+  float* ptrs[kMaxRanks] = {};
+  cudaEvent_t ev_ready[kMaxRanks] = {};
+  cudaEvent_t ev_done[kMaxRanks] = {};
+  int device[kMaxRanks] = {};
+
+  // false on timeout (a rank died or took a different path): the group is then broken
+  bool barrier() {
+    if (broken.load(std::memory_order_acquire)) return false;
+    const int g = gen.load(std::memory_order_acquire);
+    if (arrived.fetch_add(1, std::memory_order_acq_rel) == n - 1) {
+      arrived.store(0, std::memory_order_relaxed);
+      gen.fetch_add(1, std::memory_order_acq_rel);
+      return true;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    long spins = 0;
+    while (gen.load(std::memory_order_acquire) == g) {
+      if (++spins > 64) std::this_thread::yield();
+      if ((spins & 1023) == 0 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+        broken.store(true, std::memory_order_release);
+        return false;
+      }
+      if (broken.load(std::memory_order_acquire)) return false;
+    }
+    return true;
+  }
+};
+
+namespace {
+struct LocalComm final : Comm {
+  LocalGroup* g = nullptr;
+  int r = 0;
+  int rank() const override { return r; }
+  int size() const override { return g->n; }
+  int allreduce_f32(float* buf, size_t count, cudaStream_t st, std::string* err) override {
+    const int n = g->n;
+    if (count == 0) return 0;
+    if ((reinterpret_cast<uintptr_t>(buf) & 15) != 0) {
+      if (err) *err = "local all-reduce: buffer not 16-byte aligned";
+      return -1;
+    }
+    g->ptrs[r] = buf;
+    cudaEventRecord(g->ev_ready[r], st);
+    if (!g->barrier()) {
+      if (err) *err = "tp barrier timeout (ranks diverged)";
+      return -1;
+    }
+    for (int j = 0; j < n; ++j)
+      if (j != r) cudaStreamWaitEvent(st, g->ev_ready[j], 0);
+    PeerPtrs pp{};
+    for (int j = 0; j < n; ++j) pp.p[j] = g->ptrs[j];
+    const size_t per4 = (count / 4 + n - 1) / n;
+    const int blocks = (int)std::max<size_t>(1, std::min<size_t>((per4 + 255) / 256, 148 * 4));
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+    peer_allreduce_kernel<<<blocks, 256, 0, st>>>(pp, n, r, count);
+    cudaError_t e = cudaGetLastError();
+    cudaEventRecord(g->ev_done[r], st);
+    // all slices written before anyone reads its buffer again; ptrs[] may be reused after
+    if (!g->barrier()) {
+      if (err) *err = "tp barrier timeout (ranks diverged)";
+      return -1;
+    }
+    for (int j = 0; j < n; ++j)
+      if (j != r) cudaStreamWaitEvent(st, g->ev_done[j], 0);
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("peer_allreduce_kernel: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return 0;
+  }
+};
+}  // namespace
+
+LocalGroup* local_group_create(int size, std::string* err) {
+  if (size < 1 || size > kMaxRanks) {
+    if (err) *err = "tp group size must be in [1, 8]";
+    return nullptr;
+  }
+  auto* g = new LocalGroup();
+  g->n = size;
+  for (int i = 0; i < size; ++i) g->device[i] = -1;
+  return g;
+}
+
+int local_group_size(const LocalGroup* g) { return g ? g->n : 0; }
+
+void local_group_destroy(LocalGroup* g) {
+  if (!g) return;
+  for (int i = 0; i < g->n; ++i) {
+    if (g->ev_ready[i]) cudaEventDestroy(g->ev_ready[i]);
+    if (g->ev_done[i]) cudaEventDestroy(g->ev_done[i]);
+  }
+  delete g;
+}
+
+Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err) {
+  if (!g || rank < 0 || rank >= g->n) {
+    if (err) *err = "local tp comm: bad group / rank";
+    return nullptr;
+  }
+  if (g->device[rank] != -1) {
+    if (err) *err = "local tp comm: rank already attached";
+    return nullptr;
+  }
+  // events live on the rank's device; peers may sit on other devices of this process
+  cudaEventCreateWithFlags(&g->ev_ready[rank], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&g->ev_done[rank], cudaEventDisableTiming);
+  g->device[rank] = device;
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  for (int j = 0; j < ndev; ++j) {
+    if (j == device) continue;
+    int ok = 0;
+    cudaDeviceCanAccessPeer(&ok, device, j);
+    if (ok) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    }
+  }
+  g->attached.fetch_add(1);
+  auto* c = new LocalComm();
+  c->g = g;
+  c->r = rank;
+  return c;
+}
+
+}  // namespace cs

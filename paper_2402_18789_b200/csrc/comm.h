@@ -1,0 +1,42 @@
+// comm.h -- tensor-parallel exchange for the co-serving step.
+//
+// Megatron-style TP ("dependent parallelization", north_star): QKV and gate||up are
+// column-parallel (heads / ffn columns), O and down are row-parallel; the residual stream
+// is replicated and the row-parallel partial sums are all-reduced in place:
+//   forward : 2 all-reduces [T, h] per layer (after O, after down [+ the LoRA up, folded])
+//   backward: 2 all-reduces [s, h] per window and layer (dX of gate||up and of QKV)
+//   Adam    : 1 all-reduce of dB [layers, r, h] per mini-batch (the folded LoRA layout)
+// Two backends behind one interface:
+//   * NCCL (one process per GPU, ncclCommInitRank from a unique id shared by the host),
+//   * local group (ranks are engines of one process, each driven by its own host thread):
+//     a one-shot peer all-reduce kernel -- every rank reduces its 1/tp slice of all ranks'
+//     buffers in a fixed order and writes the sum back into every buffer -- ordered by
+//     CUDA events exchanged at two host barriers.  Over NVSwitch the peer pointers are
+//     NVLink loads/stores (peer access enabled); on one device the same code runs with
+//     plain device pointers, which is how the TP math is tested on a single B200.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace cs {
+
+struct Comm {
+  virtual ~Comm() {}
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  // in-place sum over the ranks of buf[0, n), stream-ordered on st; 0 on success
+  virtual int allreduce_f32(float* buf, size_t n, cudaStream_t st, std::string* err) = 0;
+};
+
+// NCCL communicator from a 128-byte ncclUniqueId (all ranks call concurrently)
+Comm* make_nccl_comm(const void* unique_id, int rank, int size, std::string* err);
+int nccl_unique_id(void* out128, std::string* err);
+
+struct LocalGroup;
+LocalGroup* local_group_create(int size, std::string* err);
+void local_group_destroy(LocalGroup* g);
+int local_group_size(const LocalGroup* g);
+Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err);
+
+}  // namespace cs

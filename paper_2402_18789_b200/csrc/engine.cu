@@ -16,11 +16,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "coserve_cuda.h"
 #include "engine_kernels.h"
 #include "kernels.h"
@@ -42,13 +44,16 @@ struct cs_engine {
   cs_model_config cfg{};
   int device = 0;
   int tp_rank = 0, tp_size = 1;
+  cs::Comm* comm = nullptr;  // tp_size > 1: all-reduce of the row-parallel partial sums
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // dims
+  // dims (per rank: heads and ffn columns are this rank's shard; *_g = whole model)
+  int Hq_g, Hkv_g, f_g;
   int h, Hq, Hkv, d, q_dim, kv_dim, nqkv, f, V, r, NL, P, npages, gu_n, f_cat, h_cat, grp;
   int T_max, L_max, S_max, max_seg, head_chunk, max_pos;
   bool swiglu, norm, rope;
   bool use_tc_attn = true;  // CS_ATTN_TC=0 forces the mma.sync path (A/B testing)
+  bool use_dec_attn = true;  // CS_ATTN_DEC=0 sends decode rows to the mma.sync tile kernel
   // arena
   uint8_t* arena = nullptr;
   size_t arena_bytes = 0, arena_used = 0;
@@ -102,9 +107,10 @@ struct cs_engine {
   size_t ev_used = 0;
   std::vector<ProfRec> recs;
   // kinds: 0 tcgen05 GEMM, 1 attention fwd (bandwidth kernel: decode), 2 attention bwd,
-  //        3 attention fwd (tcgen05 kernel: prefill / FT windows)
-  double prof_ms[4] = {0, 0, 0, 0}, prof_flops[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};
-  long prof_n[4] = {0, 0, 0, 0};
+  //        3 attention fwd (tcgen05 kernel: prefill / FT windows), 4 TP all-reduce
+  static constexpr int kKinds = 5;
+  double prof_ms[kKinds] = {}, prof_flops[kKinds] = {}, prof_bytes[kKinds] = {};
+  long prof_n[kKinds] = {};
   double step_attn_flops = 0, step_attn_bytes = 0, step_tc_flops = 0, step_tc_bytes = 0;
 };
 
@@ -260,9 +266,11 @@ size_t meta_size(const cs_engine* e) {
 }  // namespace
 
 // =============================================================================== create
-extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
-                                const void* nccl_unique_id, cs_engine** out) {
-  (void)nccl_unique_id;
+namespace {
+using CommFactory = std::function<cs::Comm*(std::string*)>;
+
+int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                  const CommFactory& make_comm, cs_engine** out) {
   if (!cfg || !out) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: null argument");
   const cs_model_config& c = *cfg;
   if (c.n_layers < 1 || c.hidden < 1 || c.n_heads < 1 || c.n_kv_heads < 1 || c.head_dim < 1 ||
@@ -281,22 +289,27 @@ extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_r
                          "cs_engine_create: hidden/ffn must be multiples of 64, vocab of 8");
   if (c.page_size < 1 || c.n_pages < 1 || c.max_tokens < 1 || c.max_ft_len < 1)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: bad pool / capacity sizes");
-  if (tp_size != 1 || tp_rank != 0)
+  if (tp_size < 1 || tp_size > 8 || tp_rank < 0 || tp_rank >= tp_size)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: need 0 <= tp_rank < tp_size <= 8");
+  if (c.n_kv_heads % tp_size != 0 || c.ffn % tp_size != 0 || ((c.ffn / tp_size) % 64) != 0)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT,
-                         "cs_engine_create: this build runs tp_size == 1 engines (one replica per GPU)");
+                         "cs_engine_create: tp_size must divide the kv heads and ffn/tp_size be a multiple of 64");
   cs_engine* e = new cs_engine();
   e->cfg = c;
   e->device = device;
   e->tp_rank = tp_rank;
   e->tp_size = tp_size;
+  e->Hq_g = c.n_heads;
+  e->Hkv_g = c.n_kv_heads;
+  e->f_g = c.ffn;
   e->h = c.hidden;
-  e->Hq = c.n_heads;
-  e->Hkv = c.n_kv_heads;
+  e->Hq = c.n_heads / tp_size;
+  e->Hkv = c.n_kv_heads / tp_size;
   e->d = c.head_dim;
-  e->q_dim = c.n_heads * c.head_dim;
-  e->kv_dim = c.n_kv_heads * c.head_dim;
+  e->q_dim = e->Hq * c.head_dim;
+  e->kv_dim = e->Hkv * c.head_dim;
   e->nqkv = e->q_dim + 2 * e->kv_dim;
-  e->f = c.ffn;
+  e->f = c.ffn / tp_size;
   e->V = c.vocab;
   e->r = c.lora_rank;
   e->NL = c.n_layers;
@@ -317,16 +330,26 @@ extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_r
   e->max_pos = std::max((long)c.max_ft_len, std::min<long>((long)c.n_pages * c.page_size, 1 << 17)) + 1;
   e->meta_bytes = meta_size(e);
   if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
+  if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
     return cs::set_error(CS_ERR_CUDA, "cs_engine_create: cudaSetDevice failed");
+  }
+  if (tp_size > 1) {
+    std::string err;
+    e->comm = make_comm(&err);
+    if (!e->comm) {
+      delete e;
+      return cs::set_error(CS_ERR_NCCL, "cs_engine_create: " + err);
+    }
   }
   size_t total = 0;
   layout(e, true, &total);
   e->arena_bytes = total;
   cudaError_t err = cudaMalloc(&e->arena, total);
   if (err != cudaSuccess) {
+    delete e->comm;
     delete e;
     return cs::set_error(CS_ERR_OOM, "cs_engine_create: cudaMalloc(" + std::to_string(total) +
                                          ") failed: " + cudaGetErrorString(err));
@@ -358,11 +381,59 @@ extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_r
   err = cudaStreamSynchronize(e->st);
   if (err != cudaSuccess) {
     cudaFree(e->arena);
+    delete e->comm;
     delete e;
     return cs::set_error(CS_ERR_CUDA, std::string("cs_engine_create: ") + cudaGetErrorString(err));
   }
   *out = e;
   return CS_OK;
+}
+}  // namespace
+
+struct cs_tp_group {
+  cs::LocalGroup* g;
+};
+
+extern "C" int cs_engine_create(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                                const void* nccl_unique_id, cs_engine** out) {
+  if (tp_size > 1 && !nccl_unique_id)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                         "cs_engine_create: tp_size > 1 needs the NCCL unique id (or cs_engine_create_tp_local)");
+  return create_engine(cfg, device, tp_rank, tp_size,
+                       [&](std::string* err) { return cs::make_nccl_comm(nccl_unique_id, tp_rank, tp_size, err); },
+                       out);
+}
+
+extern "C" int cs_nccl_unique_id(void* out128) {
+  if (!out128) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_nccl_unique_id: null buffer");
+  std::string err;
+  if (cs::nccl_unique_id(out128, &err) != 0) return cs::set_error(CS_ERR_NCCL, err);
+  return CS_OK;
+}
+
+extern "C" int cs_tp_group_create(int tp_size, cs_tp_group** out) {
+  if (!out) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_tp_group_create: null argument");
+  std::string err;
+  cs::LocalGroup* g = cs::local_group_create(tp_size, &err);
+  if (!g) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_tp_group_create: " + err);
+  *out = new cs_tp_group{g};
+  return CS_OK;
+}
+
+extern "C" int cs_tp_group_destroy(cs_tp_group* g) {
+  if (!g) return CS_OK;
+  cs::local_group_destroy(g->g);
+  delete g;
+  return CS_OK;
+}
+
+extern "C" int cs_engine_create_tp_local(const cs_model_config* cfg, int device, int tp_rank,
+                                         cs_tp_group* group, cs_engine** out) {
+  if (!group) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create_tp_local: null group");
+  const int n = cs::local_group_size(group->g);
+  return create_engine(cfg, device, tp_rank, n,
+                       [&](std::string* err) { return cs::make_local_comm(group->g, tp_rank, device, err); },
+                       out);
 }
 
 extern "C" int cs_engine_set_profiling(cs_engine* e, int on) {
@@ -370,13 +441,14 @@ extern "C" int cs_engine_set_profiling(cs_engine* e, int on) {
   cudaStreamSynchronize(e->st);
   prof_collect(e);
   e->profiling = on != 0;
-  for (int k = 0; k < 4; ++k) e->prof_ms[k] = e->prof_flops[k] = e->prof_bytes[k] = 0, e->prof_n[k] = 0;
+  for (int k = 0; k < cs_engine::kKinds; ++k)
+    e->prof_ms[k] = e->prof_flops[k] = e->prof_bytes[k] = 0, e->prof_n[k] = 0;
   return CS_OK;
 }
 
 extern "C" int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops,
                                       double* bytes, int64_t* launches) {
-  if (!e || kind < 0 || kind > 3) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_profile: bad kind");
+  if (!e || kind < 0 || kind >= cs_engine::kKinds) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "read_profile: bad kind");
   if (ms) *ms = e->prof_ms[kind];
   if (flops) *flops = e->prof_flops[kind];
   if (bytes) *bytes = e->prof_bytes[kind];
@@ -408,6 +480,7 @@ extern "C" int cs_engine_destroy(cs_engine* e) {
   cudaEventDestroy(e->ev0);
   cudaEventDestroy(e->ev1);
   cudaStreamDestroy(e->st);
+  delete e->comm;
   delete e;
   return CS_OK;
 }
@@ -452,93 +525,108 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
   if (!global && (layer < 0 || layer >= e->NL))
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: layer out of range");
   const long count = rows * cols;
-  std::vector<float> f32(count);
-  if (dtype == 0) {
-    const double* s = static_cast<const double*>(host);
-    for (long i = 0; i < count; ++i) f32[i] = (float)s[i];
-  } else {
-    std::memcpy(f32.data(), host, count * sizeof(float));
-  }
+  // whole-model shapes (reference layout [in, out]); TP ranks keep their shard below
+  const long h = e->h, V = e->V, r = e->r, d = e->d;
+  const long qd_g = (long)e->Hq_g * d, kvd_g = (long)e->Hkv_g * d, f_g = e->f_g;
   auto expect = [&](long er, long ec) -> bool { return rows == er && cols == ec; };
+  auto bad = [&]() {
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT,
+                         "set_weight: unexpected shape for '" + n + "' [" + std::to_string(rows) +
+                             "," + std::to_string(cols) + "]");
+  };
+  // shard: rows [r0, r0+nr) x cols [c0, c0+nc) of the whole matrix (vectors: cols)
+  const long rk = e->tp_rank;
+  long r0 = 0, nr = rows, c0 = 0, nc = cols;
+  if (n == "embed") {
+    if (!expect(V, h)) return bad();
+  } else if (n == "unembed") {
+    if (!expect(h, V)) return bad();
+  } else if (n == "final_norm" || n == "norm1" || n == "norm2") {
+    if (count != h) return bad();
+    nr = 1, nc = h;
+  } else if (n == "wq") {
+    if (!expect(h, qd_g)) return bad();
+    c0 = rk * e->q_dim, nc = e->q_dim;
+  } else if (n == "wk" || n == "wv") {
+    if (!expect(h, kvd_g)) return bad();
+    c0 = rk * e->kv_dim, nc = e->kv_dim;
+  } else if (n == "bq") {
+    if (count != qd_g) return bad();
+    nr = 1, c0 = rk * e->q_dim, nc = e->q_dim;
+  } else if (n == "bk" || n == "bv") {
+    if (count != kvd_g) return bad();
+    nr = 1, c0 = rk * e->kv_dim, nc = e->kv_dim;
+  } else if (n == "wo") {
+    if (!expect(qd_g, h)) return bad();
+    r0 = rk * e->q_dim, nr = e->q_dim;
+  } else if (n == "w_gate" || n == "w_up") {
+    if (n == "w_gate" && !e->swiglu)
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: w_gate given for a ReLU model");
+    if (!expect(h, f_g)) return bad();
+    c0 = rk * e->f, nc = e->f;
+  } else if (n == "w_down") {
+    if (!expect(f_g, h)) return bad();
+    r0 = rk * e->f, nr = e->f;
+  } else if (n == "lora_a") {
+    if (!expect(f_g, r)) return bad();
+    r0 = rk * e->f, nr = e->f;
+  } else if (n == "lora_b") {
+    if (!expect(r, h)) return bad();
+  } else {
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: unknown weight '" + n + "'");
+  }
+  const long src_cols = (nr == 1 && rows != 1 && cols == 1) ? rows : cols;  // column vectors
+  std::vector<float> f32((size_t)nr * nc);
+  for (long i = 0; i < nr; ++i)
+    for (long j = 0; j < nc; ++j) {
+      const long k = (r0 + i) * src_cols + (c0 + j);
+      f32[(size_t)i * nc + j] = dtype == 0 ? (float)static_cast<const double*>(host)[k]
+                                           : static_cast<const float*>(host)[k];
+    }
+  const long lr = nr, lc = nc, lcount = nr * nc;
   const int L = layer;
-  const long h = e->h, qd = e->q_dim, kvd = e->kv_dim, f = e->f, V = e->V, r = e->r;
+  const long qd = e->q_dim, kvd = e->kv_dim, f = e->f;
   float* stage = nullptr;
-  CS_CUDA_TRY(cudaMalloc(&stage, count * sizeof(float)));
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  CS_CUDA_TRY(cudaMalloc(&stage, lcount * sizeof(float)));
   // stream-ordered upload: the engine stream is non-blocking w.r.t. the legacy stream
-  CS_CUDA_TRY(cudaMemcpyAsync(stage, f32.data(), count * sizeof(float), cudaMemcpyHostToDevice,
+  CS_CUDA_TRY(cudaMemcpyAsync(stage, f32.data(), lcount * sizeof(float), cudaMemcpyHostToDevice,
                               e->st));
   int rc = CS_OK;
-  auto bad = [&]() {
-    rc = cs::set_error(CS_ERR_INVALID_ARGUMENT,
-                       "set_weight: unexpected shape for '" + n + "' [" + std::to_string(rows) +
-                           "," + std::to_string(cols) + "]");
-  };
   cudaStream_t st = e->st;
   if (n == "embed") {
-    if (!expect(V, h)) bad();
-    else cs::cast_f32_bf16(stage, rows, cols, e->embed, h, 0, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->embed, h, 0, st);
   } else if (n == "unembed") {
-    if (!expect(h, V)) bad();
-    else {
-      cs::cast_f32_bf16(stage, rows, cols, e->unembed, V, 0, st);
-      cs::cast_f32_bf16(stage, rows, cols, e->unembed_t, h, 1, st);
-    }
+    cs::cast_f32_bf16(stage, lr, lc, e->unembed, V, 0, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->unembed_t, h, 1, st);
   } else if (n == "final_norm") {
-    if (count != h) bad();
-    else cudaMemcpyAsync(e->gf, stage, h * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(e->gf, stage, h * 4, cudaMemcpyDeviceToDevice, st);
   } else if (n == "wq" || n == "wk" || n == "wv") {
     const long off = n == "wq" ? 0 : (n == "wk" ? qd : qd + kvd);
-    const long oc = n == "wq" ? qd : kvd;
-    if (!expect(h, oc)) bad();
-    else {
-      cs::cast_f32_bf16(stage, rows, cols, e->wqkv_t + ((size_t)L * e->nqkv + off) * h, h, 1, st);
-      cs::cast_f32_bf16(stage, rows, cols, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
-    }
+    cs::cast_f32_bf16(stage, lr, lc, e->wqkv_t + ((size_t)L * e->nqkv + off) * h, h, 1, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
   } else if (n == "wo") {
-    if (!expect(qd, h)) bad();
-    else {
-      cs::cast_f32_bf16(stage, rows, cols, e->wo_t + (size_t)L * h * qd, qd, 1, st);
-      cs::cast_f32_bf16(stage, rows, cols, e->wo + (size_t)L * qd * h, h, 0, st);
-    }
+    cs::cast_f32_bf16(stage, lr, lc, e->wo_t + (size_t)L * h * qd, qd, 1, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->wo + (size_t)L * qd * h, h, 0, st);
   } else if (n == "w_gate" || n == "w_up") {
-    if (n == "w_gate" && !e->swiglu) {
-      rc = cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: w_gate given for a ReLU model");
-    } else if (!expect(h, f)) {
-      bad();
-    } else {
-      const long off = (n == "w_up" && e->swiglu) ? f : 0;
-      cs::cast_f32_bf16(stage, rows, cols, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
-      cs::cast_f32_bf16(stage, rows, cols, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
-    }
+    const long off = (n == "w_up" && e->swiglu) ? f : 0;
+    cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
   } else if (n == "w_down") {
-    if (!expect(f, h)) bad();
-    else {
-      cs::cast_f32_bf16(stage, rows, cols, e->down_cat + (size_t)L * h * e->f_cat, e->f_cat, 1, st);
-      cs::cast_f32_bf16(stage, rows, cols, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
-    }
+    cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * h * e->f_cat, e->f_cat, 1, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
   } else if (n == "lora_a") {
-    if (!expect(f, r)) bad();
-    else {
-      cudaMemcpyAsync(e->loraA + (size_t)L * f * r, stage, count * 4, cudaMemcpyDeviceToDevice, st);
-      rc = refresh_lora(e, 0, 0, 0, 0, 0);
-    }
+    cudaMemcpyAsync(e->loraA + (size_t)L * f * r, stage, lcount * 4, cudaMemcpyDeviceToDevice, st);
+    rc = refresh_lora(e, 0, 0, 0, 0, 0);
   } else if (n == "lora_b") {
-    if (!expect(r, h)) bad();
-    else {
-      cudaMemcpyAsync(e->loraB + (size_t)L * r * h, stage, count * 4, cudaMemcpyDeviceToDevice, st);
-      rc = refresh_lora(e, 0, 0, 0, 0, 0);
-    }
+    cudaMemcpyAsync(e->loraB + (size_t)L * r * h, stage, lcount * 4, cudaMemcpyDeviceToDevice, st);
+    rc = refresh_lora(e, 0, 0, 0, 0, 0);
   } else if (n == "bq" || n == "bk" || n == "bv") {
     const long off = n == "bq" ? 0 : (n == "bk" ? qd : qd + kvd);
-    const long oc = n == "bq" ? qd : kvd;
-    if (count != oc) bad();
-    else cudaMemcpyAsync(e->bqkv + (size_t)L * e->nqkv + off, stage, count * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(e->bqkv + (size_t)L * e->nqkv + off, stage, lcount * 4, cudaMemcpyDeviceToDevice, st);
   } else if (n == "norm1" || n == "norm2") {
-    if (count != h) bad();
-    else cudaMemcpyAsync((n == "norm1" ? e->g1 : e->g2) + (size_t)L * h, stage, h * 4,
-                         cudaMemcpyDeviceToDevice, st);
-  } else {
-    rc = cs::set_error(CS_ERR_INVALID_ARGUMENT, "set_weight: unknown weight '" + n + "'");
+    cudaMemcpyAsync((n == "norm1" ? e->g1 : e->g2) + (size_t)L * h, stage, h * 4,
+                    cudaMemcpyDeviceToDevice, st);
   }
   cudaStreamSynchronize(st);
   cudaFree(stage);
@@ -550,34 +638,37 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
   if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "init_random: null engine");
   cudaStream_t st = e->st;
   const float ws = 1.f / std::sqrt((float)e->h);
-  const float wf = 1.f / std::sqrt((float)e->f);
+  const float wf = 1.f / std::sqrt((float)e->f_g);
   const size_t NL = e->NL;
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  // TP: sharded matrices draw per-rank streams; replicated ones (embed, unembed, B) share one
+  const uint64_t ss = seed + 7919ull * (uint64_t)e->tp_rank;
   // tiny_model.hpp:51-63 scales; the forward/backward layouts hold identical values
   cs::init_normal_bf16(e->embed, (long)e->V * e->h, ws, seed + 1, st);
   cs::init_normal_bf16(e->unembed, (long)e->V * e->h, ws, seed + 2, st);
   cs::init_normal_bf16(e->unembed_t, (long)e->V * e->h, ws, seed + 2, st);  // same stats
-  cs::init_normal_bf16(e->wqkv_t, (long)(NL * e->nqkv * e->h), ws, seed + 3, st);
-  cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, seed + 3, st);
-  cs::init_normal_bf16(e->wo_t, (long)(NL * e->q_dim * e->h), ws, seed + 4, st);
-  cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, seed + 4, st);
-  cs::init_normal_bf16(e->wgu_t, (long)(NL * e->gu_n * e->h), ws, seed + 5, st);
-  cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, seed + 5, st);
+  cs::init_normal_bf16(e->wqkv_t, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
+  cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
+  cs::init_normal_bf16(e->wo_t, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
+  cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
+  cs::init_normal_bf16(e->wgu_t, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
+  cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
   // down: fill whole concat buffers, then the LoRA columns are rewritten by refresh_lora;
   // pad columns [f + r, f + 64) must stay zero -> fill per row via cast of random fp32
   {
     float* tmp = nullptr;
     CS_CUDA_TRY(cudaMalloc(&tmp, (size_t)e->f * e->h * sizeof(float)));
     for (size_t l = 0; l < NL; ++l) {
-      cs::init_normal_f32(tmp, (long)e->f * e->h, wf, seed + 100 + l, st);
+      cs::init_normal_f32(tmp, (long)e->f * e->h, wf, ss + 100 + l, st);
       cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->h * e->f_cat, e->f_cat, 1, st);
       cs::cast_f32_bf16(tmp, e->f, e->h, e->dbwd_cat + l * e->f * e->h_cat, e->h_cat, 0, st);
     }
     cudaStreamSynchronize(st);
     cudaFree(tmp);
   }
-  cs::init_normal_f32(e->loraA, (long)(NL * e->f * e->r), 0.2f * wf, seed + 6, st);
+  cs::init_normal_f32(e->loraA, (long)(NL * e->f * e->r), 0.2f * wf, ss + 6, st);
   cs::init_normal_f32(e->loraB, (long)(NL * e->r * e->h), 0.2f, seed + 7, st);
-  if (e->cfg.qkv_bias) cs::init_normal_f32(e->bqkv, (long)(NL * e->nqkv), 0.02f, seed + 8, st);
+  if (e->cfg.qkv_bias) cs::init_normal_f32(e->bqkv, (long)(NL * e->nqkv), 0.02f, ss + 8, st);
   int rc = refresh_lora(e, 0, 0, 0, 0, 0);
   if (rc) return rc;
   CS_CUDA_TRY(cudaStreamSynchronize(st));
@@ -610,12 +701,13 @@ struct StepPlan {
   int ft_row0 = 0;  // first FT forward row (== T if none)
   int ad_row0 = 0;  // first adapter row (== T if none)
   int n_samp = 0;
-  int n_work = 0, n_comb = 0, n_tc = 0;
+  int n_work = 0, n_comb = 0, n_tc = 0, n_dec = 0;
   // device pointers into d_meta
   int *tokens, *row_pos, *row_seg, *page_table, *samp_idx, *targets;
   cs::AttnSeg* segs;
   cs::AttnWork* work;
   cs::AttnWork* work_tc;
+  cs::AttnWork* work_dec;
   cs::AttnCombine* comb;
   std::vector<int> samp_seg;  // segment of each sampled row
 };
@@ -657,6 +749,26 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
     if (_rc) return _rc;  \
   } while (0)
 
+// in-place sum of buf[0, n) over the TP ranks (no-op at tp_size 1); SURVEY.md §8e
+int tp_allreduce(cs_engine* e, float* buf, size_t n) {
+  if (!e->comm || n == 0) return CS_OK;
+  cs_engine::ProfRec pr{};
+  if (e->profiling) {
+    pr.bytes = 2.0 * (double)n * 4.0 * (e->tp_size - 1) / e->tp_size;  // ring bus bytes
+    pr.kind = 4;
+    prof_begin(e, pr);
+  }
+  std::string err;
+  const int rc = e->comm->allreduce_f32(buf, n, e->st, &err);
+  if (e->profiling) prof_end(e, pr);
+  if (rc != 0) return cs::set_error(CS_ERR_NCCL, "tp all-reduce: " + err);
+  return CS_OK;
+}
+
+// row-parallel projections add into the replicated residual stream: rank 0 accumulates
+// (x += p_0), the other ranks overwrite (x = p_r); the all-reduce then leaves x + sum_r p_r
+int rowpar_epi(const cs_engine* e) { return (e->comm && e->tp_rank != 0) ? cs::EPI_F32 : cs::EPI_F32_ADD; }
+
 int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   const int T = plan->n_tokens;
   if (T < 0 || T > e->T_max)
@@ -695,7 +807,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   int row = 0;
   bool in_adapter_suffix = false;
   std::vector<int> samp_rows;
-  std::vector<cs::AttnWork> work, work_tc;
+  std::vector<cs::AttnWork> work, work_tc, work_dec;
   std::vector<cs::AttnCombine> comb;
   const int rpt = 64 / e->grp;
   const int rpt_tc = 128 / e->grp;
@@ -760,6 +872,10 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
         for (int kh = 0; kh < e->Hkv; ++kh)
           work_tc.push_back(cs::AttnWork{s, q0, nq, kh, 0, nkeys, -1, 0});
       }
+    } else if (g.q_len * e->grp <= 16 && e->use_dec_attn && (P % 16) == 0) {
+      // decode kernel: the whole GQA-packed segment fits one m16 tile
+      for (int kh = 0; kh < e->Hkv; ++kh)
+        work_dec.push_back(cs::AttnWork{s, 0, g.q_len, kh, 0, g.ctx_start + g.q_len, -1, 0});
     } else {
       for (int q0 = 0; q0 < g.q_len; q0 += rpt) {
         const int nq = std::min(rpt, g.q_len - q0);
@@ -807,16 +923,54 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       else comb.clear();
     }
   }
+  // decode: balance the 32-key tiles over the SMs -- split long key ranges into parts of
+  // `chunk` keys (multiples of 128 = one tile per warp) so that the grid is ~8 waves of
+  // 1 CTA/SM (small wave-quantisation tail, longest parts first), but no part is shorter
+  // than 512 keys (4 tiles per warp: the per-warp TMA ring stays full)
+  {
+    long total = 0;
+    for (const auto& w : work_dec) total += w.k_end;
+    const long target = 8L * 148;
+    long chunk = (total + target - 1) / target;
+    chunk = std::max<long>(512, (chunk + 127) / 128 * 128);
+    int part = 0;
+    for (const auto& c : comb) part = std::max(part, c.part0 + c.n_parts);
+    std::vector<cs::AttnWork> w2;
+    w2.reserve(work_dec.size());
+    for (const auto& w : work_dec) {
+      const int ns = (int)((w.k_end + chunk - 1) / chunk);
+      if (ns <= 1 || part + ns > 4096) {
+        w2.push_back(w);
+        continue;
+      }
+      const int p0 = part;
+      for (int t = 0; t < ns; ++t) {
+        cs::AttnWork x = w;
+        x.k_begin = (int)(t * chunk);
+        x.k_end = (int)std::min<long>(w.k_end, (t + 1) * chunk);
+        x.part = part++;
+        w2.push_back(x);
+      }
+      comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, ns, 0, 0});
+    }
+    // longest first: the heaviest CTAs start in the first wave
+    std::stable_sort(w2.begin(), w2.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
+      return x.k_end - x.k_begin > y.k_end - y.k_begin;
+    });
+    work_dec.swap(w2);
+  }
   // longest key ranges first (causal tiles have very different lengths)
   std::stable_sort(work_tc.begin(), work_tc.end(),
                    [](const cs::AttnWork& x, const cs::AttnWork& y) { return x.k_end > y.k_end; });
   sp.n_work = (int)work.size();
   sp.n_tc = (int)work_tc.size();
+  sp.n_dec = (int)work_dec.size();
   sp.n_comb = (int)comb.size();
-  if (sp.n_work + sp.n_tc > 65536 || sp.n_comb > 8192)
+  if (sp.n_work + sp.n_tc + sp.n_dec > 65536 || sp.n_comb > 8192)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: attention work list too large");
   const size_t o_work = take(work.size() * sizeof(cs::AttnWork));
   const size_t o_wtc = take(work_tc.size() * sizeof(cs::AttnWork));
+  const size_t o_wdec = take(work_dec.size() * sizeof(cs::AttnWork));
   const size_t o_comb = take(comb.size() * sizeof(cs::AttnCombine));
   const size_t o_samp = take(samp_rows.size() * 4);
   const int ft_s = (plan->ft.phase == CS_FT_FORWARD) ? plan->ft.s : 0;
@@ -824,6 +978,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   if (off > e->meta_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: plan too large");
   if (!work.empty()) std::memcpy(hb + o_work, work.data(), work.size() * sizeof(cs::AttnWork));
   if (!work_tc.empty()) std::memcpy(hb + o_wtc, work_tc.data(), work_tc.size() * sizeof(cs::AttnWork));
+  if (!work_dec.empty()) std::memcpy(hb + o_wdec, work_dec.data(), work_dec.size() * sizeof(cs::AttnWork));
   if (!comb.empty()) std::memcpy(hb + o_comb, comb.data(), comb.size() * sizeof(cs::AttnCombine));
   if (!samp_rows.empty()) std::memcpy(hb + o_samp, samp_rows.data(), samp_rows.size() * 4);
   if (ft_s > 0) {
@@ -846,6 +1001,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.work = reinterpret_cast<cs::AttnWork*>(db + o_work);
   sp.comb = reinterpret_cast<cs::AttnCombine*>(db + o_comb);
   sp.work_tc = reinterpret_cast<cs::AttnWork*>(db + o_wtc);
+  sp.work_dec = reinterpret_cast<cs::AttnWork*>(db + o_wdec);
   sp.samp_idx = reinterpret_cast<int*>(db + o_samp);
   sp.targets = reinterpret_cast<int*>(db + o_tg);
   return CS_OK;
@@ -920,14 +1076,25 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     ap.grp = e->grp;
     ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
     cs_engine::ProfRec apr{};
-    if (e->profiling && sp.n_work > 0) {
+    const bool bw_attn = sp.n_work + sp.n_dec > 0;
+    if (e->profiling && bw_attn) {
       apr.flops = e->step_attn_flops;
       apr.bytes = e->step_attn_bytes;
       apr.kind = 1;
       prof_begin(e, apr);
     }
+    if (sp.n_dec > 0) {
+      cs::AttnFwdParams dp = ap;
+      dp.work = sp.work_dec;
+      CUtensorMap mk, mv;
+      const long pool_rows = (long)e->npages * e->P;
+      if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
+          cs::make_map(&mv, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0)
+        return cs::set_error(CS_ERR_CUDA, "decode attention: TMA map creation failed");
+      CS_CUDA_TRY(cs::attn_decode(dp, mk, mv, e->d, sp.n_dec, st));
+    }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
-    if (e->profiling && sp.n_work > 0) prof_end(e, apr);
+    if (e->profiling && bw_attn) prof_end(e, apr);
     if (sp.n_tc > 0) {
       CUtensorMap mk, mv, mk128, mv128;
       const long pool_rows = (long)e->npages * e->P;
@@ -955,7 +1122,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                 e->lse + (size_t)sp.ft_row0 * e->Hq, e->Hq, n_ft, e->Hq);
     }
     TRY(gemm(e, e->attn, e->q_dim, e->T_max, e->wo_t + (size_t)l * h * e->q_dim, e->q_dim, h, e->x, h,
-             T, h, e->q_dim, cs::EPI_F32_ADD));
+             T, h, e->q_dim, rowpar_epi(e)));
+    TRY(tp_allreduce(e, e->x, (size_t)T * h));
     // ---- MLP block
     if (n_ft > 0 && e->norm)
       save_rows(e, e->ft_r1 + ((size_t)l * e->L_max + l0) * h, h, e->x + (size_t)sp.ft_row0 * h, h, n_ft, h);
@@ -979,7 +1147,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     }
     // x += [m | u] [W_down ; B] (tiny_model.hpp:206-211 as one K-concatenated GEMM)
     TRY(gemm(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * h * e->f_cat, e->f_cat, h, e->x,
-             h, T, h, e->f_cat, cs::EPI_F32_ADD));
+             h, T, h, e->f_cat, rowpar_epi(e)));
+    TRY(tp_allreduce(e, e->x, (size_t)T * h));
   }
   // ---- sampled rows: final norm -> logits -> argmax
   if (sp.n_samp > 0) {
@@ -1052,6 +1221,7 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   if (n > 0) {
     TRY(gemm(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2, h,
              s, h, e->gu_n, cs::EPI_F32));
+    TRY(tp_allreduce(e, e->dh2, (size_t)s * h));
     cs::rms_bwd_add(Y, h, e->ft_r1 + ((size_t)n * Lm + a) * h, h, e->g2 + (size_t)n * h,
                     e->ft_rstd2 + (size_t)n * Lm + a, e->dh2, h, e->dr1, h, e->dr1b, h, s, h,
                     e->norm, st);
@@ -1117,6 +1287,7 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
     TRY(gemm(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1, h,
              s, h, e->nqkv, cs::EPI_F32));
+    TRY(tp_allreduce(e, e->dh1, (size_t)s * h));
     cs::rms_bwd_add(e->dr1, h, e->ft_x + ((size_t)n * Lm + a) * h, h, e->g1 + (size_t)n * h,
                     e->ft_rstd1 + (size_t)n * Lm + a, e->dh1, h, Xout, h, nullptr, 0, s, h,
                     e->norm, st);
@@ -1238,6 +1409,10 @@ extern "C" int cs_adam_step(cs_engine* e, float lr, float beta1, float beta2, fl
   if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_adam_step: null engine");
   if (e->bwd_layer != -1)
     return cs::set_error(CS_ERR_ORDERING, "cs_adam_step: backward pass of the mini-batch not complete");
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  // TP: B is replicated and each rank holds the partial dB of its ffn shard (u = sum_r m_r A_r
+  // folded into the down partial sums) -> one all-reduce per mini-batch; dA stays local
+  TRY(tp_allreduce(e, e->gB, (size_t)e->NL * e->r * e->h));
   e->adam_t += 1;
   TRY(refresh_lora(e, 1, lr, beta1, beta2, eps));
   // mini-batch done: grads consumed, FT state reset

@@ -68,6 +68,10 @@ struct AttnBwdParams {
   float scale, scale_log2;
 };
 
+// decode rows (q_len * group <= 16): HBM-bound paged kernel (attn_decode.cu); run before
+// attn_fwd, whose combine pass also merges the decode partials
+cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                        int head_dim, int n_work, cudaStream_t st);
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);

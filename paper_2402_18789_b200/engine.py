@@ -112,6 +112,13 @@ def _declare_engine(L):
     L.cs_engine_set_profiling.argtypes = [vp, ctypes.c_int]
     L.cs_engine_read_profile.restype = ctypes.c_int
     L.cs_engine_read_profile.argtypes = [vp, ctypes.c_int, P(f64), P(f64), P(f64), P(i64)]
+    L.cs_nccl_unique_id.argtypes = [vp]
+    L.cs_tp_group_create.argtypes = [ctypes.c_int, P(vp)]
+    L.cs_tp_group_destroy.argtypes = [vp]
+    L.cs_engine_create_tp_local.argtypes = [P(ModelConfig), ctypes.c_int, ctypes.c_int, vp, P(vp)]
+    for name in ("cs_nccl_unique_id", "cs_tp_group_create", "cs_tp_group_destroy",
+                 "cs_engine_create_tp_local"):
+        getattr(L, name).restype = ctypes.c_int
     L.cs_engine_pool_info.restype = ctypes.c_int
     L.cs_engine_pool_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i64)]
     L.cs_sched_latency.restype = f64
@@ -174,14 +181,73 @@ def arch_config(arch, page_size=16, n_pages=256, max_tokens=256, max_ft_len=256,
     return c
 
 
-class Engine:
-    def __init__(self, cfg: ModelConfig, device: int = 0):
-        self.cfg = cfg
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; the host shares it, e.g. by torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(lib().cs_nccl_unique_id(buf), "cs_nccl_unique_id")
+    return buf.raw
+
+
+class TPGroup:
+    """Single-process tensor-parallel group (cs_tp_group): engines of this process, one host
+    thread each, all-reduce by the one-shot peer kernel.  Destroy after its engines."""
+
+    def __init__(self, size: int):
         self._L = lib()
         h = vp()
-        _lib.check(self._L.cs_engine_create(ctypes.byref(cfg), device, 0, 1, None, ctypes.byref(h)),
-                   "cs_engine_create")
+        _lib.check(self._L.cs_tp_group_create(size, ctypes.byref(h)), "cs_tp_group_create")
         self._h = h
+        self.size = size
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cs_tp_group_destroy(self._h)
+            self._h = None
+
+
+def tp_run(engines: Sequence["Engine"], fn):
+    """Run fn(engine) on every rank concurrently (one thread per rank, as cs_step requires
+    for a TP group); returns the per-rank results, re-raising the first failure."""
+    import threading
+    out = [None] * len(engines)
+    err = [None] * len(engines)
+
+    def body(i):
+        try:
+            out[i] = fn(engines[i])
+        except BaseException as ex:  # noqa: BLE001 -- re-raised below
+            err[i] = ex
+    th = [threading.Thread(target=body, args=(i,)) for i in range(len(engines))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+class Engine:
+    def __init__(self, cfg: ModelConfig, device: int = 0, tp_rank: int = 0, tp_size: int = 1,
+                 group: Optional[TPGroup] = None, nccl_uid: Optional[bytes] = None):
+        self.cfg = cfg
+        self._L = lib()
+        self.tp_rank = tp_rank
+        self.tp_size = group.size if group is not None else tp_size
+        h = vp()
+        if group is not None:
+            _lib.check(self._L.cs_engine_create_tp_local(ctypes.byref(cfg), device, tp_rank,
+                                                         group._h, ctypes.byref(h)),
+                       "cs_engine_create_tp_local")
+        else:
+            uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+            _lib.check(self._L.cs_engine_create(ctypes.byref(cfg), device, tp_rank, tp_size, uid,
+                                                ctypes.byref(h)), "cs_engine_create")
+        self._h = h
+        # this rank's shard sizes (SURVEY.md §8e)
+        self.ffn_local = cfg.ffn // self.tp_size
+        self.kv_dim_local = cfg.n_kv_heads // self.tp_size * cfg.head_dim
 
     def close(self):
         if getattr(self, "_h", None):
@@ -315,28 +381,29 @@ class Engine:
 
     # -------------------------------------------------------------- read-back
     def lora_grads(self, layer: int):
+        """(dA, dB) of this rank: dA rows = its ffn shard; dB = its partial sum (TP)."""
         c = self.cfg
-        a = np.zeros((c.ffn, c.lora_rank))
+        a = np.zeros((self.ffn_local, c.lora_rank))
         b = np.zeros((c.lora_rank, c.hidden))
         _lib.check(self._L.cs_read_lora_grads(self._h, layer, a.ctypes.data, b.ctypes.data), "read_lora_grads")
         return a, b
 
     def lora(self, layer: int):
         c = self.cfg
-        a = np.zeros((c.ffn, c.lora_rank))
+        a = np.zeros((self.ffn_local, c.lora_rank))
         b = np.zeros((c.lora_rank, c.hidden))
         _lib.check(self._L.cs_engine_get_lora(self._h, layer, a.ctypes.data, b.ctypes.data), "get_lora")
         return a, b
 
     def kvgrad(self, L: int):
-        kv = self.cfg.n_kv_heads * self.cfg.head_dim
+        kv = self.kv_dim_local
         dk = np.zeros((L, kv))
         dv = np.zeros((L, kv))
         _lib.check(self._L.cs_read_kvgrad(self._h, L, dk.ctypes.data, dv.ctypes.data), "read_kvgrad")
         return dk, dv
 
     def read_kv(self, layer: int, pages: Sequence[int], length: int):
-        kv = self.cfg.n_kv_heads * self.cfg.head_dim
+        kv = self.kv_dim_local
         pg = np.ascontiguousarray(pages, dtype=np.int32)
         k = np.zeros((length, kv))
         v = np.zeros((length, kv))

@@ -253,3 +253,50 @@ def test_d128_tcgen05_attention_parity(tc, monkeypatch):
     assert O.scaled_err(dk, bw["layers"][1]["dk"]) < FLOOR_DEEP
     assert O.scaled_err(dv, bw["layers"][1]["dv"]) < FLOOR_DEEP
     assert O.scaled_err(dys[1], bw["layers"][1]["dx"]) < FLOOR_DEEP
+
+
+ARCH_GQA4 = O.Arch(n_layers=2, hidden=512, n_heads=4, n_kv_heads=1, head_dim=128, ffn=512,
+                   vocab=128, lora_rank=8, norm="rms", act="swiglu", rope=True, qkv_bias=False,
+                   rope_theta=10000.0)
+
+
+@pytest.mark.parametrize("dec", ["1", "0"])
+def test_decode_attention_kernel_parity(dec, monkeypatch):
+    """Decode rows (q_len * group <= 16) on the HBM-bound paged decode kernel (CS_ATTN_DEC=1)
+    or the mma.sync tile kernel (0), LLaMA-8B head geometry (group 4, d=128): contexts from 1
+    to 700 keys (split across CTAs and merged by LSE), ragged pages, multi-row (q_len 3)
+    segments, all against the oracle's window forward."""
+    monkeypatch.setenv("CS_ATTN_DEC", dec)
+    arch = ARCH_GQA4
+    W = O.init_general(arch, 11)
+    P = 16
+    eng = Engine(arch_config(arch, page_size=P, n_pages=512, max_tokens=2048, max_ft_len=16,
+                             max_segments=64))
+    eng.load_weights(W)
+    rng = np.random.default_rng(3)
+    pages = Pages(512)
+    reqs = []
+    for plen in (1, 3, 5, 37, 300, 700, 129):
+        toks = [int(t) for t in rng.integers(0, arch.vocab, plen)]
+        pg = pages.take((plen + 8 + P - 1) // P)
+        pg = pg[::-1]  # non-monotone page ids
+        reqs.append({"tokens": toks, "pages": pg, "cache": O.QkvCache(arch, plen + 8), "len": 0})
+    out = eng.step([Seg(SEG_PREFILL, r["tokens"], 0, r["pages"], sample=True) for r in reqs],
+                   want_logits=True)
+    diffs = []
+    for i, r in enumerate(reqs):
+        lg, _ = O.forward_window(arch, W, r["tokens"], 0, r["cache"], lora=False)
+        r["len"] = len(r["tokens"])
+        diffs.append(O.scaled_err(out["logits"][i], lg[-1]))
+    for _ in range(3):
+        segs = []
+        for r in reqs:
+            r["pending"] = int(rng.integers(0, arch.vocab))
+            segs.append(Seg(SEG_DECODE, [r["pending"]], r["len"], r["pages"], sample=True))
+        out = eng.step(segs, want_logits=True)
+        for i, r in enumerate(reqs):
+            lg, _ = O.forward_window(arch, W, [r["pending"]], r["len"], r["cache"], lora=False)
+            r["len"] += 1
+            diffs.append(O.scaled_err(out["logits"][i], lg[-1]))
+    assert max(diffs) < 0.04, max(diffs)
+    eng.close()
