@@ -178,6 +178,13 @@ int cs_read_kv(cs_engine* e, int layer, const int32_t* pages, int32_t len, doubl
 /* dLoss/d(input of layer) rows [0, L) produced by the last backward windows. */
 int cs_read_dy(cs_engine* e, int32_t L, double* out);
 
+/* Allocation audit (Matrix::alloc_hook, matrix.hpp:16-25): hook(name, elements, elem_bytes)
+ * once per device buffer of the engine's arena (everything is carved at create time: steps
+ * allocate nothing); transient_allocs = device allocations made outside the arena so far
+ * (weight-upload staging only). */
+typedef void (*cs_alloc_hook)(const char* name, int64_t elems, int32_t elem_bytes, void* user);
+int cs_engine_alloc_audit(cs_engine* e, cs_alloc_hook hook, void* user, int64_t* transient_allocs);
+
 /* ---------------------------------------------------------------- host scheduler (no GPU) */
 typedef struct cs_latency_profile {
   double t0_ms;

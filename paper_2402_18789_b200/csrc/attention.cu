@@ -231,35 +231,47 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnFwdParams p) {
 }
 
 // Merge split-KV partials: o = sum_s o_s * exp(lse_s - lse), lse = log sum_s exp(lse_s).
+// One warp per packed row (lanes over d, 4 columns each); the part LSEs are warp-broadcast
+// loads, independent across parts.
 template <int D>
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   const AttnCombine c = p.combine[blockIdx.x];
   const AttnSeg sg = p.segs[c.seg];
   const int grp = p.grp;
-  for (int idx = threadIdx.x; idx < 64 * D; idx += blockDim.x) {
-    const int r = idx / D, d = idx % D;
-    const int qr = r / grp, g = r % grp;
-    if (qr >= c.nq) continue;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = lane * 4;
+  for (int r = warp; r < c.nq * grp; r += 4) {
     float mx = -INFINITY;
-    for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, p.part_lse[(long)(c.part0 + s) * 64 + r]);
-    float den = 0.f, acc = 0.f;
+    for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, __ldg(p.part_lse + (long)(c.part0 + s) * 64 + r));
+    float den = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (mx > -INFINITY) {
       for (int s = 0; s < c.n_parts; ++s) {
         const long pr = (long)(c.part0 + s) * 64 + r;
-        const float wgt = __expf(p.part_lse[pr] - mx);
+        const float wgt = __expf(__ldg(p.part_lse + pr) - mx);
         den += wgt;
-        acc += wgt * p.part_o[pr * D + d];
+        if (d < D) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(p.part_o + pr * D + d));
+          acc.x += wgt * v.x;
+          acc.y += wgt * v.y;
+          acc.z += wgt * v.z;
+          acc.w += wgt * v.w;
+        }
       }
     }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const int qr = r / grp, g = r - qr * grp;
     const long row = sg.q_start + c.q0 + qr;
     const int qh = c.kv_head * grp + g;
-    p.out[row * p.out_ld + (long)qh * D + d] = __float2bfloat16(den > 0.f ? acc / den : 0.f);
-    if (d == 0 && p.lse) p.lse[row * p.lse_ld + qh] = den > 0.f ? mx + __logf(den) : -INFINITY;
+    if (d < D) {
+      bf16* dst = p.out + row * p.out_ld + (long)qh * D + d;
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc.x * inv, acc.y * inv);
+      *reinterpret_cast<uint32_t*>(dst + 2) = pack_bf16(acc.z * inv, acc.w * inv);
+    }
+    if (lane == 0 && p.lse) p.lse[row * p.lse_ld + qh] = den > 0.f ? mx + __logf(den) : -INFINITY;
   }
 }
 
-// ============================================================================ backward
-// Delta_i = rowsum(dO_i * O_i) per (window row, head)
 __global__ void attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ dO, long do_ld,
                                       const __nv_bfloat16* __restrict__ O, long o_ld, int rows,
                                       int heads, int D, float* __restrict__ delta) {

@@ -110,16 +110,16 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, long ldx, const int*
 }
 void rmsnorm_cast(const float* x, long ldx, const float* g, bf16* out, long ldo, float* rstd_out,
                   int rows, int h, float eps, int use_norm, cudaStream_t st) {
-  if (rows > 0)
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
+  if (rows <= 0) return;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 void rmsnorm_cast_gather(const float* x, long ldx, const int* idx, const float* g, bf16* out,
                          long ldo, float* rstd_out, int rows, int h, float eps, int use_norm,
                          cudaStream_t st) {
-  if (rows > 0)
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
+  if (rows <= 0) return;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 
 // ---------------------------------------------------------------- RoPE + KV append
@@ -139,32 +139,38 @@ __global__ void rope_append_kernel(RopeAppendParams p, const float2* __restrict_
   const bool ft = row >= p.ft_row0 && p.q_cache;
   bf16* qc = ft ? p.q_cache + (long)pos * q_dim : nullptr;
   const float2* tab = cs_tab + (long)pos * half;
-  // q heads (in place) and k heads (to the page), pairs (i, i + d/2)
-  const int nq_pairs = p.n_heads * half, nk_pairs = p.n_kv_heads * half;
-  for (int t = threadIdx.x; t < nq_pairs + nk_pairs; t += blockDim.x) {
-    const bool isq = t < nq_pairs;
-    const int tt = isq ? t : t - nq_pairs;
-    const int hd = tt / half, i = tt % half;
+  // q heads (in place) and k heads (to the page): 8 rotate-half pairs (i, i + d/2) per thread,
+  // 16-byte loads/stores of both halves
+  const int cpr = half / 8;  // 8-pair chunks per head
+  const int nq = p.n_heads * cpr, nk = p.n_kv_heads * cpr;
+  for (int t = threadIdx.x; t < nq + nk; t += blockDim.x) {
+    const bool isq = t < nq;
+    const int tt = isq ? t : t - nq;
+    const int hd = tt / cpr, i0 = (tt % cpr) * 8;
     bf16* src = (isq ? q : k) + hd * d;
-    float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + half]);
+    uint4 a = *reinterpret_cast<const uint4*>(src + i0);
+    uint4 b = *reinterpret_cast<const uint4*>(src + i0 + half);
     if (p.use_rope) {
-      const float2 cs = tab[i];
-      const float y1 = x1 * cs.x - x2 * cs.y;
-      const float y2 = x2 * cs.x + x1 * cs.y;
-      x1 = y1;
-      x2 = y2;
+      bf16* xa = reinterpret_cast<bf16*>(&a);
+      bf16* xb = reinterpret_cast<bf16*>(&b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 cs = tab[i0 + j];
+        const float x1 = __bfloat162float(xa[j]), x2 = __bfloat162float(xb[j]);
+        xa[j] = __float2bfloat16(x1 * cs.x - x2 * cs.y);
+        xb[j] = __float2bfloat16(x2 * cs.x + x1 * cs.y);
+      }
     }
-    const bf16 b1 = __float2bfloat16(x1), b2 = __float2bfloat16(x2);
     if (isq) {
-      src[i] = b1;
-      src[i + half] = b2;
+      *reinterpret_cast<uint4*>(src + i0) = a;
+      *reinterpret_cast<uint4*>(src + i0 + half) = b;
       if (qc) {
-        qc[hd * d + i] = b1;
-        qc[hd * d + i + half] = b2;
+        *reinterpret_cast<uint4*>(qc + hd * d + i0) = a;
+        *reinterpret_cast<uint4*>(qc + hd * d + i0 + half) = b;
       }
     } else {
-      kd[hd * d + i] = b1;
-      kd[hd * d + i + half] = b2;
+      *reinterpret_cast<uint4*>(kd + hd * d + i0) = a;
+      *reinterpret_cast<uint4*>(kd + hd * d + i0 + half) = b;
     }
   }
   for (int c = threadIdx.x * 8; c < kv_dim; c += blockDim.x * 8)
@@ -229,73 +235,132 @@ void lora_pack(const float* lu, int r, bf16* m, long ldm, int f, int rows, cudaS
 }
 
 // ---------------------------------------------------------------- sampling / CE
-__global__ void argmax_kernel(const float* __restrict__ logits, long ld, int V, int* out) {
-  __shared__ float sv[32];
-  __shared__ int si[32];
+// greedy sampling: stage 1 = (row, chunk) blocks with float4 loads, each the max of an
+// order-preserving key (value bits << 32 | ~index: ties -> smallest index); stage 2 = one
+// warp per row over the chunk keys.  Deterministic, no atomics.
+constexpr int AMAX_CHUNKS = 16;
+CS_DEV unsigned long long amax_key(float v, int i) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)o << 32) | (uint32_t)(0xFFFFFFFFu - (uint32_t)i);
+}
+__global__ void __launch_bounds__(256) argmax_part_kernel(const float* __restrict__ logits, long ld,
+                                                          int V, unsigned long long* __restrict__ part) {
+  __shared__ unsigned long long red[8];
   const float* row = logits + (long)blockIdx.x * ld;
-  float best = -INFINITY;
-  int bi = 0;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    const float v = row[c];
-    if (v > best) {
-      best = v;
-      bi = c;
+  const int per = ((V + AMAX_CHUNKS - 1) / AMAX_CHUNKS + 3) & ~3;
+  const int c0 = blockIdx.y * per, c1 = min(V, c0 + per);
+  unsigned long long best = 0;
+  const bool vec = (ld % 4) == 0;
+  for (int c = c0 + threadIdx.x * 4; c < c1; c += blockDim.x * 4) {
+    if (vec && c + 3 < c1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(row + c));
+      best = max(best, amax_key(v.x, c));
+      best = max(best, amax_key(v.y, c + 1));
+      best = max(best, amax_key(v.z, c + 2));
+      best = max(best, amax_key(v.w, c + 3));
+    } else {
+      for (int k = c; k < min(c + 4, c1); ++k) best = max(best, amax_key(row[k], k));
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) {
-      best = ov;
-      bi = oi;
-    }
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    sv[w] = best;
-    si[w] = bi;
-  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
-      if (sv[i] > best || (sv[i] == best && si[i] < bi)) {
-        best = sv[i];
-        bi = si[i];
-      }
-    out[blockIdx.x] = bi;
+    for (int i = 1; i < 8; ++i) best = max(best, red[i]);
+    part[(long)blockIdx.x * AMAX_CHUNKS + blockIdx.y] = best;
   }
 }
-void argmax_rows(const float* logits, long ld, int rows, int V, int* out, cudaStream_t st) {
-  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (rows > 0) argmax_kernel<<<rows, 512, 0, st>>>(logits, ld, V, out);
+__global__ void argmax_final_kernel(const unsigned long long* __restrict__ part, int rows, int* out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  unsigned long long k = lane < AMAX_CHUNKS ? part[(long)row * AMAX_CHUNKS + lane] : 0ull;
+  for (int o = 16; o > 0; o >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, o));
+  if (lane == 0) out[row] = (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+void argmax_rows(const float* logits, long ld, int rows, int V, int* out,
+                 unsigned long long* scratch, cudaStream_t st) {
+  if (rows <= 0) return;
+  cs::g_launches.fetch_add(2, std::memory_order_relaxed);
+  argmax_part_kernel<<<dim3(rows, AMAX_CHUNKS), 256, 0, st>>>(logits, ld, V, scratch);
+  argmax_final_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(scratch, rows, out);
 }
 
-__global__ void ce_kernel(const float* __restrict__ logits, long ld, const int* __restrict__ tg,
-                          int V, float inv_norm, float* __restrict__ loss,
-                          bf16* __restrict__ dlog, long ldd) {
-  __shared__ float red[32];
+__global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, long ld,
+                                                 const int* __restrict__ tg, int V, float inv_norm,
+                                                 float* __restrict__ loss, bf16* __restrict__ dlog,
+                                                 long ldd) {
+  __shared__ float red_m[16], red_s[16];
   const int row = blockIdx.x;
   const float* x = logits + (long)row * ld;
   bf16* dx = dlog + (long)row * ldd;
   const int t = tg[row];
+  const int V4 = V & ~3;
   if (t < 0) {
-    for (int c = threadIdx.x; c < V; c += blockDim.x) dx[c] = __float2bfloat16(0.f);
+    for (int c = threadIdx.x * 4; c < V4; c += blockDim.x * 4)
+      *reinterpret_cast<uint2*>(dx + c) = make_uint2(0u, 0u);
+    for (int c = V4 + threadIdx.x; c < V; c += blockDim.x) dx[c] = __float2bfloat16(0.f);
     if (threadIdx.x == 0) loss[row] = 0.f;
     return;
   }
-  float mx = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, x[c]);
-  mx = block_max(mx, red);
-  float se = 0.f;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) se += __expf(x[c] - mx);
-  se = block_sum(se, red);
-  const float inv = 1.f / se;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    float g = __expf(x[c] - mx) * inv;
+  // pass 1: per-thread online (max, sum exp) over float4 slices, then a block merge
+  float m = -INFINITY, se = 0.f;
+  auto add = [&](float v) {
+    if (v > m) {
+      se = se * __expf(m - v) + 1.f;
+      m = v;
+    } else {
+      se += __expf(v - m);
+    }
+  };
+  for (int c = threadIdx.x * 4; c < V4; c += blockDim.x * 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + c));
+    const float mv = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+    if (mv > m) {
+      se *= __expf(m - mv);
+      m = mv;
+    }
+    se += __expf(v.x - m) + __expf(v.y - m) + __expf(v.z - m) + __expf(v.w - m);
+  }
+  for (int c = V4 + threadIdx.x; c < V; c += blockDim.x) add(x[c]);
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, se, o);
+    const float nm = fmaxf(m, om);
+    se = (m == -INFINITY ? 0.f : se * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red_m[w] = m;
+    red_s[w] = se;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) M = fmaxf(M, red_m[i]);
+  float S = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
+    S += red_m[i] == -INFINITY ? 0.f : red_s[i] * __expf(red_m[i] - M);
+  // pass 2: dlogits = (softmax - onehot) / (L-1) in bf16
+  const float inv = 1.f / S;
+  for (int c = threadIdx.x * 4; c < V4; c += blockDim.x * 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + c));
+    float g0 = __expf(v.x - M) * inv, g1 = __expf(v.y - M) * inv;
+    float g2 = __expf(v.z - M) * inv, g3 = __expf(v.w - M) * inv;
+    if (t >= c && t < c + 4) {
+      if (t == c) g0 -= 1.f;
+      if (t == c + 1) g1 -= 1.f;
+      if (t == c + 2) g2 -= 1.f;
+      if (t == c + 3) g3 -= 1.f;
+    }
+    *reinterpret_cast<uint2*>(dx + c) =
+        make_uint2(pack_bf16(g0 * inv_norm, g1 * inv_norm), pack_bf16(g2 * inv_norm, g3 * inv_norm));
+  }
+  for (int c = V4 + threadIdx.x; c < V; c += blockDim.x) {
+    float g = __expf(x[c] - M) * inv;
     if (c == t) g -= 1.f;
     dx[c] = __float2bfloat16(g * inv_norm);
   }
-  if (threadIdx.x == 0) loss[row] = (mx + __logf(se)) - x[t];
+  if (threadIdx.x == 0) loss[row] = (M + __logf(S)) - x[t];
 }
 void ce_fwd_bwd(const float* logits, long ld, const int* targets, int rows, int V,
                 float inv_norm, float* loss, bf16* dlogits, long ldd, cudaStream_t st) {
@@ -337,128 +402,147 @@ __global__ void rms_bwd_kernel(const float* __restrict__ resid, long ldr,
 void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const float* g,
                  const float* rstd, const float* dh, long ldh, float* out, long ldo,
                  bf16* out_b, long ldob, int rows, int h, int use_norm, cudaStream_t st) {
-  if (rows > 0)
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    rms_bwd_kernel<<<rows, 256, 0, st>>>(resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
-                                         ldob, h, use_norm);
+  if (rows <= 0) return;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  rms_bwd_kernel<<<rows, 256, 0, st>>>(resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
+                                       ldob, h, use_norm);
 }
 
 // MLP backward fused with the LoRA-A gradient:
 //   swiglu: g=saved[:, :f], u=saved[:, f:]; dgu = [dm*u*dsilu(g), dm*silu(g)]; m = silu(g)*u
 //   relu  : m=saved;  dgu = dm * (m > 0)            (tiny_model.hpp:285-286)
 //   dA[col, :] += sum_rows m[row, col] * dlu[row, :] (tiny_model.hpp:282)
-constexpr int MLP_ROWS = 64;
+// Thread = 2 adjacent columns (vector loads/stores), block = 512 columns x 256 rows: the dA
+// partial sums of a block go out as one fp32 atomic per (column, j).
+constexpr int MLP_ROWS = 256;
 __global__ void __launch_bounds__(256) mlp_bwd_kernel(const float* __restrict__ dm, long ld_dm,
                                                       const bf16* __restrict__ saved, long ld_s,
                                                       const float* __restrict__ dlu, int r,
                                                       bf16* __restrict__ dgu, long ld_dgu,
                                                       float* __restrict__ dA, int rows, int f,
                                                       int swiglu) {
-  __shared__ float sl[MLP_ROWS * 16];
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ __align__(16) float sl[MLP_ROWS * 16];
+  const int col = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int r0 = blockIdx.y * MLP_ROWS;
   const int nr = min(MLP_ROWS, rows - r0);
-  for (int i = threadIdx.x; i < nr * r; i += blockDim.x)
-    sl[(i / r) * 16 + (i % r)] = dlu[(long)(r0 + i / r) * r + (i % r)];
+  for (int i = threadIdx.x; i < nr * 16; i += blockDim.x) {
+    const int rr = i >> 4, j = i & 15;
+    sl[i] = j < r ? dlu[(long)(r0 + rr) * r + j] : 0.f;
+  }
   __syncthreads();
   if (col >= f) return;
-  float acc[16];
+  float acc0[16], acc1[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  for (int j = 0; j < 16; ++j) acc0[j] = acc1[j] = 0.f;
   for (int i = 0; i < nr; ++i) {
     const long row = r0 + i;
-    const float d = dm[row * ld_dm + col];
-    float mval;
+    const float2 d = *reinterpret_cast<const float2*>(dm + row * ld_dm + col);
+    float m0, m1;
     if (swiglu) {
-      const float g = __bfloat162float(saved[row * ld_s + col]);
-      const float u = __bfloat162float(saved[row * ld_s + f + col]);
-      const float sg = silu_f(g);
-      mval = sg * u;
-      dgu[row * ld_dgu + col] = __float2bfloat16(d * u * dsilu_f(g));
-      dgu[row * ld_dgu + f + col] = __float2bfloat16(d * sg);
+      const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(saved + row * ld_s + col);
+      const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(saved + row * ld_s + f + col);
+      const float g0 = __low2float(g2), g1 = __high2float(g2);
+      const float u0 = __low2float(u2), u1 = __high2float(u2);
+      const float s0 = silu_f(g0), s1 = silu_f(g1);
+      m0 = s0 * u0;
+      m1 = s1 * u1;
+      *reinterpret_cast<uint32_t*>(dgu + row * ld_dgu + col) =
+          pack_bf16(d.x * u0 * dsilu_f(g0), d.y * u1 * dsilu_f(g1));
+      *reinterpret_cast<uint32_t*>(dgu + row * ld_dgu + f + col) = pack_bf16(d.x * s0, d.y * s1);
     } else {
-      mval = fmaxf(__bfloat162float(saved[row * ld_s + col]), 0.f);  // saved = up
-      dgu[row * ld_dgu + col] = __float2bfloat16(mval > 0.f ? d : 0.f);
+      const __nv_bfloat162 up = *reinterpret_cast<const __nv_bfloat162*>(saved + row * ld_s + col);
+      m0 = fmaxf(__low2float(up), 0.f);
+      m1 = fmaxf(__high2float(up), 0.f);
+      *reinterpret_cast<uint32_t*>(dgu + row * ld_dgu + col) =
+          pack_bf16(m0 > 0.f ? d.x : 0.f, m1 > 0.f ? d.y : 0.f);
     }
+    const float4* l4 = reinterpret_cast<const float4*>(sl + i * 16);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < r) acc[j] += mval * sl[i * 16 + j];
+    for (int q = 0; q < 4; ++q) {
+      const float4 l = l4[q];
+      acc0[4 * q] += m0 * l.x;
+      acc0[4 * q + 1] += m0 * l.y;
+      acc0[4 * q + 2] += m0 * l.z;
+      acc0[4 * q + 3] += m0 * l.w;
+      acc1[4 * q] += m1 * l.x;
+      acc1[4 * q + 1] += m1 * l.y;
+      acc1[4 * q + 2] += m1 * l.z;
+      acc1[4 * q + 3] += m1 * l.w;
+    }
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    if (j < r) atomicAdd(dA + (long)col * r + j, acc[j]);
+    if (j < r) {
+      atomicAdd(dA + (long)col * r + j, acc0[j]);
+      atomicAdd(dA + (long)(col + 1) * r + j, acc1[j]);
+    }
 }
 void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st) {
   if (rows <= 0) return;
-  dim3 grid((f + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  dim3 grid((f / 2 + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   mlp_bwd_kernel<<<grid, 256, 0, st>>>(dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
                                        swiglu);
 }
 
-// per row: dlu[j] = dY . B[j] ; dycat = [bf16(dY) | bf16(dlu) | 0]  (tiny_model.hpp:281)
-__global__ void lora_dlu_kernel(const float* __restrict__ dY, long ldy, const float* __restrict__ B,
-                                int r, int h, int rows, float* __restrict__ dlu,
-                                bf16* __restrict__ dycat, long ldc) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const long row = warp;
+// dycat = [bf16(dY) | 0 (LoRA columns, filled by lora_pack after the dlu GEMM)]
+__global__ void dycat_cast_kernel(const float* __restrict__ dY, long ldy, int h,
+                                  bf16* __restrict__ dycat, long ldc) {
+  const long row = blockIdx.x;
   const float* y = dY + row * ldy;
   bf16* o = dycat + row * ldc;
-  float acc[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-  for (int c = lane; c < h; c += 32) {
-    const float v = y[c];
-    o[c] = __float2bfloat16(v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < r) acc[j] += v * B[(long)j * h + c];
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = warp_sum(acc[j]);
-  for (int c = lane; c < (int)(ldc - h); c += 32) {
-    float v = 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j == c && j < r) v = acc[j];
-    o[h + c] = __float2bfloat16(v);
-    if (c < r) dlu[row * r + c] = v;
+  for (int c = threadIdx.x * 4; c < ldc; c += blockDim.x * 4) {
+    uint2 p = make_uint2(0u, 0u);
+    if (c < h) {
+      const float4 v = *reinterpret_cast<const float4*>(y + c);
+      p = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    }
+    *reinterpret_cast<uint2*>(o + c) = p;
   }
 }
-// dB[j, c] += sum_rows lu[row, j] * dY[row, c]  (tiny_model.hpp:280)
+// dB[j, c] += sum_rows lu[row, j] * dY[row, c]  (tiny_model.hpp:280); 4 columns per thread,
+// 256 rows per block
 __global__ void __launch_bounds__(256) lora_db_kernel(const float* __restrict__ dY, long ldy,
                                                       const float* __restrict__ lu, int r,
                                                       int rows, int h, float* __restrict__ dB) {
-  __shared__ float sl[MLP_ROWS * 16];
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ __align__(16) float sl[MLP_ROWS * 16];
+  const int col = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int r0 = blockIdx.y * MLP_ROWS;
   const int nr = min(MLP_ROWS, rows - r0);
-  for (int i = threadIdx.x; i < nr * r; i += blockDim.x)
-    sl[(i / r) * 16 + (i % r)] = lu[(long)(r0 + i / r) * r + (i % r)];
+  for (int i = threadIdx.x; i < nr * 16; i += blockDim.x) {
+    const int rr = i >> 4, j = i & 15;
+    sl[i] = j < r ? lu[(long)(r0 + rr) * r + j] : 0.f;
+  }
   __syncthreads();
   if (col >= h) return;
-  float acc[16];
+  float4 acc[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  for (int j = 0; j < 16; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = 0; i < nr; ++i) {
-    const float v = dY[(long)(r0 + i) * ldy + col];
+    const float4 v = *reinterpret_cast<const float4*>(dY + (long)(r0 + i) * ldy + col);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < r) acc[j] += sl[i * 16 + j] * v;
+    for (int j = 0; j < 16; ++j) {
+      const float l = sl[i * 16 + j];
+      acc[j].x += l * v.x;
+      acc[j].y += l * v.y;
+      acc[j].z += l * v.z;
+      acc[j].w += l * v.w;
+    }
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    if (j < r) atomicAdd(dB + (long)j * h + col, acc[j]);
+    if (j < r) atomicAdd(reinterpret_cast<float4*>(dB + (long)j * h + col), acc[j]);
 }
-void lora_bwd_b(const float* dY, long ldy, const float* lu, const float* B, int r, int rows,
-                int h, float* dlu, bf16* dycat, long ldc, float* dB, cudaStream_t st) {
+void dycat_cast(const float* dY, long ldy, int rows, int h, bf16* dycat, long ldc, cudaStream_t st) {
   if (rows <= 0) return;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  lora_dlu_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(dY, ldy, B, r, h, rows, dlu, dycat, ldc);
-  dim3 grid((h + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  dycat_cast_kernel<<<rows, 128, 0, st>>>(dY, ldy, h, dycat, ldc);
+}
+void lora_db(const float* dY, long ldy, const float* lu, int r, int rows, int h, float* dB,
+             cudaStream_t st) {
+  if (rows <= 0) return;
+  dim3 grid((h / 4 + 255) / 256, (rows + MLP_ROWS - 1) / MLP_ROWS);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   lora_db_kernel<<<grid, 256, 0, st>>>(dY, ldy, lu, r, rows, h, dB);
 }
@@ -537,6 +621,7 @@ __global__ void adam_kernel(AdamParams p, int update) {
       const long rem = i % ((long)p.r * p.h);
       const int j = (int)(rem / p.h), c = (int)(rem % p.h);
       p.down_cat[(l * p.h + c) * (p.f + 64) + p.f + j] = wb;
+      p.B_t[(l * 16 + j) * p.h + c] = wb;  // [n_layers][16][h]
     }
   }
 }

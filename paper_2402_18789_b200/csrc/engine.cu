@@ -54,13 +54,21 @@ struct cs_engine {
   bool swiglu, norm, rope;
   bool use_tc_attn = true;  // CS_ATTN_TC=0 forces the mma.sync path (A/B testing)
   bool use_dec_attn = true;  // CS_ATTN_DEC=0 sends decode rows to the mma.sync tile kernel
-  // arena
+  bool use_fwd2 = true;      // CS_ATTN_FWD2=0 runs the one-query-tile tcgen05 kernel (v1)
+  // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
+  struct AuditRec {
+    const char* name;
+    long elems;
+    int elem_bytes;
+  };
+  std::vector<AuditRec> audit;
+  long transient_allocs = 0;  // device allocations outside the arena (weight upload staging)
   uint8_t* arena = nullptr;
   size_t arena_bytes = 0, arena_used = 0;
   // weights
   bf16 *embed, *unembed_t, *unembed;
   float* gf;
-  bf16 *wqkv_t, *wqkv, *wo_t, *wo, *wgu_t, *wgu, *down_cat, *dbwd_cat, *A_t;
+  bf16 *wqkv_t, *wqkv, *wo_t, *wo, *wgu_t, *wgu, *down_cat, *dbwd_cat, *A_t, *B_t;
   float *bqkv, *g1, *g2;
   float *loraA, *loraB, *gA, *gB, *mA, *vA, *mB, *vB;
   // KV
@@ -77,6 +85,7 @@ struct cs_engine {
   bf16* dlog;
   float* samp_logits;
   int* next_tok;
+  unsigned long long* amax_part;
   float *part_o, *part_lse;
   // backward scratch
   bf16 *dycat, *dgu, *dr1b, *dO, *dqkv;
@@ -165,89 +174,97 @@ struct Planner {
 
 void layout(cs_engine* e, bool measure, size_t* total) {
   Planner pl;
-  auto A = [&](auto** ptr, size_t count) {
+  auto A = [&](auto** ptr, size_t count, const char* name) {
     using T = std::remove_pointer_t<std::remove_reference_t<decltype(*ptr)>>;
-    if (measure) pl.add<T>(count);
-    else *ptr = carve<T>(e, count);
+    if (measure) {
+      pl.add<T>(count);
+    } else {
+      *ptr = carve<T>(e, count);
+      e->audit.push_back({name, (long)count, (int)sizeof(T)});
+    }
   };
+#define AL(field, count) A(&e->field, (count), #field)
   const size_t NL = e->NL, h = e->h, V = e->V, f = e->f, r = e->r;
   const size_t T = e->T_max, Lm = e->L_max, S = e->S_max;
-  A(&e->embed, V * h);
-  A(&e->unembed_t, V * h);
-  A(&e->unembed, h * V);
-  A(&e->gf, h);
-  A(&e->wqkv_t, NL * e->nqkv * h);
-  A(&e->wqkv, NL * h * e->nqkv);
-  A(&e->wo_t, NL * h * e->q_dim);
-  A(&e->wo, NL * e->q_dim * h);
-  A(&e->wgu_t, NL * e->gu_n * h);
-  A(&e->wgu, NL * h * e->gu_n);
-  A(&e->down_cat, NL * h * e->f_cat);
-  A(&e->dbwd_cat, NL * f * e->h_cat);
-  A(&e->A_t, NL * 16 * f);
-  A(&e->bqkv, NL * e->nqkv);
-  A(&e->g1, NL * h);
-  A(&e->g2, NL * h);
-  A(&e->loraA, NL * f * r);
-  A(&e->loraB, NL * r * h);
-  A(&e->gA, NL * f * r);
-  A(&e->gB, NL * r * h);
-  A(&e->mA, NL * f * r);
-  A(&e->vA, NL * f * r);
-  A(&e->mB, NL * r * h);
-  A(&e->vB, NL * r * h);
+  AL(embed, V * h);
+  AL(unembed_t, V * h);
+  AL(unembed, h * V);
+  AL(gf, h);
+  AL(wqkv_t, NL * e->nqkv * h);
+  AL(wqkv, NL * h * e->nqkv);
+  AL(wo_t, NL * h * e->q_dim);
+  AL(wo, NL * e->q_dim * h);
+  AL(wgu_t, NL * e->gu_n * h);
+  AL(wgu, NL * h * e->gu_n);
+  AL(down_cat, NL * h * e->f_cat);
+  AL(dbwd_cat, NL * f * e->h_cat);
+  AL(A_t, NL * 16 * f);
+  AL(B_t, NL * 16 * h);
+  AL(bqkv, NL * e->nqkv);
+  AL(g1, NL * h);
+  AL(g2, NL * h);
+  AL(loraA, NL * f * r);
+  AL(loraB, NL * r * h);
+  AL(gA, NL * f * r);
+  AL(gB, NL * r * h);
+  AL(mA, NL * f * r);
+  AL(vA, NL * f * r);
+  AL(mB, NL * r * h);
+  AL(vB, NL * r * h);
   const size_t kv = NL * (size_t)e->npages * e->P * e->kv_dim;
-  A(&e->k_pool, kv);
-  A(&e->v_pool, kv);
-  A(&e->ft_q, NL * Lm * e->q_dim);
-  A(&e->ft_o, NL * Lm * e->q_dim);
-  A(&e->ft_gu, NL * Lm * e->gu_n);
-  A(&e->ft_lse, NL * Lm * e->Hq);
-  A(&e->ft_x, e->norm ? NL * Lm * h : 1);
-  A(&e->ft_r1, e->norm ? NL * Lm * h : 1);
-  A(&e->ft_rstd1, NL * Lm);
-  A(&e->ft_rstd2, NL * Lm);
-  A(&e->ft_lu, NL * Lm * r);
-  A(&e->dk_acc, Lm * e->kv_dim);
-  A(&e->dv_acc, Lm * e->kv_dim);
-  A(&e->dy[0], Lm * h);
-  A(&e->dy[1], Lm * h);
-  A(&e->x, T * h);
-  A(&e->rstd, T);
-  A(&e->lu, T * r);
-  A(&e->lse, T * e->Hq);
-  A(&e->xb, T * h);
-  A(&e->qkv, T * e->nqkv);
-  A(&e->attn, T * e->q_dim);
-  A(&e->gu, T * e->gu_n);
-  A(&e->m, T * e->f_cat);
+  AL(k_pool, kv);
+  AL(v_pool, kv);
+  AL(ft_q, NL * Lm * e->q_dim);
+  AL(ft_o, NL * Lm * e->q_dim);
+  AL(ft_gu, NL * Lm * e->gu_n);
+  AL(ft_lse, NL * Lm * e->Hq);
+  AL(ft_x, e->norm ? NL * Lm * h : 1);
+  AL(ft_r1, e->norm ? NL * Lm * h : 1);
+  AL(ft_rstd1, NL * Lm);
+  AL(ft_rstd2, NL * Lm);
+  AL(ft_lu, NL * Lm * r);
+  AL(dk_acc, Lm * e->kv_dim);
+  AL(dv_acc, Lm * e->kv_dim);
+  AL(dy[0], Lm * h);
+  AL(dy[1], Lm * h);
+  AL(x, T * h);
+  AL(rstd, T);
+  AL(lu, T * r);
+  AL(lse, T * e->Hq);
+  AL(xb, T * h);
+  AL(qkv, T * e->nqkv);
+  AL(attn, T * e->q_dim);
+  AL(gu, T * e->gu_n);
+  AL(m, T * e->f_cat);
   const size_t C = e->head_chunk;
-  A(&e->hf, std::max(C, (size_t)e->max_seg) * h);
-  A(&e->logits, std::max(C, (size_t)e->max_seg) * V);
-  A(&e->dlog, C * V);
-  A(&e->dh, C * h);
-  A(&e->hrstd, C);
-  A(&e->loss_rows, Lm);
-  A(&e->samp_logits, (size_t)e->max_seg * V);
-  A(&e->next_tok, e->max_seg);
+  AL(hf, std::max(C, (size_t)e->max_seg) * h);
+  AL(logits, std::max(C, (size_t)e->max_seg) * V);
+  AL(dlog, C * V);
+  AL(dh, C * h);
+  AL(hrstd, C);
+  AL(loss_rows, Lm);
+  AL(samp_logits, (size_t)e->max_seg * V);
+  AL(next_tok, e->max_seg);
+  AL(amax_part, (size_t)e->max_seg * 16);
   const size_t max_parts = 4096;
-  A(&e->part_o, max_parts * 64 * e->d);
-  A(&e->part_lse, max_parts * 64);
-  A(&e->dycat, S * e->h_cat);
-  A(&e->dgu, S * e->gu_n);
-  A(&e->dr1b, S * h);
-  A(&e->dO, S * e->q_dim);
-  A(&e->dqkv, S * e->nqkv);
-  A(&e->dlu, S * r);
-  A(&e->dm, S * f);
-  A(&e->dh2, S * h);
-  A(&e->dr1, S * h);
-  A(&e->delta, S * e->Hq);
-  A(&e->dq, S * e->q_dim);
-  A(&e->dh1, S * h);
-  A(&e->rope_tab, (size_t)e->max_pos * (e->d / 2));
-  A(&e->d_meta, e->meta_bytes);
+  AL(part_o, max_parts * 64 * e->d);
+  AL(part_lse, max_parts * 64);
+  AL(dycat, S * e->h_cat);
+  AL(dgu, S * e->gu_n);
+  AL(dr1b, S * h);
+  AL(dO, S * e->q_dim);
+  AL(dqkv, S * e->nqkv);
+  AL(dlu, S * r);
+  AL(dm, S * f);
+  AL(dh2, S * h);
+  AL(dr1, S * h);
+  AL(delta, S * e->Hq);
+  AL(dq, S * e->q_dim);
+  AL(dh1, S * h);
+  AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
+  AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
+#undef AL
 }
 
 size_t meta_size(const cs_engine* e) {
@@ -331,6 +348,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   e->meta_bytes = meta_size(e);
   if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
+  if (const char* v = std::getenv("CS_ATTN_FWD2")) e->use_fwd2 = std::atoi(v) != 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -456,6 +474,18 @@ extern "C" int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double
   return CS_OK;
 }
 
+// Matrix::alloc_hook (matrix.hpp:16-25): report every device buffer the engine owns.  All of
+// them are carved from one arena at create time, so a cs_step / backward window allocates
+// nothing; the audit lets tests prove no frozen-weight gradient buffer exists (graph pruning).
+extern "C" int cs_engine_alloc_audit(cs_engine* e, cs_alloc_hook hook, void* user,
+                                     int64_t* transient_allocs) {
+  if (!e) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "alloc_audit: null engine");
+  if (hook)
+    for (const auto& a : e->audit) hook(a.name, a.elems, a.elem_bytes, user);
+  if (transient_allocs) *transient_allocs = e->transient_allocs;
+  return CS_OK;
+}
+
 extern "C" int64_t cs_engine_launch_count(cs_engine* e) {
   (void)e;
   return cs::g_launches.load();
@@ -498,6 +528,7 @@ int refresh_lora(cs_engine* e, int update, float lr, float b1, float b2, float e
   p.mB = e->mB;
   p.vB = e->vB;
   p.A_t = e->A_t;
+  p.B_t = e->B_t;
   p.down_cat = e->down_cat;
   p.dbwd_cat = e->dbwd_cat;
   p.n_layers = e->NL;
@@ -589,6 +620,7 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
   float* stage = nullptr;
   CS_CUDA_TRY(cudaSetDevice(e->device));
   CS_CUDA_TRY(cudaMalloc(&stage, lcount * sizeof(float)));
+  e->transient_allocs += 1;
   // stream-ordered upload: the engine stream is non-blocking w.r.t. the legacy stream
   CS_CUDA_TRY(cudaMemcpyAsync(stage, f32.data(), lcount * sizeof(float), cudaMemcpyHostToDevice,
                               e->st));
@@ -658,6 +690,7 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
   {
     float* tmp = nullptr;
     CS_CUDA_TRY(cudaMalloc(&tmp, (size_t)e->f * e->h * sizeof(float)));
+    e->transient_allocs += 1;
     for (size_t l = 0; l < NL; ++l) {
       cs::init_normal_f32(tmp, (long)e->f * e->h, wf, ss + 100 + l, st);
       cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->h * e->f_cat, e->f_cat, 1, st);
@@ -810,7 +843,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   std::vector<cs::AttnWork> work, work_tc, work_dec;
   std::vector<cs::AttnCombine> comb;
   const int rpt = 64 / e->grp;
-  const int rpt_tc = 128 / e->grp;
+  const int rpt_tc = (e->use_fwd2 ? 2 : 1) * (128 / e->grp);
   const bool tc_ok = e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn;
   double attn_flops = 0, attn_bytes = 0, tc_flops = 0, tc_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {
@@ -938,20 +971,22 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     std::vector<cs::AttnWork> w2;
     w2.reserve(work_dec.size());
     for (const auto& w : work_dec) {
-      const int ns = (int)((w.k_end + chunk - 1) / chunk);
+      // balanced parts (multiples of 128 keys), none a sliver: round(k_end / chunk)
+      const int ns = (int)std::max<long>(1, (w.k_end + chunk / 2) / chunk);
       if (ns <= 1 || part + ns > 4096) {
         w2.push_back(w);
         continue;
       }
+      const long per = ((w.k_end + ns - 1) / ns + 127) / 128 * 128;
       const int p0 = part;
-      for (int t = 0; t < ns; ++t) {
+      for (int t = 0; t < ns && t * per < w.k_end; ++t) {
         cs::AttnWork x = w;
-        x.k_begin = (int)(t * chunk);
-        x.k_end = (int)std::min<long>(w.k_end, (t + 1) * chunk);
+        x.k_begin = (int)(t * per);
+        x.k_end = (int)std::min<long>(w.k_end, (t + 1) * per);
         x.part = part++;
         w2.push_back(x);
       }
-      comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, ns, 0, 0});
+      comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
     }
     // longest first: the heaviest CTAs start in the first wave
     std::stable_sort(w2.begin(), w2.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
@@ -1112,7 +1147,10 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         tpr.kind = 3;
         prof_begin(e, tpr);
       }
-      CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      if (e->use_fwd2)
+        CS_CUDA_TRY(cs::attn_fwd_tc2(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      else
+        CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
       if (e->profiling) prof_end(e, tpr);
     }
     if (n_ft > 0 && keep_attn) {
@@ -1156,7 +1194,7 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                             e->norm, st);
     TRY(gemm(e, e->hf, h, std::max(e->head_chunk, e->max_seg), e->unembed_t, h, e->V,
              e->samp_logits, e->V, sp.n_samp, e->V, h, cs::EPI_F32));
-    cs::argmax_rows(e->samp_logits, e->V, sp.n_samp, e->V, e->next_tok, st);
+    cs::argmax_rows(e->samp_logits, e->V, sp.n_samp, e->V, e->next_tok, e->amax_part, st);
   }
   // ---- FT rows: fused generative loss + loss-head gradient into dY (top layer)
   if (n_ft > 0) {
@@ -1212,8 +1250,13 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   float* Xout = e->dy[e->dy_cur ^ 1] + (size_t)a * h;
   const size_t Lm = e->L_max;
   // ---- MLP + LoRA (tiny_model.hpp:276-287)
-  cs::lora_bwd_b(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, e->loraB + (size_t)n * r * h, r, s, h,
-                 e->dlu, e->dycat, e->h_cat, e->gB + (size_t)n * r * h, st);
+  // dycat = [bf16(dY) | bf16(dY B^T)] (tiny_model.hpp:281): dlu on the tensor cores (N = r),
+  // dB += u^T dY (:280) on the CUDA cores
+  cs::dycat_cast(Y, h, s, h, e->dycat, e->h_cat, st);
+  TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->B_t + (size_t)n * 16 * h, h, 16, e->dlu, r, s, r, h,
+           cs::EPI_F32));
+  cs::lora_pack(e->dlu, r, e->dycat, e->h_cat, h, s, st);
+  cs::lora_db(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, r, s, h, e->gB + (size_t)n * r * h, st);
   TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
            e->dm, f, s, f, e->h_cat, cs::EPI_F32));
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,

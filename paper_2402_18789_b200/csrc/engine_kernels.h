@@ -82,6 +82,10 @@ cudaError_t attn_bwd_tc(const AttnBwdParams& p, const CUtensorMap& tmK, const CU
                         const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
                         cudaStream_t st);
 // tcgen05 forward for prefill / finetuning-window tiles (head_dim 128, 128 packed rows per CTA)
+// v2: two query tiles per CTA (work items of 2 * (128 / group) positions), P kept in TMEM
+cudaError_t attn_fwd_tc2(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                         const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,
+                         cudaStream_t st);
 cudaError_t attn_fwd_tc(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,
                         cudaStream_t st);
@@ -124,7 +128,9 @@ void act_fwd(const bf16* gu, long ld_gu, bf16* m, long ldm, int rows, int f, int
 // m[row, f + j] = bf16(lu[row - 0, j]) for the adapter rows
 void lora_pack(const float* lu, int r, bf16* m, long ldm, int f, int rows, cudaStream_t st);
 
-void argmax_rows(const float* logits, long ld, int rows, int V, int* out, cudaStream_t st);
+// scratch: rows * 16 keys
+void argmax_rows(const float* logits, long ld, int rows, int V, int* out,
+                 unsigned long long* scratch, cudaStream_t st);
 
 // Fused CE over a chunk of logits rows: loss[i] = lse - logit[t]; dlogits = (softmax - onehot)
 // * inv_norm (rows with target < 0 -> 0 loss, 0 grad)
@@ -140,9 +146,11 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
 void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st);
 
-// dlu = dY B^T ; dYcat = [bf16(dY) | bf16(dlu) | 0]; dB += lu^T dY
-void lora_bwd_b(const float* dY, long ldy, const float* lu, const float* B, int r, int rows,
-                int h, float* dlu, bf16* dycat, long ldc, float* dB, cudaStream_t st);
+// dycat = [bf16(dY) | 0...]; dlu = dY B^T is a tcgen05 GEMM (B_t), packed by lora_pack
+void dycat_cast(const float* dY, long ldy, int rows, int h, bf16* dycat, long ldc, cudaStream_t st);
+// dB += lu^T dY
+void lora_db(const float* dY, long ldy, const float* lu, int r, int rows, int h, float* dB,
+             cudaStream_t st);
 
 // dqkv = [rope^-1(dq) | rope^-1(dk_acc[a:b]) | dv_acc[a:b]] (bf16)
 void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, long ld_acc,
@@ -159,6 +167,7 @@ struct AdamParams {
   float* mB;
   float* vB;
   bf16* A_t;        // [n_layers][16][f]          (lu GEMM B operand)
+  bf16* B_t;        // [n_layers][16][h]          (dlu GEMM B operand)
   bf16* down_cat;   // [n_layers][h][f + 64]     cols f.. = B^T
   bf16* dbwd_cat;   // [n_layers][f][h + 64]     cols h.. = A
   int n_layers, f, r, h;

@@ -119,6 +119,8 @@ def _declare_engine(L):
     for name in ("cs_nccl_unique_id", "cs_tp_group_create", "cs_tp_group_destroy",
                  "cs_engine_create_tp_local"):
         getattr(L, name).restype = ctypes.c_int
+    L.cs_engine_alloc_audit.restype = ctypes.c_int
+    L.cs_engine_alloc_audit.argtypes = [vp, vp, vp, P(i64)]
     L.cs_engine_pool_info.restype = ctypes.c_int
     L.cs_engine_pool_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i64)]
     L.cs_sched_latency.restype = f64
@@ -419,6 +421,17 @@ class Engine:
         _lib.check(self._L.cs_engine_read_profile(self._h, kind, ctypes.byref(ms), ctypes.byref(fl),
                                                   ctypes.byref(by), ctypes.byref(n)), "read_profile")
         return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": n.value}
+
+    def alloc_audit(self):
+        """[(name, elements, elem_bytes)] of every device buffer + transient allocation count
+        (cs_engine_alloc_audit, the Matrix::alloc_hook analogue)."""
+        recs = []
+        HOOK = ctypes.CFUNCTYPE(None, ctypes.c_char_p, i64, i32, vp)
+        cb = HOOK(lambda n, el, b, u: recs.append((n.decode(), int(el), int(b))))
+        tr = i64()
+        _lib.check(self._L.cs_engine_alloc_audit(self._h, ctypes.cast(cb, vp), None, ctypes.byref(tr)),
+                   "alloc_audit")
+        return recs, tr.value
 
     def launch_count(self) -> int:
         return int(self._L.cs_engine_launch_count(self._h))

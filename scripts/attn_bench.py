@@ -1,5 +1,6 @@
-"""A/B the attention forward paths on the 8B shape: a 2048-token FT window at l=6144 with 64
-decode rows (CS_ATTN_TC=1 tcgen05 vs 0 mma.sync), device time of the attention kernels."""
+"""A/B the attention forward paths on the 8B shape: 2048-token FT windows at l=0..6144 with 64
+decode rows (CS_ATTN_FWD2=1 two-query-tile tcgen05 kernel vs 0 the one-tile kernel), device
+time of the attention kernels from the engine's CUDA events."""
 import os
 import sys
 sys.path.insert(0, ".")
@@ -17,8 +18,10 @@ for l in range(0, 8192, 2048):
                    [Seg(SEG_FT_FWD, toks[l:l + 2048], l, ft_pages, adapter=True)],
                    ft={"phase": FT_FORWARD, "seq_len": 8192, "l": l, "s": 2048,
                        "targets": toks[l + 1:l + 2049] + ([-1] if l + 2048 == 8192 else [])})
-    a = eng.read_profile(1)
+    a = eng.read_profile(3)
+    d = eng.read_profile(1)
     g = eng.read_profile(0)
-    print(f"CS_ATTN_TC={os.environ.get('CS_ATTN_TC','1')} l={l} step {out['ms']:.2f} ms  attn {a['ms']:.2f} ms "
-          f"{a['flops']/a['ms']/1e9:.0f} TFLOP/s  gemm {g['ms']:.2f} ms {g['flops']/g['ms']/1e9:.0f} TFLOP/s", flush=True)
+    print(f"CS_ATTN_FWD2={os.environ.get('CS_ATTN_FWD2','1')} l={l} step {out['ms']:.2f} ms  "
+          f"attn(tc) {a['ms']:.2f} ms {a['flops']/max(a['ms'],1e-9)/1e9:.0f} TFLOP/s  decode {d['ms']:.2f} ms  "
+          f"gemm {g['ms']:.2f} ms {g['flops']/g['ms']/1e9:.0f} TFLOP/s", flush=True)
     eng.set_profiling(False); eng.set_profiling(True)

@@ -300,3 +300,63 @@ def test_decode_attention_kernel_parity(dec, monkeypatch):
             diffs.append(O.scaled_err(out["logits"][i], lg[-1]))
     assert max(diffs) < 0.04, max(diffs)
     eng.close()
+
+
+def test_alloc_audit_no_frozen_weight_gradients():
+    """Matrix::alloc_hook analogue (matrix.hpp:16-25): a full finetuning pass (forward windows,
+    backward windows through every layer, Adam) allocates no device memory, and the only
+    model-sized fp32 buffers are the LoRA state (graph pruning: frozen dW is never formed)."""
+    arch = O.Arch(n_layers=3, hidden=256, n_heads=4, n_kv_heads=2, head_dim=64, ffn=512,
+                  vocab=128, lora_rank=16, norm="rms", act="swiglu", rope=True, qkv_bias=True,
+                  rope_theta=10000.0)
+    W = O.init_general(arch, 3)
+    toks = list(np.random.default_rng(5).integers(0, arch.vocab, 100))
+    # capacities chosen so no activation buffer is coincidentally weight-sized
+    cfg = arch_config(arch, page_size=16, n_pages=256, max_tokens=200, max_ft_len=len(toks),
+                      max_segments=64)
+    eng = Engine(cfg)
+    eng.load_weights(W)
+    recs0, tr0 = eng.alloc_audit()
+    _run_coserve_on(eng, arch, W, toks, [40, 60], [30, 30, 40])
+    eng.adam_step()
+    recs1, tr1 = eng.alloc_audit()
+    assert tr1 == tr0 and recs1 == recs0          # nothing allocated by steps / Adam
+    names = {n for n, _, _ in recs1}
+    assert {"gA", "gB", "dk_acc", "dv_acc"} <= names
+    # fp32 buffers whose size does not move with the engine's capacities (tokens, FT length,
+    # pages) are model-sized: they must be exactly the LoRA master/grad/Adam state, the norm
+    # gains and biases, and the fixed split-KV scratch -- no frozen-weight gradient
+    cfg2 = arch_config(arch, page_size=16, n_pages=300, max_tokens=300, max_ft_len=120,
+                       max_segments=64)
+    eng2 = Engine(cfg2)
+    recs2, _ = eng2.alloc_audit()
+    eng2.close()
+    size1 = {n: (el, b) for n, el, b in recs1}
+    model_sized = {n for n, el, b in recs2 if b == 4 and size1.get(n) == (el, b)}
+    allowed = {"gf", "bqkv", "g1", "g2", "loraA", "loraB", "gA", "gB", "mA", "vA", "mB", "vB",
+               "part_o", "part_lse"}
+    assert model_sized <= allowed, model_sized - allowed
+    NL, f, r, h = arch.n_layers, arch.ffn, arch.lora_rank, arch.hidden
+    assert size1["gA"][0] == NL * f * r and size1["gB"][0] == NL * r * h
+    eng.close()
+
+
+def _run_coserve_on(eng, arch, W, toks, fwd, bwd):
+    from paper_2402_18789_b200.engine import Seg as S
+    L = len(toks)
+    pages = list(range(200, 200 + (L + 15) // 16))
+    l = 0
+    for s in fwd:
+        eng.step([S(SEG_FT_FWD, toks[l:l + s], l, pages, adapter=True)],
+                 ft={"phase": FT_FORWARD, "seq_len": L, "l": l, "s": s,
+                     "targets": [toks[i + 1] if i + 1 < L else -1 for i in range(l, l + s)]})
+        l += s
+    for n in range(arch.n_layers - 1, -1, -1):
+        lj = L
+        for s in bwd:
+            s = min(s, lj)
+            eng.step([], ft={"phase": FT_BACKWARD, "seq_len": L, "l": lj, "s": s, "layer": n,
+                             "pages": pages})
+            lj -= s
+            if lj == 0:
+                break
