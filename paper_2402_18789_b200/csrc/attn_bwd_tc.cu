@@ -216,21 +216,26 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(s_free);
       const int kb = j * 128 + hh * 64;
+      // P = 2^(s*scale*log2e - lse*log2e) (FFMA2 + SFU), dS = P (dP - Delta) (FFMA2 pairs);
+      // the causal / k_end mask only on tiles that reach the diagonal
+      const bool full = kb + 63 <= pos && kb + 64 <= p.b;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
+      const float2 nd2 = make_float2(-dlt, -dlt);
       uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float d2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = kb + c * 32 + i + e;
-            const float pv = (key <= pos && key < p.b)
-                                 ? exp2f(__uint_as_float(sv[c][i + e]) * p.scale_log2 - lse2)
-                                 : 0.f;
-            d2[e] = pv * (__uint_as_float(dv[c][i + e]) - dlt);
+          float2 x = ffma2(make_float2(__uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1])), sc2, nl2);
+          float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          if (!full) {
+            const int key = kb + c * 32 + i;
+            if (!(key <= pos && key < p.b)) pv.x = 0.f;
+            if (!(key + 1 <= pos && key + 1 < p.b)) pv.y = 0.f;
           }
-          pk[(c * 32 + i) / 2] = pack_bf16(d2[0], d2[1]);
+          const float2 dd = fadd2(make_float2(__uint_as_float(dv[c][i]), __uint_as_float(dv[c][i + 1])), nd2);
+          const float2 d2 = fmul2(pv, dd);
+          pk[(c * 32 + i) / 2] = pack_bf16(d2.x, d2.y);
         }
       if (j > 0) {
         mbar_wait(ds_empty, (j - 1) & 1);
@@ -414,6 +419,9 @@ __global__ void __launch_bounds__(384, 1)
     const int t = threadIdx.x - 128;                      // 0..255
     const int key = k0 + ew * 32 + lane;                  // TMEM lane == key row
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    int cq[32];  // position offset (within a query tile) of this thread's 32 packed columns
+#pragma unroll
+    for (int j = 0; j < 32; ++j) cq[j] = (hh * 32 + j) / grp;
     for (int i = 0; i < n; ++i) {
       const int st = i & 1;
       const int qt = qt0 + i;
@@ -439,20 +447,27 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(&st_free[st]);
       uint32_t pp[16], pd[16];
+      // column c is query position a + qt*rpt + cq[c]: the tile is fully unmasked for this key
+      // when key <= its first position and every column is a real row
+      const int qbase = qt * rpt;
+      const bool full = key < p.b && key <= p.a + qbase && qbase + cq[31] < nrows;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        float pv[2], dsv[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = hh * 32 + j + e;
-          const int qr = qt * rpt + col / grp;
-          const int pos = p.a + qr;
-          const bool ok = qr < nrows && key <= pos && key < p.b;
-          pv[e] = ok ? exp2f(__uint_as_float(sv[j + e]) * p.scale_log2 - xs[col]) : 0.f;
-          dsv[e] = pv[e] * (__uint_as_float(dv[j + e]) - xs[64 + col]);
+        const int col = hh * 32 + j;
+        float2 x = ffma2(make_float2(__uint_as_float(sv[j]), __uint_as_float(sv[j + 1])), sc2,
+                         make_float2(-xs[col], -xs[col + 1]));
+        float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        if (!full) {
+          const int q0r = qbase + cq[j], q1r = qbase + cq[j + 1];
+          if (!(q0r < nrows && key <= p.a + q0r && key < p.b)) pv.x = 0.f;
+          if (!(q1r < nrows && key <= p.a + q1r && key < p.b)) pv.y = 0.f;
         }
-        pp[j / 2] = pack_bf16(pv[0], pv[1]);
-        pd[j / 2] = pack_bf16(dsv[0], dsv[1]);
+        const float2 dd = fadd2(make_float2(__uint_as_float(dv[j]), __uint_as_float(dv[j + 1])),
+                                make_float2(-xs[64 + col], -xs[64 + col + 1]));
+        const float2 ds = fmul2(pv, dd);
+        pp[j / 2] = pack_bf16(pv.x, pv.y);
+        pd[j / 2] = pack_bf16(ds.x, ds.y);
       }
       if (i > 0) {
         mbar_wait(pds_empty, (i - 1) & 1);

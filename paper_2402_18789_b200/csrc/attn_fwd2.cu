@@ -232,45 +232,45 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[c][i]);
       }
+      // raw scores: max first (scale > 0), masking only on tiles that touch the diagonal /
+      // k_end; then x = s * scale_log2 - m (FFMA2), 2^x on the SFU, row sums on FADD2
       const int kbase = j * BN2;
-      float mx = -INFINITY;
-      if (kbase + BN2 - 1 <= pos && kbase + BN2 <= w.k_end) {
+      if (!(kbase + BN2 - 1 <= pos && kbase + BN2 <= w.k_end)) {
 #pragma unroll
-        for (int i = 0; i < BN2; ++i) {
-          s[i] *= p.scale_log2;
-          mx = fmaxf(mx, s[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < BN2; ++i) {
-          float v = s[i] * p.scale_log2;
-          if (kbase + i > pos || kbase + i >= w.k_end) v = -INFINITY;
-          s[i] = v;
-          mx = fmaxf(mx, v);
-        }
+        for (int i = 0; i < BN2; ++i)
+          if (kbase + i > pos || kbase + i >= w.k_end) s[i] = -INFINITY;
       }
+      float mr = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BN2; i += 2) mr = fmaxf(mr, fmaxf(s[i], s[i + 1]));
+      const float mx = mr * p.scale_log2;
       bool rescale = false;
       float factor = 1.f;
       if (mx > m_ref + kRescale2 || (m_ref == -INFINITY && mx > -INFINITY)) {
-        factor = (m_ref == -INFINITY) ? 0.f : exp2f(m_ref - mx);
+        factor = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - mx);
         rescale = j > 0 && m_ref != -INFINITY;
         m_ref = mx;
         l_sum *= factor;
       }
-      const float base = m_ref == -INFINITY ? 0.f : m_ref;
-      float rs = 0.f;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      const float nb = m_ref == -INFINITY ? 0.f : -m_ref;
+      const float2 nb2 = make_float2(nb, nb);
+      float2 rs2 = make_float2(0.f, 0.f);
       // P (bf16) into the first 64 columns of S_i: every S column was read above
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a = exp2f(s[c * 32 + 2 * i] - base), b = exp2f(s[c * 32 + 2 * i + 1] - base);
-          rs += a + b;
-          pk[i] = pack_bf16(a, b);
+          float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nb2);
+          x.x = ex2_approx(x.x);
+          x.y = ex2_approx(x.y);
+          rs2 = fadd2(rs2, x);
+          pk[i] = pack_bf16(x.x, x.y);
         }
         tmem_st_x16(tS + c * 16, pk);
       }
+      const float rs = rs2.x + rs2.y;
       l_sum += rs;
       // O rescale (warp-collective tcgen05.ld/st): PV_i(j-1) must be complete first
       if (__any_sync(0xffffffffu, rescale)) {
@@ -283,7 +283,12 @@ __global__ void __launch_bounds__(384, 1)
           tmem_ld_32x32b_x32(tO + c * 32, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+          for (int i = 0; i < 32; i += 2) {
+            const float2 v = fmul2(make_float2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])),
+                                   make_float2(factor, factor));
+            o[i] = __float_as_uint(v.x);
+            o[i + 1] = __float_as_uint(v.y);
+          }
           tmem_st_32x32b_x32(tO + c * 32, o);
         }
       }

@@ -324,10 +324,10 @@ def test_alloc_audit_no_frozen_weight_gradients():
     names = {n for n, _, _ in recs1}
     assert {"gA", "gB", "dk_acc", "dv_acc"} <= names
     # fp32 buffers whose size does not move with the engine's capacities (tokens, FT length,
-    # pages) are model-sized: they must be exactly the LoRA master/grad/Adam state, the norm
+    # pages, segments) are model-sized: they must be exactly the LoRA master/grad/Adam state, the norm
     # gains and biases, and the fixed split-KV scratch -- no frozen-weight gradient
     cfg2 = arch_config(arch, page_size=16, n_pages=300, max_tokens=300, max_ft_len=120,
-                       max_segments=64)
+                       max_segments=80)
     eng2 = Engine(cfg2)
     recs2, _ = eng2.alloc_audit()
     eng2.close()
