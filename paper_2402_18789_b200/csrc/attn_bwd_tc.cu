@@ -535,6 +535,25 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// single-kernel launchers (A/B against attn_bwd2.cu)
+void attn_bwd_dq_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                    const CUtensorMap& tmK128, const CUtensorMap& tmV128, dim3 grid, cudaStream_t st) {
+  static bool once = (cudaFuncSetAttribute(attn_bwd_dq_tc_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM_TOTAL),
+                      true);
+  (void)once;
+  attn_bwd_dq_tc_kernel<<<grid, 384, dq::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, p);
+}
+void attn_bwd_dkdv_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                      const CUtensorMap& tmK128, const CUtensorMap& tmV128, const CUtensorMap& tmQ3,
+                      const CUtensorMap& tmO3, dim3 grid, cudaStream_t st) {
+  static bool once = (cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kv::SMEM_TOTAL),
+                      true);
+  (void)once;
+  attn_bwd_dkdv_tc_kernel<<<grid, 384, kv::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
+}
+
 // ============================================================================ launcher
 cudaError_t attn_bwd_tc(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         const CUtensorMap& tmK128, const CUtensorMap& tmV128,

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------------------ TMA producer
       for (int j = 0; j < nt; ++j) {
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------------------ softmax / epilogue
     const int qt = (warp - 4) >> 2;       // query tile of this warpgroup
     const int ew = warp & 3;              // TMEM lane quarter

@@ -55,6 +55,7 @@ struct cs_engine {
   bool use_tc_attn = true;  // CS_ATTN_TC=0 forces the mma.sync path (A/B testing)
   bool use_dec_attn = true;  // CS_ATTN_DEC=0 sends decode rows to the mma.sync tile kernel
   bool use_fwd2 = true;      // CS_ATTN_FWD2=0 runs the one-query-tile tcgen05 kernel (v1)
+  bool use_bwd2 = true;      // CS_ATTN_BWD2=0 runs the shared-memory-staged backward (v1)
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
     const char* name;
@@ -349,6 +350,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_FWD2")) e->use_fwd2 = std::atoi(v) != 0;
+  if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -1312,16 +1314,21 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     if (bwd_tc) {
       CUtensorMap mk, mv, mk128, mv128, mq3, mo3;
       const long pool_rows = (long)e->npages * e->P;
+      const bool v2 = e->use_bwd2;
+      const int qbox = 64 / e->grp;  // 3-D boxes: 64 packed (position, head) rows
       if (cs::make_map(&mk, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mv, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mk128, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
           cs::make_map(&mv128, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
           cs::make_map_3d(&mq3, bp.q_cache, 128, e->Hq, e->L_max, 256, (long)e->q_dim * 2, e->grp,
-                          64 / e->grp) != 0 ||
+                          qbox) != 0 ||
           cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
-                          64 / e->grp) != 0)
+                          qbox) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
-      CS_CUDA_TRY(cs::attn_bwd_tc(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
+      if (v2)
+        CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
+      else
+        CS_CUDA_TRY(cs::attn_bwd_tc(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
     } else {
       CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
     }

@@ -77,6 +77,16 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
 void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st);
 // tcgen05 backward (dQ and dK/dV kernels); head_dim 128, 64 % grp == 0
+void attn_bwd_dq_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                    const CUtensorMap& tmK128, const CUtensorMap& tmV128, dim3 grid, cudaStream_t st);
+void attn_bwd_dkdv_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                      const CUtensorMap& tmK128, const CUtensorMap& tmV128, const CUtensorMap& tmQ3,
+                      const CUtensorMap& tmO3, dim3 grid, cudaStream_t st);
+// v2: P^T / dS^T / dS kept in TMEM (TS-MMA), ping-pong elementwise warpgroups
+cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                         const CUtensorMap& tmK128, const CUtensorMap& tmV128,
+                         const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
+                         cudaStream_t st);
 cudaError_t attn_bwd_tc(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         const CUtensorMap& tmK128, const CUtensorMap& tmV128,
                         const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
