@@ -57,7 +57,7 @@ def timed(eng, fn, reps=5):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--out", default="gpurun_out/kernel_sweep.json")
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
@@ -70,6 +70,7 @@ def main():
     res = {"layers": a.layers, "shape": "llama-3.1-8b", "peaks": {"hbm_gbs": hbm, "bf16_tflops": tc_peak,
                                                                   "kind": kind}, "decode": [], "finetune": [], "mixed": []}
     # ---------------------------------------------------------------- decode only
+    marks = []  # decode configs in launch order (for the ncu launch-list reduction below)
     Bs = [1, 8, 32, 64, 128, 256]
     Cs = [512, 1024, 2048, 4096, 8192]
     if a.quick:
@@ -83,6 +84,8 @@ def main():
             segs = [Seg(SEG_DECODE, [i % 1000], c, pts[i], sample=False) for i in range(B)]
             ms, prof = timed(eng, lambda: eng.step(segs)["ms"])
             d = prof[1]
+            marks.append({"B": B, "ctx": c, "launches": 6 * a.layers,
+                          "bytes_per_launch": d["bytes"] / max(1, d["launches"])})
             gbs = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] else 0.0
             row = {"B": B, "ctx": c, "step_ms": round(ms, 3),
                    "attn_us_per_layer": round(d["ms"] * 1e3 / max(1, d["launches"]), 2),
@@ -161,10 +164,63 @@ def main():
                "gemm_share": round(g["ms"] / (ms * 5 + 1e-9) if g["ms"] else 0, 3)}
         res["mixed"].append(row)
         print("mixed", row, flush=True)
+    res["decode_launch_marks"] = marks
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(res, f, indent=1)
 
 
+def reduce_ncu(sweep_json, launches_csv, out_json):
+    """Decode rows of the sweep from ncu device times: `ncu --metrics gpu__time_duration.sum,
+    dram__bytes_read.sum -k regex:"attn_decode|attn_combine"` over this script.  Each decode
+    config issues 6 steps x layers decode launches (each followed by its combine launch when the
+    key ranges were split); the engine's CUDA events time decode-only steps with host launch
+    gaps inside, so the roofline fraction is taken from the ncu durations."""
+    import csv
+    res = json.load(open(sweep_json))
+    hdr, per = None, {}
+    for r in csv.reader(open(launches_csv)):
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            e = per.setdefault(int(d["ID"]), {"name": d["Kernel Name"]})
+            v = float(d["Metric Value"])
+            u = d.get("Metric Unit", "")
+            if d["Metric Name"] == "gpu__time_duration.sum":
+                e["ns"] = v * {"ns": 1, "us": 1e3, "usecond": 1e3, "msecond": 1e6, "nsecond": 1}.get(u, 1)
+            else:
+                e["bytes"] = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+    seq = [per[k] for k in sorted(per)]
+    # fold each combine into the preceding decode launch
+    groups = []
+    for e in seq:
+        if "attn_decode" in e["name"]:
+            groups.append({"ns": e.get("ns", 0.0), "bytes": e.get("bytes", 0.0)})
+        elif groups:
+            groups[-1]["ns"] += e.get("ns", 0.0)
+    hbm = res["peaks"]["hbm_gbs"]
+    rows, pos = [], 0
+    for m in res["decode_launch_marks"]:
+        g = groups[pos:pos + m["launches"]][m["launches"] // 6:]  # drop the warm-up step
+        pos += m["launches"]
+        if not g:
+            break
+        ns = sum(x["ns"] for x in g) / len(g)
+        gbs = m["bytes_per_launch"] / (ns * 1e-9) / 1e9
+        rows.append({"B": m["B"], "ctx": m["ctx"], "kernel_us": round(ns / 1e3, 2),
+                     "algorithmic_MB": round(m["bytes_per_launch"] / 1e6, 2),
+                     "dram_MB": round(sum(x["bytes"] for x in g) / len(g) / 1e6, 2),
+                     "gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4)})
+    res["decode_ncu"] = rows
+    json.dump(res, open(out_json, "w"), indent=1)
+    for r in rows:
+        print(r)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--reduce":
+        reduce_ncu(sys.argv[2], sys.argv[3], sys.argv[4])
+    else:
+        main()
