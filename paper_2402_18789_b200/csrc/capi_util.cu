@@ -1,4 +1,5 @@
 // capi_util.cu -- C-ABI error state + primitive entry points (GEMM) of libcoserve_cuda.so.
+#include <cstdlib>
 #include <string>
 
 #include "coserve_cuda.h"
@@ -6,6 +7,13 @@
 
 namespace cs {
 std::atomic<long> g_launches{0};
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CS_PDL");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
 thread_local std::string g_last_error;
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;

@@ -184,6 +184,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with cs::launch_pdl may start while its predecessor on the stream is still
+// running: everything before griddep_wait() must only touch kernel-private state (barriers,
+// TMEM, tensor-map prefetch); griddep_launch() lets the successor begin its own prologue.
+CS_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+CS_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- packed fp32 / SFU
 // 2^x on the SFU without the denormal pre/post scaling exp2f() adds (ftz; exp2(-inf) = +0)
 CS_DEV float ex2_approx(float x) {

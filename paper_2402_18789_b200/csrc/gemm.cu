@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <unordered_map>
@@ -163,6 +164,10 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: barrier init / TMEM alloc / descriptor prefetch above overlapped the previous kernel;
+  // all CTAs of this persistent grid are resident, so the successor may start its prologue
+  griddep_launch();
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -265,6 +270,208 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ 2-SM (CTA pair) variant
+// cta_group::2: a cluster of 2 CTAs on one TPC computes a 256 x BN tile; CTA r loads A rows
+// [128r, 128r+128) and B rows [BN/2 r, BN/2 r + BN/2) of the tile into its own shared memory,
+// the leader (rank 0) issues tcgen05.mma.cta_group::2 (M=256), and each CTA's TMEM receives
+// its 128 accumulator rows x BN.  Per SM that halves the B-operand shared-memory traffic of
+// the 1-SM kernel (the tensor pipe stalls on operand delivery at M=128, N=256).
+//   full[s]   (leader)     : leader arrive.expect_tx(both CTAs' bytes); both CTAs' TMA
+//                            complete_tx on it (2-SM TMA form, peer bit cleared)
+//   empty[s]  (each CTA)   : leader's MMA commit, multicast to both CTAs
+//   tfull[a]  (each CTA)   : leader's accumulator commit, multicast
+//   tempty[a] (leader)     : 256 arrivals, the peer's epilogue arrives remotely (mapa)
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = 128 * BK * 2;        // this CTA's 128 rows of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;   // this CTA's half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+namespace {
+CS_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+CS_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-SM TMA load: data into this CTA's smem, transaction bytes to the leader CTA's mbarrier
+CS_DEV void tma_load_2d_2sm(const CUtensorMap* m, uint64_t* bar, void* smem, int c0, int c1) {
+  const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(c0), "r"(c1)
+      : "memory");
+}
+CS_DEV void mma_bf16_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+CS_DEV void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3)
+      : "memory");
+}
+// arrive on the leader CTA's copy of `bar`
+CS_DEV void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+}  // namespace
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tn2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs args) {
+  using Cfg = Gemm2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int total = args.num_m * args.num_n * args.splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch();
+  griddep_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = pair; w < total; w += n_pairs) {
+        int mb, nb, kb0, kb1;
+        decode_work(w, args, mb, nb, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+          tma_load_2d_2sm(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * 256 + (int)rank * 128);
+          tma_load_2d_2sm(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = pair; w < total; w += n_pairs) {
+        int mb, nb, kb0, kb1;
+        decode_work(w, args, mb, nb, kb0, kb1);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+          const uint64_t ad = umma_desc_sw128(sa);
+          const uint64_t bd = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < Cfg::BK / 16; ++k)
+            mma_bf16_2sm(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                         (kb > kb0 || k > 0) ? 1u : 0u);
+          mma_commit_2sm(&empty_bar[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = pair; w < total; w += n_pairs) {
+      int mb, nb, kb0, kb1;
+      decode_work(w, args, mb, nb, kb0, kb1);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + (int)rank * 128 + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int col0 = nb * BN + c0;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + c0, r);
+        tmem_ld_wait();
+        if (col0 < args.N) epilogue_store<BN>(args, row, col0, r, 32);
+      }
+      tc_fence_before();
+      mbar_arrive_leader(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // every MMA into / operand read from both CTAs has completed
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 namespace {
 
@@ -361,8 +568,7 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmAr
     attr_set = true;
   }
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  gemm_tn_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, a);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tn_kernel<BN>, dim3(grid), dim3(256), Cfg::SMEM, st, ma, mb, a);
 }
 
 }  // namespace
@@ -378,11 +584,64 @@ int gemm_pick_bn(long M, long N) {
   return 64;
 }
 
+namespace {
+bool use_2sm() {
+  static const bool on = [] {
+    const char* v = std::getenv("CS_GEMM_2SM");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
+// 256 x 256 tiles on CTA pairs, persistent over the pairs (<= 74 pairs on 148 SMs)
+cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
+  constexpr int BN = 256;
+  using Cfg = Gemm2Cfg<BN>;
+  GemmArgs a;
+  a.M = (int)d.M;
+  a.N = (int)d.N;
+  a.K = (int)d.K;
+  a.kb_total = (int)((d.K + 63) / 64);
+  a.num_m = (int)((d.M + 255) / 256);
+  a.num_n = (int)((d.N + BN - 1) / BN);
+  a.epi = d.epi;
+  a.C = d.C;
+  a.ldc = d.ldc;
+  a.bias = d.bias;
+  a.splits = 1;
+  CUtensorMap ma, mb;
+  const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
+  const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
+  if (make_map(&ma, d.A, a_rows, d.K, d.lda, 128) != 0) return cudaErrorInvalidValue;
+  if (make_map(&mb, d.B, b_rows, d.K, d.ldb, BN / 2) != 0) return cudaErrorInvalidValue;
+  const long work = (long)a.num_m * a.num_n;
+  const int pairs = (int)std::min<long>(work, kNumSMs / 2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  return launch_pdl(gemm_tn2_kernel<BN>, dim3(2 * pairs), dim3(256), Cfg::SMEM, st, ma, mb, a);
+}
+}  // namespace
+
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
   if (d.K <= 0 || (d.K % 8) != 0 || (d.lda % 8) != 0 || (d.ldb % 8) != 0)
     return cudaErrorInvalidValue;
+  // large GEMMs (at least one wave of 256 x 256 tiles): CTA-pair kernel
+  if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 512 &&
+      ((d.M + 255) / 256) * ((d.N + 255) / 256) >= kNumSMs / 2)
+    return gemm_tn_2sm(d, st);
   int bn = d.bn > 0 ? d.bn : gemm_pick_bn(d.M, d.N);
+  // small-M fp32-epilogue GEMMs (the O / down projections of inference-only rows): weight
+  // streaming is latency-bound per CTA, so wider tiles split along K beat narrow tiles
+  // (scripts/gemm_smallm.py: down T=64 38 us at bn 128 x 4 splits vs 51 us at bn 64 x 3)
+  const bool small_f32 = d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.M <= 256 && d.N >= 1024;
+  if (small_f32) bn = 128;
   GemmArgs a;
   a.M = (int)d.M;
   a.N = (int)d.N;
@@ -398,7 +657,10 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {
     splits = 1;
-    if (d.epi != EPI_BF16 && tiles < kNumSMs) {
+    if (small_f32) {
+      splits = (int)((kNumSMs + tiles / 2) / tiles);
+      splits = std::max(1, std::min(splits, a.kb_total / 8));
+    } else if (d.epi != EPI_BF16 && tiles < kNumSMs) {
       splits = (int)((kNumSMs + tiles - 1) / tiles);
       splits = std::min(splits, std::max(1, a.kb_total / 4));
     }

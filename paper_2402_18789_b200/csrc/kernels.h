@@ -11,6 +11,26 @@ namespace cs {
 
 extern std::atomic<long> g_launches;  // kernels launched by this library (process-wide)
 
+// Launch with programmatic stream serialization (PDL): the kernel's prologue overlaps the
+// previous kernel's tail; the kernel must call griddep_wait() before touching shared data.
+// CS_PDL=0 disables it (plain stream order).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 enum GemmEpi : int {
   EPI_BF16 = 0,        // C_bf16 = acc (+ bias)
