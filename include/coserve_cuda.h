@@ -50,6 +50,8 @@ extern "C" {
 
 const char* cs_last_error(void);
 int cs_version(void);
+/* debugging: SM-clock event timeline of one CTA of the instrumented kernels */
+int64_t cs_debug_trace(int cta, void* dev_buf, int64_t capacity);
 
 /* ---------------------------------------------------------------- primitives (device ptrs) */
 /* C[M,N] (op)= A[M,K] . B[N,K]^T, bf16 operands (K contiguous), fp32 accumulate on

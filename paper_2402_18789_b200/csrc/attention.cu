@@ -37,6 +37,7 @@ CS_DEV int page_row(const int* __restrict__ pt, int page_off, int j, int P) {
 // ============================================================================ forward
 template <int D>
 __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnFwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   constexpr int BM = 64, BN = 64, CH = D / 8;
   constexpr int TILE = BN * D * 2;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnFwdParams p) {
 // loads, independent across parts.
 template <int D>
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const AttnCombine c = p.combine[blockIdx.x];
   const AttnSeg sg = p.segs[c.seg];
   const int grp = p.grp;

@@ -25,6 +25,20 @@
 
 namespace cs {
 
+// ---- in-kernel event trace (debugging): SM-clock timeline of one CTA (blockIdx.x == cta,
+// blockIdx.y == 0) of the backward kernels, set by cs_debug_trace(); off (cta -1) by default
+__device__ int g_trace_cta = -1;
+__device__ int g_trace_n = 0;
+__device__ int g_trace_cap = 0;
+__device__ unsigned long long* g_trace_buf = nullptr;
+__device__ __forceinline__ void trace_ev(int ev, int idx) {
+  if ((int)blockIdx.x != g_trace_cta || blockIdx.y != 0) return;
+  const int k = atomicAdd(&g_trace_n, 1);
+  if (k < g_trace_cap)
+    g_trace_buf[k] = ((unsigned long long)(ev & 0xFF) << 56) |
+                     ((unsigned long long)(idx & 0xFFFF) << 40) | (clock64() & 0xFFFFFFFFFFull);
+}
+
 namespace {
 constexpr float kLog2eC = 1.4426950408889634f;
 constexpr int DB = 128;
@@ -108,7 +122,7 @@ constexpr int NB = 128 / QB;           // TMEM buffers (S^T / dP^T per tile): 2
 constexpr int LA = NB - 2;             // S^T issue lookahead beyond the next tile
 constexpr int HALFQ = QB * 128;        // 8 KB
 constexpr int QTILE = 2 * HALFQ;       // 16 KB
-constexpr int QST = 3;                 // Q / dO ring depth
+constexpr int QST = 4;                 // Q / dO ring depth (tiles are held from S^T(i) to grad(i): 4 keeps ~2 in flight)
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + TILEB;
 constexpr int SMEM_Q = SMEM_V + TILEB;
@@ -124,6 +138,7 @@ __global__ void __launch_bounds__(384, 1)
                           const __grid_constant__ CUtensorMap tmV128,
                           const __grid_constant__ CUtensorMap tmQ3,
                           const __grid_constant__ CUtensorMap tmO3, AttnBwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   using namespace kv2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -205,8 +220,10 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_s = [&](int i) {
         const int st = i % QST, b = i % NB;
         mbar_wait(&q_full[st], (i / QST) & 1);
+        trace_ev(33, i);
         if (i >= NB) mbar_wait(&buf_free[b], ((i / NB) - 1) & 1);
         tc_fence_after();
+        trace_ev(30, i);
         const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
         const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
 #pragma unroll
@@ -229,6 +246,7 @@ __global__ void __launch_bounds__(384, 1)
         const int b = i % NB, st = i % QST;
         mbar_wait(&pds_full[b], (i / NB) & 1);
         tc_fence_after();
+        trace_ev(31, i);
         const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
         const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
 #pragma unroll
@@ -280,6 +298,7 @@ __global__ void __launch_bounds__(384, 1)
       xnext = fetch_x(i + 2);
       mbar_wait(&st_full[b], k & 1);
       tc_fence_after();
+      if (tw == 0) trace_ev(40 + wg, i);
       // full tile: every column is a real row whose position >= key, and the key is in range
       const bool full = key < p.b && key <= p.a + qbase && qbase + ((QB - 1) >> lg) < nrows;
       // 32-column chunks (register budget); the packed P^T / dS^T of chunk h land on TMEM
@@ -313,6 +332,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       tmem_st_wait();
       tc_fence_before();
+      if (tw == 0) trace_ev(42 + wg, i);
       mbar_arrive(&pds_full[b]);
     }
     // ΔKVAccum rows [k0, k0+128) of this head: WG wg owns dV / dK columns [64 wg, 64 wg + 64)
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmK128,
                         const __grid_constant__ CUtensorMap tmV128, AttnBwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   using namespace dq2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -462,8 +483,10 @@ __global__ void __launch_bounds__(384, 1)
         if (j < nt) {
           const int ks = j % KST, vs = j % VST, b = j & 1;
           mbar_wait(&k_full[ks], (j / KST) & 1);
+          trace_ev(14, j);
           if (j >= 2) mbar_wait(&sbuf_free[b], ((j >> 1) - 1) & 1);
           tc_fence_after();
+          trace_ev(10, j);
           const uint32_t sK = smem_u32(smem + SMEM_K + ks * TILEB);
           const uint32_t sV = smem_u32(smem + SMEM_V + vs * TILEB);
 #pragma unroll
@@ -473,8 +496,10 @@ __global__ void __launch_bounds__(384, 1)
           }
           mma_commit(&s_full[b]);
           mbar_wait(&v_full[vs], (j / VST) & 1);
+          trace_ev(15, j);
           if (j >= 1) mbar_wait(dp_free, (j - 1) & 1);
           tc_fence_after();
+          trace_ev(11, j);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * HALFB + (kk & 3) * 32;
@@ -487,6 +512,7 @@ __global__ void __launch_bounds__(384, 1)
           const int jj = j - 1, b = jj & 1, ks = jj % KST;
           mbar_wait(&ds_full[b], (jj >> 1) & 1);
           tc_fence_after();
+          trace_ev(12, jj);
           const uint32_t sK = smem_u32(smem + SMEM_K + ks * TILEB);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
@@ -537,6 +563,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&s_full[b], (j >> 1) & 1);
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
+      if (lane == 0 && ew == 0) trace_ev(20 + hh, j);
       uint32_t sv[2][32], dv[2][32];
       tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + hh * 64, sv[0]);
       tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + hh * 64 + 32, sv[1]);
@@ -544,6 +571,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld_32x32b_x32(tmem + lane_base + 256 + hh * 64 + 32, dv[1]);
       tmem_ld_wait();
       tc_fence_before();
+      if (lane == 0 && ew == 0) trace_ev(22 + hh, j);
       mbar_arrive(dp_free);  // the next dP may overwrite its TMEM columns
       const int kb = j * 128 + hh * 64;
       const bool full = kb + 63 <= pos && kb + 64 <= p.b;
@@ -567,6 +595,7 @@ __global__ void __launch_bounds__(384, 1)
       tst_x16(tmem + lane_base + b * 128 + hh * 64 + 16, pk + 16);
       tmem_st_wait();
       tc_fence_before();
+      if (lane == 0 && ew == 0) trace_ev(24 + hh, j);
       mbar_arrive(&ds_full[b]);
     }
     if (nt > 0) {
@@ -629,3 +658,14 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
 }
 
 }  // namespace cs
+
+extern "C" int64_t cs_debug_trace(int cta, void* dev_buf, int64_t capacity) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, cs::g_trace_n, sizeof(int));
+  const int zero = 0, cap = (int)capacity;
+  cudaMemcpyToSymbol(cs::g_trace_n, &zero, sizeof(int));
+  cudaMemcpyToSymbol(cs::g_trace_cap, &cap, sizeof(int));
+  cudaMemcpyToSymbol(cs::g_trace_buf, &dev_buf, sizeof(void*));
+  cudaMemcpyToSymbol(cs::g_trace_cta, &cta, sizeof(int));
+  return n;
+}

@@ -55,6 +55,7 @@ template <int D>
 __global__ void __launch_bounds__(NWARP * 32, 1)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        AttnFwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   constexpr int NH = D / 64;                       // 64-column halves
   constexpr int HALF = KT * 128;                   // one half of a K (or V) tile
   constexpr int TILE = NH * HALF;                  // K (or V) tile bytes

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmK128,
                         const __grid_constant__ CUtensorMap tmV128, AttnFwdParams p) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(384, 1)
   const int rpt = BM2 / grp;  // query positions per tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (w.k_end + BN2 - 1) / BN2;
+  const int ntile = w.nq > rpt ? 2 : 1;  // query tiles of this item (small calls use 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmK);
@@ -159,8 +161,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + SM_K + st * TILE2);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < ntile; ++i) {
           if (j > 0) {  // P_i(j-1) aliases S_i: PV_i(j-1) must have consumed it
             mbar_wait(&pv_done[i], (j - 1) & 1);
             tc_fence_after();
@@ -177,8 +178,7 @@ __global__ void __launch_bounds__(384, 1)
         mma_commit(&k_empty[st]);
         mbar_wait(&v_full[st], (j >> 1) & 1);
         const uint32_t sV = smem_u32(smem + SM_V + st * TILE2);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < ntile; ++i) {
           mbar_wait(&p_full[i], j & 1);
           tc_fence_after();
 #pragma unroll
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(q_full);
     }
     float m_ref = -INFINITY, l_sum = 0.f;
-    for (int j = 0; j < nt; ++j) {
+    const int nt_me = qt < ntile ? nt : 0;
+    for (int j = 0; j < nt_me; ++j) {
       mbar_wait(&s_full[qt], j & 1);
       tc_fence_after();
       float s[BN2];
@@ -296,9 +297,9 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(&p_full[qt]);
     }
-    // epilogue: wait for the last PV of this tile, O / l, LSE
-    if (nt > 0) {
-      mbar_wait(&pv_done[qt], (nt - 1) & 1);
+    // epilogue: wait for the last PV of this tile, O / l, LSE (an unused tile has no rows)
+    if (nt_me > 0) {
+      mbar_wait(&pv_done[qt], (nt_me - 1) & 1);
       tc_fence_after();
     }
     const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;

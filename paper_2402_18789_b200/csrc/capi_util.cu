@@ -25,6 +25,8 @@ extern "C" {
 
 const char* cs_last_error(void) { return cs::g_last_error.c_str(); }
 
+
+
 int cs_version(void) { return CS_ABI_VERSION; }
 
 int cs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,

@@ -78,6 +78,7 @@ void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, 
 __global__ void rmsnorm_kernel(const float* __restrict__ x, long ldx, const int* __restrict__ idx,
                                const float* __restrict__ g, bf16* __restrict__ out, long ldo,
                                float* __restrict__ rstd_out, int h, float eps, int use_norm) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   __shared__ float red[32];
   const long src_row = idx ? idx[blockIdx.x] : blockIdx.x;
   const float* xr = x + src_row * ldx;
@@ -124,6 +125,7 @@ void rmsnorm_cast_gather(const float* x, long ldx, const int* idx, const float* 
 
 // ---------------------------------------------------------------- RoPE + KV append
 __global__ void rope_append_kernel(RopeAppendParams p, const float2* __restrict__ cs_tab) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const int row = blockIdx.x;
   const int pos = p.row_pos[row];
   const AttnSeg sg = p.segs[p.row_seg[row]];
@@ -187,6 +189,7 @@ void rope_append(const RopeAppendParams& p, cudaStream_t st) {
 // ---------------------------------------------------------------- activations
 __global__ void act_kernel(const bf16* __restrict__ gu, long ld_gu, bf16* __restrict__ m,
                            long ldm, int f, int swiglu) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const long row = blockIdx.y;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c >= ldm) return;
@@ -224,6 +227,7 @@ void act_fwd(const bf16* gu, long ld_gu, bf16* m, long ldm, int rows, int f, int
 
 __global__ void lora_pack_kernel(const float* __restrict__ lu, int r, bf16* __restrict__ m,
                                  long ldm, int f, int rows) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= rows * r) return;
   const int row = t / r, j = t % r;
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
                                                  const int* __restrict__ tg, int V, float inv_norm,
                                                  float* __restrict__ loss, bf16* __restrict__ dlog,
                                                  long ldd) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   __shared__ float red_m[16], red_s[16];
   const int row = blockIdx.x;
   const float* x = logits + (long)row * ld;
@@ -374,6 +379,7 @@ __global__ void rms_bwd_kernel(const float* __restrict__ resid, long ldr,
                                const float* __restrict__ rstd, const float* __restrict__ dh,
                                long ldh, float* __restrict__ out, long ldo, bf16* __restrict__ ob,
                                long ldob, int h, int use_norm) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   __shared__ float red[32];
   const long row = blockIdx.x;
   const float* dr = dh + row * ldh;
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(256) mlp_bwd_kernel(const float* __restrict__ 
                                                       bf16* __restrict__ dgu, long ld_dgu,
                                                       float* __restrict__ dA, int rows, int f,
                                                       int swiglu) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   __shared__ __align__(16) float sl[MLP_ROWS * 16];
   const int col = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int r0 = blockIdx.y * MLP_ROWS;
@@ -489,6 +496,7 @@ void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const fl
 // dycat = [bf16(dY) | 0 (LoRA columns, filled by lora_pack after the dlu GEMM)]
 __global__ void dycat_cast_kernel(const float* __restrict__ dY, long ldy, int h,
                                   bf16* __restrict__ dycat, long ldc) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const long row = blockIdx.x;
   const float* y = dY + row * ldy;
   bf16* o = dycat + row * ldc;
@@ -506,6 +514,7 @@ __global__ void dycat_cast_kernel(const float* __restrict__ dY, long ldy, int h,
 __global__ void __launch_bounds__(256) lora_db_kernel(const float* __restrict__ dY, long ldy,
                                                       const float* __restrict__ lu, int r,
                                                       int rows, int h, float* __restrict__ dB) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   __shared__ __align__(16) float sl[MLP_ROWS * 16];
   const int col = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int r0 = blockIdx.y * MLP_ROWS;
@@ -553,6 +562,7 @@ __global__ void rope_bwd_pack_kernel(const float* __restrict__ dq, long ldq,
                                      long ld_acc, int a, int n_heads, int n_kv, int d,
                                      int use_rope, const float2* __restrict__ tab,
                                      bf16* __restrict__ out, long ldo) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   const int i = blockIdx.x;  // window-local row
   const int pos = a + i;
   const int half = d / 2;

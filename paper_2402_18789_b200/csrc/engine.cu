@@ -763,6 +763,7 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
   g.K = K;
   g.epi = epi;
   g.bias = bias;
+  g.b_const = 1;  // every engine GEMM's B operand is a (frozen or LoRA) weight
   e->launches++;
   cs_engine::ProfRec pr{};
   if (e->profiling) {
@@ -845,7 +846,22 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   std::vector<cs::AttnWork> work, work_tc, work_dec;
   std::vector<cs::AttnCombine> comb;
   const int rpt = 64 / e->grp;
-  const int rpt_tc = (e->use_fwd2 ? 2 : 1) * (128 / e->grp);
+  // tcgen05 attention items: two 128-row query tiles per CTA (v2) when the call has enough of
+  // them to fill ~2 waves of SMs, else one tile per CTA (more CTAs for small windows)
+  int rpt_tc = 128 / e->grp;
+  if (e->use_fwd2) {
+    long n2 = 0;
+    for (int s2 = 0; plan->segments && s2 < plan->n_segments; ++s2) {
+      const int ql = plan->segments[s2].q_len;
+      if (e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn && ql >= 16)
+        n2 += (long)((ql + 2 * rpt_tc - 1) / (2 * rpt_tc)) * e->Hkv;
+    }
+    static const bool one_tile = [] {  // measured slightly negative in the bench: off
+      const char* v = std::getenv("CS_ATTN_FWD2_1T");
+      return v && std::atoi(v) != 0;
+    }();
+    if (n2 >= 2L * 148 || !one_tile) rpt_tc *= 2;
+  }
   const bool tc_ok = e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn;
   double attn_flops = 0, attn_bytes = 0, tc_flops = 0, tc_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {

@@ -39,13 +39,20 @@ struct GemmArgs {
   void* C;
   long ldc;
   const float* bias;
+  int b_const;  // B is not written by the previous kernel on the stream (weights): its first
+                // stages may be fetched before griddepcontrol.wait
 };
 
-template <int BN>
+// SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
+// rows from whatever follows in shared memory and those accumulator rows are never stored.  The
+// freed 8 KB per stage go to more weight (B) stages in flight -- small-M GEMMs are weight
+// streams, bounded by the bytes each SM keeps in flight.
+template <int BN, bool SM = false>
 struct GemmCfg {
   static constexpr int BM = 128;
   static constexpr int BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_ROWS = SM ? 64 : 128;
+  static constexpr int A_BYTES = A_ROWS * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
@@ -128,11 +135,11 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int row, int c
   }
 }
 
-template <int BN>
+template <int BN, bool SM>
 __global__ void __launch_bounds__(256, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, SM>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -167,27 +174,47 @@ __global__ void __launch_bounds__(256, 1)
   // PDL: barrier init / TMEM alloc / descriptor prefetch above overlapped the previous kernel;
   // all CTAs of this persistent grid are resident, so the successor may start its prologue
   griddep_launch();
-  griddep_wait();
+  if (warp != 0 || lane != 0) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // weights do not depend on the previous kernel: the first tile's B stages are in flight
+      // before griddepcontrol.wait (the weight-stream fill overlaps the predecessor's tail)
+      int pre = 0;
+      if (args.b_const && (int)blockIdx.x < total) {
+        int mb, nb, kb0, kb1;
+        decode_work(blockIdx.x, args, mb, nb, kb0, kb1);
+        pre = min(Cfg::STAGES, kb1 - kb0);
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
+          tma_load_2d(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES,
+                      (kb0 + i) * Cfg::BK, nb * BN);
+        }
+      }
+      griddep_wait();
+      bool first = true;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         int mb, nb, kb0, kb1;
         decode_work(w, args, mb, nb, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * Cfg::BM);
-          tma_load_2d(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN);
+          if (first && kb - kb0 < pre) {  // B already issued for this stage
+            tma_load_2d(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * Cfg::BM);
+          } else {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * Cfg::BM);
+            tma_load_2d(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        first = false;
       }
     }
   } else if (warp == 1) {
@@ -376,27 +403,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch();
-  griddep_wait();
+  if (warp != 0 || lane != 0) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int pre = 0;  // first tile's B (weight) stages issued before griddepcontrol.wait
+      if (args.b_const && pair < total) {
+        int mb, nb, kb0, kb1;
+        decode_work(pair, args, mb, nb, kb0, kb1);
+        pre = min(Cfg::STAGES, kb1 - kb0);
+        for (int i = 0; i < pre; ++i) {
+          if (leader) mbar_arrive_expect_tx(&full_bar[i], 2 * Cfg::STAGE_BYTES);
+          tma_load_2d_2sm(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES,
+                          (kb0 + i) * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+        }
+      }
+      griddep_wait();
+      bool first = true;
       for (int w = pair; w < total; w += n_pairs) {
         int mb, nb, kb0, kb1;
         decode_work(w, args, mb, nb, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
-          tma_load_2d_2sm(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * 256 + (int)rank * 128);
-          tma_load_2d_2sm(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+          if (first && kb - kb0 < pre) {
+            tma_load_2d_2sm(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * 256 + (int)rank * 128);
+          } else {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_2sm(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * 256 + (int)rank * 128);
+            tma_load_2d_2sm(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        first = false;
       }
     }
   } else if (warp == 1) {
@@ -556,19 +601,19 @@ int make_map_3d(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, lo
 
 namespace {
 
-template <int BN>
+template <int BN, bool SM = false>
 cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
                       int grid, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, SM>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, SM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  return launch_pdl(gemm_tn_kernel<BN>, dim3(grid), dim3(256), Cfg::SMEM, st, ma, mb, a);
+  return launch_pdl(gemm_tn_kernel<BN, SM>, dim3(grid), dim3(256), Cfg::SMEM, st, ma, mb, a);
 }
 
 }  // namespace
@@ -593,9 +638,9 @@ bool use_2sm() {
   return on;
 }
 
-// 256 x 256 tiles on CTA pairs, persistent over the pairs (<= 74 pairs on 148 SMs)
+// 256 x BN tiles on CTA pairs, persistent over the pairs (<= 74 pairs on 148 SMs)
+template <int BN>
 cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
-  constexpr int BN = 256;
   using Cfg = Gemm2Cfg<BN>;
   GemmArgs a;
   a.M = (int)d.M;
@@ -608,6 +653,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.C = d.C;
   a.ldc = d.ldc;
   a.bias = d.bias;
+  a.b_const = d.b_const;
   a.splits = 1;
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
@@ -630,17 +676,48 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
+  static FILE* glog = [] {  // CS_GEMM_LOG=<file>: one line per GEMM (shape census, debugging)
+    const char* v = std::getenv("CS_GEMM_LOG");
+    return v ? std::fopen(v, "w") : nullptr;
+  }();
+  if (glog) std::fprintf(glog, "%ld %ld %ld %d\n", d.M, d.N, d.K, d.epi);
   if (d.K <= 0 || (d.K % 8) != 0 || (d.lda % 8) != 0 || (d.ldb % 8) != 0)
     return cudaErrorInvalidValue;
-  // large GEMMs (at least one wave of 256 x 256 tiles): CTA-pair kernel
-  if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 512 &&
-      ((d.M + 255) / 256) * ((d.N + 255) / 256) >= kNumSMs / 2)
-    return gemm_tn_2sm(d, st);
+  // large GEMMs (at least one wave of 256 x BN tiles): CTA-pair kernel
+  if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 256) {
+    const long mt = (d.M + 255) / 256;
+    if (d.M >= 512 && mt * ((d.N + 255) / 256) >= kNumSMs / 2) return gemm_tn_2sm<256>(d, st);
+    static const bool bn128 = [] {  // measured neutral-to-negative in the co-serving bench
+      const char* v = std::getenv("CS_GEMM_2SM128");
+      return v && std::atoi(v) != 0;
+    }();
+    if (bn128 && mt * ((d.N + 127) / 128) >= kNumSMs / 2) return gemm_tn_2sm<128>(d, st);
+  }
   int bn = d.bn > 0 ? d.bn : gemm_pick_bn(d.M, d.N);
   // small-M fp32-epilogue GEMMs (the O / down projections of inference-only rows): weight
   // streaming is latency-bound per CTA, so wider tiles split along K beat narrow tiles
   // (scripts/gemm_smallm.py: down T=64 38 us at bn 128 x 4 splits vs 51 us at bn 64 x 3)
-  const bool small_f32 = d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.M <= 256 && d.N >= 1024;
+  // M <= 64 (decode-only rows): half-height A stages (GemmCfg<.., true>), tile width chosen to
+  // minimise waves x bytes-per-stage, fp32 epilogues split along K over ~one wave
+  static const bool smallm_on = [] {
+    const char* v = std::getenv("CS_GEMM_SMALLM");
+    return !(v && std::atoi(v) == 0);
+  }();
+  const bool tiny_m = smallm_on && d.bn <= 0 && d.splits <= 0 && d.M <= 64 && d.N >= 1024;
+  if (tiny_m) {
+    if (d.epi == EPI_BF16) {
+      long best = -1;
+      for (int c : {256, 128, 64}) {  // >= 64: the MMA's phantom A rows stay inside the stage
+        const long waves = (((d.N + c - 1) / c) + kNumSMs - 1) / kNumSMs;
+        const long cost = waves * (8192 + (long)c * 128);
+        if (best < 0 || cost < best) best = cost, bn = c;
+      }
+    } else {
+      bn = 256;
+    }
+  }
+  const bool small_f32 = !tiny_m && d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.M <= 256 &&
+                         d.N >= 1024;
   if (small_f32) bn = 128;
   GemmArgs a;
   a.M = (int)d.M;
@@ -653,11 +730,12 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.C = d.C;
   a.ldc = d.ldc;
   a.bias = d.bias;
+  a.b_const = d.b_const;
   int splits = d.splits;
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {
     splits = 1;
-    if (small_f32) {
+    if (small_f32 || (tiny_m && d.epi != EPI_BF16)) {
       splits = (int)((kNumSMs + tiles / 2) / tiles);
       splits = std::max(1, std::min(splits, a.kb_total / 8));
     } else if (d.epi != EPI_BF16 && tiles < kNumSMs) {
@@ -675,10 +753,18 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
   const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
-  if (make_map(&ma, d.A, a_rows, d.K, d.lda, 128) != 0) return cudaErrorInvalidValue;
+  if (make_map(&ma, d.A, a_rows, d.K, d.lda, tiny_m ? 64 : 128) != 0) return cudaErrorInvalidValue;
   if (make_map(&mb, d.B, b_rows, d.K, d.ldb, bn) != 0) return cudaErrorInvalidValue;
   const long work = tiles * splits;
   const int grid = (int)std::min<long>(work, d.max_ctas > 0 ? d.max_ctas : kNumSMs);
+  if (tiny_m) {
+    switch (bn) {
+      case 64: return launch_bn<64, true>(ma, mb, a, grid, st);
+      case 128: return launch_bn<128, true>(ma, mb, a, grid, st);
+      case 256: return launch_bn<256, true>(ma, mb, a, grid, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (bn) {
     case 16: return launch_bn<16>(ma, mb, a, grid, st);
     case 32: return launch_bn<32>(ma, mb, a, grid, st);

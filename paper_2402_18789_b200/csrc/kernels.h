@@ -54,6 +54,7 @@ struct GemmDesc {
   int bn = 0;                   // 0 = heuristic
   int splits = 0;               // 0 = heuristic (fp32 epilogues only)
   int max_ctas = 0;             // 0 = #SMs
+  int b_const = 0;              // B not produced by the preceding kernel (weights): PDL prefetch
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);

@@ -24,7 +24,10 @@ def _gemm(A, B, C, epi, bias=None, bn=0, splits=0, M=None):
                                       (77, 96, 256, 32), (1000, 1536, 512, 0), (5, 16, 1088, 16),
                                       (4096, 4096, 4096, 0), (64, 6144, 4096, 0),
                                       # CTA-pair (cta_group::2) kernel: >= 74 tiles of 256 x 256
-                                      (3000, 4000, 1024, 0), (2048, 28672, 512, 0)])
+                                      (3000, 4000, 1024, 0), (2048, 28672, 512, 0),
+                                      (300, 6144, 1024, 0),
+                                      # M <= 64: half-height A stages
+                                      (64, 28672, 4096, 0), (17, 6144, 4096, 0), (40, 2048, 576, 0)])
 def test_gemm_bf16_out(cuda, M, N, K, bn):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
@@ -39,7 +42,8 @@ def test_gemm_bf16_out(cuda, M, N, K, bn):
 
 @pytest.mark.parametrize("M,N,K,splits", [(128, 256, 1024, 1), (64, 4096, 4096, 0), (256, 512, 2048, 4),
                                           (16, 4096, 14400, 0), (2048, 4096, 4096, 0),
-                                          (1500, 4104, 512, 0)])
+                                          (1500, 4104, 512, 0), (64, 4096, 14400, 0),
+                                          (33, 4096, 4096, 0)])
 def test_gemm_f32_add_splitk(cuda, M, N, K, splits):
     g = torch.Generator(device="cuda").manual_seed(3)
     A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
