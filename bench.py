@@ -204,15 +204,17 @@ def make_engine(device: int, ft_len: int):
 def offline_profile(eng, ft_len: int):
     """Fit f(c, s) = t0 + b (c + s) and the backward-token weight on this B200 (SPEC.md:395,
     PAPER.md §6.2 'derived via offline profiling').  Doubles as warm-up of every kernel."""
-    from paper_2402_18789_b200.engine import (Seg, SEG_DECODE, SEG_FT_FWD, FT_FORWARD,
+    from paper_2402_18789_b200.engine import (Seg, SEG_DECODE, SEG_PREFILL, SEG_FT_FWD, FT_FORWARD,
                                               FT_BACKWARD)
     P = 16
     n_dec, ctx = 32, 512
     base = 0
     dec_pages = []
-    for i in range(n_dec):
+    for i in range(64):
         dec_pages.append(list(range(base, base + ctx // P + 2)))
         base += ctx // P + 2
+    pf_pages = list(range(base, base + 512 // P + 1))
+    base += 512 // P + 1
     ft_pages = list(range(base, base + (ft_len + P - 1) // P))
 
     def decs(k=n_dec):
@@ -243,10 +245,14 @@ def offline_profile(eng, ft_len: int):
     toks = [(7 * i) % 1000 for i in range(ft_len)]
     ft_pass(2048, None, None)  # warm-up: first launches, TMA maps, attributes
     eng.reset_ft()
-    t_dec = []
-    for _ in range(3):
-        t_dec.append(eng.step(decs())["ms"])
-    t0 = min(t_dec)
+    # inference rows: decode-row slope from 16 vs 64 rows, prefill-token slope from a 512 chunk
+    t16 = min(eng.step(decs(16))["ms"] for _ in range(3))
+    t64 = min(eng.step(decs(64))["ms"] for _ in range(3))
+    d_row = max((t64 - t16) / 48.0, 0.0)
+    t_fixed = max(t16 - 16 * d_row, 0.1)
+    t0 = t_fixed + n_dec * d_row  # the profiling steps below carry n_dec decode rows
+    t_pf = min(eng.step(decs() + [Seg(SEG_PREFILL, toks[:512], 0, pf_pages)])["ms"] for _ in range(3))
+    pf_tok = max((t_pf - t0) / 512.0, 1e-6)
     fwd, bwd, layer0 = [], [], []
     ft_pass(1024, fwd, bwd)
     def linfit(xs, ys):
@@ -265,7 +271,8 @@ def offline_profile(eng, ft_len: int):
         s0, lj0, ms0 = layer0[0]
         full = wb * s0 + a_b * s0 * (lj0 - s0 / 2.0)
         w0 = min(1.0, max(0.05, (ms0 - t0) / full)) if full > 0 else 1.0
-    return {"t0_ms": t0, "slope_ms_per_token": b, "bwd_token_weight": max(wb, 1e-6) / b,
+    return {"t0_ms": t_fixed, "decode_ms_per_row": d_row, "prefill_ms_per_token": pf_tok,
+            "slope_ms_per_token": b, "bwd_token_weight": max(wb, 1e-6) / b,
             "attn_fwd_ms_per_token_ctx": a_f, "attn_bwd_ms_per_token_ctx": a_b,
             "bwd_layer0_weight": w0,
             "fwd_samples": fwd, "bwd_samples": bwd[:8]}
@@ -287,7 +294,8 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False)
     c.max_ft_window = 8192
     c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
                                prof["bwd_token_weight"], prof["attn_fwd_ms_per_token_ctx"],
-                               prof["attn_bwd_ms_per_token_ctx"], prof["bwd_layer0_weight"])
+                               prof["attn_bwd_ms_per_token_ctx"], prof["bwd_layer0_weight"],
+                               prof["decode_ms_per_row"], prof["prefill_ms_per_token"])
     c.multi_layer_bwd = 1
     c.ft_seq_len = ft_len
     c.growth_tokens = 128

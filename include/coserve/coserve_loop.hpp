@@ -185,6 +185,8 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       prof.slope_ms_per_token *= corr[cph];
       prof.attn_fwd_ms_per_token_ctx *= corr[cph];
       prof.attn_bwd_ms_per_token_ctx *= corr[cph];
+      prof.decode_ms_per_row *= corr[cph];
+      prof.prefill_ms_per_token *= corr[cph];
     }
     IterationPlan plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
     if (!enforce_dependencies(plan, ft)) {

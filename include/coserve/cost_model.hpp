@@ -28,8 +28,17 @@ struct LatencyProfile {
   // cost of a layer-0 backward window relative to another layer's (graph pruning leaves only
   // the MLP/LoRA part there); 1 = no distinction
   double bwd_layer0_weight = 1.0;
+  // Inference rows are not finetuning rows (no loss head, no saved activations): a measured
+  // profile charges decode rows and prefill tokens their own slopes (0 = the common slope).
+  double decode_ms_per_row = 0.0;
+  double prefill_ms_per_token = 0.0;
   bool has_ctx_terms() const { return attn_fwd_ms_per_token_ctx > 0 || attn_bwd_ms_per_token_ctx > 0; }
+  bool has_row_terms() const { return decode_ms_per_row > 0 || prefill_ms_per_token > 0; }
 };
+
+// Base cost of an iteration's inference rows (n_dec decode rows + n_pre prefill tokens); equals
+// latency(p, n_dec + n_pre, 0) unless the profile has per-kind row slopes.
+inline double inference_cost(const LatencyProfile& p, int64_t n_dec, int64_t n_pre);
 
 // t0 + b*min(c+s, k) + 2b*max(0, c+s-k)
 inline double latency(const LatencyProfile& p, int64_t c, int64_t s) {
@@ -55,6 +64,13 @@ inline int64_t max_finetune_tokens(const LatencyProfile& p, int64_t c, double sl
   while (s > 0 && latency(p, c, s) > slo_step_ms) --s;
   while (latency(p, c, s + 1) <= slo_step_ms) ++s;
   return s;
+}
+
+inline double inference_cost(const LatencyProfile& p, int64_t n_dec, int64_t n_pre) {
+  if (!p.has_row_terms()) return latency(p, n_dec + n_pre, 0);
+  const double d = p.decode_ms_per_row > 0 ? p.decode_ms_per_row : p.slope_ms_per_token;
+  const double f = p.prefill_ms_per_token > 0 ? p.prefill_ms_per_token : p.slope_ms_per_token;
+  return p.t0_ms + d * (double)n_dec + f * (double)n_pre;
 }
 
 // Marginal cost of finetuning windows on top of latency(c, 0) (profile with context terms).

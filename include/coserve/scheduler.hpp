@@ -173,7 +173,7 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
     return p;
   }
   // profile with context terms: exact argmax of the window cost within the remaining budget
-  const double base = latency(prof, c, 0);
+  const double base = inference_cost(prof, (int64_t)p.decode.size(), c - (int64_t)p.decode.size());
   double room = budget_ms - base;
   double cost = 0.0;
   if (ft.phase == FtPhase::Forward) {

@@ -196,6 +196,8 @@ typedef struct cs_latency_profile {
   double attn_fwd_ms_per_token_ctx; /* forward window extra: a_f * s * (l + s/2)         */
   double attn_bwd_ms_per_token_ctx; /* backward window extra: a_b * s * (l_j - s/2)      */
   double bwd_layer0_weight;  /* layer-0 (pruned) backward window cost factor; <= 0 -> 1     */
+  double decode_ms_per_row;    /* inference decode row slope; <= 0 -> slope_ms_per_token     */
+  double prefill_ms_per_token; /* inference prefill token slope; <= 0 -> slope_ms_per_token  */
 } cs_latency_profile;
 
 double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);

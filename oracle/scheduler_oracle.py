@@ -32,9 +32,23 @@ class Profile:
     attn_fwd: float = 0.0   # B200 runtime extension: context term of a forward window
     attn_bwd: float = 0.0   # ... of a backward window
     layer0: float = 1.0     # cost factor of a (pruned) layer-0 backward window
+    decode: float = 0.0     # per-decode-row slope of the inference rows (0 = slope)
+    prefill: float = 0.0    # per-prefill-token slope (0 = slope)
 
     def has_ctx(self):
         return self.attn_fwd > 0 or self.attn_bwd > 0
+
+    def has_rows(self):
+        return self.decode > 0 or self.prefill > 0
+
+
+def inference_cost(p: "Profile", n_dec: int, n_pre: int) -> float:
+    """coserve::inference_cost (include/coserve/cost_model.hpp)."""
+    if not p.has_rows():
+        return latency(p, n_dec + n_pre, 0)
+    d = p.decode if p.decode > 0 else p.slope
+    f = p.prefill if p.prefill > 0 else p.slope
+    return p.t0_ms + d * float(n_dec) + f * float(n_pre)
 
 
 def ft_fwd_cost(p: Profile, l: int, s: int) -> float:
@@ -291,7 +305,7 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
         s_eq = int(math.ceil(s * w_b)) if (phase == BWD and w_b != 1.0) else s
         pred = latency(prof, c, s_eq)
     else:
-        base = latency(prof, c, 0)
+        base = inference_cost(prof, len(decode), c - len(decode))
         room = budget - base
         cost = 0.0
         if ft.phase == FWD:

@@ -244,12 +244,12 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   const int d = lane * 4;
   for (int r = warp; r < c.nq * grp; r += 4) {
     float mx = -INFINITY;
-    for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, __ldg(p.part_lse + (long)(c.part0 + s) * 64 + r));
+    for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, __ldg(p.part_lse + (long)(c.part0 + s) * p.part_rows + r));
     float den = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (mx > -INFINITY) {
       for (int s = 0; s < c.n_parts; ++s) {
-        const long pr = (long)(c.part0 + s) * 64 + r;
+        const long pr = (long)(c.part0 + s) * p.part_rows + r;
         const float wgt = __expf(__ldg(p.part_lse + pr) - mx);
         den += wgt;
         if (d < D) {
@@ -673,6 +673,15 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
   } else {
     return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cudaStream_t st) {
+  if (n_combine <= 0) return cudaSuccess;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (head_dim == 128) attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
+  else if (head_dim == 64) attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

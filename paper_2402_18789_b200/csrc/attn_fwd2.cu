@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(384, 1)
   const int grp = p.grp;
   const int rpt = BM2 / grp;  // query positions per tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt = (w.k_end + BN2 - 1) / BN2;
+  // keys [k_begin, k_end) of the item (k_begin a multiple of 128; > 0 for split-KV parts)
+  const int j0 = w.k_begin / BN2;
+  const int nt = (w.k_end + BN2 - 1) / BN2 - j0;
   const int ntile = w.nq > rpt ? 2 : 1;  // query tiles of this item (small calls use 1)
 
   if (warp == 0 && lane == 0) {
@@ -144,11 +146,11 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&k_empty[st], ph);
         mbar_arrive_expect_tx(&k_full[st], TILE2);
         load_tile2(&tmK, &tmK128, &k_full[st], smem + SM_K + st * TILE2, p.page_table, sg.page_off,
-                   p.page_size, j * BN2, w.k_end, w.kv_head);
+                   p.page_size, (j0 + j) * BN2, w.k_end, w.kv_head);
         mbar_wait(&v_empty[st], ph);
         mbar_arrive_expect_tx(&v_full[st], TILE2);
         load_tile2(&tmV, &tmV128, &v_full[st], smem + SM_V + st * TILE2, p.page_table, sg.page_off,
-                   p.page_size, j * BN2, w.k_end, w.kv_head);
+                   p.page_size, (j0 + j) * BN2, w.k_end, w.kv_head);
       }
     } else if (warp == 1 && lane == 0) {
       // ------------------------------------------------------------ MMA issuer
@@ -198,10 +200,10 @@ __global__ void __launch_bounds__(384, 1)
     const int qt = (warp - 4) >> 2;       // query tile of this warpgroup
     const int ew = warp & 3;              // TMEM lane quarter
     const int r = ew * 32 + lane;         // packed row in the tile == TMEM lane
-    const int qr = qt * rpt + r / grp, g = r % grp;
+    const int qr = qt * rpt + r / grp, gi = r % grp;
     const bool valid = (r / grp) < rpt && qr < w.nq;
     const int pos = valid ? sg.ctx_start + w.q0 + qr : -1;
-    const int qh = w.kv_head * grp + g;
+    const int qh = w.kv_head * grp + gi;
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
     const uint32_t tS = tmem + lane_base + qt * 128;
     const uint32_t tO = tmem + lane_base + 256 + qt * 128;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       // raw scores: max first (scale > 0), masking only on tiles that touch the diagonal /
       // k_end; then x = s * scale_log2 - m (FFMA2), 2^x on the SFU, row sums on FADD2
-      const int kbase = j * BN2;
+      const int kbase = (j0 + j) * BN2;
       if (!(kbase + BN2 - 1 <= pos && kbase + BN2 <= w.k_end)) {
 #pragma unroll
         for (int i = 0; i < BN2; ++i)
@@ -303,27 +305,47 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
     }
     const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-    bf16* dst = p.out + (long)(sg.q_start + w.q0 + (valid ? qr : 0)) * p.out_ld + (long)qh * D2;
+    const float lse_v = l_sum > 0.f ? (m_ref + __log2f(l_sum)) * kLn2f : -INFINITY;
+    if (w.part >= 0) {
+      // split-KV part: normalised O (fp32) and LSE, dense (position, head) rows of the item;
+      // attn_combine_kernel (part_rows = 256) merges the parts
+      const long prow = (long)w.part * 256 + (long)(qr * grp + gi);
+      float* dst = p.part_o + prow * D2;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tO + c * 32, o);
-      tmem_ld_wait();
-      if (valid) {
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tO + c * 32, o);
+        tmem_ld_wait();
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c * 32 + i) =
+                make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                            __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
         }
       }
+      if (valid) p.part_lse[prow] = lse_v;
+    } else {
+      bf16* dst = p.out + (long)(sg.q_start + w.q0 + (valid ? qr : 0)) * p.out_ld + (long)qh * D2;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tO + c * 32, o);
+        tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
+          }
+        }
+      }
+      if (valid && p.lse) p.lse[(long)(sg.q_start + w.q0 + qr) * p.lse_ld + qh] = lse_v;
     }
-    if (valid && p.lse)
-      p.lse[(long)(sg.q_start + w.q0 + qr) * p.lse_ld + qh] =
-          l_sum > 0.f ? (m_ref + __log2f(l_sum)) * kLn2f : -INFINITY;
     tc_fence_before();
   }
   __syncthreads();

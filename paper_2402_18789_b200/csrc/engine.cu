@@ -736,7 +736,7 @@ struct StepPlan {
   int ft_row0 = 0;  // first FT forward row (== T if none)
   int ad_row0 = 0;  // first adapter row (== T if none)
   int n_samp = 0;
-  int n_work = 0, n_comb = 0, n_tc = 0, n_dec = 0;
+  int n_work = 0, n_comb = 0, n_tc = 0, n_dec = 0, n_comb_tc = 0;
   // device pointers into d_meta
   int *tokens, *row_pos, *row_seg, *page_table, *samp_idx, *targets;
   cs::AttnSeg* segs;
@@ -744,6 +744,7 @@ struct StepPlan {
   cs::AttnWork* work_tc;
   cs::AttnWork* work_dec;
   cs::AttnCombine* comb;
+  cs::AttnCombine* comb_tc;  // split-KV parts of the tcgen05 kernel (256-row parts)
   std::vector<int> samp_seg;  // segment of each sampled row
 };
 
@@ -844,7 +845,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   bool in_adapter_suffix = false;
   std::vector<int> samp_rows;
   std::vector<cs::AttnWork> work, work_tc, work_dec;
-  std::vector<cs::AttnCombine> comb;
+  std::vector<cs::AttnCombine> comb, comb_tc;
   const int rpt = 64 / e->grp;
   // tcgen05 attention items: two 128-row query tiles per CTA (v2) when the call has enough of
   // them to fill ~2 waves of SMs, else one tile per CTA (more CTAs for small windows)
@@ -1012,19 +1013,53 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     });
     work_dec.swap(w2);
   }
+  // tcgen05 items: when a call has few of them (a short window at a long context), split the
+  // key ranges into parts of >= 1024 keys so ~2 waves of SMs share the work (flash-decoding
+  // style; parts merged by the LSE combine) -- otherwise a 45-token window at 8K context ran
+  // on 8 CTAs
+  if (e->use_fwd2 && !work_tc.empty() && (long)work_tc.size() < 148) {
+    long total = 0;
+    for (const auto& w : work_tc) total += w.k_end;
+    long chunk = (total + 2L * 148 - 1) / (2L * 148);
+    chunk = std::max<long>(1024, (chunk + 127) / 128 * 128);
+    int part = 0;
+    std::vector<cs::AttnWork> w2;
+    for (const auto& w : work_tc) {
+      const int ns = (int)std::max<long>(1, (w.k_end + chunk / 2) / chunk);
+      if (ns <= 1 || part + ns > 1024) {
+        w2.push_back(w);
+        continue;
+      }
+      const long per = ((w.k_end + ns - 1) / ns + 127) / 128 * 128;
+      const int p0 = part;
+      for (int t = 0; t < ns && t * per < w.k_end; ++t) {
+        cs::AttnWork x = w;
+        x.k_begin = (int)(t * per);
+        x.k_end = (int)std::min<long>(w.k_end, (t + 1) * per);
+        x.part = part++;
+        w2.push_back(x);
+      }
+      comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
+    }
+    work_tc.swap(w2);
+  }
   // longest key ranges first (causal tiles have very different lengths)
   std::stable_sort(work_tc.begin(), work_tc.end(),
-                   [](const cs::AttnWork& x, const cs::AttnWork& y) { return x.k_end > y.k_end; });
+                   [](const cs::AttnWork& x, const cs::AttnWork& y) {
+                     return x.k_end - x.k_begin > y.k_end - y.k_begin;
+                   });
   sp.n_work = (int)work.size();
   sp.n_tc = (int)work_tc.size();
   sp.n_dec = (int)work_dec.size();
   sp.n_comb = (int)comb.size();
-  if (sp.n_work + sp.n_tc + sp.n_dec > 65536 || sp.n_comb > 8192)
+  sp.n_comb_tc = (int)comb_tc.size();
+  if (sp.n_work + sp.n_tc + sp.n_dec > 65536 || sp.n_comb + sp.n_comb_tc > 8192)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: attention work list too large");
   const size_t o_work = take(work.size() * sizeof(cs::AttnWork));
   const size_t o_wtc = take(work_tc.size() * sizeof(cs::AttnWork));
   const size_t o_wdec = take(work_dec.size() * sizeof(cs::AttnWork));
   const size_t o_comb = take(comb.size() * sizeof(cs::AttnCombine));
+  const size_t o_comb_tc = take(comb_tc.size() * sizeof(cs::AttnCombine));
   const size_t o_samp = take(samp_rows.size() * 4);
   const int ft_s = (plan->ft.phase == CS_FT_FORWARD) ? plan->ft.s : 0;
   const size_t o_tg = take((size_t)std::max(ft_s, 0) * 4);
@@ -1032,6 +1067,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   if (!work.empty()) std::memcpy(hb + o_work, work.data(), work.size() * sizeof(cs::AttnWork));
   if (!work_tc.empty()) std::memcpy(hb + o_wtc, work_tc.data(), work_tc.size() * sizeof(cs::AttnWork));
   if (!work_dec.empty()) std::memcpy(hb + o_wdec, work_dec.data(), work_dec.size() * sizeof(cs::AttnWork));
+  if (!comb_tc.empty()) std::memcpy(hb + o_comb_tc, comb_tc.data(), comb_tc.size() * sizeof(cs::AttnCombine));
   if (!comb.empty()) std::memcpy(hb + o_comb, comb.data(), comb.size() * sizeof(cs::AttnCombine));
   if (!samp_rows.empty()) std::memcpy(hb + o_samp, samp_rows.data(), samp_rows.size() * 4);
   if (ft_s > 0) {
@@ -1053,6 +1089,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.page_table = reinterpret_cast<int*>(db + o_pt);
   sp.work = reinterpret_cast<cs::AttnWork*>(db + o_work);
   sp.comb = reinterpret_cast<cs::AttnCombine*>(db + o_comb);
+  sp.comb_tc = reinterpret_cast<cs::AttnCombine*>(db + o_comb_tc);
   sp.work_tc = reinterpret_cast<cs::AttnWork*>(db + o_wtc);
   sp.work_dec = reinterpret_cast<cs::AttnWork*>(db + o_wdec);
   sp.samp_idx = reinterpret_cast<int*>(db + o_samp);
@@ -1165,10 +1202,17 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         tpr.kind = 3;
         prof_begin(e, tpr);
       }
-      if (e->use_fwd2)
+      if (e->use_fwd2) {
         CS_CUDA_TRY(cs::attn_fwd_tc2(tp, mk, mv, mk128, mv128, sp.n_tc, st));
-      else
+        if (sp.n_comb_tc > 0) {  // after the decode combine: the part buffers are reused
+          cs::AttnFwdParams cp = ap;
+          cp.combine = sp.comb_tc;
+          cp.part_rows = 256;
+          CS_CUDA_TRY(cs::attn_combine(cp, e->d, sp.n_comb_tc, st));
+        }
+      } else {
         CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      }
       if (e->profiling) prof_end(e, tpr);
     }
     if (n_ft > 0 && keep_attn) {

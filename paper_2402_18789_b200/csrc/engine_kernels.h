@@ -40,6 +40,7 @@ struct AttnFwdParams {
   float* part_lse;
   int grp;
   float scale_log2;
+  int part_rows = 64;  // rows per split-KV part in part_o / part_lse (combine)
 };
 
 struct AttnBwdParams {
@@ -72,6 +73,8 @@ struct AttnBwdParams {
 // attn_fwd, whose combine pass also merges the decode partials
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         int head_dim, int n_work, cudaStream_t st);
+// merge split-KV partials listed in p.combine (p.part_rows rows per part)
+cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cudaStream_t st);
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);

@@ -20,6 +20,8 @@ coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
   q.attn_fwd_ms_per_token_ctx = p->attn_fwd_ms_per_token_ctx;
   q.attn_bwd_ms_per_token_ctx = p->attn_bwd_ms_per_token_ctx;
   q.bwd_layer0_weight = p->bwd_layer0_weight > 0 ? p->bwd_layer0_weight : 1.0;
+  q.decode_ms_per_row = p->decode_ms_per_row > 0 ? p->decode_ms_per_row : 0.0;
+  q.prefill_ms_per_token = p->prefill_ms_per_token > 0 ? p->prefill_ms_per_token : 0.0;
   return q;
 }
 }  // namespace

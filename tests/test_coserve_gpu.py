@@ -360,3 +360,26 @@ def _run_coserve_on(eng, arch, W, toks, fwd, bwd):
             lj -= s
             if lj == 0:
                 break
+
+
+def test_tc_attention_split_kv_parity():
+    """Prefill chunks at long context on the tcgen05 attention kernel: few work items, so the
+    key ranges are split into parts merged by the LSE combine (flash-decoding style)."""
+    arch = ARCH_GQA4
+    W = O.init_general(arch, 13)
+    P = 16
+    L = 2600
+    eng = Engine(arch_config(arch, page_size=P, n_pages=256, max_tokens=1024, max_ft_len=16,
+                             max_segments=8))
+    eng.load_weights(W)
+    toks = [int(t) for t in np.random.default_rng(21).integers(0, arch.vocab, L)]
+    pages = list(range(200))[::-1][: (L + 8 + P - 1) // P]
+    cache = O.QkvCache(arch, L + 8)
+    diffs = []
+    for c0 in range(0, L, 512):
+        chunk = toks[c0:c0 + 512]
+        out = eng.step([Seg(SEG_PREFILL, chunk, c0, pages, sample=True)], want_logits=True)
+        lg, _ = O.forward_window(arch, W, chunk, c0, cache, lora=False)
+        diffs.append(O.scaled_err(out["logits"][0], lg[-1]))
+    assert max(diffs) < 0.04, diffs
+    eng.close()
