@@ -242,7 +242,10 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   const int grp = p.grp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = lane * 4;
-  for (int r = warp; r < c.nq * grp; r += 4) {
+  // blockIdx.y: 16-row slice of the item (a 256-row tcgen05 part needs 16 CTAs: one CTA per
+  // item left the merge latency-bound)
+  const int r_end = min(c.nq * grp, (int)(blockIdx.y + 1) * 16);
+  for (int r = blockIdx.y * 16 + warp; r < r_end; r += 4) {
     float mx = -INFINITY;
     for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, __ldg(p.part_lse + (long)(c.part0 + s) * p.part_rows + r));
     float den = 0.f;
@@ -656,7 +659,7 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
+      attn_combine_kernel<128><<<dim3(n_combine, 4), 128, 0, st>>>(p);
     }
   } else if (head_dim == 64) {
     constexpr int smem = 64 * 64 * 2 * 5;
@@ -668,7 +671,7 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
+      attn_combine_kernel<64><<<dim3(n_combine, 4), 128, 0, st>>>(p);
     }
   } else {
     return cudaErrorInvalidValue;
@@ -679,8 +682,9 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
 cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cudaStream_t st) {
   if (n_combine <= 0) return cudaSuccess;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (head_dim == 128) attn_combine_kernel<128><<<n_combine, 128, 0, st>>>(p);
-  else if (head_dim == 64) attn_combine_kernel<64><<<n_combine, 128, 0, st>>>(p);
+  const dim3 grid(n_combine, (p.part_rows + 15) / 16);
+  if (head_dim == 128) attn_combine_kernel<128><<<grid, 128, 0, st>>>(p);
+  else if (head_dim == 64) attn_combine_kernel<64><<<grid, 128, 0, st>>>(p);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
