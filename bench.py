@@ -37,12 +37,27 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+MODEL_NAMES = {"llama-3.1-8b": "LLaMA-3.1-8B", "qwen-2.5-14b": "Qwen-2.5-14B",
+               "qwen-2.5-32b": "Qwen-2.5-32B"}
 METRIC = "finetune tokens/s under inference SLO at N req/s; co-serve iteration ms"
 SLO_MS = 50.0
 
 # LLaMA-3.1-8B shape
 L8B = dict(n_layers=32, hidden=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn=14336,
            vocab=128256, lora_rank=16)
+# BASELINE.json configs 2-4; TPOT SLO per PAPER.md:430
+MODELS = {
+    "llama-3.1-8b": dict(shape=L8B, qkv_bias=0, rope_theta=500000.0, rms_eps=1e-5, slo_ms=50.0,
+                         n_pages=12288),
+    "qwen-2.5-14b": dict(shape=dict(n_layers=48, hidden=5120, n_heads=40, n_kv_heads=8,
+                                    head_dim=128, ffn=13824, vocab=152064, lora_rank=16),
+                         qkv_bias=1, rope_theta=1000000.0, rms_eps=1e-6, slo_ms=75.0,
+                         n_pages=12288),
+    "qwen-2.5-32b": dict(shape=dict(n_layers=64, hidden=5120, n_heads=40, n_kv_heads=8,
+                                    head_dim=128, ffn=27648, vocab=152064, lora_rank=16),
+                         qkv_bias=1, rope_theta=1000000.0, rms_eps=1e-6, slo_ms=75.0,
+                         n_pages=8192),
+}
 
 
 def parse():
@@ -54,6 +69,11 @@ def parse():
     ap.add_argument("--rate", type=float, default=20.0)
     ap.add_argument("--rates", default="4,10,20")
     ap.add_argument("--ft-len", type=int, default=8192)
+    ap.add_argument("--model", default="llama-3.1-8b", choices=sorted(MODELS))
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel degree (ranks per co-serving replica; NCCL under torchrun)")
+    ap.add_argument("--ft-window", type=int, default=8192,
+                    help="largest token-level finetuning window (config 3: 256 / 1024)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--log", default="")
     return ap.parse_args()
@@ -184,24 +204,26 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
-def make_engine(device: int, ft_len: int):
+def make_engine(device: int, ft_len: int, model: str = "llama-3.1-8b", tp_rank: int = 0,
+                tp_size: int = 1, uid=None):
     from paper_2402_18789_b200.engine import Engine, ModelConfig
+    m = MODELS[model]
     c = ModelConfig()
-    for k, v in L8B.items():
+    for k, v in m["shape"].items():
         setattr(c, k, v)
-    c.norm, c.act, c.rope, c.qkv_bias = 1, 1, 1, 0
-    c.rope_theta, c.rms_eps = 500000.0, 1e-5
+    c.norm, c.act, c.rope, c.qkv_bias = 1, 1, 1, m["qkv_bias"]
+    c.rope_theta, c.rms_eps = m["rope_theta"], m["rms_eps"]
     c.page_size = 16
-    c.n_pages = 12288          # 196,608 KV token slots per layer (~24 GiB of KV)
+    c.n_pages = m["n_pages"]   # 8B: 196,608 KV token slots per layer (~24 GiB of KV)
     c.max_tokens = 8192
     c.max_ft_len = ft_len
     c.max_segments = 96
-    eng = Engine(c, device=device)
+    eng = Engine(c, device=device, tp_rank=tp_rank, tp_size=tp_size, nccl_uid=uid)
     eng.init_random(1234)
     return eng
 
 
-def offline_profile(eng, ft_len: int):
+def offline_profile(eng, ft_len: int, n_layers: int = 32, max_window: int = 8192):
     """Fit f(c, s) = t0 + b (c + s) and the backward-token weight on this B200 (SPEC.md:395,
     PAPER.md §6.2 'derived via offline profiling').  Doubles as warm-up of every kernel."""
     from paper_2402_18789_b200.engine import (Seg, SEG_DECODE, SEG_PREFILL, SEG_FT_FWD, FT_FORWARD,
@@ -229,10 +251,10 @@ def offline_profile(eng, ft_len: int):
                                "targets": toks[l + 1:l + s + 1] + ([-1] if l + s == ft_len else [])})
             if record_f is not None:
                 record_f.append((s, l, out["ms"]))
-        for n in range(L8B["n_layers"] - 1, -1, -1):
+        for n in range(n_layers - 1, -1, -1):
             lj = ft_len
             while lj > 0:
-                s = min(2048 if n == L8B["n_layers"] - 1 else ft_len, lj)
+                s = min(2048 if n == n_layers - 1 else ft_len, max_window, lj)
                 out = eng.step(decs(), ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": lj,
                                            "s": s, "layer": n, "pages": ft_pages})
                 if record_b is not None and n >= 1:
@@ -243,7 +265,7 @@ def offline_profile(eng, ft_len: int):
         eng.adam_step(1e-4)
 
     toks = [(7 * i) % 1000 for i in range(ft_len)]
-    ft_pass(2048, None, None)  # warm-up: first launches, TMA maps, attributes
+    ft_pass(min(2048, max_window), None, None)  # warm-up: first launches, TMA maps, attributes
     eng.reset_ft()
     # inference rows: decode-row slope from 16 vs 64 rows, prefill-token slope from a 512 chunk
     t16 = min(eng.step(decs(16))["ms"] for _ in range(3))
@@ -254,7 +276,7 @@ def offline_profile(eng, ft_len: int):
     t_pf = min(eng.step(decs() + [Seg(SEG_PREFILL, toks[:512], 0, pf_pages)])["ms"] for _ in range(3))
     pf_tok = max((t_pf - t0) / 512.0, 1e-6)
     fwd, bwd, layer0 = [], [], []
-    ft_pass(1024, fwd, bwd)
+    ft_pass(min(1024, max_window), fwd, bwd)
     def linfit(xs, ys):
         mx, my = statistics.mean(xs), statistics.mean(ys)
         vx = sum((x - mx) ** 2 for x in xs)
@@ -278,20 +300,21 @@ def offline_profile(eng, ft_len: int):
             "fwd_samples": fwd, "bwd_samples": bwd[:8]}
 
 
-def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False):
+def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False,
+                   slo_ms=SLO_MS, max_window=8192):
     from paper_2402_18789_b200.engine import CoserveConfig, profile_struct
     c = CoserveConfig()
     c.rate_rps = rate
     c.duration_s = 3600.0
     c.burst_amplitude = 0.0
     c.burst_period_s = 60.0
-    c.tpot_slo_ms = SLO_MS
+    c.tpot_slo_ms = slo_ms
     c.ttft_slo_ms = 5000.0
-    c.budget_ms = 0.9 * SLO_MS   # planner budget; the adaptive correction tracks measured ms
+    c.budget_ms = 0.9 * slo_ms   # planner budget; the adaptive correction tracks measured ms
     c.max_batch = 64
     c.chunk_size = 512
     c.max_tokens = 8192
-    c.max_ft_window = 8192
+    c.max_ft_window = max_window
     c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
                                prof["bwd_token_weight"], prof["attn_fwd_ms_per_token_ctx"],
                                prof["attn_bwd_ms_per_token_ctx"], prof["bwd_layer0_weight"],
@@ -332,18 +355,40 @@ def run_ours(a):
     from paper_2402_18789_b200.engine import coserve_run
     from paper_2402_18789_b200.replicas import ft_rate_per_ms
 
+    m = MODELS[a.model]
+    n_layers = m["shape"]["n_layers"]
+    slo = m["slo_ms"]
+    tp = a.tp
+    if tp < 1 or world % tp != 0:
+        raise SystemExit(f"--tp {tp} must divide the number of ranks ({world})")
+    # ranks [g*tp, (g+1)*tp) form tensor-parallel group g (one co-serving replica); the group
+    # leader's ncclUniqueId reaches its ranks through the bench's own process group
+    group, tp_rank = rank // tp, rank % tp
+    uid = None
+    if tp > 1:
+        from paper_2402_18789_b200.engine import nccl_unique_id
+        mine = nccl_unique_id() if tp_rank == 0 else None
+        allu = [None] * world
+        dist.all_gather_object(allu, mine)
+        uid = allu[group * tp]
+
     t_setup = time.time()
-    eng = make_engine(local, a.ft_len)
-    prof = offline_profile(eng, a.ft_len)
+    eng = make_engine(local, a.ft_len, a.model, tp_rank, tp, uid)
+    prof = offline_profile(eng, a.ft_len, n_layers, a.ft_window)
+    if tp > 1:  # every rank of a group must plan with the same profile: the leader's
+        allp = [None] * world
+        dist.all_gather_object(allp, prof)
+        prof = allp[group * tp]
     rates = sorted({float(x) for x in a.rates.split(",") if x} | {a.rate})
     side = {}
     for r in rates:
         if r == a.rate:
             continue
         st, _ = coserve_run(eng, coserve_config(r, prof, min(a.steps, 60), a.warmup, a.ft_len,
-                                                seed=11 + int(r)))
+                                                seed=11 + int(r), slo_ms=slo,
+                                                max_window=a.ft_window))
         side[str(int(r) if r.is_integer() else r)] = {
-            "value": round(1000.0 * ft_rate_per_ms(st, L8B["n_layers"]), 1),
+            "value": round(1000.0 * ft_rate_per_ms(st, n_layers), 1),
             "iter_p99_ms": round(st["iter_p99_ms"], 2),
             "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4)}
     setup_s = time.time() - t_setup
@@ -354,7 +399,8 @@ def run_ours(a):
     torch.cuda.synchronize()
     clk.start()
     st, log = coserve_run(eng, coserve_config(a.rate, prof, a.steps, a.warmup, a.ft_len,
-                                               seed=7 + rank, profile_timed=True))
+                                               seed=7 + group, profile_timed=True, slo_ms=slo,
+                                               max_window=a.ft_window))
     torch.cuda.synchronize()
     clocks = clk.stop()
     if dist:
@@ -363,10 +409,11 @@ def run_ours(a):
     attn = eng.read_profile(1)
     attn_b = eng.read_profile(2)
     attn_tc = eng.read_profile(3)
+    comm = eng.read_profile(4)
 
-    n_layers = L8B["n_layers"]
     from paper_2402_18789_b200.replicas import aggregate
-    value, e2e = aggregate(st, n_layers, dist, device="cuda")
+    # a TP group is one replica: only its leader's finetuning progress counts
+    value, e2e = aggregate(st, n_layers, dist, device="cuda", count=(tp_rank == 0))
     dev_ms = st["timed_device_ms"]
     wall_ms = st["timed_ms"]
 
@@ -376,14 +423,14 @@ def run_ours(a):
     peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     gemm_tf = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else 0.0
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath) and a.model == "llama-3.1-8b":
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     cpu = None
-    if world == 1 and not a.no_cpu_baseline:
+    if world == 1 and not a.no_cpu_baseline and a.model == "llama-3.1-8b":
         try:
             from oracle import ref as R
             if R.available():
@@ -415,13 +462,15 @@ def run_ours(a):
         "dtype": "bf16",
         "data": "synthetic: random-init weights (reference init scales), Poisson arrivals, "
                 "lognormal ShareGPT-like lengths, random tokens",
-        "config": {"workload": "LLaMA-3.1-8B-shaped co-serving, LoRA r=16 on down-proj, "
-                               f"{a.rate:g} req/s Poisson arrivals per GPU, TPOT SLO {SLO_MS:g} ms, "
-                               f"finetuning sequences L={a.ft_len}",
-                   "model": "llama-3.1-8b-shaped", "rate_rps_per_gpu": a.rate,
-                   "ft_seq_len": a.ft_len, "parallelism": f"replicas x{world} (TP=1)",
+        "config": {"workload": f"{MODEL_NAMES[a.model]}-shaped co-serving, LoRA r=16 on down-proj, "
+                               f"{a.rate:g} req/s Poisson arrivals per replica, TPOT SLO {slo:g} ms, "
+                               f"finetuning sequences L={a.ft_len}"
+                               + (f", windows <= {a.ft_window}" if a.ft_window < a.ft_len else ""),
+                   "model": f"{a.model}-shaped", "rate_rps_per_replica": a.rate,
+                   "ft_seq_len": a.ft_len, "ft_window_max": a.ft_window,
+                   "parallelism": f"replicas x{world // tp} (TP={tp})",
                    "max_batch": 64, "chunk": 512,
-                   "l2": "working set (16 GB weights streamed per iteration) >> 126 MB L2"},
+                   "l2": "working set (>= 16 GB weights streamed per iteration) >> 126 MB L2"},
         "e2e": {"value": round(e2e, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all projections)",
@@ -437,13 +486,16 @@ def run_ours(a):
                       "decode_share": round(attn["ms"] / dev_ms, 4) if dev_ms else None,
                       "bwd_tflops": round(attn_b["flops"] / (attn_b["ms"] * 1e-3) / 1e12, 1) if attn_b["ms"] else None,
                       "bwd_share": round(attn_b["ms"] / dev_ms, 4) if dev_ms else None},
+        "tp_allreduce": ({"share": round(comm["ms"] / dev_ms, 4) if dev_ms else None,
+                          "busbw_gbs": round(comm["bytes"] / (comm["ms"] * 1e-3) / 1e9, 1) if comm["ms"] else None,
+                          "launches": comm["launches"]} if tp > 1 else None),
         "cpu_baseline": cpu,
         "gpu_launches": int(st["gpu_launches"]),
         "clocks": clocks,
         "inference": {"iter_p50_ms": round(st["iter_p50_ms"], 2),
                       "iter_p99_ms": round(st["iter_p99_ms"], 2),
                       "iter_max_ms": round(st["iter_max_ms"], 2),
-                      "slo_ms": SLO_MS,
+                      "slo_ms": slo,
                       "requests_done": st["requests_done"],
                       "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4),
                       "tpot_p99_ms": round(st["tpot_p99_ms"], 2),
@@ -457,7 +509,8 @@ def run_ours(a):
                     if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",
                              "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx",
                              "bwd_layer0_weight")},
-        "context": {"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200},
+        "context": ({"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200}
+                    if a.model == "llama-3.1-8b" else None),
         "setup_s": round(setup_s, 1),
         "profile_samples": {"fwd": [[s_, l_, round(m_, 2)] for s_, l_, m_ in prof["fwd_samples"]],
                             "bwd": [[s_, l_, round(m_, 2)] for s_, l_, m_ in prof["bwd_samples"]]},

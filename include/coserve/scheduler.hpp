@@ -60,7 +60,8 @@ struct SchedulerConfig {
   double tpot_slo_ms = 50.0;   // step budget = TPOT SLO
   double ttft_slo_ms = 5000.0;
   int max_tokens = 8192;       // engine capacity per iteration
-  int max_ft_window = 8192;    // cap on s
+  int max_ft_window = 8192;    // cap on s (multi_layer_bwd: on each backward window; an
+                               // iteration may then carry several windows of one layer)
   // B200 runtime extension: one iteration may carry consecutive backward windows across
   // layers (layer n to 0, then n-1 from L) when the budget allows -- Alg. 2 order is kept.
   // false reproduces SPEC.md:433 (one layer per iteration).
@@ -177,8 +178,12 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
   double room = budget_ms - base;
   double cost = 0.0;
   if (ft.phase == FtPhase::Forward) {
-    const int64_t cap = std::min<int64_t>({(int64_t)(ft.L - ft.l), (int64_t)cfg.max_ft_window,
-                                           (int64_t)cfg.max_tokens - c});
+    // multi-window iterations: consecutive forward windows fuse into one segment (Alg. 2
+    // windows are additive), so the window cap does not bind
+    const int64_t cap = cfg.multi_layer_bwd
+                            ? std::min<int64_t>((int64_t)(ft.L - ft.l), (int64_t)cfg.max_tokens - c)
+                            : std::min<int64_t>({(int64_t)(ft.L - ft.l), (int64_t)cfg.max_ft_window,
+                                                 (int64_t)cfg.max_tokens - c});
     const int64_t l0 = ft.l;
     const int64_t s = max_tokens_within([&](int64_t x) { return ft_fwd_cost(prof, l0, x); }, cap, room);
     if (s > 0) {
@@ -202,7 +207,11 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
       cost += cw;
       room -= cw;
       lj -= (int)s;
-      if (lj > 0 || !cfg.multi_layer_bwd) break;
+      if (!cfg.multi_layer_bwd) break;
+      if (lj > 0) {
+        if (s < cap) break;  // budget-bound: the iteration is full
+        continue;            // window-bound: the next window of the same layer
+      }
       layer -= 1;
       lj = ft.L;
     }

@@ -252,6 +252,10 @@ int64_t cs_engine_launch_count(cs_engine* e);
 int cs_engine_set_profiling(cs_engine* e, int on);
 int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops, double* bytes,
                            int64_t* launches);
+/* Max over the engine's TP group of n <= 8 host doubles, in place, identical on every rank
+ * (no-op at tp_size 1; every rank calls it, like cs_step).  cs_coserve_run uses it so the
+ * per-rank loops of one TP group see the same clock and plan the same iterations. */
+int cs_engine_tp_sync_max(cs_engine* e, double* vals, int n);
 /* model depth, vocab and KV pool geometry of an engine */
 int cs_engine_pool_info(cs_engine* e, int32_t* n_layers, int32_t* vocab, int32_t* page_size,
                         int64_t* n_pages);

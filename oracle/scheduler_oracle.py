@@ -309,7 +309,10 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
         room = budget - base
         cost = 0.0
         if ft.phase == FWD:
-            cap = min(ft.L - ft.l, max_ft_window, max_tokens - c)
+            # multi-window iterations: consecutive forward windows fuse into one segment
+            # (Alg. 2 windows are additive), so the window cap does not bind
+            cap = min(ft.L - ft.l, max_tokens - c) if multi_layer else \
+                min(ft.L - ft.l, max_ft_window, max_tokens - c)
             l0 = ft.l
             s = max_tokens_within(lambda x: ft_fwd_cost(prof, l0, x), cap, room)
             if s > 0:
@@ -329,8 +332,12 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
                 cost += cw
                 room -= cw
                 lj -= sw
-                if lj > 0 or not multi_layer:
+                if not multi_layer:
                     break
+                if lj > 0:
+                    if sw < cap:   # budget-bound: the iteration is full
+                        break
+                    continue       # window-bound: the next window of the same layer
                 ly -= 1
                 lj = ft.L
             if bwd:

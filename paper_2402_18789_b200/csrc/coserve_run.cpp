@@ -89,6 +89,12 @@ class GpuExecutor : public coserve::StepExecutor {
     out.next_tokens.assign(next_.begin(), next_.begin() + in.segs.size());
     out.ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     out.device_ms = r.iteration_ms;
+    // TP group: one loop per rank -> the clock must be rank-invariant (max over ranks), so
+    // every rank admits, plans and corrects identically
+    double clk[2] = {out.ms, out.device_ms};
+    if (cs_engine_tp_sync_max(e_, clk, 2) != CS_OK) return false;
+    out.ms = clk[0];
+    out.device_ms = clk[1];
     return true;
   }
   bool adam() override { return cs_adam_step(e_, 1e-4f, 0.9f, 0.999f, 1e-8f) == CS_OK; }

@@ -88,6 +88,7 @@ struct cs_engine {
   int* next_tok;
   unsigned long long* amax_part;
   float *part_o, *part_lse;
+  float* tp_sync;  // [8 ranks][8 values]: cs_engine_tp_sync_max
   // backward scratch
   bf16 *dycat, *dgu, *dr1b, *dO, *dqkv;
   float *dlu, *dm, *dh2, *dr1, *delta, *dq, *dh1;
@@ -263,6 +264,7 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(dq, S * e->q_dim);
   AL(dh1, S * h);
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
+  AL(tp_sync, 64);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
 #undef AL
@@ -500,6 +502,32 @@ extern "C" int cs_engine_pool_info(cs_engine* e, int32_t* n_layers, int32_t* voc
   if (vocab) *vocab = e->V;
   if (page_size) *page_size = e->P;
   if (n_pages) *n_pages = e->npages;
+  return CS_OK;
+}
+
+// Max over the TP group of n <= 8 host doubles (identical result on every rank; no-op at
+// tp_size 1).  The co-serving loop of a TP group runs once per rank and must plan the same
+// iteration on every rank: its clock (step wall / device ms) is made rank-invariant here.
+// Sum-only all-reduce: each rank writes its values into its own slot of a zeroed
+// [ranks][8] buffer, the sum then holds every rank's values, the host takes the max.
+extern "C" int cs_engine_tp_sync_max(cs_engine* e, double* vals, int n) {
+  if (!e || (!vals && n > 0) || n < 0 || n > 8)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "tp_sync_max: need an engine and 0 <= n <= 8");
+  if (!e->comm || n == 0) return CS_OK;
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  float h[64] = {};
+  for (int i = 0; i < n; ++i) h[e->tp_rank * 8 + i] = (float)vals[i];
+  CS_CUDA_TRY(cudaMemcpyAsync(e->tp_sync, h, sizeof(h), cudaMemcpyHostToDevice, e->st));
+  std::string err;
+  if (e->comm->allreduce_f32(e->tp_sync, 8 * e->tp_size, e->st, &err) != 0)
+    return cs::set_error(CS_ERR_NCCL, "tp_sync_max: " + err);
+  CS_CUDA_TRY(cudaMemcpyAsync(h, e->tp_sync, sizeof(h), cudaMemcpyDeviceToHost, e->st));
+  CS_CUDA_TRY(cudaStreamSynchronize(e->st));
+  for (int i = 0; i < n; ++i) {
+    float m = h[i];
+    for (int rk = 1; rk < e->tp_size; ++rk) m = std::max(m, h[rk * 8 + i]);
+    vals[i] = (double)m;
+  }
   return CS_OK;
 }
 

@@ -123,6 +123,8 @@ def _declare_engine(L):
     L.cs_engine_alloc_audit.restype = ctypes.c_int
     L.cs_engine_alloc_audit.argtypes = [vp, vp, vp, P(i64)]
     L.cs_engine_pool_info.restype = ctypes.c_int
+    L.cs_engine_tp_sync_max.restype = ctypes.c_int
+    L.cs_engine_tp_sync_max.argtypes = [vp, P(f64), ctypes.c_int]
     L.cs_engine_pool_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i64)]
     L.cs_sched_latency.restype = f64
     L.cs_sched_latency.argtypes = [P(LatencyProfileC), i64, i64]
@@ -433,6 +435,12 @@ class Engine:
         _lib.check(self._L.cs_engine_alloc_audit(self._h, ctypes.cast(cb, vp), None, ctypes.byref(tr)),
                    "alloc_audit")
         return recs, tr.value
+
+    def tp_sync_max(self, vals: Sequence[float]) -> List[float]:
+        """Max over this engine's TP group (every rank calls it; identity at tp_size 1)."""
+        buf = (f64 * len(vals))(*vals)
+        _lib.check(self._L.cs_engine_tp_sync_max(self._h, buf, len(vals)), "tp_sync_max")
+        return list(buf)
 
     def launch_count(self) -> int:
         return int(self._L.cs_engine_launch_count(self._h))

@@ -334,7 +334,7 @@ def test_alloc_audit_no_frozen_weight_gradients():
     size1 = {n: (el, b) for n, el, b in recs1}
     model_sized = {n for n, el, b in recs2 if b == 4 and size1.get(n) == (el, b)}
     allowed = {"gf", "bqkv", "g1", "g2", "loraA", "loraB", "gA", "gB", "mA", "vA", "mB", "vB",
-               "part_o", "part_lse"}
+               "part_o", "part_lse", "tp_sync"}
     assert model_sized <= allowed, model_sized - allowed
     NL, f, r, h = arch.n_layers, arch.ffn, arch.lora_rank, arch.hidden
     assert size1["gA"][0] == NL * f * r and size1["gB"][0] == NL * r * h
@@ -382,4 +382,35 @@ def test_tc_attention_split_kv_parity():
         lg, _ = O.forward_window(arch, W, chunk, c0, cache, lora=False)
         diffs.append(O.scaled_err(out["logits"][0], lg[-1]))
     assert max(diffs) < 0.04, diffs
+    eng.close()
+
+
+ARCH_QWEN5 = O.Arch(n_layers=2, hidden=640, n_heads=10, n_kv_heads=2, head_dim=128, ffn=512,
+                    vocab=128, lora_rank=16, norm="rms", act="swiglu", rope=True, qkv_bias=True,
+                    rope_theta=1000000.0)
+
+
+def test_qwen_geometry_gqa5_parity():
+    """Qwen-2.5 head geometry (40 q / 8 kv heads -> GQA group 5, d=128,
+    QKV bias, rope theta 1e6) scaled down: a group that does not divide the 128-row packed
+    query tiles (25 positions x 5 heads + 3 pad rows) on the tcgen05 forward, the decode kernel
+    (5 rows of the m16 tile) and the backward (group 5 does not divide 64 -> the tile kernel)."""
+    arch = ARCH_QWEN5
+    W = O.init_general(arch, 17)
+    toks = list(np.random.default_rng(23).integers(0, arch.vocab, 300))
+    tr = O.forward_full(arch, W, toks)
+    bw = O.backward_full(arch, W, tr)
+    eng, loss_sum, kvg, dys, _ = _run_coserve(arch, W, toks, [100, 200], [150, 150], n_inf=5,
+                                              logit_tol=0.04)
+    assert O.rel_err(loss_sum / 299.0, tr["loss"]) < TOL
+    for l in range(arch.n_layers):
+        ga, gb = eng.lora_grads(l)
+        assert O.max_rel_err(ga, bw["grads"]["a"][l]) < TOL, l
+        assert O.max_rel_err(gb, bw["grads"]["b"][l]) < TOL, l
+        assert O.scaled_err(ga, bw["grads"]["a"][l]) < FLOOR_DEEP, l
+        assert O.scaled_err(gb, bw["grads"]["b"][l]) < FLOOR_DEEP, l
+    dk, dv = kvg[1]
+    assert O.scaled_err(dk, bw["layers"][1]["dk"]) < FLOOR_DEEP
+    assert O.scaled_err(dv, bw["layers"][1]["dv"]) < FLOOR_DEEP
+    assert O.scaled_err(dys[1], bw["layers"][1]["dx"]) < FLOOR_DEEP
     eng.close()

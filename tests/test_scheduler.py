@@ -7,7 +7,7 @@ from paper_2402_18789_b200 import engine as E
 
 
 def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth=128,
-         max_batch=64, chunk=512, budget=50.0, amplitude=0.0, multi_layer=False):
+         max_batch=64, chunk=512, budget=50.0, amplitude=0.0, multi_layer=False, window=8192):
     c = E.CoserveConfig()
     c.rate_rps = rate
     c.duration_s = 600.0
@@ -19,7 +19,7 @@ def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth
     c.max_batch = max_batch
     c.chunk_size = chunk
     c.max_tokens = 8192
-    c.max_ft_window = 8192
+    c.max_ft_window = window
     c.profile = E.profile_struct(prof.t0_ms, prof.slope, 0.0 if prof.knee == S.INF else prof.knee,
                                  prof.bwd_weight, prof.attn_fwd, prof.attn_bwd, prof.layer0)
     c.multi_layer_bwd = 1 if multi_layer else 0
@@ -89,6 +89,28 @@ def test_sim_plans_bit_exact_ctx_multilayer(case):
             assert a["pred_ms"] <= budget + 1e-9
     assert multi > 0  # some iterations carried windows of several layers
     assert stats["minibatches_done"] >= 1
+
+
+@pytest.mark.parametrize("window", [256, 1024])
+def test_sim_plans_bit_exact_small_windows(window):
+    """BASELINE config 3's token-level windows of 256 / 1024: with multi-window iterations a
+    window-bound backward iteration carries several consecutive windows of one layer (and the
+    forward fuses consecutive windows); C++ plans == Python restatement, bit-exact."""
+    prof = S.Profile(7.0, 0.02, S.INF, 0.06, 1.5e-6, 1e-7, 0.3)
+    stats, log = E.coserve_run(None, _cfg(20.0, prof, 400, 8192, 48, 9, 32, 8192, 128,
+                                          budget=67.5, multi_layer=True, window=window))
+    w = S.Workload(rate=20.0, duration_s=600.0, amplitude=0.0, period_s=20.0)
+    ref = S.run(prof, w, 9, 48, 16, 8192, 128, 8192, 400, prepopulate=32, budget=67.5,
+                multi_layer=True, max_ft_window=window)
+    same_layer = 0
+    for i, (a, b) in enumerate(zip(log, ref)):
+        for k in ("c", "s", "phase", "layer", "l", "n_decode", "n_prefill", "n_running", "n_queue"):
+            assert a[k] == b[k], (i, k, a[k], b[k])
+        assert a["t_ms"] == b["t_ms"] and a["pred_ms"] == b["pred"], i
+        assert all(sw <= window for _, _, sw in b["bwd"])
+        layers = [ly for ly, _, _ in b["bwd"]]
+        same_layer += len(layers) != len(set(layers))
+    assert same_layer > 0  # window-bound iterations packed several windows of one layer
 
 
 def test_token_accounting_and_work_conservation():

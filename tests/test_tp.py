@@ -220,3 +220,40 @@ def test_tp2_engine_matches_oracle_and_tp1():
         e.close()
     single.close()
     group.close()
+
+
+@pytest.mark.gpu
+def test_tp2_coserve_loop_ranks_plan_identically():
+    """A TP group runs the C++ co-serving loop once per rank (cs_coserve_run): the step clock
+    is max-reduced over the group (cs_engine_tp_sync_max), so both ranks admit, plan, correct
+    and log exactly the same iterations (no host broadcast of plans needed)."""
+    from paper_2402_18789_b200.engine import (CoserveConfig, Engine, TPGroup, arch_config,
+                                              coserve_run, profile_struct, tp_run)
+    arch = ARCH
+    cfg = arch_config(arch, page_size=16, n_pages=2048, max_tokens=1024, max_ft_len=256,
+                      max_segments=80)
+    group = TPGroup(2)
+    ranks = [Engine(cfg, device=0, tp_rank=r, group=group) for r in range(2)]
+    tp_run(ranks, lambda e: e.init_random(5))
+    vals = tp_run(ranks, lambda e: e.tp_sync_max([1.0 + e.tp_rank, 7.0 - e.tp_rank]))
+    assert vals[0] == vals[1] == [2.0, 7.0]
+    c = CoserveConfig()
+    c.rate_rps, c.duration_s, c.burst_period_s = 40.0, 600.0, 60.0
+    c.tpot_slo_ms, c.ttft_slo_ms, c.budget_ms = 50.0, 5000.0, 20.0
+    c.max_batch, c.chunk_size, c.max_tokens, c.max_ft_window = 32, 128, 1024, 1024
+    c.profile = profile_struct(0.5, 0.002, 0.0, 0.5)
+    c.multi_layer_bwd, c.ft_seq_len, c.growth_tokens = 1, 256, 32
+    c.warmup_iters, c.timed_iters, c.prepopulate, c.adaptive, c.seed = 2, 60, 8, 1, 3
+    res = tp_run(ranks, lambda e: coserve_run(e, c))
+    (st0, log0), (st1, log1) = res
+    assert len(log0) == len(log1) > 0
+    keys = ("t_ms", "pred_ms", "ms", "device_ms", "c", "s", "phase", "layer", "l", "n_decode",
+            "n_prefill", "n_running", "n_queue")
+    for a, b in zip(log0, log1):
+        assert all(a[k] == b[k] for k in keys), (a, b)
+    for k in ("ft_fwd_tokens", "ft_bwd_tokens", "requests_done", "gen_tokens", "iter_p99_ms"):
+        assert st0[k] == st1[k], k
+    assert st0["ft_fwd_tokens"] > 0 and st0["gen_tokens"] > 0
+    for e in ranks:
+        e.close()
+    group.close()
