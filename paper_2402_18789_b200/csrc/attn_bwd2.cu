@@ -132,6 +132,11 @@ constexpr int SMEM_BAR = SMEM_X + 2 * 2 * 2 * QB * 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 }  // namespace kv2
 
+// GRP: GQA group (query heads per KV head).  A 64-row packed query tile holds RPT = 64 / GRP
+// positions x GRP heads = ROWS rows; when GRP does not divide 64 (Qwen-2.5: 40 / 8 = 5 -> 60
+// rows) the last 64 - ROWS rows of every Q / dO stage are zeroed once and never written by
+// TMA (finite zeros: their P^T / dS^T columns are masked to 0, and 0 x stale NaN would not be)
+template <int GRP>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmK128,
@@ -153,9 +158,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* acc_done = buf_free + NB;          // all dV/dK MMAs done (completes once)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
-  const int grp = p.grp;
-  const int lg = __ffs(grp) - 1;           // grp is a power of two (QB % grp == 0)
-  const int rpt = QB / grp;                // positions per query tile
+  constexpr int grp = GRP;
+  constexpr int rpt = QB / GRP;            // positions per query tile
+  constexpr int ROWS = rpt * GRP;          // real packed rows per tile (<= QB)
   const int k0 = blockIdx.x * 128;
   const int kvh = blockIdx.y;
   const int nrows = p.b - p.a;
@@ -180,6 +185,14 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
+  if constexpr (ROWS < QB) {  // pad rows [ROWS, QB) of every Q / dO stage, both 128-B halves
+    constexpr int PADB = (QB - ROWS) * 128;
+    for (int i = threadIdx.x; i < 2 * QST * 2 * (PADB / 16); i += blockDim.x) {
+      const int half = i / (PADB / 16), o = (i % (PADB / 16)) * 16;  // half: (Q|O, stage, h)
+      *reinterpret_cast<uint4*>(smem + SMEM_Q + half * HALFQ + ROWS * 128 + o) = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+  }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -200,7 +213,7 @@ __global__ void __launch_bounds__(384, 1)
         const int st = i % QST;
         const int qt = qt0 + i;
         mbar_wait(&q_empty[st], ((i / QST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[st], 2 * QTILE);
+        mbar_arrive_expect_tx(&q_full[st], 2 * 2 * ROWS * 128);
         for (int h = 0; h < 2; ++h) {
           tma_load_3d(&tmQ3, &q_full[st], smem + SMEM_Q + st * QTILE + h * HALFQ, h * 64, kvh * grp,
                       p.a + qt * rpt);
@@ -280,7 +293,7 @@ __global__ void __launch_bounds__(384, 1)
       float v = 0.f;
       if (i < n && tw < 2 * QB) {
         const int col = tw & (QB - 1);
-        const int qr = (qt0 + i) * rpt + (col >> lg), g = col & (grp - 1);
+        const int qr = (qt0 + i) * rpt + col / grp, g = col % grp;
         if (qr < nrows) {
           if (tw < QB) v = p.lse[(long)(p.a + qr) * p.lse_ld + kvh * grp + g] * kLog2eC;
           else v = p.delta[(long)qr * p.delta_ld + kvh * grp + g];
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       if (tw == 0) trace_ev(40 + wg, i);
       // full tile: every column is a real row whose position >= key, and the key is in range
-      const bool full = key < p.b && key <= p.a + qbase && qbase + ((QB - 1) >> lg) < nrows;
+      const bool full = key < p.b && key <= p.a + qbase && qbase + rpt - 1 < nrows;
       // 32-column chunks (register budget); the packed P^T / dS^T of chunk h land on TMEM
       // columns [16h, 16h+16), i.e. over S^T / dP^T columns this thread has already read
 #pragma unroll 1
@@ -317,9 +330,13 @@ __global__ void __launch_bounds__(384, 1)
                            make_float2(-xs[c], -xs[c + 1]));
           float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
           if (!full) {
-            const int q0r = qbase + (c >> lg), q1r = qbase + ((c + 1) >> lg);
+            const int q0r = qbase + c / grp, q1r = qbase + (c + 1) / grp;
             if (!(q0r < nrows && key <= p.a + q0r && key < p.b)) pv.x = 0.f;
             if (!(q1r < nrows && key <= p.a + q1r && key < p.b)) pv.y = 0.f;
+          }
+          if constexpr (ROWS < QB) {  // pad columns (q0r above may alias the next tile's rows)
+            if (c >= ROWS) pv.x = 0.f;
+            if (c + 1 >= ROWS) pv.y = 0.f;
           }
           const float2 dd = fadd2(make_float2(__uint_as_float(dv[cc]), __uint_as_float(dv[cc + 1])),
                                   make_float2(-xs[QB + c], -xs[QB + c + 1]));
@@ -625,19 +642,27 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+using Dkdv2Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const CUtensorMap, const CUtensorMap, AttnBwdParams);
+static const Dkdv2Fn kDkdv2[8] = {attn_bwd_dkdv2_kernel<1>, attn_bwd_dkdv2_kernel<2>,
+                                  attn_bwd_dkdv2_kernel<3>, attn_bwd_dkdv2_kernel<4>,
+                                  attn_bwd_dkdv2_kernel<5>, attn_bwd_dkdv2_kernel<6>,
+                                  attn_bwd_dkdv2_kernel<7>, attn_bwd_dkdv2_kernel<8>};
+
 cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          const CUtensorMap& tmK128, const CUtensorMap& tmV128,
                          const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
                          cudaStream_t st) {
   const int rows = p.b - p.a;
   if (rows <= 0) return cudaSuccess;
-  static bool once = (cudaFuncSetAttribute(attn_bwd_dq2_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           dq2::SMEM_TOTAL),
-                      cudaFuncSetAttribute(attn_bwd_dkdv2_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kv2::SMEM_TOTAL),
-                      true);
+  if (p.grp < 1 || p.grp > 8) return cudaErrorInvalidValue;
+  static bool once = [] {
+    cudaFuncSetAttribute(attn_bwd_dq2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         dq2::SMEM_TOTAL);
+    for (auto k : kDkdv2)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kv2::SMEM_TOTAL);
+    return true;
+  }();
   (void)once;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   attn_bwd_delta_kernel_launch(p, rows, n_heads, st);
@@ -651,8 +676,8 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
   }();
   if (mask & 1) attn_bwd_dq2_kernel<<<gq, 384, dq2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, p);
   else attn_bwd_dq_v1(p, tmK, tmV, tmK128, tmV128, gq, st);
-  if (mask & 2)
-    attn_bwd_dkdv2_kernel<<<gk, 384, kv2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
+  if ((mask & 2) || (64 % p.grp) != 0)
+    kDkdv2[p.grp - 1]<<<gk, 384, kv2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
   else attn_bwd_dkdv_v1(p, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, gk, st);
   return cudaGetLastError();
 }

@@ -1398,12 +1398,15 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       bpr.kind = 2;
       prof_begin(e, bpr);
     }
-    const bool bwd_tc = e->use_tc_attn && e->d == 128 && (e->P % 16) == 0 && (64 % e->grp) == 0;
+    // v2 takes any GQA group <= 8 (groups that do not divide 64 leave pad rows in a query
+    // tile); the v1 kernels need 64 % group == 0
+    const bool bwd_tc = e->use_tc_attn && e->d == 128 && (e->P % 16) == 0 &&
+                        (e->use_bwd2 ? e->grp <= 8 : (64 % e->grp) == 0);
     if (bwd_tc) {
       CUtensorMap mk, mv, mk128, mv128, mq3, mo3;
       const long pool_rows = (long)e->npages * e->P;
       const bool v2 = e->use_bwd2;
-      const int qbox = 64 / e->grp;  // 3-D boxes: 64 packed (position, head) rows
+      const int qbox = 64 / e->grp;  // 3-D boxes: 64 / grp positions x grp heads packed rows
       if (cs::make_map(&mk, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mv, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mk128, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 128) != 0 ||
