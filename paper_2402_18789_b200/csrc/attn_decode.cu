@@ -18,7 +18,9 @@
 // in the loop: the algorithmic traffic is 2 * ctx * d * 2 B per (request, kv head).
 #include <cfloat>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "engine_kernels.h"
@@ -28,30 +30,30 @@
 namespace cs {
 
 namespace {
-constexpr int KT = 32;      // keys per warp tile (two 16-row TMA boxes)
-constexpr int STAGES = 3;   // TMA ring depth per warp
-constexpr int NWARP = 4;
 constexpr float kLn2 = 0.6931471805599453f;
 
-template <int D>
+template <int D, int KT>
 constexpr int stage_bytes() {
   return 2 * KT * D * 2;  // K + V
 }
-template <int D>
+template <int D, int KT, int NWARP, int STAGES>
 constexpr int dec_smem() {
-  return 1024 + NWARP * STAGES * stage_bytes<D>() + NWARP * STAGES * 8;
+  return 1024 + NWARP * STAGES * stage_bytes<D, KT>() + NWARP * STAGES * 8;
 }
 
 CS_DEV uint32_t ld_u32(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
 
 // byte offset of 16-byte chunk c (0..D/8-1) of key row r in a [KT x D] bf16 tile that TMA
 // wrote as D/64 column halves of [KT rows x 128 B] with SWIZZLE_128B
+template <int KT>
 CS_DEV uint32_t tile_off(int r, int c) {
   return (uint32_t)((c >> 3) * (KT * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 }  // namespace
 
-template <int D>
+// NWARP warps per CTA, each with a STAGES-deep ring; (NWARP, STAGES) set the CTAs per SM
+// (shared memory) and so how many items' prologues / epilogues overlap other items' streams
+template <int D, int KT, int NWARP, int STAGES>
 __global__ void __launch_bounds__(NWARP * 32, 1)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        AttnFwdParams p) {
@@ -62,8 +64,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
-  const AttnWork w = p.work[blockIdx.x];
-  const AttnSeg sg = p.segs[w.seg];
+  const AttnDecWork* wp = p.dwork + blockIdx.x;
+  struct {
+    int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
+  } w;
+  {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(wp));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(wp) + 1);
+    w = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = p.grp;
   const int nrows = w.nq * grp;  // <= 16
@@ -91,7 +100,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 #pragma unroll
     for (int b = 0; b < KT / 16; ++b) {
       const int jb = min(kt * KT + b * 16, last_box);
-      const int prow = __ldg(p.page_table + sg.page_off + jb / p.page_size) * p.page_size + jb % p.page_size;
+      const int bi = (jb - w.k_begin) >> 4;  // host-resolved rows for the first 8 boxes
+      const int prow = bi < 8 ? __ldg(wp->prow + bi)
+                              : __ldg(p.page_table + w.page_off + jb / p.page_size) * p.page_size + jb % p.page_size;
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh) {
         const int col = w.kv_head * D + hh * 64;
@@ -111,9 +122,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   const __nv_bfloat16* qa = nullptr;
   const __nv_bfloat16* qb = nullptr;
   if (ra < nrows)
-    qa = p.q + (long)(sg.q_start + w.q0 + ra / grp) * p.q_ld + (long)(w.kv_head * grp + ra % grp) * D;
+    qa = p.q + (long)(w.q_row + ra / grp) * p.q_ld + (long)(w.kv_head * grp + ra % grp) * D;
   if (rb < nrows)
-    qb = p.q + (long)(sg.q_start + w.q0 + rb / grp) * p.q_ld + (long)(w.kv_head * grp + rb % grp) * D;
+    qb = p.q + (long)(w.q_row + rb / grp) * p.q_ld + (long)(w.kv_head * grp + rb % grp) * D;
   uint32_t qf[D / 16][4];
 #pragma unroll
   for (int kk = 0; kk < D / 16; ++kk) {
@@ -123,8 +134,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     qf[kk][2] = qa ? ld_u32(qa + col + 8) : 0u;
     qf[kk][3] = qb ? ld_u32(qb + col + 8) : 0u;
   }
-  const int pos_a = ra < nrows ? sg.ctx_start + w.q0 + ra / grp : -1;
-  const int pos_b = rb < nrows ? sg.ctx_start + w.q0 + rb / grp : -1;
+  const int pos_a = ra < nrows ? w.pos0 + ra / grp : -1;
+  const int pos_b = rb < nrows ? w.pos0 + rb / grp : -1;
 
   float o[D / 8][4];
 #pragma unroll
@@ -146,7 +157,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 #pragma unroll
       for (int nbp = 0; nbp < KT / 16; ++nbp) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + tile_off(nbp * 16 + (lane & 7) + ((lane >> 4) << 3), kk * 2 + ((lane >> 3) & 1)),
+        ldsm_x4(kb + tile_off<KT>(nbp * 16 + (lane & 7) + ((lane >> 4) << 3), kk * 2 + ((lane >> 3) & 1)),
                 b0, b1, b2, b3);
         mma16816(s[2 * nbp], qf[kk], b0, b1);
         mma16816(s[2 * nbp + 1], qf[kk], b2, b3);
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 #pragma unroll
       for (int dp = 0; dp < D / 16; ++dp) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + tile_off(kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), dp * 2 + (lane >> 4)),
+        ldsm_x4_t(vb + tile_off<KT>(kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), dp * 2 + (lane >> 4)),
                   b0, b1, b2, b3);
         mma16816(o[2 * dp], a, b0, b1);
         mma16816(o[2 * dp + 1], a, b2, b3);
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     const float lse = L > 0.f ? (M + __log2f(L)) * kLn2 : -INFINITY;
     const int qr = r / grp, g = r - qr * grp;
     if (w.part < 0) {
-      const long row = sg.q_start + w.q0 + qr;
+      const long row = w.q_row + qr;
       const int qh = w.kv_head * grp + g;
       __nv_bfloat16* dst = p.out + row * p.out_ld + (long)qh * D + d;
       *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc.x * inv, acc.y * inv);
@@ -283,29 +294,66 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   }
 }
 
+namespace {
+struct DecVariant {
+  int kt, nwarp, stages;
+};
+// CS_DEC_CFG=<kt><nwarp><stages> (A/B testing), e.g. 3243 = 32-key tiles, 4 warps x 3 stages
+DecVariant dec_variant() {
+  static const DecVariant v = [] {
+    DecVariant d{32, 2, 2};
+    if (const char* e = std::getenv("CS_DEC_CFG")) {
+      const int x = std::atoi(e);
+      d = DecVariant{x / 100, (x / 10) % 10, x % 10};
+    }
+    return d;
+  }();
+  return v;
+}
+
+template <int D, int KT, int NW, int ST>
+cudaError_t launch_dec(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                       int n_work, cudaStream_t st) {
+  constexpr int smem = dec_smem<D, KT, NW, ST>();
+  static bool once = (cudaFuncSetAttribute(attn_decode_kernel<D, KT, NW, ST>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                      true);
+  (void)once;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  attn_decode_kernel<D, KT, NW, ST><<<n_work, NW * 32, smem, st>>>(tmK, tmV, p);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                         int n_work, cudaStream_t st) {
+  const DecVariant v = dec_variant();
+  switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
+    case 3243: return launch_dec<D, 32, 4, 3>(p, tmK, tmV, n_work, st);
+    case 3223: return launch_dec<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
+    case 1643: return launch_dec<D, 16, 4, 3>(p, tmK, tmV, n_work, st);
+    case 1623: return launch_dec<D, 16, 2, 3>(p, tmK, tmV, n_work, st);
+    case 1644: return launch_dec<D, 16, 4, 4>(p, tmK, tmV, n_work, st);
+    case 1614: return launch_dec<D, 16, 1, 4>(p, tmK, tmV, n_work, st);
+    default: return launch_dec<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
+  }
+}
+}  // namespace
+
+void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm) {
+  const DecVariant v = dec_variant();
+  const int smem = 1024 + v.nwarp * v.stages * 2 * v.kt * head_dim * 2 + v.nwarp * v.stages * 8;
+  *keys_per_tile = v.kt;
+  *nwarp = v.nwarp;
+  *ctas_per_sm = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
+}
+
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         int head_dim, int n_work, cudaStream_t st) {
   if (n_work <= 0) return cudaSuccess;
-  if (head_dim == 128) {
-    constexpr int smem = dec_smem<128>();
-    static bool once = (cudaFuncSetAttribute(attn_decode_kernel<128>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        true);
-    (void)once;
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    attn_decode_kernel<128><<<n_work, NWARP * 32, smem, st>>>(tmK, tmV, p);
-  } else if (head_dim == 64) {
-    constexpr int smem = dec_smem<64>();
-    static bool once = (cudaFuncSetAttribute(attn_decode_kernel<64>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        true);
-    (void)once;
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    attn_decode_kernel<64><<<n_work, NWARP * 32, smem, st>>>(tmK, tmV, p);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  if (head_dim == 128) return launch_dec_d<128>(p, tmK, tmV, n_work, st);
+  if (head_dim == 64) return launch_dec_d<64>(p, tmK, tmV, n_work, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace cs

@@ -276,7 +276,7 @@ size_t meta_size(const cs_engine* e) {
   b += T * 4 * 3;                          // tokens, row_pos, row_seg
   b += S * sizeof(cs::AttnSeg);
   b += (size_t)e->npages * 4 + 4096 * 4;   // page table (upper bound)
-  b += 65536 * sizeof(cs::AttnWork);
+  b += 65536 * sizeof(cs::AttnWork) + 16384 * sizeof(cs::AttnDecWork);
   b += 8192 * sizeof(cs::AttnCombine);
   b += S * 4 * 2;                          // samp idx
   b += (size_t)e->L_max * 4;               // targets
@@ -770,7 +770,7 @@ struct StepPlan {
   cs::AttnSeg* segs;
   cs::AttnWork* work;
   cs::AttnWork* work_tc;
-  cs::AttnWork* work_dec;
+  cs::AttnDecWork* work_dec;
   cs::AttnCombine* comb;
   cs::AttnCombine* comb_tc;  // split-KV parts of the tcgen05 kernel (256-row parts)
   std::vector<int> samp_seg;  // segment of each sampled row
@@ -1008,11 +1008,14 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // 1 CTA/SM (small wave-quantisation tail, longest parts first), but no part is shorter
   // than 512 keys (4 tiles per warp: the per-warp TMA ring stays full)
   {
+    int dec_kt = 32, dec_nw = 4, dec_cps = 1;
+    cs::attn_decode_geometry(e->d, &dec_kt, &dec_nw, &dec_cps);
     long total = 0;
     for (const auto& w : work_dec) total += w.k_end;
-    const long target = 8L * 148;
+    const long target = 8L * 148 * dec_cps;
+    const long tile_round = (long)dec_kt * dec_nw;  // one tile per warp
     long chunk = (total + target - 1) / target;
-    chunk = std::max<long>(512, (chunk + 127) / 128 * 128);
+    chunk = std::max<long>(4 * tile_round, (chunk + tile_round - 1) / tile_round * tile_round);
     int part = 0;
     for (const auto& c : comb) part = std::max(part, c.part0 + c.n_parts);
     std::vector<cs::AttnWork> w2;
@@ -1024,7 +1027,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
         w2.push_back(w);
         continue;
       }
-      const long per = ((w.k_end + ns - 1) / ns + 127) / 128 * 128;
+      const long per = ((w.k_end + ns - 1) / ns + tile_round - 1) / tile_round * tile_round;
       const int p0 = part;
       for (int t = 0; t < ns && t * per < w.k_end; ++t) {
         cs::AttnWork x = w;
@@ -1085,7 +1088,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: attention work list too large");
   const size_t o_work = take(work.size() * sizeof(cs::AttnWork));
   const size_t o_wtc = take(work_tc.size() * sizeof(cs::AttnWork));
-  const size_t o_wdec = take(work_dec.size() * sizeof(cs::AttnWork));
+  const size_t o_wdec = take(work_dec.size() * sizeof(cs::AttnDecWork));
   const size_t o_comb = take(comb.size() * sizeof(cs::AttnCombine));
   const size_t o_comb_tc = take(comb_tc.size() * sizeof(cs::AttnCombine));
   const size_t o_samp = take(samp_rows.size() * 4);
@@ -1094,7 +1097,28 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   if (off > e->meta_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_step: plan too large");
   if (!work.empty()) std::memcpy(hb + o_work, work.data(), work.size() * sizeof(cs::AttnWork));
   if (!work_tc.empty()) std::memcpy(hb + o_wtc, work_tc.data(), work_tc.size() * sizeof(cs::AttnWork));
-  if (!work_dec.empty()) std::memcpy(hb + o_wdec, work_dec.data(), work_dec.size() * sizeof(cs::AttnWork));
+  if (!work_dec.empty()) {  // resolve segment fields and the first boxes' pool rows (P % 16 == 0)
+    cs::AttnDecWork* dw = reinterpret_cast<cs::AttnDecWork*>(hb + o_wdec);
+    for (size_t i = 0; i < work_dec.size(); ++i) {
+      const cs::AttnWork& w = work_dec[i];
+      const cs::AttnSeg& g = h_segs[w.seg];
+      cs::AttnDecWork d{};
+      d.q_row = g.q_start + w.q0;
+      d.pos0 = g.ctx_start + w.q0;
+      d.page_off = g.page_off;
+      d.kv_head = w.kv_head;
+      d.k_begin = w.k_begin;
+      d.k_end = w.k_end;
+      d.part = w.part;
+      d.nq = w.nq;
+      const int last_box = (w.k_end - 1) & ~15;
+      for (int b = 0; b < 8; ++b) {
+        const int jb = std::min(w.k_begin + 16 * b, last_box);
+        d.prow[b] = plan->page_table[g.page_off + jb / P] * P + jb % P;
+      }
+      dw[i] = d;
+    }
+  }
   if (!comb_tc.empty()) std::memcpy(hb + o_comb_tc, comb_tc.data(), comb_tc.size() * sizeof(cs::AttnCombine));
   if (!comb.empty()) std::memcpy(hb + o_comb, comb.data(), comb.size() * sizeof(cs::AttnCombine));
   if (!samp_rows.empty()) std::memcpy(hb + o_samp, samp_rows.data(), samp_rows.size() * 4);
@@ -1119,7 +1143,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.comb = reinterpret_cast<cs::AttnCombine*>(db + o_comb);
   sp.comb_tc = reinterpret_cast<cs::AttnCombine*>(db + o_comb_tc);
   sp.work_tc = reinterpret_cast<cs::AttnWork*>(db + o_wtc);
-  sp.work_dec = reinterpret_cast<cs::AttnWork*>(db + o_wdec);
+  sp.work_dec = reinterpret_cast<cs::AttnDecWork*>(db + o_wdec);
   sp.samp_idx = reinterpret_cast<int*>(db + o_samp);
   sp.targets = reinterpret_cast<int*>(db + o_tg);
   return CS_OK;
@@ -1203,7 +1227,7 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     }
     if (sp.n_dec > 0) {
       cs::AttnFwdParams dp = ap;
-      dp.work = sp.work_dec;
+      dp.dwork = sp.work_dec;
       CUtensorMap mk, mv;
       const long pool_rows = (long)e->npages * e->P;
       if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||

@@ -18,6 +18,14 @@ struct AttnWork {  // one CTA of attn_fwd_kernel
   int seg, q0, nq, kv_head, k_begin, k_end, part, pad;
 };
 
+// one CTA of attn_decode_kernel: the segment fields and the KV-pool rows of the first 8
+// 16-key boxes are resolved on the host, so the kernel's prologue is one load deep (work item
+// -> TMA issue / Q loads) instead of three (work -> segment -> page table -> TMA)
+struct AttnDecWork {
+  int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
+  int prow[8];
+};
+
 struct AttnCombine {  // one CTA of attn_combine_kernel
   int seg, q0, nq, kv_head, part0, n_parts, pad0, pad1;
 };
@@ -31,6 +39,7 @@ struct AttnFwdParams {
   const int* page_table;
   const AttnSeg* segs;
   const AttnWork* work;
+  const AttnDecWork* dwork;  // attn_decode_kernel only
   const AttnCombine* combine;
   bf16* out;
   long out_ld;
@@ -73,6 +82,8 @@ struct AttnBwdParams {
 // attn_fwd, whose combine pass also merges the decode partials
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         int head_dim, int n_work, cudaStream_t st);
+// keys per warp tile, warps per decode CTA and resident CTAs per SM of the launched variant (host work split)
+void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm);
 // merge split-KV partials listed in p.combine (p.part_rows rows per part)
 cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cudaStream_t st);
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
