@@ -14,6 +14,7 @@
 #include <deque>
 #include <vector>
 
+#include "coserve/baselines.hpp"
 #include "coserve/cost_model.hpp"
 #include "coserve/scheduler.hpp"
 #include "coserve/workload.hpp"
@@ -66,6 +67,11 @@ struct LoopConfig {
   int prepopulate = 0;          // requests already decoding at t=0 (steady-state start)
   bool adaptive = false;        // correct the profile with measured/predicted ratios
   uint64_t seed = 0;
+  // scheduling policy (§8.2 baselines, coserve/baselines.hpp): co-serving, or
+  // temporal sharing -- inference-only iterations interleaved with whole finetuning
+  // iterations, after temporal_n inference iterations (fixed) or when DTS says so
+  Policy policy = Policy::Coserve;
+  int temporal_n = 128;
   WorkloadConfig workload;
 };
 
@@ -146,10 +152,16 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
   }
   double corr[3] = {1.0, 1.0, 1.0};  // adaptive, per FT phase (none / forward / backward)
+  const bool temporal = cfg.policy != Policy::Coserve;
+  DtsState dts;
+  int inf_since_ft = 0;   // inference-only iterations since the last finetuning iteration
+  bool ft_block = false;  // temporal sharing: inside a finetuning iteration (inference blocked)
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
   for (int it = 0; it < total_iters; ++it) {
     const bool timed = it >= cfg.warmup_iters;
+    int64_t arrived = 0;
     while (next_arrival < trace.size() && trace[next_arrival].time_ms <= now) {
+      ++arrived;
       const Arrival& a = trace[next_arrival++];
       Request r;
       r.id = next_id++;
@@ -188,7 +200,20 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       prof.decode_ms_per_row *= corr[cph];
       prof.prefill_ms_per_token *= corr[cph];
     }
-    IterationPlan plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
+    IterationPlan plan;
+    if (!temporal) {
+      plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
+    } else if (ft_block) {
+      plan = plan_ft_block(ft, prof, cfg.sched);
+    } else {
+      FtState idle = ft;  // inference-only iteration
+      idle.phase = FtPhase::Idle;
+      plan = plan_iteration(queue, running, idle, prof, cfg.sched, mem, cfg.budget_ms);
+      if (plan.c == 0 && ft.L > 0) {  // nothing to serve: the finetuning iteration runs now
+        ft_block = true;
+        plan = plan_ft_block(ft, prof, cfg.sched);
+      }
+    }
     if (!enforce_dependencies(plan, ft)) {
       st.ok = false;
       return st;
@@ -279,9 +304,11 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       ++seg;
     }
     // retire finished requests
+    int64_t completed = 0;
     for (size_t i = 0; i < running.size();) {
       Request& r = running[i];
       if (r.done()) {
+        ++completed;
         if (r.arrival_ms > -1e17) {
           const double ttft = r.first_token_ms - r.arrival_ms;
           const double tpot = r.gen_len > 1 ? (r.completion_ms - r.first_token_ms) / (r.gen_len - 1) : 0.0;
@@ -315,7 +342,20 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       st.timed_ms += out.ms;
       st.timed_device_ms += out.device_ms;
     }
+    // temporal sharing: count inference-only iterations, decide the next finetuning one
+    if (temporal && !ft_block && ft.L > 0) {
+      ++inf_since_ft;
+      if (cfg.policy == Policy::TemporalFixed) {
+        ft_block = inf_since_ft >= std::max(1, cfg.temporal_n);
+      } else {
+        ft_block = dts_step(dts, (double)queue.size(),
+                            (double)(plan.decode.size() + plan.prefill.size()), (double)arrived,
+                            (double)completed);
+      }
+    }
     if (ft.phase == FtPhase::Done) {
+      ft_block = false;
+      inf_since_ft = 0;
       if (exec && !exec->adam()) {
         st.ok = false;
         return st;

@@ -220,6 +220,9 @@ typedef struct cs_coserve_config {
   /* simulation-only (engine == NULL): model depth, vocab and KV pool */
   int32_t n_layers, vocab, page_size;
   int64_t total_pages;
+  /* scheduling policy (§8.2): 0 co-serving, 1 temporal sharing with a fixed
+   * inference frequency temporal_n, 2 dynamic temporal sharing */
+  int32_t policy, temporal_n;
 } cs_coserve_config;
 
 typedef struct cs_coserve_stats {

@@ -347,10 +347,87 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
             "layer": layer, "l": l, "pred": pred, "bwd": bwd}
 
 
+# ---------------------------------------------------------------- baseline policies
+# PAPER.md §8.2 / SPEC.md:474-548 (include/coserve/baselines.hpp)
+COSERVE, TEMPORAL, DTS = 0, 1, 2
+
+
+class DtsState:
+    """PAPER.md:536-541 state; f_p starts at 64 (SPEC.md design decision)."""
+
+    def __init__(self):
+        self.Q, self.B = [], []
+        self.r_a = self.r_c = 0.0
+        self.s = 64.0
+        self.f_p = 64.0
+        self.d = 0
+
+
+def dts_compute_interval(st: DtsState) -> float:
+    """Compute_Next_Interval (PAPER.md:563-589)."""
+    if not st.Q:
+        return 64.0
+    n = float(len(st.Q))
+    qbar = sum(st.Q) / n
+    qmax = max(st.Q)
+    lam, mu = st.r_a / n, st.r_c / n
+    p = min(1.0, qbar / 20.0) + min(0.5, qmax / 25.0) + max(0.0, (lam - mu) / 8.0)
+    if p <= 0.8:
+        f = 64.0
+    elif p >= 2.0:
+        f = 512.0
+    else:
+        f = 64.0 + (p - 0.8) / 1.2 * 0.6 * (512.0 - 64.0)
+    f *= 1.35
+    fs = (f + 2.0 * st.f_p) / 3.0
+    st.f_p = fs
+    fs = max(fs, 64.0 + 16.0)
+    return min(512.0, max(64.0, fs))
+
+
+def dts_step(st: DtsState, q, b, a, c) -> bool:
+    """Scheduler_Step: True = switch to finetuning."""
+    st.r_a += a
+    st.r_c += c
+    st.Q.append(float(q))
+    st.B.append(float(b))
+    st.s -= 1.0
+    if st.s <= 0.0:
+        st.d += 1
+        if st.d >= 3:
+            st.s = dts_compute_interval(st)
+            st.d = 0
+        else:
+            st.s = min(512.0, st.f_p * 1.1)
+        st.Q, st.B, st.r_a, st.r_c = [], [], 0.0, 0.0
+        return True
+    return False
+
+
+def plan_ft_block(ft: "FtState", prof: Profile, max_tokens: int, max_ft_window: int):
+    """One step of a temporal-sharing finetuning iteration (baselines.hpp plan_ft_block)."""
+    pred = inference_cost(prof, 0, 0)
+    s, phase, layer, l, bwd = 0, 0, -1, 0, []
+    if ft.phase == FWD:
+        s = min(ft.L - ft.l, max_tokens)
+        if s > 0:
+            phase, l = FWD, ft.l
+            pred += ft_fwd_cost(prof, ft.l, s)
+    elif ft.phase == BWD:
+        s = min(ft.lj, max_ft_window, max_tokens)
+        if s > 0:
+            phase, layer, l = BWD, ft.layer, ft.lj
+            bwd = [(ft.layer, ft.lj, s)]
+            pred += ft_bwd_cost(prof, ft.lj, s, ft.layer)
+    return {"decode": [], "prefill": [], "c": 0, "s": s, "phase": phase, "layer": layer,
+            "l": l, "pred": pred, "bwd": bwd}
+
+
 def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, total_pages: int,
         growth: int, ft_len: int, iters: int, prepopulate: int = 0, max_batch: int = 64,
         chunk: int = 512, max_tokens: int = 8192, max_ft_window: int = 8192,
-        budget: Optional[float] = None, tpot_slo: float = 50.0, multi_layer: bool = False):
+        budget: Optional[float] = None, tpot_slo: float = 50.0, multi_layer: bool = False,
+        policy: int = COSERVE, temporal_n: int = 128):
     """coserve_loop.hpp run_coserve on the simulated clock.
     Returns the per-iteration log (list of dicts)."""
     budget = tpot_slo if budget is None else budget
@@ -383,12 +460,17 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
         r.pages = pages
         running.append(r)
     log = []
+    temporal = policy != COSERVE
+    dts = DtsState()
+    inf_since_ft, ft_block = 0, False
     for _ in range(iters):
+        arrived = 0
         while nxt < len(trace) and trace[nxt][0] <= now:
             t, p, g = trace[nxt]
             nxt += 1
             queue.append(Request(next_id, p, g, t))
             next_id += 1
+            arrived += 1
         i = 0
         while i < len(running):
             r = running[i]
@@ -402,8 +484,19 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                     running.pop(i)
                     continue
             i += 1
-        plan = plan_iteration(queue, running, ft, prof, max_batch, chunk, max_tokens,
-                              max_ft_window, mem, budget, multi_layer)
+        if not temporal:
+            plan = plan_iteration(queue, running, ft, prof, max_batch, chunk, max_tokens,
+                                  max_ft_window, mem, budget, multi_layer)
+        elif ft_block:
+            plan = plan_ft_block(ft, prof, max_tokens, max_ft_window)
+        else:
+            idle = FtState(L=ft.L, n_layers=ft.n_layers, phase=0, minibatch=ft.minibatch,
+                           l=ft.l, layer=ft.layer, lj=ft.lj)
+            plan = plan_iteration(queue, running, idle, prof, max_batch, chunk, max_tokens,
+                                  max_ft_window, mem, budget, multi_layer)
+            if plan["c"] == 0 and ft.L > 0:
+                ft_block = True
+                plan = plan_ft_block(ft, prof, max_tokens, max_ft_window)
         entry = {"c": plan["c"], "s": plan["s"], "phase": plan["phase"], "layer": plan["layer"],
                  "l": plan["l"], "n_decode": len(plan["decode"]), "n_prefill": len(plan["prefill"]),
                  "pred": plan["pred"], "bwd": plan["bwd"],
@@ -425,10 +518,12 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                 if r.done():
                     r.completion_ms = now
         i = 0
+        completed = 0
         while i < len(running):
             if running[i].done():
                 mem.release(running[i].pages)
                 running.pop(i)
+                completed += 1
             else:
                 i += 1
         if plan["phase"] == BWD:
@@ -436,7 +531,15 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                 advance_finetune(ft, sw)
         else:
             advance_finetune(ft, plan["s"])
+        if temporal and not ft_block and ft.L > 0:
+            inf_since_ft += 1
+            if policy == TEMPORAL:
+                ft_block = inf_since_ft >= max(1, temporal_n)
+            else:
+                ft_block = dts_step(dts, len(queue), len(plan["decode"]) + len(plan["prefill"]),
+                                    arrived, completed)
         if ft.phase == DONE:
+            ft_block, inf_since_ft = False, 0
             ft.phase, ft.minibatch, ft.l, ft.layer, ft.lj = FWD, ft.minibatch + 1, 0, 0, 0
         entry["t_ms"] = now
         entry["n_running"] = len(running)

@@ -66,7 +66,10 @@ class CoserveConfig(ctypes.Structure):
                 ("prepopulate", i32), ("adaptive", i32), ("profile_timed", i32),
                 ("multi_layer_bwd", i32),
                 ("seed", ctypes.c_uint64),
-                ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64)]
+                ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64),
+                ("policy", i32), ("temporal_n", i32)]
+
+POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS = 0, 1, 2
 
 
 class CoserveStats(ctypes.Structure):

@@ -34,6 +34,7 @@ def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth
     c.vocab = 1000
     c.page_size = 16
     c.total_pages = pages
+    c.policy, c.temporal_n = 0, 128
     return c
 
 
@@ -140,3 +141,74 @@ def test_spec_examples_via_oracle():
         S.advance_finetune(ft, s)
         trace.append(ft.l)
     assert trace == [3, 6, 8] and ft.phase == S.BWD
+
+
+# ---------------------------------------------------------------- baseline policies
+def test_dts_known_answers():
+    """PAPER.md:528-590 Algorithm 'Dynamic Temporal Sharing' / SPEC.md:485-506 examples."""
+    st = S.DtsState()
+    assert S.dts_compute_interval(st) == 64.0                       # Q empty -> 64
+    flips = [S.dts_step(st, 0, 0, 0, 0) for _ in range(64)]
+    assert flips[:63] == [False] * 63 and flips[63]                  # fresh s=64: 64th switches
+    assert st.d == 1 and st.s == pytest.approx(64 * 1.1)             # s <- min(512, f_p*1.1)
+    st = S.DtsState()
+    st.Q, st.r_a, st.r_c = [8.0, 12.0, 10.0], 30.0, 24.0            # qbar 10, qmax 12, l 10, m 8
+    out = S.dts_compute_interval(st)
+    f_pre = 64 + (1.23 - 0.8) / 1.2 * 0.6 * 448                      # p = 1.23 -> f ~ 160.3
+    assert f_pre == pytest.approx(160.32, abs=0.01)
+    assert out == pytest.approx((f_pre * 1.35 + 2 * 64) / 3)
+    st = S.DtsState()
+    st.Q, st.r_a, st.r_c = [4.0, 6.0], 0.0, 0.0                      # p = 0.25 + 0.24 = 0.49
+    assert S.dts_compute_interval(st) == pytest.approx(80.0)         # (86.4+128)/3=71.5 -> 80
+    # the third decision takes the full recompute path
+    st = S.DtsState()
+    n = 0
+    while st.d < 2:
+        S.dts_step(st, 30, 10, 2, 1)
+        n += 1
+    for _ in range(10000):
+        if S.dts_step(st, 30, 10, 2, 1):
+            break
+    assert st.d == 0 and 80.0 <= st.s <= 512.0
+
+
+@pytest.mark.parametrize("policy,n", [(S.TEMPORAL, 16), (S.TEMPORAL, 64), (S.DTS, 0)])
+def test_temporal_policies_bit_exact(policy, n):
+    """Temporal-sharing baselines (§8.2): the C++ loop (coserve/baselines.hpp) and the
+    Python restatement plan identical iterations on the simulated clock."""
+    prof = S.Profile(5.0, 0.01, S.INF, 0.3, 1e-6, 1e-7, 0.4)
+    c = _cfg(12.0, prof, 500, 1024, 4, 5, 16, 4096, 64, budget=45.0, multi_layer=True)
+    c.policy, c.temporal_n = policy, n
+    stats, log = E.coserve_run(None, c)
+    w = S.Workload(rate=12.0, duration_s=600.0, amplitude=0.0, period_s=20.0)
+    ref = S.run(prof, w, 5, 4, 16, 4096, 64, 1024, 500, prepopulate=16, budget=45.0,
+                multi_layer=True, policy=policy, temporal_n=n)
+    assert len(log) == len(ref) == 500
+    for i, (a, b) in enumerate(zip(log, ref)):
+        for k in ("c", "s", "phase", "layer", "l", "n_decode", "n_prefill", "n_running", "n_queue"):
+            assert a[k] == b[k], (i, k, a[k], b[k])
+        assert a["t_ms"] == b["t_ms"] and a["pred_ms"] == b["pred"], i
+        assert not (a["c"] > 0 and a["s"] > 0)      # never co-served: inference xor finetuning
+    assert stats["minibatches_done"] >= 1
+    if policy == S.TEMPORAL:  # every finetuning iteration follows >= n inference iterations
+        runs, cur = [], 0
+        for a in log:
+            if a["s"] > 0 and cur:
+                runs.append(cur)
+                cur = 0
+            elif a["c"] > 0:
+                cur += 1
+        assert runs and all(r >= n for r in runs[1:])
+
+
+def test_coserve_beats_temporal_in_simulation():
+    """at the same SLO, co-serving sustains more finetuning than temporal
+    sharing at frequency 128 (simulated clock, same profile and trace)."""
+    prof = S.Profile(5.0, 0.01, S.INF, 0.3, 1e-6, 1e-7, 0.4)
+    res = {}
+    for pol, n in ((S.COSERVE, 0), (S.TEMPORAL, 128)):
+        c = _cfg(20.0, prof, 1500, 2048, 8, 2, 32, 8192, 64, budget=45.0, multi_layer=True)
+        c.policy, c.temporal_n = pol, n
+        st, _ = E.coserve_run(None, c)
+        res[pol] = (st["ft_fwd_tokens"] + st["ft_bwd_tokens"] / 8) / st["timed_ms"]
+    assert res[S.COSERVE] > 1.2 * res[S.TEMPORAL], res
