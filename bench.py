@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--ft-window", type=int, default=8192,
                     help="largest token-level finetuning window (config 3: 256 / 1024)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-profile", type=int, default=1,
+                    help="CUDA events around every GEMM / attention launch in the timed region")
     ap.add_argument("--log", default="")
     return ap.parse_args()
 
@@ -408,12 +410,21 @@ def run_ours(a):
     torch.cuda.synchronize()
     clk.start()
     st, log = coserve_run(eng, coserve_config(a.rate, prof, a.steps, a.warmup, a.ft_len,
-                                               seed=7 + group, profile_timed=True, slo_ms=slo,
+                                               seed=7 + group, slo_ms=slo,
                                                max_window=a.ft_window))
     torch.cuda.synchronize()
     clocks = clk.stop()
     if dist:
         dist.barrier()
+    # roofline pass: the same workload again with CUDA events around every GEMM / attention
+    # launch.  The events break the PDL chains between kernels (measured -3.5% throughput),
+    # so they stay out of the timed region that `value` / `e2e` come from.
+    prof_steps = min(a.steps, 100) if a.kernel_profile else 0
+    pst = st
+    if prof_steps:
+        pst, _ = coserve_run(eng, coserve_config(a.rate, prof, prof_steps, a.warmup, a.ft_len,
+                                                 seed=7 + group, profile_timed=True, slo_ms=slo,
+                                                 max_window=a.ft_window))
     gemm = eng.read_profile(0)
     attn = eng.read_profile(1)
     attn_b = eng.read_profile(2)
@@ -423,7 +434,7 @@ def run_ours(a):
     from paper_2402_18789_b200.replicas import aggregate
     # a TP group is one replica: only its leader's finetuning progress counts
     value, e2e = aggregate(st, n_layers, dist, device="cuda", count=(tp_rank == 0))
-    dev_ms = st["timed_device_ms"]
+    dev_ms = pst["timed_device_ms"]   # kernel shares: the profiled pass
     wall_ms = st["timed_ms"]
 
     if rank != 0:
@@ -487,6 +498,8 @@ def run_ours(a):
                      "frac": round(gemm_tf / peak_tf, 4) if peak_tf else None,
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
                      "launches": gemm["launches"],
+                     "region": f"profiled pass: {prof_steps} steps of the same workload (CUDA "
+                               "events around every GEMM launch on the engine stream)",
                      "share_of_step": round(gemm["ms"] / dev_ms, 4) if dev_ms else None},
         "attention": {"fwd_tc_tflops": round(attn_tc["flops"] / (attn_tc["ms"] * 1e-3) / 1e12, 1) if attn_tc["ms"] else None,
                       "fwd_tc_share": round(attn_tc["ms"] / dev_ms, 4) if dev_ms else None,

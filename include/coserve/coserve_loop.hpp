@@ -72,6 +72,7 @@ struct LoopConfig {
   // iterations, after temporal_n inference iterations (fixed) or when DTS says so
   Policy policy = Policy::Coserve;
   int temporal_n = 128;
+  bool sim_clock = false;       // advance the clock by predicted latency even with an executor
   WorkloadConfig workload;
 };
 
@@ -281,6 +282,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));
       corr[ph] = std::max(0.5, std::min(2.0, 0.8 * corr[ph] + 0.2 * r));
     }
+    if (exec && cfg.sim_clock) out.ms = plan.predicted_ms;
     now += out.ms;
     // advance request state
     int seg = 0;

@@ -223,6 +223,9 @@ typedef struct cs_coserve_config {
   /* scheduling policy (§8.2): 0 co-serving, 1 temporal sharing with a fixed
    * inference frequency temporal_n, 2 dynamic temporal sharing */
   int32_t policy, temporal_n;
+  /* 1: advance the loop clock by the planner's predicted latency even with an engine (a
+   * timing-independent plan sequence, e.g. for profiling runs under ncu) */
+  int32_t sim_clock;
 } cs_coserve_config;
 
 typedef struct cs_coserve_stats {

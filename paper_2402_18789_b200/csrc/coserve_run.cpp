@@ -153,6 +153,7 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_coserve_run: policy must be 0, 1 or 2");
   L.policy = (coserve::Policy)c->policy;
   L.temporal_n = c->temporal_n > 0 ? c->temporal_n : 128;
+  L.sim_clock = c->sim_clock != 0;
   L.workload.rate_rps = c->rate_rps;
   L.workload.duration_s = c->duration_s;
   L.workload.burst_amplitude = c->burst_amplitude;

@@ -97,7 +97,8 @@ struct cs_engine {
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
   size_t meta_bytes = 0;
-  std::vector<float> h_loss;
+  float* h_loss = nullptr;  // pinned [L_max]: the FT window's per-row losses (async D2H)
+  int h_loss_n = 0;
   // FT state machine
   int ft_len = 0;          // QKV cache length (forward progress)
   int ft_L = 0;            // sequence length of the active mini-batch
@@ -381,6 +382,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   cudaEventCreate(&e->ev0);
   cudaEventCreate(&e->ev1);
   cudaMallocHost(&e->h_meta, e->meta_bytes);
+  cudaMallocHost(&e->h_loss, (size_t)e->L_max * sizeof(float));
   // zero everything that has padding semantics (concat pad columns, LoRA state, norms)
   cudaMemsetAsync(e->arena, 0, e->arena_used, e->st);
   // RoPE table in double precision on the host
@@ -537,6 +539,7 @@ extern "C" int cs_engine_destroy(cs_engine* e) {
   cudaStreamSynchronize(e->st);
   cudaFree(e->arena);
   cudaFreeHost(e->h_meta);
+  cudaFreeHost(e->h_loss);
   cudaEventDestroy(e->ev0);
   cudaEventDestroy(e->ev1);
   cudaStreamDestroy(e->st);
@@ -1327,8 +1330,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
       cs::rms_bwd_add(nullptr, 0, xs, h, e->gf, e->hrstd, e->dh, h,
                       e->dy[e->dy_cur] + (size_t)(l0 + c0) * h, h, nullptr, 0, cn, h, e->norm, st);
     }
-    e->h_loss.resize(n_ft);
-    CS_CUDA_TRY(cudaMemcpyAsync(e->h_loss.data(), e->loss_rows, n_ft * 4, cudaMemcpyDeviceToHost, st));
+    e->h_loss_n = n_ft;
+    CS_CUDA_TRY(cudaMemcpyAsync(e->h_loss, e->loss_rows, n_ft * 4, cudaMemcpyDeviceToHost, st));
   }
   (void)loss_sum;
   return CS_OK;
@@ -1539,7 +1542,7 @@ int step_impl(cs_engine* e, const cs_iteration_plan* plan, bool sync, cs_step_re
   if (res) {
     double ls = 0.0;
     if (w.phase == CS_FT_FORWARD)
-      for (int i = 0; i < (int)std::min<size_t>(e->h_loss.size(), (size_t)w.s); ++i) ls += e->h_loss[i];
+      for (int i = 0; i < std::min(e->h_loss_n, w.s); ++i) ls += e->h_loss[i];
     res->ft_loss_sum = ls;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev0, e->ev1);

@@ -67,7 +67,7 @@ class CoserveConfig(ctypes.Structure):
                 ("multi_layer_bwd", i32),
                 ("seed", ctypes.c_uint64),
                 ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64),
-                ("policy", i32), ("temporal_n", i32)]
+                ("policy", i32), ("temporal_n", i32), ("sim_clock", i32)]
 
 POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS = 0, 1, 2
 
