@@ -530,7 +530,7 @@ def run_ours(a):
         "profile": {k: (float(f"{v:.4g}") if isinstance(v, float) else v) for k, v in prof.items()
                     if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",
                              "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx",
-                             "bwd_layer0_weight")},
+                             "bwd_layer0_weight", "decode_ms_per_row", "prefill_ms_per_token")},
         "context": ({"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200}
                     if a.model == "llama-3.1-8b" else None),
         "setup_s": round(setup_s, 1),

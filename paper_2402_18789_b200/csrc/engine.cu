@@ -305,6 +305,8 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: head_dim must be 64 or 128");
   if (c.n_heads / c.n_kv_heads > 64)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: GQA group too large");
+  if (c.hidden > 8192)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_engine_create: hidden must be <= 8192");
   if ((c.hidden % 64) != 0 || (c.ffn % 64) != 0 || (c.vocab % 8) != 0)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT,
                          "cs_engine_create: hidden/ffn must be multiples of 64, vocab of 8");

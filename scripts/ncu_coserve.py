@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--rate", type=float, default=20.0)
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--reduce", default="")
+    ap.add_argument("--fixed-profile", action="store_true",
+                    help="skip the offline profile (a recorded B200 profile instead): only the "
+                         "loop's own launches run, e.g. for CS_GEMM_LOG shape censuses")
     a = ap.parse_args()
     if a.reduce:
         return reduce(a.reduce)
@@ -47,7 +50,13 @@ def main():
     import bench
     from paper_2402_18789_b200.engine import coserve_run
     eng = bench.make_engine(0, 8192)
-    prof = bench.offline_profile(eng, 8192)
+    if a.fixed_profile:  # bench.py's offline profile on a B200 (profiles/r1_bench_latest.log)
+        prof = {"t0_ms": 5.46, "decode_ms_per_row": 0.0105, "prefill_ms_per_token": 0.0178,
+                "slope_ms_per_token": 0.01864, "bwd_token_weight": 0.02548,
+                "attn_fwd_ms_per_token_ctx": 7.99e-07, "attn_bwd_ms_per_token_ctx": 8.65e-08,
+                "bwd_layer0_weight": 0.2545}
+    else:
+        prof = bench.offline_profile(eng, 8192)
     c = bench.coserve_config(a.rate, prof, a.iters, 0, 8192, seed=7)
     c.sim_clock, c.adaptive = 1, 0
     torch.cuda.nvtx.range_push("coserve")
