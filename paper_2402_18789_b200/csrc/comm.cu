@@ -106,6 +106,8 @@ struct LocalGroup {
   std::atomic<int> attached{0};
   std::atomic<bool> broken{false};
   float* ptrs[kMaxRanks] = {};
+  void* xptrs[kMaxRanks] = {};                // exchange_ptr
+  cudaEvent_t ev_sb[2][kMaxRanks] = {};       // stream_barrier (alternating sets)
   cudaEvent_t ev_ready[kMaxRanks] = {};
   cudaEvent_t ev_done[kMaxRanks] = {};
   int device[kMaxRanks] = {};
@@ -138,6 +140,35 @@ namespace {
 struct LocalComm final : Comm {
   LocalGroup* g = nullptr;
   int r = 0;
+  int sb_parity = 0;
+  bool peer_capable() const override { return true; }
+  int exchange_ptr(void* local, void** out, std::string* err) override {
+    g->xptrs[r] = local;
+    if (!g->barrier()) {
+      if (err) *err = "tp barrier timeout (ranks diverged)";
+      return -1;
+    }
+    for (int j = 0; j < g->n; ++j) out[j] = g->xptrs[j];
+    if (!g->barrier()) {  // nobody overwrites xptrs before every rank has read them
+      if (err) *err = "tp barrier timeout (ranks diverged)";
+      return -1;
+    }
+    return 0;
+  }
+  // one host barrier per call; the event set alternates, so a rank re-records set p only
+  // after the barrier of set 1-p, which every rank reaches after its waits on set p
+  int stream_barrier(cudaStream_t st, std::string* err) override {
+    const int p = sb_parity;
+    sb_parity ^= 1;
+    cudaEventRecord(g->ev_sb[p][r], st);
+    if (!g->barrier()) {
+      if (err) *err = "tp barrier timeout (ranks diverged)";
+      return -1;
+    }
+    for (int j = 0; j < g->n; ++j)
+      if (j != r) cudaStreamWaitEvent(st, g->ev_sb[p][j], 0);
+    return 0;
+  }
   int rank() const override { return r; }
   int size() const override { return g->n; }
   int allreduce_f32(float* buf, size_t count, cudaStream_t st, std::string* err) override {
@@ -179,6 +210,44 @@ struct LocalComm final : Comm {
 };
 }  // namespace
 
+__global__ void __launch_bounds__(256) tp_reduce_bcast_kernel(float* __restrict__ stage, long ld,
+                                                              int nranks, int rank, int rpo, int M,
+                                                              int h, PeerPtrs dst, long ldd,
+                                                              int add_old) {
+  const int row0 = rank * rpo;
+  const int nrows = min(rpo, M - row0);
+  const int h4 = h / 4;
+  const long total = (long)max(nrows, 0) * h4;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int lr = (int)(i / h4), c = (int)(i % h4) * 4;
+    const long drow = (long)(row0 + lr) * ldd + c;
+    float4 v = add_old ? *reinterpret_cast<const float4*>(dst.p[rank] + drow) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nranks; ++s) {
+      float4* sp = reinterpret_cast<float4*>(stage + ((long)s * rpo + lr) * ld + c);
+      const float4 t = *sp;
+      v.x += t.x;
+      v.y += t.y;
+      v.z += t.z;
+      v.w += t.w;
+      *sp = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int j = 0; j < nranks; ++j) *reinterpret_cast<float4*>(dst.p[j] + drow) = v;
+  }
+}
+
+cudaError_t tp_reduce_bcast(float* stage, long ld, int nranks, int rank, int rpo, int M, int h,
+                            float* const* dst, long ldd, int add_old, cudaStream_t st) {
+  if (nranks < 1 || nranks > kMaxRanks || (h % 4) != 0 || rpo < 1) return cudaErrorInvalidValue;
+  PeerPtrs pp{};
+  for (int j = 0; j < nranks; ++j) pp.p[j] = dst[j];
+  const long work = (long)std::max(0, std::min(rpo, M - rank * rpo)) * (h / 4);
+  if (work <= 0) return cudaSuccess;
+  const int blocks = (int)std::max<long>(1, std::min<long>((work + 255) / 256, 148 * 8));
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  tp_reduce_bcast_kernel<<<blocks, 256, 0, st>>>(stage, ld, nranks, rank, rpo, M, h, pp, ldd, add_old);
+  return cudaGetLastError();
+}
+
 LocalGroup* local_group_create(int size, std::string* err) {
   if (size < 1 || size > kMaxRanks) {
     if (err) *err = "tp group size must be in [1, 8]";
@@ -197,6 +266,8 @@ void local_group_destroy(LocalGroup* g) {
   for (int i = 0; i < g->n; ++i) {
     if (g->ev_ready[i]) cudaEventDestroy(g->ev_ready[i]);
     if (g->ev_done[i]) cudaEventDestroy(g->ev_done[i]);
+    for (int p = 0; p < 2; ++p)
+      if (g->ev_sb[p][i]) cudaEventDestroy(g->ev_sb[p][i]);
   }
   delete g;
 }
@@ -213,6 +284,7 @@ Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err) {
   // events live on the rank's device; peers may sit on other devices of this process
   cudaEventCreateWithFlags(&g->ev_ready[rank], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&g->ev_done[rank], cudaEventDisableTiming);
+  for (int p = 0; p < 2; ++p) cudaEventCreateWithFlags(&g->ev_sb[p][rank], cudaEventDisableTiming);
   g->device[rank] = device;
   int ndev = 0;
   cudaGetDeviceCount(&ndev);

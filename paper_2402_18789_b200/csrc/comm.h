@@ -27,7 +27,31 @@ struct Comm {
   virtual int size() const = 0;
   // in-place sum over the ranks of buf[0, n), stream-ordered on st; 0 on success
   virtual int allreduce_f32(float* buf, size_t n, cudaStream_t st, std::string* err) = 0;
+  // Peer-memory groups (every rank's device buffers are addressable from every rank: the
+  // ranks of one process over NVLink / NVSwitch peer access) run the fused row-parallel GEMM
+  // + all-reduce (engine.cu tp_rowpar): false for NCCL.
+  virtual bool peer_capable() const { return false; }
+  // every rank passes its local device pointer; out[r] = rank r's (host barrier); 0 on success
+  virtual int exchange_ptr(void* local, void** out, std::string* err) {
+    if (err) *err = "exchange_ptr: not a peer-memory group";
+    return -1;
+  }
+  // cross-rank stream ordering point: work enqueued on every rank's stream before the call
+  // completes before work any rank enqueues after it; 0 on success
+  virtual int stream_barrier(cudaStream_t st, std::string* err) {
+    if (err) *err = "stream_barrier: not a peer-memory group";
+    return -1;
+  }
 };
+
+// Second half of the fused row-parallel GEMM + all-reduce: rank `rank` owns rows
+// [rank * rpo, min(M, (rank + 1) * rpo)); it sums the ranks' partial slots of its local
+// staging buffer [nranks][rpo][ld] in rank order (+ the replicated old value of the
+// destination when add_old), zeroes the slots (the GEMM's split-K atomics rely on zeroed
+// slots), and stores the sum into every rank's destination (peer stores): bit-identical on
+// every rank.
+cudaError_t tp_reduce_bcast(float* stage, long ld, int nranks, int rank, int rpo, int M, int h,
+                            float* const* dst, long ldd, int add_old, cudaStream_t st);
 
 // NCCL communicator from a 128-byte ncclUniqueId (all ranks call concurrently)
 Comm* make_nccl_comm(const void* unique_id, int rank, int size, std::string* err);

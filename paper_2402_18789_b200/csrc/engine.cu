@@ -89,6 +89,12 @@ struct cs_engine {
   unsigned long long* amax_part;
   float *part_o, *part_lse;
   float* tp_sync;  // [8 ranks][8 values]: cs_engine_tp_sync_max
+  // fused row-parallel GEMM + all-reduce (peer-memory groups): staging [ranks][rpo][h] fp32,
+  // zero between uses; peer tables exchanged lazily (same call order on every rank)
+  float* tp_stage = nullptr;
+  bool tp_fused = false;
+  float* stage_tab[8] = {};
+  std::vector<std::pair<void*, std::vector<float*>>> dst_tabs;
   // backward scratch
   bf16 *dycat, *dgu, *dr1b, *dO, *dqkv;
   float *dlu, *dm, *dh2, *dr1, *delta, *dq, *dh1;
@@ -266,6 +272,7 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(dh1, S * h);
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
   AL(tp_sync, 64);
+  AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
 #undef AL
@@ -368,6 +375,9 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
       delete e;
       return cs::set_error(CS_ERR_NCCL, "cs_engine_create: " + err);
     }
+    // CS_TP_FUSED=0 keeps GEMM + separate all-reduce on peer-memory groups (A/B)
+    const char* v = std::getenv("CS_TP_FUSED");
+    e->tp_fused = e->comm->peer_capable() && !(v && std::atoi(v) == 0);
   }
   size_t total = 0;
   layout(e, true, &total);
@@ -782,8 +792,10 @@ struct StepPlan {
 };
 
 int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb, long b_rows,
-         void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr) {
+         void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr,
+         const cs::GemmScatter* sc = nullptr) {
   cs::GemmDesc g;
+  if (sc) g.scatter = *sc;
   g.A = A;
   g.lda = lda;
   g.a_rows = a_rows;
@@ -838,6 +850,61 @@ int tp_allreduce(cs_engine* e, float* buf, size_t n) {
 // row-parallel projections add into the replicated residual stream: rank 0 accumulates
 // (x += p_0), the other ranks overwrite (x = p_r); the all-reduce then leaves x + sum_r p_r
 int rowpar_epi(const cs_engine* e) { return (e->comm && e->tp_rank != 0) ? cs::EPI_F32 : cs::EPI_F32_ADD; }
+
+// Row-parallel GEMM whose fp32 output is summed over the TP ranks into dst [M, h] (add_old:
+// dst += sum_r partial_r, the replicated residual stream; else dst = sum_r partial_r).
+// Peer-memory groups run it FUSED: the GEMM epilogue stores each
+// partial tile straight into the owning rank's staging slot over NVLink (rows are owned in
+// M / ranks blocks) while the other tiles are still in the tensor pipe; after a cross-rank
+// stream barrier each owner sums its rows' slots in rank order and stores the result into
+// every rank's dst (peer stores), then a second barrier.  Otherwise (NCCL, tp 1, or
+// CS_TP_FUSED=0): GEMM into dst + in-place all-reduce.
+int tp_rowpar(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb,
+              long b_rows, float* dst, long M, long K, bool add_old) {
+  const long h = e->h;
+  if (!e->tp_fused) {
+    const int epi = add_old ? rowpar_epi(e) : cs::EPI_F32;
+    TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, dst, h, M, h, K, epi));
+    return tp_allreduce(e, dst, (size_t)M * h);
+  }
+  if (M <= 0) return CS_OK;
+  std::string err;
+  const int n = e->tp_size;
+  if (!e->stage_tab[0]) {
+    void* out[8] = {};
+    if (e->comm->exchange_ptr(e->tp_stage, out, &err) != 0) return cs::set_error(CS_ERR_NCCL, err);
+    for (int j = 0; j < n; ++j) e->stage_tab[j] = static_cast<float*>(out[j]);
+  }
+  const std::vector<float*>* dtab = nullptr;
+  for (const auto& d : e->dst_tabs)
+    if (d.first == dst) dtab = &d.second;
+  if (!dtab) {
+    void* out[8] = {};
+    if (e->comm->exchange_ptr(dst, out, &err) != 0) return cs::set_error(CS_ERR_NCCL, err);
+    std::vector<float*> t(n);
+    for (int j = 0; j < n; ++j) t[j] = static_cast<float*>(out[j]);
+    e->dst_tabs.emplace_back(dst, std::move(t));
+    dtab = &e->dst_tabs.back().second;
+  }
+  const int rpo = (int)((M + n - 1) / n);
+  cs::GemmScatter sc;
+  for (int j = 0; j < n; ++j) sc.peer[j] = e->stage_tab[j];
+  sc.rows_per_owner = rpo;
+  sc.rank = e->tp_rank;
+  cs_engine::ProfRec pr{};
+  TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, nullptr, h, M, h, K, cs::EPI_F32_SCATTER, nullptr, &sc));
+  if (e->profiling) {
+    pr.bytes = 2.0 * (double)M * h * 4.0 * (n - 1) / n;
+    pr.kind = 4;
+    prof_begin(e, pr);
+  }
+  if (e->comm->stream_barrier(e->st, &err) != 0) return cs::set_error(CS_ERR_NCCL, err);
+  CS_CUDA_TRY(cs::tp_reduce_bcast(e->tp_stage, h, n, e->tp_rank, rpo, (int)M, (int)h, dtab->data(), h,
+                                  add_old ? 1 : 0, e->st));
+  if (e->comm->stream_barrier(e->st, &err) != 0) return cs::set_error(CS_ERR_NCCL, err);
+  if (e->profiling) prof_end(e, pr);
+  return CS_OK;
+}
 
 int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   const int T = plan->n_tokens;
@@ -1278,9 +1345,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
       save_rows(e, e->ft_lse + ((size_t)l * e->L_max + l0) * e->Hq, e->Hq,
                 e->lse + (size_t)sp.ft_row0 * e->Hq, e->Hq, n_ft, e->Hq);
     }
-    TRY(gemm(e, e->attn, e->q_dim, e->T_max, e->wo_t + (size_t)l * h * e->q_dim, e->q_dim, h, e->x, h,
-             T, h, e->q_dim, rowpar_epi(e)));
-    TRY(tp_allreduce(e, e->x, (size_t)T * h));
+    TRY(tp_rowpar(e, e->attn, e->q_dim, e->T_max, e->wo_t + (size_t)l * h * e->q_dim, e->q_dim, h, e->x,
+                  T, e->q_dim, true));
     // ---- MLP block
     if (n_ft > 0 && e->norm)
       save_rows(e, e->ft_r1 + ((size_t)l * e->L_max + l0) * h, h, e->x + (size_t)sp.ft_row0 * h, h, n_ft, h);
@@ -1303,9 +1369,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                   e->lu + (size_t)(sp.ft_row0 - sp.ad_row0) * r, r, n_ft, r);
     }
     // x += [m | u] [W_down ; B] (tiny_model.hpp:206-211 as one K-concatenated GEMM)
-    TRY(gemm(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * h * e->f_cat, e->f_cat, h, e->x,
-             h, T, h, e->f_cat, rowpar_epi(e)));
-    TRY(tp_allreduce(e, e->x, (size_t)T * h));
+    TRY(tp_rowpar(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * h * e->f_cat, e->f_cat, h,
+                  e->x, T, e->f_cat, true));
   }
   // ---- sampled rows: final norm -> logits -> argmax
   if (sp.n_samp > 0) {
@@ -1381,9 +1446,8 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
               e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
   if (n > 0) {
-    TRY(gemm(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2, h,
-             s, h, e->gu_n, cs::EPI_F32));
-    TRY(tp_allreduce(e, e->dh2, (size_t)s * h));
+    TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2,
+                  s, e->gu_n, false));
     cs::rms_bwd_add(Y, h, e->ft_r1 + ((size_t)n * Lm + a) * h, h, e->g2 + (size_t)n * h,
                     e->ft_rstd2 + (size_t)n * Lm + a, e->dh2, h, e->dr1, h, e->dr1b, h, s, h,
                     e->norm, st);
@@ -1455,9 +1519,8 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     if (e->profiling) prof_end(e, bpr);
     cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
-    TRY(gemm(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1, h,
-             s, h, e->nqkv, cs::EPI_F32));
-    TRY(tp_allreduce(e, e->dh1, (size_t)s * h));
+    TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1,
+                  s, e->nqkv, false));
     cs::rms_bwd_add(e->dr1, h, e->ft_x + ((size_t)n * Lm + a) * h, h, e->g1 + (size_t)n * h,
                     e->ft_rstd1 + (size_t)n * Lm + a, e->dh1, h, Xout, h, nullptr, 0, s, h,
                     e->norm, st);

@@ -41,6 +41,7 @@ struct GemmArgs {
   const float* bias;
   int b_const;  // B is not written by the previous kernel on the stream (weights): its first
                 // stages may be fetched before griddepcontrol.wait
+  GemmScatter sc;  // EPI_F32_SCATTER destination (peer staging slots)
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -103,7 +104,13 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int row, int c
         if (col0 + i < a.N) C[i] = __float2bfloat16(v[i]);
     }
   } else {
-    float* C = reinterpret_cast<float*>(a.C) + (long)row * a.ldc + col0;
+    float* C;
+    if (a.epi == EPI_F32_SCATTER) {  // fused TP all-reduce: partial -> owner's staging slot
+      const int rpo = a.sc.rows_per_owner, owner = row / rpo;
+      C = a.sc.peer[owner] + ((long)a.sc.rank * rpo + (row - owner * rpo)) * a.ldc + col0;
+    } else {
+      C = reinterpret_cast<float*>(a.C) + (long)row * a.ldc + col0;
+    }
     const bool atomic = a.splits > 1 || a.epi == EPI_F32_ATOMIC;
     if (full) {
 #pragma unroll
@@ -654,6 +661,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.ldc = d.ldc;
   a.bias = d.bias;
   a.b_const = d.b_const;
+  a.sc = d.scatter;
   a.splits = 1;
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
@@ -731,6 +739,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.ldc = d.ldc;
   a.bias = d.bias;
   a.b_const = d.b_const;
+  a.sc = d.scatter;
   int splits = d.splits;
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {

@@ -37,6 +37,17 @@ enum GemmEpi : int {
   EPI_F32 = 1,         // C_f32  = acc
   EPI_F32_ADD = 2,     // C_f32 += acc   (residual stream; split-K via atomics)
   EPI_F32_ATOMIC = 3,  // C_f32 += acc with atomics (caller-initialised C)
+  EPI_F32_SCATTER = 4, // row-parallel TP partial -> the owning rank's staging slot (GemmScatter)
+};
+
+// EPI_F32_SCATTER: output row `row` belongs to rank owner = row / rows_per_owner; the fp32
+// partial goes to peer[owner] + ((rank * rows_per_owner) + row - owner * rows_per_owner) * ldc,
+// i.e. slot `rank` of the owner's [ranks][rows_per_owner][ldc] staging buffer (peer memory over
+// NVLink / NVSwitch; plain stores, or fp32 atomics into the zeroed slot for split-K).
+struct GemmScatter {
+  float* peer[8] = {};
+  int rows_per_owner = 0;
+  int rank = 0;
 };
 
 struct GemmDesc {
@@ -55,6 +66,7 @@ struct GemmDesc {
   int splits = 0;               // 0 = heuristic (fp32 epilogues only)
   int max_ctas = 0;             // 0 = #SMs
   int b_const = 0;              // B not produced by the preceding kernel (weights): PDL prefetch
+  GemmScatter scatter;          // EPI_F32_SCATTER only
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);

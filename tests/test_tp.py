@@ -145,7 +145,12 @@ def _plan_steps(arch, ft_tokens, fwd_windows, bwd_windows, n_inf, seed, P):
 
 
 @pytest.mark.gpu
-def test_tp2_engine_matches_oracle_and_tp1():
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_tp2_engine_matches_oracle_and_tp1(fused, monkeypatch):
+    """TP=2 as two engines on one B200 (single-process group).  fused=1: the row-parallel
+    GEMMs scatter their partial tiles into the owning rank's staging slots from the epilogue
+    and the owners reduce + broadcast (CS_TP_FUSED); fused=0: GEMM + one-shot all-reduce."""
+    monkeypatch.setenv("CS_TP_FUSED", fused)
     from paper_2402_18789_b200.engine import Engine, TPGroup, arch_config, tp_run
     arch = ARCH
     W = O.init_general(arch, 3)
