@@ -294,21 +294,268 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------- persistent streams
+// Every warp is an independent, persistent stream over whole work items (items gw, gw + W,
+// ... for W warps in the grid; the host sorts items longest first): no cross-warp merge, the
+// item's normalised output (or split-KV partial + LSE) leaves straight from the mma
+// fragments.  The warp's TMA ring runs ACROSS item boundaries -- while the last tiles of item
+// i are in the tensor pipe, lane 0 already has item i+1's first tiles in flight -- so the
+// per-item prologue (work load, first TMA round trip) and epilogue (stores) overlap the
+// stream instead of idling the SM (the per-item CTA version spent ~40% of a bench-sized
+// launch there: ncu long-scoreboard stalls on the work / page-table loads).
+template <int D, int KT, int NWARP, int STAGES>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+    attn_decode_stream_kernel(const __grid_constant__ CUtensorMap tmK,
+                              const __grid_constant__ CUtensorMap tmV, AttnFwdParams p, int n_items) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  constexpr int NH = D / 64;
+  constexpr int HALF = KT * 128;
+  constexpr int TILE = NH * HALF;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TW = gridDim.x * NWARP;
+  const int gw = blockIdx.x * NWARP + warp;
+  uint8_t* ws = smem + warp * (STAGES * 2 * TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NWARP * STAGES * 2 * TILE) + warp * STAGES;
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  __syncwarp();
+  if (gw >= n_items) return;
+  const int grp = p.grp;
+  struct Item {
+    int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
+  };
+  auto load_item = [&](int it) {
+    const int4* q = reinterpret_cast<const int4*>(p.dwork + it);
+    const int4 a = __ldg(q), b = __ldg(q + 1);
+    return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  };
+  // ---- issue side (lane 0): (item, tile) cursor running up to STAGES-1 tiles ahead
+  int is_item = gw, is_t = 0, is_n = 0;  // item, next tile in it, tiles in it
+  Item iw{};
+  long g_issue = 0, g_cons = 0;
+  auto issue_open = [&]() {
+    iw = load_item(is_item);
+    is_t = 0;
+    is_n = (iw.k_end + KT - 1) / KT - iw.k_begin / KT;
+  };
+  auto top_up = [&]() {
+    while (is_item < n_items && g_issue < g_cons + STAGES) {
+      const int st = (int)(g_issue % STAGES);
+      uint8_t* dk = ws + st * 2 * TILE;
+      uint8_t* dv = dk + TILE;
+      mbar_arrive_expect_tx(&full[st], 2 * TILE);
+      const int kt = iw.k_begin / KT + is_t;
+      const int last_box = (iw.k_end - 1) & ~15;
+      const AttnDecWork* wp = p.dwork + is_item;
+#pragma unroll
+      for (int b = 0; b < KT / 16; ++b) {
+        const int jb = min(kt * KT + b * 16, last_box);
+        const int bi = (jb - iw.k_begin) >> 4;
+        const int prow = bi < 8 ? __ldg(wp->prow + bi)
+                                : __ldg(p.page_table + iw.page_off + jb / p.page_size) * p.page_size + jb % p.page_size;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          const int col = iw.kv_head * D + hh * 64;
+          tma_load_2d(&tmK, &full[st], dk + hh * HALF + b * 2048, col, prow);
+          tma_load_2d(&tmV, &full[st], dv + hh * HALF + b * 2048, col, prow);
+        }
+      }
+      ++g_issue;
+      if (++is_t == is_n) {
+        is_item += TW;
+        if (is_item < n_items) issue_open();
+      }
+    }
+  };
+  if (lane == 0) {
+    issue_open();
+    top_up();
+  }
+  const int ra = lane >> 2, rb = ra + 8;
+  for (int item = gw; item < n_items; item += TW) {
+    const Item w = load_item(item);
+    const int nrows = w.nq * grp;
+    const __nv_bfloat16* qa = nullptr;
+    const __nv_bfloat16* qb = nullptr;
+    if (ra < nrows) qa = p.q + (long)(w.q_row + ra / grp) * p.q_ld + (long)(w.kv_head * grp + ra % grp) * D;
+    if (rb < nrows) qb = p.q + (long)(w.q_row + rb / grp) * p.q_ld + (long)(w.kv_head * grp + rb % grp) * D;
+    uint32_t qf[D / 16][4];
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const int col = kk * 16 + 2 * (lane & 3);
+      qf[kk][0] = qa ? ld_u32(qa + col) : 0u;
+      qf[kk][1] = qb ? ld_u32(qb + col) : 0u;
+      qf[kk][2] = qa ? ld_u32(qa + col + 8) : 0u;
+      qf[kk][3] = qb ? ld_u32(qb + col + 8) : 0u;
+    }
+    const int pos_a = ra < nrows ? w.pos0 + ra / grp : -1;
+    const int pos_b = rb < nrows ? w.pos0 + rb / grp : -1;
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    const int kt0 = w.k_begin / KT, nt = (w.k_end + KT - 1) / KT - kt0;
+    for (int t = 0; t < nt; ++t) {
+      if (lane == 0) top_up();
+      const int st = (int)(g_cons % STAGES);
+      mbar_wait(&full[st], (uint32_t)((g_cons / STAGES) & 1));
+      const uint32_t kb = smem_u32(ws + st * 2 * TILE), vb = kb + TILE;
+      const int kt = kt0 + t;
+      float s[KT / 8][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int nbp = 0; nbp < KT / 16; ++nbp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + tile_off<KT>(nbp * 16 + (lane & 7) + ((lane >> 4) << 3), kk * 2 + ((lane >> 3) & 1)),
+                  b0, b1, b2, b3);
+          mma16816(s[2 * nbp], qf[kk], b0, b1);
+          mma16816(s[2 * nbp + 1], qf[kk], b2, b3);
+        }
+      }
+      float mx_a = -INFINITY, mx_b = -INFINITY;
+#pragma unroll
+      for (int nb = 0; nb < KT / 8; ++nb) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = kt * KT + nb * 8 + 2 * (lane & 3) + (e & 1);
+          const int pos = e < 2 ? pos_a : pos_b;
+          float v = s[nb][e] * p.scale_log2;
+          if (j > pos || j >= w.k_end) v = -INFINITY;
+          s[nb][e] = v;
+        }
+        mx_a = fmaxf(mx_a, fmaxf(s[nb][0], s[nb][1]));
+        mx_b = fmaxf(mx_b, fmaxf(s[nb][2], s[nb][3]));
+      }
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
+      const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+      const float mu_a = mn_a == -INFINITY ? 0.f : mn_a;
+      const float mu_b = mn_b == -INFINITY ? 0.f : mn_b;
+      float rs_a = 0.f, rs_b = 0.f;
+#pragma unroll
+      for (int nb = 0; nb < KT / 8; ++nb) {
+        s[nb][0] = exp2f(s[nb][0] - mu_a);
+        s[nb][1] = exp2f(s[nb][1] - mu_a);
+        s[nb][2] = exp2f(s[nb][2] - mu_b);
+        s[nb][3] = exp2f(s[nb][3] - mu_b);
+        rs_a += s[nb][0] + s[nb][1];
+        rs_b += s[nb][2] + s[nb][3];
+      }
+      if (__any_sync(0xffffffffu, mn_a != m_a || mn_b != m_b)) {
+        const float c_a = exp2f(m_a - mu_a), c_b = exp2f(m_b - mu_b);
+        l_a *= c_a;
+        l_b *= c_b;
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          o[n][0] *= c_a;
+          o[n][1] *= c_a;
+          o[n][2] *= c_b;
+          o[n][3] *= c_b;
+        }
+      }
+      m_a = mn_a;
+      m_b = mn_b;
+      l_a += rs_a;
+      l_b += rs_b;
+#pragma unroll
+      for (int kk = 0; kk < KT / 16; ++kk) {
+        uint32_t a[4];
+        a[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+        a[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+        a[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+        a[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+        for (int dp = 0; dp < D / 16; ++dp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + tile_off<KT>(kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), dp * 2 + (lane >> 4)),
+                    b0, b1, b2, b3);
+          mma16816(o[2 * dp], a, b0, b1);
+          mma16816(o[2 * dp + 1], a, b2, b3);
+        }
+      }
+      __syncwarp();  // every lane is done reading this stage before lane 0 refills it
+      ++g_cons;
+    }
+    // ---- epilogue straight from the fragments (the next item's tiles are already in flight)
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int r = half ? rb : ra;
+      if (r >= nrows) continue;
+      const float L = half ? l_b : l_a, M = half ? m_b : m_a;
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      const float lse = L > 0.f ? (M + __log2f(L)) * kLn2 : -INFINITY;
+      const int qr = r / grp, g = r - qr * grp;
+      if (w.part < 0) {
+        const long row = w.q_row + qr;
+        const int qh = w.kv_head * grp + g;
+        __nv_bfloat16* dst = p.out + row * p.out_ld + (long)qh * D;
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          const int d = n * 8 + 2 * (lane & 3);
+          *reinterpret_cast<uint32_t*>(dst + d) = pack_bf16(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+        }
+        if ((lane & 3) == 0 && p.lse) p.lse[row * p.lse_ld + qh] = lse;
+      } else {
+        float* dst = p.part_o + ((long)w.part * 64 + r) * D;
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          const int d = n * 8 + 2 * (lane & 3);
+          *reinterpret_cast<float2*>(dst + d) = make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+        }
+        if ((lane & 3) == 0) p.part_lse[(long)w.part * 64 + r] = lse;
+      }
+    }
+  }
+}
+
 namespace {
 struct DecVariant {
-  int kt, nwarp, stages;
+  int stream, kt, nwarp, stages;
 };
-// CS_DEC_CFG=<kt><nwarp><stages> (A/B testing), e.g. 3243 = 32-key tiles, 4 warps x 3 stages
+// CS_DEC_CFG=[9]<kt><nwarp><stages> (A/B testing): 3243 = per-item CTAs, 32-key tiles, 4 warps
+// x 3 stages; a leading 9 = persistent per-warp streams (attn_decode_stream_kernel)
 DecVariant dec_variant() {
   static const DecVariant v = [] {
-    DecVariant d{32, 2, 2};
+    DecVariant d{0, 32, 2, 2};
     if (const char* e = std::getenv("CS_DEC_CFG")) {
-      const int x = std::atoi(e);
-      d = DecVariant{x / 100, (x / 10) % 10, x % 10};
+      int x = std::atoi(e);
+      const int stream = x >= 10000 ? 1 : 0;
+      x %= 10000;
+      d = DecVariant{stream, x / 100, (x / 10) % 10, x % 10};
     }
     return d;
   }();
   return v;
+}
+
+template <int D, int KT, int NW, int ST>
+cudaError_t launch_dec_stream(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                              int n_work, cudaStream_t st) {
+  constexpr int smem = dec_smem<D, KT, NW, ST>();
+  static bool once = (cudaFuncSetAttribute(attn_decode_stream_kernel<D, KT, NW, ST>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                      true);
+  (void)once;
+  const int cps = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
+  const int grid = std::max(1, std::min((n_work + NW - 1) / NW, 148 * cps));
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  attn_decode_stream_kernel<D, KT, NW, ST><<<grid, NW * 32, smem, st>>>(tmK, tmV, p, n_work);
+  return cudaGetLastError();
 }
 
 template <int D, int KT, int NW, int ST>
@@ -328,6 +575,15 @@ template <int D>
 cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          int n_work, cudaStream_t st) {
   const DecVariant v = dec_variant();
+  if (v.stream) {
+    switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
+      case 3222: return launch_dec_stream<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
+      case 3242: return launch_dec_stream<D, 32, 4, 2>(p, tmK, tmV, n_work, st);
+      case 1624: return launch_dec_stream<D, 16, 2, 4>(p, tmK, tmV, n_work, st);
+      case 1644: return launch_dec_stream<D, 16, 4, 4>(p, tmK, tmV, n_work, st);
+      default: return launch_dec_stream<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
+    }
+  }
   switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
     case 3243: return launch_dec<D, 32, 4, 3>(p, tmK, tmV, n_work, st);
     case 3223: return launch_dec<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
@@ -340,12 +596,14 @@ cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const C
 }
 }  // namespace
 
-void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm) {
+void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm,
+                          int* streams) {
   const DecVariant v = dec_variant();
   const int smem = 1024 + v.nwarp * v.stages * 2 * v.kt * head_dim * 2 + v.nwarp * v.stages * 8;
   *keys_per_tile = v.kt;
   *nwarp = v.nwarp;
   *ctas_per_sm = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
+  *streams = v.stream;
 }
 
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,

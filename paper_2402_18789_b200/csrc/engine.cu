@@ -1080,12 +1080,14 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // 1 CTA/SM (small wave-quantisation tail, longest parts first), but no part is shorter
   // than 512 keys (4 tiles per warp: the per-warp TMA ring stays full)
   {
-    int dec_kt = 32, dec_nw = 4, dec_cps = 1;
-    cs::attn_decode_geometry(e->d, &dec_kt, &dec_nw, &dec_cps);
+    int dec_kt = 32, dec_nw = 4, dec_cps = 1, dec_stream = 0;
+    cs::attn_decode_geometry(e->d, &dec_kt, &dec_nw, &dec_cps, &dec_stream);
     long total = 0;
     for (const auto& w : work_dec) total += w.k_end;
-    const long target = 8L * 148 * dec_cps;
-    const long tile_round = (long)dec_kt * dec_nw;  // one tile per warp
+    // per-item CTAs: ~8 waves of CTAs; persistent streams (one warp per item): ~3 items per
+    // warp of the grid, enough to balance a longest-first round robin
+    const long target = dec_stream ? 3L * 148 * dec_cps * dec_nw : 8L * 148 * dec_cps;
+    const long tile_round = dec_stream ? (long)dec_kt : (long)dec_kt * dec_nw;
     long chunk = (total + target - 1) / target;
     chunk = std::max<long>(4 * tile_round, (chunk + tile_round - 1) / tile_round * tile_round);
     int part = 0;

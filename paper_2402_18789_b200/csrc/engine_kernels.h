@@ -82,8 +82,10 @@ struct AttnBwdParams {
 // attn_fwd, whose combine pass also merges the decode partials
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                         int head_dim, int n_work, cudaStream_t st);
-// keys per warp tile, warps per decode CTA and resident CTAs per SM of the launched variant (host work split)
-void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm);
+// keys per warp tile, warps per decode CTA, resident CTAs per SM and whether the variant is
+// the persistent per-warp stream kernel (one warp per item) -- the host work split follows it
+void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm,
+                          int* streams);
 // merge split-KV partials listed in p.combine (p.part_rows rows per part)
 cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cudaStream_t st);
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
