@@ -727,6 +727,25 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   const bool small_f32 = !tiny_m && d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.M <= 256 &&
                          d.N >= 1024;
   if (small_f32) bn = 128;
+  // mid-M fp32 epilogues that missed the CTA-pair kernel (the O / down projections and dX
+  // GEMMs of backward-phase iterations, M ~ 500-1100): pick tile width x K splits by waves x
+  // per-unit time, a unit = its K blocks + a fixed ~14-block cost (pipeline fill, fp32
+  // epilogue; fitted on scripts/gemm_cfg_sweep.py), a BN=128 tile doing half the work of a
+  // 256 one at ~85% of its per-FLOP rate.  M=640 N=4096 K=14400: 130 us (bn 128, 1 split,
+  // 160 tiles = 1.08 waves) -> 80 us (bn 256 x 3 splits)
+  int mid_splits = 0;
+  if (!tiny_m && !small_f32 && d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.N >= 1024) {
+    const long kb = (d.K + 63) / 64;
+    double best = 0;
+    for (int c : {256, 128}) {
+      const long tiles = ((d.M + 127) / 128) * ((d.N + c - 1) / c);
+      for (long sp = 1; sp <= 8 && (sp == 1 || kb / sp >= 8); ++sp) {
+        const long waves = (tiles * sp + kNumSMs - 1) / kNumSMs;
+        const double cost = (double)waves * ((double)kb / (double)sp + 14.0) * c / (c == 256 ? 1.0 : 0.85);
+        if (best == 0 || cost < best - 1e-9) best = cost, bn = c, mid_splits = (int)sp;
+      }
+    }
+  }
   GemmArgs a;
   a.M = (int)d.M;
   a.N = (int)d.N;
@@ -740,7 +759,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.bias = d.bias;
   a.b_const = d.b_const;
   a.sc = d.scatter;
-  int splits = d.splits;
+  int splits = d.splits > 0 ? d.splits : mid_splits;
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {
     splits = 1;
