@@ -694,6 +694,8 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   // large GEMMs (at least one wave of 256 x BN tiles): CTA-pair kernel
   if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 256) {
     const long mt = (d.M + 255) / 256;
+    // (256 x 128 pair tiles measured slower even where they quantise better onto the 74
+    // pairs: QKV M=1728 78 -> 108 us, scripts/gemm_cfg_sweep.py)
     if (d.M >= 512 && mt * ((d.N + 255) / 256) >= kNumSMs / 2) return gemm_tn_2sm<256>(d, st);
     static const bool bn128 = [] {  // measured neutral-to-negative in the co-serving bench
       const char* v = std::getenv("CS_GEMM_2SM128");

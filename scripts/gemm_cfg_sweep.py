@@ -16,6 +16,8 @@ SHAPES = [  # (M, N, K, epi): 8B projections at the backward-phase iterations' i
     (640, 4096, 14400, 2), (704, 4096, 14400, 2), (1728, 4096, 14400, 2), (2112, 4096, 14400, 2),
     (640, 6144, 4096, 0), (1728, 6144, 4096, 0), (2112, 6144, 4096, 0),
     (640, 4096, 4096, 2), (2112, 4096, 4096, 2), (1024, 4096, 128256, 1),
+    (1600, 6144, 4096, 0), (1856, 6144, 4096, 0), (1984, 6144, 4096, 0), (1728, 4096, 4096, 2),
+    (1600, 28672, 4096, 0), (1600, 4096, 14400, 2),
 ]
 
 
