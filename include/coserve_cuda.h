@@ -60,6 +60,11 @@ int64_t cs_debug_trace(int cta, void* dev_buf, int64_t capacity);
 int cs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, int epi, const float* bias, int bn, int splits,
                  void* stream);
+/* Same with B stored [K, N] row-major (N contiguous, ldb >= N): the MN-major B operand the
+ * engine's backward dX GEMMs use to read the forward weight layout (one copy of the frozen
+ * weights serves x.W and dY.W^T).  bn in {0, 64, 128, 256}; no bias. */
+int cs_gemm_bf16_mn(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                    int64_t M, int64_t N, int64_t K, int epi, int bn, int splits, void* stream);
 
 /* ---------------------------------------------------------------- engine */
 typedef struct cs_model_config {

@@ -54,6 +54,9 @@ def _declare(L):
     L.cs_gemm_bf16.restype = ctypes.c_int
     L.cs_gemm_bf16.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, ctypes.c_int, vp,
                                ctypes.c_int, ctypes.c_int, vp]
+    L.cs_gemm_bf16_mn.restype = ctypes.c_int
+    L.cs_gemm_bf16_mn.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, ctypes.c_int,
+                                  ctypes.c_int, ctypes.c_int, vp]
 
 
 def check(rc: int, what: str = ""):

@@ -56,6 +56,9 @@ struct cs_engine {
   bool use_dec_attn = true;  // CS_ATTN_DEC=0 sends decode rows to the mma.sync tile kernel
   bool use_fwd2 = true;      // CS_ATTN_FWD2=0 runs the one-query-tile tcgen05 kernel (v1)
   bool use_bwd2 = true;      // CS_ATTN_BWD2=0 runs the shared-memory-staged backward (v1)
+  // dX GEMMs read the forward weight layout as an MN-major B operand: one copy of the frozen
+  // QKV / O / gate||up / unembedding weights (CS_BWD_MN=0 keeps the reference-layout copies)
+  bool bwd_mn = true;
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
     const char* name;
@@ -195,16 +198,17 @@ void layout(cs_engine* e, bool measure, size_t* total) {
 #define AL(field, count) A(&e->field, (count), #field)
   const size_t NL = e->NL, h = e->h, V = e->V, f = e->f, r = e->r;
   const size_t T = e->T_max, Lm = e->L_max, S = e->S_max;
+  const bool dup = !e->bwd_mn;  // reference-layout copies only without MN-major dX GEMMs
   AL(embed, V * h);
   AL(unembed_t, V * h);
-  AL(unembed, h * V);
+  AL(unembed, dup ? h * V : 1);
   AL(gf, h);
   AL(wqkv_t, NL * e->nqkv * h);
-  AL(wqkv, NL * h * e->nqkv);
+  AL(wqkv, dup ? NL * h * e->nqkv : 1);
   AL(wo_t, NL * h * e->q_dim);
-  AL(wo, NL * e->q_dim * h);
+  AL(wo, dup ? NL * e->q_dim * h : 1);
   AL(wgu_t, NL * e->gu_n * h);
-  AL(wgu, NL * h * e->gu_n);
+  AL(wgu, dup ? NL * h * e->gu_n : 1);
   AL(down_cat, NL * h * e->f_cat);
   AL(dbwd_cat, NL * f * e->h_cat);
   AL(A_t, NL * 16 * f);
@@ -363,6 +367,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_FWD2")) e->use_fwd2 = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
+  if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -674,21 +679,21 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
   if (n == "embed") {
     cs::cast_f32_bf16(stage, lr, lc, e->embed, h, 0, st);
   } else if (n == "unembed") {
-    cs::cast_f32_bf16(stage, lr, lc, e->unembed, V, 0, st);
+    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->unembed, V, 0, st);
     cs::cast_f32_bf16(stage, lr, lc, e->unembed_t, h, 1, st);
   } else if (n == "final_norm") {
     cudaMemcpyAsync(e->gf, stage, h * 4, cudaMemcpyDeviceToDevice, st);
   } else if (n == "wq" || n == "wk" || n == "wv") {
     const long off = n == "wq" ? 0 : (n == "wk" ? qd : qd + kvd);
     cs::cast_f32_bf16(stage, lr, lc, e->wqkv_t + ((size_t)L * e->nqkv + off) * h, h, 1, st);
-    cs::cast_f32_bf16(stage, lr, lc, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
+    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
   } else if (n == "wo") {
     cs::cast_f32_bf16(stage, lr, lc, e->wo_t + (size_t)L * h * qd, qd, 1, st);
-    cs::cast_f32_bf16(stage, lr, lc, e->wo + (size_t)L * qd * h, h, 0, st);
+    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wo + (size_t)L * qd * h, h, 0, st);
   } else if (n == "w_gate" || n == "w_up") {
     const long off = (n == "w_up" && e->swiglu) ? f : 0;
     cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
-    cs::cast_f32_bf16(stage, lr, lc, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
+    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
   } else if (n == "w_down") {
     cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * h * e->f_cat, e->f_cat, 1, st);
     cs::cast_f32_bf16(stage, lr, lc, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
@@ -722,14 +727,16 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
   const uint64_t ss = seed + 7919ull * (uint64_t)e->tp_rank;
   // tiny_model.hpp:51-63 scales; the forward/backward layouts hold identical values
   cs::init_normal_bf16(e->embed, (long)e->V * e->h, ws, seed + 1, st);
-  cs::init_normal_bf16(e->unembed, (long)e->V * e->h, ws, seed + 2, st);
-  cs::init_normal_bf16(e->unembed_t, (long)e->V * e->h, ws, seed + 2, st);  // same stats
+  cs::init_normal_bf16(e->unembed_t, (long)e->V * e->h, ws, seed + 2, st);
   cs::init_normal_bf16(e->wqkv_t, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
-  cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
   cs::init_normal_bf16(e->wo_t, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
-  cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
   cs::init_normal_bf16(e->wgu_t, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
-  cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
+  if (!e->bwd_mn) {  // reference-layout copies (same statistics, not transposes)
+    cs::init_normal_bf16(e->unembed, (long)e->V * e->h, ws, seed + 2, st);
+    cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
+    cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
+    cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
+  }
   // down: fill whole concat buffers, then the LoRA columns are rewritten by refresh_lora;
   // pad columns [f + r, f + 64) must stay zero -> fill per row via cast of random fp32
   {
@@ -793,9 +800,10 @@ struct StepPlan {
 
 int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb, long b_rows,
          void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr,
-         const cs::GemmScatter* sc = nullptr) {
+         const cs::GemmScatter* sc = nullptr, int b_mn = 0) {
   cs::GemmDesc g;
   if (sc) g.scatter = *sc;
+  g.b_mn = b_mn;
   g.A = A;
   g.lda = lda;
   g.a_rows = a_rows;
@@ -860,11 +868,11 @@ int rowpar_epi(const cs_engine* e) { return (e->comm && e->tp_rank != 0) ? cs::E
 // every rank's dst (peer stores), then a second barrier.  Otherwise (NCCL, tp 1, or
 // CS_TP_FUSED=0): GEMM into dst + in-place all-reduce.
 int tp_rowpar(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb,
-              long b_rows, float* dst, long M, long K, bool add_old) {
+              long b_rows, float* dst, long M, long K, bool add_old, int b_mn = 0) {
   const long h = e->h;
   if (!e->tp_fused) {
     const int epi = add_old ? rowpar_epi(e) : cs::EPI_F32;
-    TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, dst, h, M, h, K, epi));
+    TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, dst, h, M, h, K, epi, nullptr, nullptr, b_mn));
     return tp_allreduce(e, dst, (size_t)M * h);
   }
   if (M <= 0) return CS_OK;
@@ -892,7 +900,7 @@ int tp_rowpar(cs_engine* e, const void* A, long lda, long a_rows, const void* B,
   sc.rows_per_owner = rpo;
   sc.rank = e->tp_rank;
   cs_engine::ProfRec pr{};
-  TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, nullptr, h, M, h, K, cs::EPI_F32_SCATTER, nullptr, &sc));
+  TRY(gemm(e, A, lda, a_rows, B, ldb, b_rows, nullptr, h, M, h, K, cs::EPI_F32_SCATTER, nullptr, &sc, b_mn));
   if (e->profiling) {
     pr.bytes = 2.0 * (double)M * h * 4.0 * (n - 1) / n;
     pr.kind = 4;
@@ -1394,8 +1402,12 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                e->V, cn, e->V, h, cs::EPI_F32));
       cs::ce_fwd_bwd(e->logits, e->V, sp.targets + c0, cn, e->V, inv, e->loss_rows + c0, e->dlog,
                      e->V, st);
-      TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed, e->V, h, e->dh, h, cn, h, e->V,
-               cs::EPI_F32));
+      if (e->bwd_mn)  // dH = dlogits . U^T, U^T read from the [V, h] forward copy (MN-major)
+        TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed_t, h, e->V, e->dh, h, cn, h, e->V,
+                 cs::EPI_F32, nullptr, nullptr, 1));
+      else
+        TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed, e->V, h, e->dh, h, cn, h, e->V,
+                 cs::EPI_F32));
       cs::rms_bwd_add(nullptr, 0, xs, h, e->gf, e->hrstd, e->dh, h,
                       e->dy[e->dy_cur] + (size_t)(l0 + c0) * h, h, nullptr, 0, cn, h, e->norm, st);
     }
@@ -1448,13 +1460,21 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
               e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
   if (n > 0) {
-    TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2,
-                  s, e->gu_n, false));
+    if (e->bwd_mn)
+      TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu_t + (size_t)n * e->gu_n * h, h, e->gu_n, e->dh2,
+                    s, e->gu_n, false, 1));
+    else
+      TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2,
+                    s, e->gu_n, false));
     cs::rms_bwd_add(Y, h, e->ft_r1 + ((size_t)n * Lm + a) * h, h, e->g2 + (size_t)n * h,
                     e->ft_rstd2 + (size_t)n * Lm + a, e->dh2, h, e->dr1, h, e->dr1b, h, s, h,
                     e->norm, st);
     // ---- attention (tiny_model.hpp:289-315)
-    TRY(gemm(e, e->dr1b, h, e->S_max, e->wo + (size_t)n * e->q_dim * h, h, e->q_dim, e->dO,
+    if (e->bwd_mn)
+      TRY(gemm(e, e->dr1b, h, e->S_max, e->wo_t + (size_t)n * h * e->q_dim, e->q_dim, h, e->dO,
+               e->q_dim, s, e->q_dim, h, cs::EPI_BF16, nullptr, nullptr, 1));
+    else
+      TRY(gemm(e, e->dr1b, h, e->S_max, e->wo + (size_t)n * e->q_dim * h, h, e->q_dim, e->dO,
              e->q_dim, s, e->q_dim, h, cs::EPI_BF16));
     const size_t kv_layer = (size_t)e->npages * e->P * e->kv_dim;
     cs::AttnBwdParams bp;
@@ -1521,8 +1541,12 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     if (e->profiling) prof_end(e, bpr);
     cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
-    TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1,
-                  s, e->nqkv, false));
+    if (e->bwd_mn)
+      TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv_t + (size_t)n * e->nqkv * h, h, e->nqkv,
+                    e->dh1, s, e->nqkv, false, 1));
+    else
+      TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1,
+                    s, e->nqkv, false));
     cs::rms_bwd_add(e->dr1, h, e->ft_x + ((size_t)n * Lm + a) * h, h, e->g1 + (size_t)n * h,
                     e->ft_rstd1 + (size_t)n * Lm + a, e->dh1, h, Xout, h, nullptr, 0, s, h,
                     e->norm, st);

@@ -42,6 +42,7 @@ struct GemmArgs {
   int b_const;  // B is not written by the previous kernel on the stream (weights): its first
                 // stages may be fetched before griddepcontrol.wait
   GemmScatter sc;  // EPI_F32_SCATTER destination (peer staging slots)
+  int b_mn;        // 1: B stored [K rows][N cols] (N contiguous): MN-major B operand
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -142,6 +143,19 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int row, int c
   }
 }
 
+// B stage of BN columns x 64 K: K-major = one box {64 K, BN rows}; MN-major (B stored
+// [K][N]) = BN/64 boxes {64 N, 64 K rows}, 8 KB apart
+template <int BN>
+__device__ __forceinline__ void load_b(const CUtensorMap* tmB, uint64_t* bar, uint8_t* sb, int kb, int n0,
+                                       int b_mn) {
+  if (!b_mn) {
+    tma_load_2d(tmB, bar, sb, kb * 64, n0);
+  } else {
+#pragma unroll
+    for (int c = 0; c < BN / 64; ++c) tma_load_2d(tmB, bar, sb + c * 8192, n0 + c * 64, kb * 64);
+  }
+}
+
 template <int BN, bool SM>
 __global__ void __launch_bounds__(256, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -196,8 +210,8 @@ __global__ void __launch_bounds__(256, 1)
         pre = min(Cfg::STAGES, kb1 - kb0);
         for (int i = 0; i < pre; ++i) {
           mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
-          tma_load_2d(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES,
-                      (kb0 + i) * Cfg::BK, nb * BN);
+          load_b<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i, nb * BN,
+                     args.b_mn);
         }
       }
       griddep_wait();
@@ -214,7 +228,7 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&empty_bar[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
             tma_load_2d(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * Cfg::BM);
-            tma_load_2d(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN);
+            load_b<BN>(&tmB, &full_bar[stage], sb, kb, nb * BN, args.b_mn);
           }
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      const uint32_t idesc = args.b_mn ? idesc_bf16_f32_major(128, BN, 0, 1) : idesc_bf16_f32(128, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -246,9 +260,11 @@ __global__ void __launch_bounds__(256, 1)
           const uint64_t bd = umma_desc_sw128(sb);
 #pragma unroll
           for (int k = 0; k < Cfg::BK / 16; ++k) {
-            // +32 bytes per K=16 step inside the 128B swizzle atom (16-byte units)
-            mma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
-                     (kb > kb0 || k > 0) ? 1u : 0u);
+            // K-major: +32 bytes per K=16 step inside the 128B swizzle atom (16-byte units);
+            // MN-major: +16 rows x 128 B, 64-column chunks 8 KB apart (LBO), 8-row groups (SBO)
+            const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
+                                         : bd + (uint64_t)(k * 2);
+            mma_bf16(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty_bar[stage]);
           if (++stage == Cfg::STAGES) {
@@ -364,6 +380,16 @@ CS_DEV void mbar_arrive_leader(uint64_t* bar) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// this CTA's half of a B stage (BN/2 columns x 64 K), 2-SM TMA
+template <int BN>
+CS_DEV void load_b_2sm(const CUtensorMap* tmB, uint64_t* bar, uint8_t* sb, int kb, int n0, int b_mn) {
+  if (!b_mn) {
+    tma_load_2d_2sm(tmB, bar, sb, kb * 64, n0);
+  } else {
+#pragma unroll
+    for (int c = 0; c < BN / 128; ++c) tma_load_2d_2sm(tmB, bar, sb + c * 8192, n0 + c * 64, kb * 64);
+  }
+}
 }  // namespace
 
 template <int BN>
@@ -423,8 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         pre = min(Cfg::STAGES, kb1 - kb0);
         for (int i = 0; i < pre; ++i) {
           if (leader) mbar_arrive_expect_tx(&full_bar[i], 2 * Cfg::STAGE_BYTES);
-          tma_load_2d_2sm(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES,
-                          (kb0 + i) * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+          load_b_2sm<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i,
+                         nb * BN + (int)rank * (BN / 2), args.b_mn);
         }
       }
       griddep_wait();
@@ -441,7 +467,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             mbar_wait(&empty_bar[stage], phase ^ 1);
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
             tma_load_2d_2sm(&tmA, &full_bar[stage], sa, kb * Cfg::BK, mb * 256 + (int)rank * 128);
-            tma_load_2d_2sm(&tmB, &full_bar[stage], sb, kb * Cfg::BK, nb * BN + (int)rank * (BN / 2));
+            load_b_2sm<BN>(&tmB, &full_bar[stage], sb, kb, nb * BN + (int)rank * (BN / 2), args.b_mn);
           }
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -453,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      const uint32_t idesc = args.b_mn ? idesc_bf16_f32_major(256, BN, 0, 1) : idesc_bf16_f32(256, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -472,9 +498,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint64_t ad = umma_desc_sw128(sa);
           const uint64_t bd = umma_desc_sw128(sb);
 #pragma unroll
-          for (int k = 0; k < Cfg::BK / 16; ++k)
-            mma_bf16_2sm(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
-                         (kb > kb0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < Cfg::BK / 16; ++k) {
+            const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
+                                         : bd + (uint64_t)(k * 2);
+            mma_bf16_2sm(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
           mma_commit_2sm(&empty_bar[stage]);
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -663,11 +691,14 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.b_const = d.b_const;
   a.sc = d.scatter;
   a.splits = 1;
+  a.b_mn = d.b_mn;
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
   const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
   if (make_map(&ma, d.A, a_rows, d.K, d.lda, 128) != 0) return cudaErrorInvalidValue;
-  if (make_map(&mb, d.B, b_rows, d.K, d.ldb, BN / 2) != 0) return cudaErrorInvalidValue;
+  if (d.b_mn ? make_map(&mb, d.B, d.K, d.N, d.ldb, 64) != 0
+             : make_map(&mb, d.B, b_rows, d.K, d.ldb, BN / 2) != 0)
+    return cudaErrorInvalidValue;
   const long work = (long)a.num_m * a.num_n;
   const int pairs = (int)std::min<long>(work, kNumSMs / 2);
   static bool attr_set = false;
@@ -748,6 +779,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
       }
     }
   }
+  if (d.b_mn && bn < 64) bn = 64;  // MN-major B stages are 64-column chunks
   GemmArgs a;
   a.M = (int)d.M;
   a.N = (int)d.N;
@@ -780,11 +812,13 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
     cudaError_t e = cudaMemset2DAsync(d.C, d.ldc * sizeof(float), 0, d.N * sizeof(float), d.M, st);
     if (e != cudaSuccess) return e;
   }
+  a.b_mn = d.b_mn;
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
   const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
   if (make_map(&ma, d.A, a_rows, d.K, d.lda, tiny_m ? 64 : 128) != 0) return cudaErrorInvalidValue;
-  if (make_map(&mb, d.B, b_rows, d.K, d.ldb, bn) != 0) return cudaErrorInvalidValue;
+  if (d.b_mn ? make_map(&mb, d.B, d.K, d.N, d.ldb, 64) != 0 : make_map(&mb, d.B, b_rows, d.K, d.ldb, bn) != 0)
+    return cudaErrorInvalidValue;
   const long work = tiles * splits;
   const int grid = (int)std::min<long>(work, d.max_ctas > 0 ? d.max_ctas : kNumSMs);
   if (tiny_m) {

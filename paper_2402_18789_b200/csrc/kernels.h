@@ -67,6 +67,7 @@ struct GemmDesc {
   int max_ctas = 0;             // 0 = #SMs
   int b_const = 0;              // B not produced by the preceding kernel (weights): PDL prefetch
   GemmScatter scatter;          // EPI_F32_SCATTER only
+  int b_mn = 0;                 // 1: B stored [K rows][N cols] (ldb >= N): MN-major operand
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);

@@ -72,3 +72,39 @@ def test_gemm_f32_store_bias(cuda):
     assert (C.float() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
     ref2 = A.float() @ B.float().T
     assert (C2 - ref2).abs().max().item() / ref2.abs().max().item() < 1e-4
+
+
+def _gemm_mn(A, Bkn, C, epi, bn=0, splits=0):
+    """C = A . Bkn with Bkn stored [K, N] (MN-major B operand)."""
+    L = _lib.lib()
+    M, K = A.shape
+    N = Bkn.shape[1]
+    rc = L.cs_gemm_bf16_mn(A.data_ptr(), A.stride(0), Bkn.data_ptr(), Bkn.stride(0), C.data_ptr(),
+                           C.stride(0), M, N, K, epi, bn, splits,
+                           torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "cs_gemm_bf16_mn")
+
+
+@pytest.mark.parametrize("M,N,K,epi,bn,splits", [
+    (128, 256, 64, 0, 256, 0), (300, 200, 320, 0, 64, 0), (1000, 1536, 512, 0, 0, 0),
+    (3000, 4096, 1024, 0, 0, 0),          # CTA pair
+    (8192, 4096, 28672 // 8, 1, 0, 0),    # dX of gate|up at a full window (K scaled down)
+    (640, 4096, 4096, 2, 0, 0),           # mid-M split-K fp32 add
+    (64, 6144, 4096, 0, 0, 0), (17, 4096, 4096, 1, 0, 0),   # small M (half-height A)
+    (200, 136, 256, 1, 0, 2),             # N tail, forced split
+])
+def test_gemm_mn_major_b(cuda, M, N, K, epi, bn, splits):
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    Bkn = torch.randn(K, N, device=cuda, generator=g).bfloat16()
+    if epi == 0:
+        C = torch.zeros(M, N, device=cuda, dtype=torch.bfloat16)
+        base = 0.0
+    else:
+        C = torch.randn(M, N, device=cuda, generator=g)
+        base = C.clone() if epi == 2 else 0.0
+    _gemm_mn(A, Bkn, C, epi, bn=bn, splits=splits)
+    ref = base + A.float() @ Bkn.float()
+    torch.cuda.synchronize()
+    err = (C.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < (1e-2 if epi == 0 else 1e-4), err
