@@ -59,6 +59,7 @@ struct cs_engine {
   // dX GEMMs read the forward weight layout as an MN-major B operand: one copy of the frozen
   // QKV / O / gate||up / unembedding weights (CS_BWD_MN=0 keeps the reference-layout copies)
   bool bwd_mn = true;
+  int down_rows = 0;  // per-layer rows of down_cat: h (+ 64 LoRA-A^T rows when bwd_mn)
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
     const char* name;
@@ -209,8 +210,8 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(wo, dup ? NL * e->q_dim * h : 1);
   AL(wgu_t, NL * e->gu_n * h);
   AL(wgu, dup ? NL * h * e->gu_n : 1);
-  AL(down_cat, NL * h * e->f_cat);
-  AL(dbwd_cat, NL * f * e->h_cat);
+  AL(down_cat, NL * e->down_rows * e->f_cat);
+  AL(dbwd_cat, dup ? NL * f * e->h_cat : 1);
   AL(A_t, NL * 16 * f);
   AL(B_t, NL * 16 * h);
   AL(bqkv, NL * e->nqkv);
@@ -368,6 +369,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_FWD2")) e->use_fwd2 = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
+  e->down_rows = e->h + (e->bwd_mn ? 64 : 0);
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -581,6 +583,8 @@ int refresh_lora(cs_engine* e, int update, float lr, float b1, float b2, float e
   p.B_t = e->B_t;
   p.down_cat = e->down_cat;
   p.dbwd_cat = e->dbwd_cat;
+  p.down_rows = e->down_rows;
+  p.a_in_down = e->bwd_mn ? 1 : 0;
   p.n_layers = e->NL;
   p.f = e->f;
   p.r = e->r;
@@ -695,8 +699,9 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
     cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
     if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
   } else if (n == "w_down") {
-    cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * h * e->f_cat, e->f_cat, 1, st);
-    cs::cast_f32_bf16(stage, lr, lc, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
+    cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * e->down_rows * e->f_cat, e->f_cat, 1, st);
+    if (!e->bwd_mn)
+      cs::cast_f32_bf16(stage, lr, lc, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
   } else if (n == "lora_a") {
     cudaMemcpyAsync(e->loraA + (size_t)L * f * r, stage, lcount * 4, cudaMemcpyDeviceToDevice, st);
     rc = refresh_lora(e, 0, 0, 0, 0, 0);
@@ -745,8 +750,9 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
     e->transient_allocs += 1;
     for (size_t l = 0; l < NL; ++l) {
       cs::init_normal_f32(tmp, (long)e->f * e->h, wf, ss + 100 + l, st);
-      cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->h * e->f_cat, e->f_cat, 1, st);
-      cs::cast_f32_bf16(tmp, e->f, e->h, e->dbwd_cat + l * e->f * e->h_cat, e->h_cat, 0, st);
+      cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->down_rows * e->f_cat, e->f_cat, 1, st);
+      if (!e->bwd_mn)
+        cs::cast_f32_bf16(tmp, e->f, e->h, e->dbwd_cat + l * e->f * e->h_cat, e->h_cat, 0, st);
     }
     cudaStreamSynchronize(st);
     cudaFree(tmp);
@@ -1379,7 +1385,7 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                   e->lu + (size_t)(sp.ft_row0 - sp.ad_row0) * r, r, n_ft, r);
     }
     // x += [m | u] [W_down ; B] (tiny_model.hpp:206-211 as one K-concatenated GEMM)
-    TRY(tp_rowpar(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * h * e->f_cat, e->f_cat, h,
+    TRY(tp_rowpar(e, e->m, e->f_cat, e->T_max, e->down_cat + (size_t)l * e->down_rows * e->f_cat, e->f_cat, h,
                   e->x, T, e->f_cat, true));
   }
   // ---- sampled rows: final norm -> logits -> argmax
@@ -1455,8 +1461,12 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
            cs::EPI_F32));
   cs::lora_pack(e->dlu, r, e->dycat, e->h_cat, h, s, st);
   cs::lora_db(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, r, s, h, e->gB + (size_t)n * r * h, st);
-  TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
-           e->dm, f, s, f, e->h_cat, cs::EPI_F32));
+  if (e->bwd_mn)  // dm = [dY | dU] . [W_down^T ; A^T]: down_cat's [h + 64, f] block, MN-major
+    TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->down_cat + (size_t)n * e->down_rows * e->f_cat,
+             e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_F32, nullptr, nullptr, 1));
+  else
+    TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
+             e->dm, f, s, f, e->h_cat, cs::EPI_F32));
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
               e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
   if (n > 0) {

@@ -194,8 +194,10 @@ struct AdamParams {
   float* vB;
   bf16* A_t;        // [n_layers][16][f]          (lu GEMM B operand)
   bf16* B_t;        // [n_layers][16][h]          (dlu GEMM B operand)
-  bf16* down_cat;   // [n_layers][h][f + 64]     cols f.. = B^T
-  bf16* dbwd_cat;   // [n_layers][f][h + 64]     cols h.. = A
+  bf16* down_cat;   // [n_layers][down_rows][f + 64]  rows < h: cols f.. = B^T; rows h.. = A^T
+  bf16* dbwd_cat;   // [n_layers][f][h + 64]     cols h.. = A   (a_in_down == 0 only)
+  int down_rows;    // h (+ 64 when A^T rides in down_cat: the MN-major backward operand)
+  int a_in_down;
   int n_layers, f, r, h;
   float lr, b1, b2, eps, bc1, bc2;
 };
