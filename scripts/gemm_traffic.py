@@ -1,7 +1,7 @@
 """DRAM traffic of the tcgen05 GEMM vs its algorithmic bytes, for bench.py's `roofline.traffic`.
 
 Run under ncu (one GPU):
-  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:gemm_tn_kernel --csv \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:gemm_tn --csv \
       --log-file gpurun_out/gemm_traffic.csv python scripts/gemm_traffic.py
 then `python scripts/gemm_traffic.py --reduce gpurun_out/gemm_traffic.csv` writes
 profiles/gemm_traffic.json: DRAM bytes per launch (ncu) next to the engine's algorithmic
@@ -60,7 +60,7 @@ def reduce(path):
     n = len(ids)
     res = {"dram_bytes_per_launch": tot / n, "algorithmic_bytes_per_launch": alg["algorithmic_bytes"] / alg["launches"],
            "launches_ncu": n, "launches_engine": alg["launches"],
-           "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:gemm_tn_kernel "
+           "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:gemm_tn "
                      "over scripts/gemm_traffic.py (cold-cache, serialised replays)"}
     res["traffic_over_algorithmic"] = res["dram_bytes_per_launch"] / res["algorithmic_bytes_per_launch"]
     json.dump(res, open(os.path.join(ROOT, "profiles", "gemm_traffic.json"), "w"), indent=1)
