@@ -523,24 +523,276 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------- swapped operands
+// Decode rows are the GQA group of ONE query position (4 rows for LLaMA-8B, 5 for Qwen): the
+// kernels above put them on the M=16 side of mma.m16n8k16 and waste 3/4 of every MMA.  Here the
+// keys and head dims take the M side and the (<= 8) packed query rows the N=8 side:
+//   S^T[32 keys x 8 rows] = K . Q^T   (A = K tile via ldmatrix, B = Q^T fragments in registers)
+//   O^T[128 d x 8 rows]  += V^T . P^T (A = V^T via ldmatrix.trans, B = P^T)
+// P^T's accumulator fragment (key rows, query columns) becomes the B fragment (query rows,
+// key columns) with one movmatrix.trans per 8x8 block.  Half the MMAs and half the exp2 per
+// K/V byte of the M=16 formulation; the per-query softmax statistics are column reductions
+// (shuffles across the 8 lanes that share a column pair).  Persistent per-warp streams over
+// whole items with the TMA ring running across item boundaries, as above.
+CS_DEV uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+template <int D, int KT, int NWARP, int STAGES>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+    attn_decode_swap_kernel(const __grid_constant__ CUtensorMap tmK,
+                            const __grid_constant__ CUtensorMap tmV, AttnFwdParams p, int n_items) {
+  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  constexpr int NH = D / 64;
+  constexpr int HALF = KT * 128;
+  constexpr int TILE = NH * HALF;
+  constexpr int MT = KT / 16;  // 16-key m-tiles of S^T (= k-steps of the PV product)
+  constexpr int DM = D / 16;   // 16-dim m-tiles of O^T
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TW = gridDim.x * NWARP;
+  const int gw = blockIdx.x * NWARP + warp;
+  uint8_t* ws = smem + warp * (STAGES * 2 * TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NWARP * STAGES * 2 * TILE) + warp * STAGES;
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  __syncwarp();
+  if (gw >= n_items) return;
+  const int grp = p.grp;
+  struct Item {
+    int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
+  };
+  auto load_item = [&](int it) {
+    const int4* q = reinterpret_cast<const int4*>(p.dwork + it);
+    const int4 a = __ldg(q), b = __ldg(q + 1);
+    return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  };
+  int is_item = gw, is_t = 0, is_n = 0;
+  Item iw{};
+  long g_issue = 0, g_cons = 0;
+  auto issue_open = [&]() {
+    iw = load_item(is_item);
+    is_t = 0;
+    is_n = (iw.k_end + KT - 1) / KT - iw.k_begin / KT;
+  };
+  auto top_up = [&]() {
+    while (is_item < n_items && g_issue < g_cons + STAGES) {
+      const int st = (int)(g_issue % STAGES);
+      uint8_t* dk = ws + st * 2 * TILE;
+      uint8_t* dv = dk + TILE;
+      mbar_arrive_expect_tx(&full[st], 2 * TILE);
+      const int kt = iw.k_begin / KT + is_t;
+      const int last_box = (iw.k_end - 1) & ~15;
+      const AttnDecWork* wp = p.dwork + is_item;
+#pragma unroll
+      for (int b = 0; b < KT / 16; ++b) {
+        const int jb = min(kt * KT + b * 16, last_box);
+        const int bi = (jb - iw.k_begin) >> 4;
+        const int prow = bi < 8 ? __ldg(wp->prow + bi)
+                                : __ldg(p.page_table + iw.page_off + jb / p.page_size) * p.page_size + jb % p.page_size;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          const int col = iw.kv_head * D + hh * 64;
+          tma_load_2d(&tmK, &full[st], dk + hh * HALF + b * 2048, col, prow);
+          tma_load_2d(&tmV, &full[st], dv + hh * HALF + b * 2048, col, prow);
+        }
+      }
+      ++g_issue;
+      if (++is_t == is_n) {
+        is_item += TW;
+        if (is_item < n_items) issue_open();
+      }
+    }
+  };
+  if (lane == 0) {
+    issue_open();
+    top_up();
+  }
+  const int g = lane >> 2, t = lane & 3;
+  for (int item = gw; item < n_items; item += TW) {
+    const Item w = load_item(item);
+    const int nrows = w.nq * grp;  // <= 8
+    // B fragments of Q^T: lane holds Q[row g][d = 16 kk + 2t (+8), +1]
+    uint32_t qf[D / 16][2];
+    {
+      const __nv_bfloat16* qr = g < nrows
+                                    ? p.q + (long)(w.q_row + g / grp) * p.q_ld + (long)(w.kv_head * grp + g % grp) * D
+                                    : nullptr;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        qf[kk][0] = qr ? ld_u32(qr + kk * 16 + 2 * t) : 0u;
+        qf[kk][1] = qr ? ld_u32(qr + kk * 16 + 8 + 2 * t) : 0u;
+      }
+    }
+    // this lane's two query columns 2t, 2t+1
+    const int c0 = 2 * t, c1 = 2 * t + 1;
+    const int pos_0 = c0 < nrows ? w.pos0 + c0 / grp : -1;
+    const int pos_1 = c1 < nrows ? w.pos0 + c1 / grp : -1;
+    float o[DM][4];
+#pragma unroll
+    for (int i = 0; i < DM; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_0 = -INFINITY, m_1 = -INFINITY, l_0 = 0.f, l_1 = 0.f;
+    const int kt0 = w.k_begin / KT, nt = (w.k_end + KT - 1) / KT - kt0;
+    for (int tt = 0; tt < nt; ++tt) {
+      if (lane == 0) top_up();
+      const int st = (int)(g_cons % STAGES);
+      mbar_wait(&full[st], (uint32_t)((g_cons / STAGES) & 1));
+      const uint32_t kb = smem_u32(ws + st * 2 * TILE), vb = kb + TILE;
+      const int kt = kt0 + tt;
+      // ---- S^T = K Q^T
+      float s[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) s[mt][0] = s[mt][1] = s[mt][2] = s[mt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t a[4];
+          ldsm_x4(kb + tile_off<KT>(mt * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), kk * 2 + (lane >> 4)),
+                  a[0], a[1], a[2], a[3]);
+          mma16816(s[mt], a, qf[kk][0], qf[kk][1]);
+        }
+      }
+      // ---- mask + column (per query) online softmax
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = kt * KT + mt * 16 + g + ((e >> 1) << 3);
+          const int pos = (e & 1) ? pos_1 : pos_0;
+          float v = s[mt][e] * p.scale_log2;
+          if (j > pos || j >= w.k_end) v = -INFINITY;
+          s[mt][e] = v;
+        }
+        mx0 = fmaxf(mx0, fmaxf(s[mt][0], s[mt][2]));
+        mx1 = fmaxf(mx1, fmaxf(s[mt][1], s[mt][3]));
+      }
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, x));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, x));
+      }
+      const float mn0 = fmaxf(m_0, mx0), mn1 = fmaxf(m_1, mx1);
+      const float mu0 = mn0 == -INFINITY ? 0.f : mn0;
+      const float mu1 = mn1 == -INFINITY ? 0.f : mn1;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t pb[MT][2];  // P^T as B fragments of the PV product
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const float p0 = ex2_approx(s[mt][0] - mu0), p1 = ex2_approx(s[mt][1] - mu1);
+        const float p2 = ex2_approx(s[mt][2] - mu0), p3 = ex2_approx(s[mt][3] - mu1);
+        rs0 += p0 + p2;
+        rs1 += p1 + p3;
+        pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));  // keys 16mt + 0..7
+        pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));  // keys 16mt + 8..15
+      }
+      if (__any_sync(0xffffffffu, mn0 != m_0 || mn1 != m_1)) {
+        const float f0 = ex2_approx(m_0 - mu0), f1 = ex2_approx(m_1 - mu1);
+        l_0 *= f0;
+        l_1 *= f1;
+#pragma unroll
+        for (int i = 0; i < DM; ++i) {
+          o[i][0] *= f0;
+          o[i][1] *= f1;
+          o[i][2] *= f0;
+          o[i][3] *= f1;
+        }
+      }
+      m_0 = mn0;
+      m_1 = mn1;
+      l_0 += rs0;
+      l_1 += rs1;
+      // ---- O^T += V^T P^T
+#pragma unroll
+      for (int ks = 0; ks < MT; ++ks) {
+#pragma unroll
+        for (int dm = 0; dm < DM; ++dm) {
+          uint32_t a[4];
+          ldsm_x4_t(vb + tile_off<KT>(ks * 16 + (lane & 7) + ((lane >> 4) << 3), dm * 2 + ((lane >> 3) & 1)),
+                    a[0], a[1], a[2], a[3]);
+          mma16816(o[dm], a, pb[ks][0], pb[ks][1]);
+        }
+      }
+      __syncwarp();  // every lane is done reading this stage before lane 0 refills it
+      ++g_cons;
+    }
+    // ---- epilogue: column sums, normalise, store O[q][d] (the next item's tiles are in flight)
+#pragma unroll
+    for (int x = 4; x < 32; x <<= 1) {
+      l_0 += __shfl_xor_sync(0xffffffffu, l_0, x);
+      l_1 += __shfl_xor_sync(0xffffffffu, l_1, x);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int q = cc ? c1 : c0;
+      if (q >= nrows) continue;
+      const float L = cc ? l_1 : l_0, M = cc ? m_1 : m_0;
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      const int qr = q / grp, hq = w.kv_head * grp + (q - qr * grp);
+      if (w.part < 0) {
+        const long row = w.q_row + qr;
+        __nv_bfloat16* dst = p.out + row * p.out_ld + (long)hq * D;
+#pragma unroll
+        for (int dm = 0; dm < DM; ++dm) {
+          dst[dm * 16 + g] = __float2bfloat16(o[dm][cc] * inv);
+          dst[dm * 16 + g + 8] = __float2bfloat16(o[dm][2 + cc] * inv);
+        }
+        if (g == 0 && p.lse) p.lse[row * p.lse_ld + hq] = L > 0.f ? (M + __log2f(L)) * kLn2 : -INFINITY;
+      } else {
+        float* dst = p.part_o + ((long)w.part * 64 + q) * D;
+#pragma unroll
+        for (int dm = 0; dm < DM; ++dm) {
+          dst[dm * 16 + g] = o[dm][cc] * inv;
+          dst[dm * 16 + g + 8] = o[dm][2 + cc] * inv;
+        }
+        if (g == 0) p.part_lse[(long)w.part * 64 + q] = L > 0.f ? (M + __log2f(L)) * kLn2 : -INFINITY;
+      }
+    }
+  }
+}
+
 namespace {
 struct DecVariant {
   int stream, kt, nwarp, stages;
 };
-// CS_DEC_CFG=[9]<kt><nwarp><stages> (A/B testing): 3243 = per-item CTAs, 32-key tiles, 4 warps
-// x 3 stages; a leading 9 = persistent per-warp streams (attn_decode_stream_kernel)
+// CS_DEC_CFG=[k]<kt><nwarp><stages> (A/B testing): 3243 = per-item CTAs, 32-key tiles, 4 warps
+// x 3 stages; a leading 1 = persistent per-warp streams (attn_decode_stream_kernel), 2 = the
+// swapped-operand streams (attn_decode_swap_kernel)
 DecVariant dec_variant() {
   static const DecVariant v = [] {
-    DecVariant d{0, 32, 2, 2};
+    DecVariant d{2, 32, 2, 2};
     if (const char* e = std::getenv("CS_DEC_CFG")) {
       int x = std::atoi(e);
-      const int stream = x >= 10000 ? 1 : 0;
+      const int stream = x / 10000;  // 0 per-item CTAs, 1 streams, 2 swapped-operand streams
       x %= 10000;
       d = DecVariant{stream, x / 100, (x / 10) % 10, x % 10};
     }
     return d;
   }();
   return v;
+}
+
+template <int D, int KT, int NW, int ST>
+cudaError_t launch_dec_swap(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                            int n_work, cudaStream_t st) {
+  constexpr int smem = dec_smem<D, KT, NW, ST>();
+  static bool once = (cudaFuncSetAttribute(attn_decode_swap_kernel<D, KT, NW, ST>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                      true);
+  (void)once;
+  const int cps = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
+  const int grid = std::max(1, std::min((n_work + NW - 1) / NW, 148 * cps));
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  attn_decode_swap_kernel<D, KT, NW, ST><<<grid, NW * 32, smem, st>>>(tmK, tmV, p, n_work);
+  return cudaGetLastError();
 }
 
 template <int D, int KT, int NW, int ST>
@@ -575,6 +827,17 @@ template <int D>
 cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          int n_work, cudaStream_t st) {
   const DecVariant v = dec_variant();
+  if (v.stream == 2) {  // swapped operands: every item's packed rows must fit N = 8
+    if (p.max_dec_rows <= 8) {
+      switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
+        case 3223: return launch_dec_swap<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
+        case 1624: return launch_dec_swap<D, 16, 2, 4>(p, tmK, tmV, n_work, st);
+        case 3242: return launch_dec_swap<D, 32, 4, 2>(p, tmK, tmV, n_work, st);
+        default: return launch_dec_swap<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
+      }
+    }
+    return launch_dec_stream<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
+  }
   if (v.stream) {
     switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
       case 3222: return launch_dec_stream<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
