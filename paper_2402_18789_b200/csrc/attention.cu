@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnFwdParams p) {
 template <int D>
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  // launched with PDL: the CTAs are resident while the producing attention kernel drains;
+  // its partials are visible after the wait
+  griddep_wait();
   const AttnCombine c = p.combine[blockIdx.x];
   const AttnSeg sg = p.segs[c.seg];
   const int grp = p.grp;
@@ -659,7 +662,8 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      attn_combine_kernel<128><<<dim3(n_combine, 4), 128, 0, st>>>(p);
+      const cudaError_t e = launch_pdl(attn_combine_kernel<128>, dim3(n_combine, 4), dim3(128), 0, st, p);
+      if (e != cudaSuccess) return e;
     }
   } else if (head_dim == 64) {
     constexpr int smem = 64 * 64 * 2 * 5;
@@ -671,7 +675,8 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      attn_combine_kernel<64><<<dim3(n_combine, 4), 128, 0, st>>>(p);
+      const cudaError_t e = launch_pdl(attn_combine_kernel<64>, dim3(n_combine, 4), dim3(128), 0, st, p);
+      if (e != cudaSuccess) return e;
     }
   } else {
     return cudaErrorInvalidValue;
@@ -683,9 +688,9 @@ cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cu
   if (n_combine <= 0) return cudaSuccess;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   const dim3 grid(n_combine, (p.part_rows + 15) / 16);
-  if (head_dim == 128) attn_combine_kernel<128><<<grid, 128, 0, st>>>(p);
-  else if (head_dim == 64) attn_combine_kernel<64><<<grid, 128, 0, st>>>(p);
-  else return cudaErrorInvalidValue;
+  if (head_dim == 128) return launch_pdl(attn_combine_kernel<128>, grid, dim3(128), 0, st, p);
+  if (head_dim == 64) return launch_pdl(attn_combine_kernel<64>, grid, dim3(128), 0, st, p);
+  return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -93,7 +93,6 @@ struct cs_engine {
   unsigned long long* amax_part;
   float *part_o, *part_lse;
   float* tp_sync;  // [8 ranks][8 values]: cs_engine_tp_sync_max
-  int* dec_counters;  // [8192] split-group counters of the swapped decode kernel (self-resetting)
   // fused row-parallel GEMM + all-reduce (peer-memory groups): staging [ranks][rpo][h] fp32,
   // zero between uses; peer tables exchanged lazily (same call order on every rank)
   float* tp_stage = nullptr;
@@ -278,7 +277,6 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(dh1, S * h);
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
   AL(tp_sync, 64);
-  AL(dec_counters, 8192);
   AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
@@ -1092,8 +1090,6 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       else comb.clear();
     }
   }
-  std::vector<int> part_group;                   // decode part -> in-kernel merge group
-  std::vector<std::pair<int, int>> group_range;  // group -> (first part, parts)
   // decode: balance the 32-key tiles over the SMs -- split long key ranges into parts of
   // `chunk` keys (multiples of 128 = one tile per warp) so that the grid is ~8 waves of
   // 1 CTA/SM (small wave-quantisation tail, longest parts first), but no part is shorter
@@ -1111,9 +1107,8 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     chunk = std::max<long>(4 * tile_round, (chunk + tile_round - 1) / tile_round * tile_round);
     int part = 0;
     for (const auto& c : comb) part = std::max(part, c.part0 + c.n_parts);
-    // (merging the split groups inside the decode kernel -- last part merges -- measured
-    // slower than the separate combine launch: one warp serialises the merge at the tail)
-    const bool fused_merge = false;
+    // (merging the split groups inside the decode kernel -- the last part merges -- measured
+    // slower than the separate, PDL-overlapped combine launch: one warp serialised the merge)
     std::vector<cs::AttnWork> w2;
     w2.reserve(work_dec.size());
     for (const auto& w : work_dec) {
@@ -1132,13 +1127,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
         x.part = part++;
         w2.push_back(x);
       }
-      if (fused_merge) {
-        if ((int)part_group.size() < part) part_group.resize(part, -1);
-        for (int q = p0; q < part; ++q) part_group[q] = (int)group_range.size();
-        group_range.push_back({p0, part - p0});
-      } else {
-        comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
-      }
+      comb.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
     }
     // longest first: the heaviest CTAs start in the first wave
     std::stable_sort(w2.begin(), w2.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
@@ -1219,12 +1208,6 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       for (int b = 0; b < 8; ++b) {
         const int jb = std::min(w.k_begin + 16 * b, last_box);
         d.prow[b] = plan->page_table[g.page_off + jb / P] * P + jb % P;
-      }
-      d.group = -1;
-      if (w.part >= 0 && w.part < (int)part_group.size() && part_group[w.part] >= 0) {
-        d.group = part_group[w.part];
-        d.part0 = group_range[d.group].first;
-        d.n_parts = group_range[d.group].second;
       }
       dw[i] = d;
     }
@@ -1339,7 +1322,6 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
       cs::AttnFwdParams dp = ap;
       dp.dwork = sp.work_dec;
       dp.max_dec_rows = sp.dec_max_rows;
-      dp.dec_counters = e->dec_counters;
       CUtensorMap mk, mv;
       const long pool_rows = (long)e->npages * e->P;
       if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||

@@ -24,8 +24,6 @@ struct AttnWork {  // one CTA of attn_fwd_kernel
 struct AttnDecWork {
   int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
   int prow[8];
-  // split group of this part (group / first part / parts; -1 = merged by attn_combine)
-  int group, part0, n_parts, pad;
 };
 
 struct AttnCombine {  // one CTA of attn_combine_kernel
@@ -53,7 +51,6 @@ struct AttnFwdParams {
   float scale_log2;
   int part_rows = 64;  // rows per split-KV part in part_o / part_lse (combine)
   int max_dec_rows = 16;  // attn_decode: max packed rows (q_len x group) over the work items
-  int* dec_counters = nullptr;  // per split group, zero between launches (self-resetting)
 };
 
 struct AttnBwdParams {
