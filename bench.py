@@ -96,28 +96,36 @@ def dist_env():
 
 # ----------------------------------------------------------------------------- reference arm
 def _ref_worker(args):
-    """One host process: the reference's forward_full + backward_full on an 8B-shaped layer."""
-    L_tok, samples, seed = args
+    """One host process: the reference's forward_full + backward_full on an 8B-shaped layer;
+    `warm` untimed steps, then `samples` timed ones (at most `budget_s` seconds of them)."""
+    L_tok, samples, seed = args[:3]
+    warm = args[3] if len(args) > 3 else 0
+    budget_s = args[4] if len(args) > 4 else 1e9
     sys.path.insert(0, ROOT)
     from oracle import ref as R  # noqa: E402  (reference CPU path = the measured thing here)
     m = R.RefTinyModel(depth=1, hidden=4096, heads=32, ffn_mult=4, vocab=64, rank=16, seed=seed)
     toks = list(range(L_tok))
+    for _ in range(warm):
+        m.time_forward_backward(toks, 1)
     ts = []
+    t_start = time.time()
     for _ in range(samples):
         ts.append(m.time_forward_backward(toks, 1))
+        if time.time() - t_start > budget_s:
+            break
     return ts
 
 
-def reference_rate(L_tok: int, samples: int, procs: int):
+def reference_rate(L_tok: int, samples: int, procs: int, warm: int = 0, budget_s: float = 1e9):
     """FT tokens/s of the reference CPU path: one layer fwd+bwd on L_tok tokens, extrapolated x32
     layers (the reference cannot express f=14336 / GQA / V=128256: ffn_mult=4, MHA, V=64)."""
     import multiprocessing as mp
     if procs <= 1:
-        ts = _ref_worker((L_tok, samples, 1))
+        ts = _ref_worker((L_tok, samples, 1, warm, budget_s))
         per = [L_tok / (t * L8B["n_layers"]) for t in ts]
         return statistics.median(per), ts
     with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_ref_worker, [(L_tok, samples, 1 + i) for i in range(procs)])
+        res = pool.map(_ref_worker, [(L_tok, samples, 1 + i, warm, budget_s) for i in range(procs)])
     # aggregate throughput: each process contributes its own rate
     rate = sum(statistics.median([L_tok / (t * L8B["n_layers"]) for t in ts]) for ts in res)
     return rate, [t for ts in res for t in ts]
@@ -137,14 +145,16 @@ def run_reference(a):
     cores = os.cpu_count() or 1
     L_tok = 4
     t0 = time.time()
-    # warmup W and K steps are bounded samples: each step = one fwd+bwd of L_tok tokens through
-    # one 8B-shaped layer in every worker process
-    steps = max(1, min(a.steps, 3))
-    rate, ts = reference_rate(L_tok, steps, cores)
+    # W warm-up and K timed steps, each a bounded sample: one fwd+bwd of L_tok tokens through
+    # one 8B-shaped layer in every worker process (~2 s); the timed steps stop after ~150 s so
+    # the run ends within a few minutes whatever K is
+    warm = max(0, min(a.warmup, 2))
+    rate, ts = reference_rate(L_tok, max(1, a.steps), cores, warm=warm, budget_s=150.0)
+    steps = max(1, len(ts) // max(1, cores))
     wall = time.time() - t0
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 6), "unit": "tokens/s",
-        "n_gpus": world, "steps": steps, "warmup": 0,
+        "n_gpus": world, "steps": steps, "warmup": warm, "steps_requested": a.steps,
         "ms_per_step": round(1000.0 * statistics.median(ts), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic tokens, reference TinyModel::init weights",
