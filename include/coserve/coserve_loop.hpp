@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "coserve/baselines.hpp"
+#include "coserve/vtc.hpp"
 #include "coserve/cost_model.hpp"
 #include "coserve/scheduler.hpp"
 #include "coserve/workload.hpp"
@@ -73,6 +74,11 @@ struct LoopConfig {
   Policy policy = Policy::Coserve;
   int temporal_n = 128;
   bool sim_clock = false;       // advance the clock by predicted latency even with an executor
+  // Virtual Token Counter fair admission across tenants (coserve/vtc.hpp, App. C);
+  // finetuning tokens are charged to ft_tenant (-1: to nobody)
+  bool vtc = false;
+  double vtc_wp = 1.0, vtc_wq = 2.0, vtc_wr = 1.0;
+  int ft_tenant = -1;
   WorkloadConfig workload;
 };
 
@@ -96,6 +102,12 @@ struct LoopStats {
   std::vector<double> ttft_ms, tpot_ms;
   std::vector<IterLog> log;
   bool ok = true;
+  // VTC: cumulative weighted service and completed requests per tenant, max spread of the
+  // queued tenants' counters (Lemma 1), max |W_0 - W_1| gap over intervals where tenants 0
+  // and 1 are both backlogged (Theorem 1)
+  std::vector<double> tenant_service;
+  std::vector<int64_t> tenant_done;
+  double vtc_spread_max = 0.0, vtc_pair_gap_max = 0.0;
 };
 
 // deterministic synthetic token ids (data: synthetic)
@@ -155,6 +167,14 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
   double corr[3] = {1.0, 1.0, 1.0};  // adaptive, per FT phase (none / forward / backward)
   const bool temporal = cfg.policy != Policy::Coserve;
   DtsState dts;
+  VtcLedger vtc;
+  vtc.w_p = cfg.vtc_wp;
+  vtc.w_q = cfg.vtc_wq;
+  vtc.w_r = cfg.vtc_wr;
+  SchedulerConfig sched = cfg.sched;
+  sched.external_admission = cfg.vtc;
+  bool pair_on = false;  // tenants 0 and 1 both backlogged
+  double pair_lo = 0.0, pair_hi = 0.0;
   int inf_since_ft = 0;   // inference-only iterations since the last finetuning iteration
   bool ft_block = false;  // temporal sharing: inside a finetuning iteration (inference blocked)
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
@@ -170,6 +190,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       r.prompt_len = a.prompt_len;
       r.gen_len = a.gen_len;
       r.arrival_ms = a.time_ms;
+      if (cfg.vtc) vtc.on_arrival(r.tenant);
       queue.push_back(std::move(r));
     }
     // decode growth: make room for each decoding request's next token (eviction if none)
@@ -184,6 +205,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
           r.emitted = 0;
           r.evictions += 1;
           st.evictions += 1;
+          if (cfg.vtc) vtc.on_arrival(r.tenant);
           queue.push_front(std::move(r));
           running.erase(running.begin() + i);
           continue;
@@ -201,15 +223,18 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       prof.decode_ms_per_row *= corr[cph];
       prof.prefill_ms_per_token *= corr[cph];
     }
+    std::vector<int64_t> vtc_admitted;
+    if (cfg.vtc && !(temporal && ft_block))
+      vtc_admitted = admit_requests_vtc(queue, running, mem, sched, vtc);
     IterationPlan plan;
     if (!temporal) {
-      plan = plan_iteration(queue, running, ft, prof, cfg.sched, mem, cfg.budget_ms);
+      plan = plan_iteration(queue, running, ft, prof, sched, mem, cfg.budget_ms);
     } else if (ft_block) {
       plan = plan_ft_block(ft, prof, cfg.sched);
     } else {
       FtState idle = ft;  // inference-only iteration
       idle.phase = FtPhase::Idle;
-      plan = plan_iteration(queue, running, idle, prof, cfg.sched, mem, cfg.budget_ms);
+      plan = plan_iteration(queue, running, idle, prof, sched, mem, cfg.budget_ms);
       if (plan.c == 0 && ft.L > 0) {  // nothing to serve: the finetuning iteration runs now
         ft_block = true;
         plan = plan_ft_block(ft, prof, cfg.sched);
@@ -305,6 +330,23 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       }
       ++seg;
     }
+    if (cfg.vtc) {  // generated tokens w_q (decodes + prefill-completing first tokens), FT w_r
+      for (int i : plan.decode) vtc.charge(running[i].tenant, vtc.w_q);
+      for (const PrefillChunk& pc : plan.prefill)
+        if (!running[pc.req].in_prefill()) vtc.charge(running[pc.req].tenant, vtc.w_q);
+      if (cfg.ft_tenant >= 0 && s > 0) vtc.charge(cfg.ft_tenant, vtc.w_r * (double)s);
+      st.vtc_spread_max = std::max(st.vtc_spread_max, vtc.queued_spread());
+      const bool both = vtc.queued.size() > 1 && vtc.queued[0] > 0 && vtc.queued[1] > 0;
+      const double dW = vtc.service.size() > 1 ? vtc.service[0] - vtc.service[1] : 0.0;
+      if (both) {
+        if (!pair_on) pair_on = true, pair_lo = pair_hi = dW;
+        pair_lo = std::min(pair_lo, dW);
+        pair_hi = std::max(pair_hi, dW);
+        st.vtc_pair_gap_max = std::max(st.vtc_pair_gap_max, pair_hi - pair_lo);
+      } else {
+        pair_on = false;
+      }
+    }
     // retire finished requests
     int64_t completed = 0;
     for (size_t i = 0; i < running.size();) {
@@ -318,6 +360,8 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
           st.tpot_ms.push_back(tpot);
           st.requests_done += 1;
           if (tpot <= cfg.sched.tpot_slo_ms && ttft <= cfg.sched.ttft_slo_ms) st.requests_slo_ok += 1;
+          if ((int)st.tenant_done.size() <= r.tenant) st.tenant_done.resize(r.tenant + 1, 0);
+          st.tenant_done[r.tenant] += 1;
         }
         mem.release(r.pages);
         running.erase(running.begin() + i);
@@ -388,6 +432,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     st.log.push_back(lg);
     st.iters += 1;
   }
+  st.tenant_service = vtc.service;
   return st;
 }
 

@@ -66,6 +66,8 @@ struct SchedulerConfig {
   // layers (layer n to 0, then n-1 from L) when the budget allows -- Alg. 2 order is kept.
   // false reproduces SPEC.md:433 (one layer per iteration).
   bool multi_layer_bwd = false;
+  // admission done by the caller before planning (VTC fair admission, coserve/vtc.hpp)
+  bool external_admission = false;
 };
 
 struct BwdWindow {
@@ -123,7 +125,7 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
                                     const SchedulerConfig& cfg, MemoryModel& mem,
                                     double budget_ms) {
   IterationPlan p;
-  p.admitted = admit_requests(queue, running, mem, cfg);
+  if (!cfg.external_admission) p.admitted = admit_requests(queue, running, mem, cfg);
   // token budget at the SLO for inference work (the inverse model with c = 0)
   const int64_t tok_budget =
       std::min<int64_t>(max_finetune_tokens(prof, 0, budget_ms), cfg.max_tokens);

@@ -62,6 +62,11 @@ struct WorkloadConfig {
   int prompt_min = 16, prompt_max = 4096;
   double gen_mu = 4.5, gen_sigma = 0.7;
   int gen_min = 8, gen_max = 1024;
+  // tenants (VTC fairness runs): arrival i goes to tenant 0 with probability tenant0_share,
+  // else uniformly to 1..n_tenants-1; drawn from a separate stream, so times and lengths are
+  // the single-tenant trace's
+  int n_tenants = 1;
+  double tenant0_share = 0.5;
 };
 
 inline int clip_len(double v, int lo, int hi) {
@@ -90,6 +95,13 @@ inline std::vector<Arrival> generate_trace(const WorkloadConfig& c, uint64_t see
     a.prompt_len = clip_len(rng.lognormal(c.prompt_mu, c.prompt_sigma), c.prompt_min, c.prompt_max);
     a.gen_len = clip_len(rng.lognormal(c.gen_mu, c.gen_sigma), c.gen_min, c.gen_max);
     out.push_back(a);
+  }
+  if (c.n_tenants > 1) {
+    TraceRng trng(seed ^ 0x7E7A7E7Aull);
+    for (auto& a : out) {
+      const double u = trng.uniform();
+      a.tenant = u < c.tenant0_share ? 0 : 1 + (int)trng.uniform_int(0, c.n_tenants - 2);
+    }
   }
   return out;
 }

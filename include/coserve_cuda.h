@@ -231,6 +231,12 @@ typedef struct cs_coserve_config {
   /* 1: advance the loop clock by the planner's predicted latency even with an engine (a
    * timing-independent plan sequence, e.g. for profiling runs under ncu) */
   int32_t sim_clock;
+  /* Virtual Token Counter fair admission (Appendix C): vtc = 1 enables it; arrivals
+   * go to tenant 0 with probability tenant0_share, else uniformly to 1..n_tenants-1; charges
+   * w_p per prompt token at admission, w_q per generated token, w_r per finetuning token to
+   * ft_tenant (-1: nobody) */
+  int32_t vtc, n_tenants, ft_tenant;
+  double tenant0_share, vtc_wp, vtc_wq, vtc_wr;
 } cs_coserve_config;
 
 typedef struct cs_coserve_stats {
@@ -244,6 +250,12 @@ typedef struct cs_coserve_stats {
   double iter_p50_ms, iter_p99_ms, iter_max_ms; /* timed iterations with inference work */
   int64_t gpu_launches;                        /* kernels launched in the timed region   */
   int64_t h2d_bytes, d2h_bytes;                /* host<->device bytes in the timed region */
+  /* VTC (tenants 0..7): cumulative weighted service, completed requests, max spread of the
+   * backlogged tenants' counters (Lemma 1), max |W_0 - W_1| over intervals where tenants 0
+   * and 1 are both backlogged (Theorem 1) */
+  double tenant_service[8];
+  int64_t tenant_done[8];
+  double vtc_spread_max, vtc_pair_gap_max;
 } cs_coserve_stats;
 
 typedef struct cs_iter_log {

@@ -154,6 +154,15 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.policy = (coserve::Policy)c->policy;
   L.temporal_n = c->temporal_n > 0 ? c->temporal_n : 128;
   L.sim_clock = c->sim_clock != 0;
+  L.vtc = c->vtc != 0;
+  if (L.vtc) {
+    L.vtc_wp = c->vtc_wp > 0 ? c->vtc_wp : 1.0;
+    L.vtc_wq = c->vtc_wq > 0 ? c->vtc_wq : 2.0;
+    L.vtc_wr = c->vtc_wr > 0 ? c->vtc_wr : 1.0;
+    L.ft_tenant = c->ft_tenant;
+  }
+  L.workload.n_tenants = std::max(1, std::min(8, (int)c->n_tenants));
+  L.workload.tenant0_share = c->tenant0_share > 0 ? c->tenant0_share : 0.5;
   L.workload.rate_rps = c->rate_rps;
   L.workload.duration_s = c->duration_s;
   L.workload.burst_amplitude = c->burst_amplitude;
@@ -230,6 +239,12 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   stats->iter_p50_ms = pct(its, 0.5);
   stats->iter_p99_ms = pct(its, 0.99);
   stats->iter_max_ms = its.empty() ? 0.0 : *std::max_element(its.begin(), its.end());
+  for (int t = 0; t < 8; ++t) {
+    stats->tenant_service[t] = t < (int)st.tenant_service.size() ? st.tenant_service[t] : 0.0;
+    stats->tenant_done[t] = t < (int)st.tenant_done.size() ? st.tenant_done[t] : 0;
+  }
+  stats->vtc_spread_max = st.vtc_spread_max;
+  stats->vtc_pair_gap_max = st.vtc_pair_gap_max;
   if (ex) {
     stats->gpu_launches = cs_engine_launch_count(e) - counting.launches0;
     stats->h2d_bytes = ex->h2d;

@@ -67,7 +67,9 @@ class CoserveConfig(ctypes.Structure):
                 ("multi_layer_bwd", i32),
                 ("seed", ctypes.c_uint64),
                 ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64),
-                ("policy", i32), ("temporal_n", i32), ("sim_clock", i32)]
+                ("policy", i32), ("temporal_n", i32), ("sim_clock", i32),
+                ("vtc", i32), ("n_tenants", i32), ("ft_tenant", i32),
+                ("tenant0_share", f64), ("vtc_wp", f64), ("vtc_wq", f64), ("vtc_wr", f64)]
 
 POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS = 0, 1, 2
 
@@ -80,7 +82,9 @@ class CoserveStats(ctypes.Structure):
                 ("evictions", i64), ("ttft_p50_ms", f64), ("ttft_p99_ms", f64),
                 ("tpot_p50_ms", f64), ("tpot_p99_ms", f64), ("iter_p50_ms", f64),
                 ("iter_p99_ms", f64), ("iter_max_ms", f64), ("gpu_launches", i64),
-                ("h2d_bytes", i64), ("d2h_bytes", i64)]
+                ("h2d_bytes", i64), ("d2h_bytes", i64),
+                ("tenant_service", f64 * 8), ("tenant_done", i64 * 8),
+                ("vtc_spread_max", f64), ("vtc_pair_gap_max", f64)]
 
 
 class IterLogC(ctypes.Structure):
@@ -455,7 +459,11 @@ class Engine:
 
 
 def _struct_dict(st) -> Dict:
-    return {name: getattr(st, name) for name, _ in st._fields_}
+    out = {}
+    for name, _ in st._fields_:
+        v = getattr(st, name)
+        out[name] = list(v) if isinstance(v, ctypes.Array) else v
+    return out
 
 
 def coserve_run(engine: Optional["Engine"], cfg: CoserveConfig, log_cap: int = 100000):

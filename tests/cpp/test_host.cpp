@@ -13,6 +13,7 @@
 #include "coserve/coserve_loop.hpp"
 #include "coserve/cost_model.hpp"
 #include "coserve/scheduler.hpp"
+#include "coserve/vtc.hpp"
 #include "coserve/workload.hpp"
 
 using namespace coserve;
@@ -241,6 +242,44 @@ static void test_sim_loop() {
     if (lg.c > 0) CHECK(lg.pred_ms <= 50.0 + 1e-9);
 }
 
+// SPEC.md fairness_vtc examples (Appendix C)
+static void test_vtc() {
+  VtcLedger v;  // sole tenant rejoining an empty system after tenant l left with c_l = 500
+  v.ensure(1);
+  v.counter[1] = 100.0;
+  v.c_last = 500.0;
+  v.on_arrival(1);
+  CHECK(near(v.counter[1], 500.0));
+  VtcLedger a;  // active tenants {200, 300}, rejoiner at 50 -> lifted to 200
+  a.ensure(2);
+  a.counter = {200.0, 300.0, 50.0};
+  a.queued = {1, 1, 0};
+  a.on_arrival(2);
+  CHECK(near(a.counter[2], 200.0));
+  a.counter[2] = 250.0;  // already queued -> no lift
+  a.on_arrival(2);
+  CHECK(near(a.counter[2], 250.0) && a.queued[2] == 2);
+  VtcLedger s;  // select: counters {A:10, B:5} -> B ; tie 7 vs 7 -> lowest id
+  s.ensure(1);
+  s.counter = {10.0, 5.0};
+  std::deque<Request> q(2);
+  q[0].tenant = 0;
+  q[1].tenant = 1;
+  CHECK(s.select(q) == 1);
+  s.counter = {7.0, 7.0};
+  CHECK(s.select(q) == 0);
+  VtcLedger c;  // charges: w_p = 1 prompt 100 -> +100 ; w_q = 2, 5 tokens -> +10 ; w_r = 0.5 x 64 -> +32
+  c.w_r = 0.5;
+  c.ensure(0);
+  c.queued[0] = 1;
+  c.on_admit(0, 100);
+  CHECK(near(c.counter[0], 100.0) && near(c.c_last, 100.0));
+  c.charge(0, c.w_q * 5);
+  CHECK(near(c.counter[0], 110.0));
+  c.charge(0, c.w_r * 64);
+  CHECK(near(c.counter[0], 142.0) && near(c.service[0], 142.0));
+}
+
 int main() {
   test_cost_model();
   test_memory_model();
@@ -248,6 +287,7 @@ int main() {
   test_plan_iteration();
   test_workload();
   test_sim_loop();
+  test_vtc();
   if (failures) {
     std::printf("%d failure(s)\n", failures);
     return 1;

@@ -212,3 +212,37 @@ def test_coserve_beats_temporal_in_simulation():
         st, _ = E.coserve_run(None, c)
         res[pol] = (st["ft_fwd_tokens"] + st["ft_bwd_tokens"] / 8) / st["timed_ms"]
     assert res[S.COSERVE] > 1.2 * res[S.TEMPORAL], res
+
+
+# ---------------------------------------------------------------- VTC fairness (App. C)
+def _vtc_cfg(vtc, tenants=2, share=0.85, rate=45.0, iters=1500):
+    prof = S.Profile(5.0, 0.01, S.INF, 0.3, 1e-6, 1e-7, 0.4)
+    c = _cfg(rate, prof, iters, 2048, 8, 3, 0, 6000, 64, budget=45.0, multi_layer=True)
+    c.vtc, c.n_tenants, c.tenant0_share, c.ft_tenant = (1 if vtc else 0), tenants, share, -1
+    c.vtc_wp, c.vtc_wq, c.vtc_wr = 1.0, 2.0, 1.0
+    return c
+
+
+def test_vtc_off_tenants_do_not_change_plans():
+    """Tenant labels come from a separate stream: with VTC off the plans are the 1-tenant ones."""
+    a = E.coserve_run(None, _vtc_cfg(False, tenants=1))[1]
+    b = E.coserve_run(None, _vtc_cfg(False, tenants=3))[1]
+    assert [(x["c"], x["s"], x["n_queue"]) for x in a] == [(x["c"], x["s"], x["n_queue"]) for x in b]
+
+
+def test_vtc_fairness_bounds_overloaded_tenants():
+    """Overload (45 req/s; tenant 0 sends 85%): with VTC the backlogged tenants' counters stay
+    within Lemma 1's spread max(w_p L_input, max(w_q, w_r) M) and their service within Theorem
+    1's 2x that over every interval both are backlogged; the light tenant gets more service than
+    under FIFO admission."""
+    st_v, _ = E.coserve_run(None, _vtc_cfg(True))
+    st_f, _ = E.coserve_run(None, _vtc_cfg(False))
+    L_input, M = 4096, 1024          # workload prompt / generation caps
+    lemma = max(1.0 * L_input, max(2.0, 1.0) * M)
+    assert st_v["vtc_spread_max"] <= lemma + 1e-6, st_v["vtc_spread_max"]
+    assert st_v["vtc_pair_gap_max"] <= 2 * lemma + 1e-6, st_v["vtc_pair_gap_max"]
+    assert st_v["vtc_pair_gap_max"] > 0                     # both tenants were backlogged
+    # FIFO admission serves requests in arrival order: the light tenant waits behind the heavy
+    # one; VTC admits the light tenant's requests first while its counter is lower
+    done_v, done_f = st_v["tenant_done"], st_f["tenant_done"]
+    assert done_v[1] / max(1, sum(done_v)) > done_f[1] / max(1, sum(done_f))
