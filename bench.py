@@ -45,6 +45,9 @@ MODEL_NAMES = {"llama-3.1-8b": "LLaMA-3.1-8B", "qwen-2.5-14b": "Qwen-2.5-14B",
 # bound (scripts/policy_compare.py measured 82% SLO attainment over 25 s).  256 slots keep the
 # inference side stable, so the finetuning number is measured at a sustainable operating point.
 MAX_BATCH = 256
+# iteration-latency tail control: the planner budget is TAIL_TARGET x SLO / q95(actual /
+# predicted) over recent iterations, so the p99 iteration sits just inside the SLO on any box
+TAIL_TARGET = 0.97
 METRIC = "finetune tokens/s under inference SLO at N req/s; co-serve iteration ms"
 SLO_MS = 50.0
 
@@ -328,7 +331,8 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False,
     c.burst_period_s = 60.0
     c.tpot_slo_ms = slo_ms
     c.ttft_slo_ms = 5000.0
-    c.budget_ms = 0.9 * slo_ms   # planner budget; the adaptive correction tracks measured ms
+    c.budget_ms = 0.9 * slo_ms   # initial planner budget; the adaptive correction tracks measured ms
+    c.tail_target = TAIL_TARGET  # then the budget follows the measured tail (q95 of actual/predicted)
     c.max_batch = MAX_BATCH
     c.chunk_size = 512
     c.max_tokens = 8192

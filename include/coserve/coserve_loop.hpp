@@ -67,6 +67,10 @@ struct LoopConfig {
   int timed_iters = 100;
   int prepopulate = 0;          // requests already decoding at t=0 (steady-state start)
   bool adaptive = false;        // correct the profile with measured/predicted ratios
+  // tail control (adaptive only; 0 = off): the planner budget becomes
+  // tail_target x TPOT SLO / q95(measured / predicted over the last 96 inference iterations),
+  // so the iteration-latency tail -- not the mean -- sits at the SLO on any box
+  double tail_target = 0.0;
   uint64_t seed = 0;
   // scheduling policy (§8.2 baselines, coserve/baselines.hpp): co-serving, or
   // temporal sharing -- inference-only iterations interleaved with whole finetuning
@@ -177,6 +181,9 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
   double pair_lo = 0.0, pair_hi = 0.0;
   int inf_since_ft = 0;   // inference-only iterations since the last finetuning iteration
   bool ft_block = false;  // temporal sharing: inside a finetuning iteration (inference blocked)
+  std::vector<double> resid;  // ring of measured / predicted (tail control)
+  size_t resid_pos = 0;
+  double budget = cfg.budget_ms;
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
   for (int it = 0; it < total_iters; ++it) {
     const bool timed = it >= cfg.warmup_iters;
@@ -228,13 +235,13 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       vtc_admitted = admit_requests_vtc(queue, running, mem, sched, vtc);
     IterationPlan plan;
     if (!temporal) {
-      plan = plan_iteration(queue, running, ft, prof, sched, mem, cfg.budget_ms);
+      plan = plan_iteration(queue, running, ft, prof, sched, mem, budget);
     } else if (ft_block) {
       plan = plan_ft_block(ft, prof, cfg.sched);
     } else {
       FtState idle = ft;  // inference-only iteration
       idle.phase = FtPhase::Idle;
-      plan = plan_iteration(queue, running, idle, prof, sched, mem, cfg.budget_ms);
+      plan = plan_iteration(queue, running, idle, prof, sched, mem, budget);
       if (plan.c == 0 && ft.L > 0) {  // nothing to serve: the finetuning iteration runs now
         ft_block = true;
         plan = plan_ft_block(ft, prof, cfg.sched);
@@ -306,6 +313,18 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       // the step ran with corr[cph]; blend towards the measured ratio of its own phase
       const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));
       corr[ph] = std::max(0.5, std::min(2.0, 0.8 * corr[ph] + 0.2 * r));
+      if (cfg.tail_target > 0 && plan.c > 0) {
+        const double x = out.device_ms / plan.predicted_ms;
+        if (resid.size() < 96) resid.push_back(x);
+        else resid[resid_pos++ % 96] = x;
+        if (resid.size() >= 24) {
+          std::vector<double> srt(resid);
+          const size_t k = (size_t)std::ceil(0.95 * (double)srt.size()) - 1;
+          std::nth_element(srt.begin(), srt.begin() + k, srt.end());
+          const double q95 = std::max(1.0, srt[k]);
+          budget = std::max(0.5 * cfg.budget_ms, cfg.tail_target * cfg.sched.tpot_slo_ms / q95);
+        }
+      }
     }
     if (exec && cfg.sim_clock) out.ms = plan.predicted_ms;
     now += out.ms;

@@ -237,6 +237,9 @@ typedef struct cs_coserve_config {
    * ft_tenant (-1: nobody) */
   int32_t vtc, n_tenants, ft_tenant;
   double tenant0_share, vtc_wp, vtc_wq, vtc_wr;
+  /* tail control (adaptive runs; 0 = off): planner budget = tail_target x TPOT SLO / q95 of
+   * the recent measured/predicted iteration-time ratios */
+  double tail_target;
 } cs_coserve_config;
 
 typedef struct cs_coserve_stats {

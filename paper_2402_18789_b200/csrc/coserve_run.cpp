@@ -154,6 +154,7 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.policy = (coserve::Policy)c->policy;
   L.temporal_n = c->temporal_n > 0 ? c->temporal_n : 128;
   L.sim_clock = c->sim_clock != 0;
+  L.tail_target = c->tail_target > 0 && c->tail_target <= 1.0 ? c->tail_target : 0.0;
   L.vtc = c->vtc != 0;
   if (L.vtc) {
     L.vtc_wp = c->vtc_wp > 0 ? c->vtc_wp : 1.0;

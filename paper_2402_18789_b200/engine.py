@@ -69,7 +69,8 @@ class CoserveConfig(ctypes.Structure):
                 ("n_layers", i32), ("vocab", i32), ("page_size", i32), ("total_pages", i64),
                 ("policy", i32), ("temporal_n", i32), ("sim_clock", i32),
                 ("vtc", i32), ("n_tenants", i32), ("ft_tenant", i32),
-                ("tenant0_share", f64), ("vtc_wp", f64), ("vtc_wq", f64), ("vtc_wr", f64)]
+                ("tenant0_share", f64), ("vtc_wp", f64), ("vtc_wq", f64), ("vtc_wr", f64),
+                ("tail_target", f64)]
 
 POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS = 0, 1, 2
 
