@@ -317,7 +317,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
         const double x = out.device_ms / plan.predicted_ms;
         if (resid.size() < 96) resid.push_back(x);
         else resid[resid_pos++ % 96] = x;
-        if (resid.size() >= 24) {
+        if (resid.size() >= 12) {
           std::vector<double> srt(resid);
           const size_t k = (size_t)std::ceil(0.95 * (double)srt.size()) - 1;
           std::nth_element(srt.begin(), srt.begin() + k, srt.end());
