@@ -158,40 +158,70 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idO = idesc_bf16_f32_major(128, 128, 0, 1);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(smem + SM_K + st * TILE2);
-        for (int i = 0; i < ntile; ++i) {
-          if (j > 0) {  // P_i(j-1) aliases S_i: PV_i(j-1) must have consumed it
-            mbar_wait(&pv_done[i], (j - 1) & 1);
+      auto qk = [&](int i, uint32_t sK) {
+        const uint32_t sQ = smem_u32(smem + SM_Q + i * TILE2);
+#pragma unroll
+        for (int kk = 0; kk < D2 / 16; ++kk) {
+          const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * HALF2 + (kk & 3) * 32);
+          const uint64_t b = umma_desc_sw128(sK + (kk >> 2) * HALF2 + (kk & 3) * 32);
+          mma_bf16(tmem + i * 128, a, b, idS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[i]);
+      };
+      auto pv = [&](int i, uint32_t sV, int j) {
+#pragma unroll
+        for (int kk = 0; kk < BN2 / 16; ++kk) {
+          const uint64_t b = umma_desc_sw128_mn(sV + kk * 2048, HALF2, 1024);
+          mma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, b, idO, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&pv_done[i]);
+      };
+      if (ntile == 2) {
+        // ping-pong: while the softmax of query tile 0 runs on S_0(j), the tensor pipe does
+        // PV_1(j-1) and QK_1(j); while tile 1's softmax runs, PV_0(j) and QK_0(j+1)
+        for (int j = 0; j < nt; ++j) {
+          const int st = j & 1, pst = (j - 1) & 1;
+          mbar_wait(&k_full[st], (j >> 1) & 1);
+          if (j > 0) mbar_wait(&pv_done[0], (j - 1) & 1);  // P_0(j-1) (aliases S_0) consumed
+          tc_fence_after();
+          const uint32_t sK = smem_u32(smem + SM_K + st * TILE2);
+          qk(0, sK);
+          if (j > 0) {
+            mbar_wait(&p_full[1], (j - 1) & 1);
+            tc_fence_after();
+            pv(1, smem_u32(smem + SM_V + pst * TILE2), j - 1);
+            mma_commit(&v_empty[pst]);  // V(j-1) fully consumed
+            mbar_wait(&pv_done[1], (j - 1) & 1);
             tc_fence_after();
           }
-          const uint32_t sQ = smem_u32(smem + SM_Q + i * TILE2);
-#pragma unroll
-          for (int kk = 0; kk < D2 / 16; ++kk) {
-            const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * HALF2 + (kk & 3) * 32);
-            const uint64_t b = umma_desc_sw128(sK + (kk >> 2) * HALF2 + (kk & 3) * 32);
-            mma_bf16(tmem + i * 128, a, b, idS, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&s_full[i]);
-        }
-        mma_commit(&k_empty[st]);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
-        const uint32_t sV = smem_u32(smem + SM_V + st * TILE2);
-        for (int i = 0; i < ntile; ++i) {
-          mbar_wait(&p_full[i], j & 1);
+          qk(1, sK);
+          mma_commit(&k_empty[st]);
+          mbar_wait(&v_full[st], (j >> 1) & 1);
+          mbar_wait(&p_full[0], j & 1);
           tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BN2 / 16; ++kk) {
-            const uint64_t b = umma_desc_sw128_mn(sV + kk * 2048, HALF2, 1024);
-            mma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, b, idO,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&pv_done[i]);
+          pv(0, smem_u32(smem + SM_V + st * TILE2), j);
         }
-        mma_commit(&v_empty[st]);
+        if (nt > 0) {
+          const int lst = (nt - 1) & 1;
+          mbar_wait(&p_full[1], (nt - 1) & 1);
+          tc_fence_after();
+          pv(1, smem_u32(smem + SM_V + lst * TILE2), nt - 1);
+          mma_commit(&v_empty[lst]);
+        }
+      } else {
+        for (int j = 0; j < nt; ++j) {
+          const int st = j & 1;
+          mbar_wait(&k_full[st], (j >> 1) & 1);
+          if (j > 0) mbar_wait(&pv_done[0], (j - 1) & 1);  // P_0(j-1) aliases S_0
+          tc_fence_after();
+          qk(0, smem_u32(smem + SM_K + st * TILE2));
+          mma_commit(&k_empty[st]);
+          mbar_wait(&v_full[st], (j >> 1) & 1);
+          mbar_wait(&p_full[0], j & 1);
+          tc_fence_after();
+          pv(0, smem_u32(smem + SM_V + st * TILE2), j);
+          mma_commit(&v_empty[st]);
+        }
       }
     }
   } else {
