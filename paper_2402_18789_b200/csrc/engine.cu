@@ -1099,9 +1099,14 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     cs::attn_decode_geometry(e->d, &dec_kt, &dec_nw, &dec_cps, &dec_stream);
     long total = 0;
     for (const auto& w : work_dec) total += w.k_end;
-    // per-item CTAs: ~8 waves of CTAs; persistent streams (one warp per item): ~3 items per
-    // warp of the grid, enough to balance a longest-first round robin
-    const long target = dec_stream ? 3L * 148 * dec_cps * dec_nw : 8L * 148 * dec_cps;
+    // per-item CTAs: ~8 waves of CTAs; persistent streams (one warp per item): ~2 parts per
+    // warp of the grid (scripts/decode_variants.py A/B over CS_DEC_TARGET 1/2/3/6: 2 is the
+    // best compromise between balance and combine work)
+    static const long stream_mult = [] {  // CS_DEC_TARGET: items per warp of the stream grid
+      const char* v = std::getenv("CS_DEC_TARGET");
+      return v ? std::max(1L, std::atol(v)) : 2L;
+    }();
+    const long target = dec_stream ? stream_mult * 148 * dec_cps * dec_nw : 8L * 148 * dec_cps;
     const long tile_round = dec_stream ? (long)dec_kt : (long)dec_kt * dec_nw;
     long chunk = (total + target - 1) / target;
     chunk = std::max<long>(4 * tile_round, (chunk + tile_round - 1) / tile_round * tile_round);
