@@ -549,15 +549,19 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const float* __res
     uv = swiglu ? __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + f + col)) : make_uint2(0u, 0u);
   };
   int i = 0;
-  for (; i + 1 < nr; i += 2) {
-    float4 d0, d1;
-    uint2 g0, g1, u0, u1;
+  for (; i + 3 < nr; i += 4) {  // four rows' loads in flight before any is used
+    float4 d0, d1, d2, d3;
+    uint2 g0, g1, g2, g3, u0, u1, u2, u3;
     ld(i, d0, g0, u0);
     ld(i + 1, d1, g1, u1);
+    ld(i + 2, d2, g2, u2);
+    ld(i + 3, d3, g3, u3);
     body(i, d0, g0, u0);
     body(i + 1, d1, g1, u1);
+    body(i + 2, d2, g2, u2);
+    body(i + 3, d3, g3, u3);
   }
-  if (i < nr) {
+  for (; i < nr; ++i) {
     float4 d0;
     uint2 g0, u0;
     ld(i, d0, g0, u0);
