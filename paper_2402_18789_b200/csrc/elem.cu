@@ -629,9 +629,7 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
   float2 a01[16], a23[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
-#pragma unroll 2
-  for (int i = 0; i < nr; ++i) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(dY + (long)(r0 + i) * ldy + col));
+  auto row = [&](int i, const float4& v) {
     const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
     const float4* l4 = reinterpret_cast<const float4*>(sl + i * 16);
 #pragma unroll
@@ -644,7 +642,20 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
         a23[4 * q + t] = ffma2(v23, make_float2(lj[t], lj[t]), a23[4 * q + t]);
       }
     }
+  };
+  const float* yp = dY + (long)r0 * ldy + col;
+  int i = 0;
+  for (; i + 3 < nr; i += 4) {  // four rows' loads in flight before any is used
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(yp + (long)i * ldy));
+    const float4 v1 = __ldg(reinterpret_cast<const float4*>(yp + (long)(i + 1) * ldy));
+    const float4 v2 = __ldg(reinterpret_cast<const float4*>(yp + (long)(i + 2) * ldy));
+    const float4 v3 = __ldg(reinterpret_cast<const float4*>(yp + (long)(i + 3) * ldy));
+    row(i, v0);
+    row(i + 1, v1);
+    row(i + 2, v2);
+    row(i + 3, v3);
   }
+  for (; i < nr; ++i) row(i, __ldg(reinterpret_cast<const float4*>(yp + (long)i * ldy)));
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if (j < r)
