@@ -444,6 +444,7 @@ def run_ours(a):
     attn_b = eng.read_profile(2)
     attn_tc = eng.read_profile(3)
     comm = eng.read_profile(4)
+    dec_k = eng.read_profile(5)
 
     from paper_2402_18789_b200.replicas import aggregate
     # a TP group is one replica: only its leader's finetuning progress counts
@@ -520,6 +521,7 @@ def run_ours(a):
                       "decode_gbs": round(attn["bytes"] / (attn["ms"] * 1e-3) / 1e9, 1) if attn["ms"] else None,
                       "decode_hbm_frac": round(attn["bytes"] / (attn["ms"] * 1e-3) / 1e9 / float(load_peaks()[0].get("hbm_gbs", 6650.0)), 4) if attn["ms"] else None,
                       "decode_share": round(attn["ms"] / dev_ms, 4) if dev_ms else None,
+                      "decode_kernel_hbm_frac": round(dec_k["bytes"] / (dec_k["ms"] * 1e-3) / 1e9 / float(load_peaks()[0].get("hbm_gbs", 6650.0)), 4) if dec_k["ms"] else None,
                       "bwd_tflops": round(attn_b["flops"] / (attn_b["ms"] * 1e-3) / 1e12, 1) if attn_b["ms"] else None,
                       "bwd_share": round(attn_b["ms"] / dev_ms, 4) if dev_ms else None},
         "tp_allreduce": ({"share": round(comm["ms"] / dev_ms, 4) if dev_ms else None,

@@ -273,7 +273,8 @@ int64_t cs_engine_launch_count(cs_engine* e);
 /* Live profiling: when on, every GEMM / attention launch is bracketed by CUDA events on the
  * engine stream; cs_engine_read_profile returns the summed device ms, algorithmic FLOPs and
  * bytes and launch count per kind (0 = tcgen05 GEMM, 1 = attention fwd bandwidth kernel
- * (decode rows), 2 = attention bwd, 3 = attention fwd tcgen05 kernel (prefill / FT rows))
+ * (decode rows, incl. the split-KV combine), 2 = attention bwd, 3 = attention fwd tcgen05
+ * kernel (prefill / FT rows), 4 = TP all-reduce, 5 = the decode kernel alone)
  * since profiling was switched on. */
 int cs_engine_set_profiling(cs_engine* e, int on);
 int cs_engine_read_profile(cs_engine* e, int kind, double* ms, double* flops, double* bytes,

@@ -130,7 +130,7 @@ struct cs_engine {
   std::vector<ProfRec> recs;
   // kinds: 0 tcgen05 GEMM, 1 attention fwd (bandwidth kernel: decode), 2 attention bwd,
   //        3 attention fwd (tcgen05 kernel: prefill / FT windows), 4 TP all-reduce
-  static constexpr int kKinds = 5;
+  static constexpr int kKinds = 6;  // 5: the decode kernel alone (kind 1 minus combine / gaps)
   double prof_ms[kKinds] = {}, prof_flops[kKinds] = {}, prof_bytes[kKinds] = {};
   long prof_n[kKinds] = {};
   double step_attn_flops = 0, step_attn_bytes = 0, step_tc_flops = 0, step_tc_bytes = 0;
@@ -1332,7 +1332,15 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
       if (cs::make_map(&mk, rp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mv, rp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0)
         return cs::set_error(CS_ERR_CUDA, "decode attention: TMA map creation failed");
+      cs_engine::ProfRec dpr{};
+      if (e->profiling) {
+        dpr.bytes = e->step_attn_bytes;  // decode rows' K/V bytes (the bandwidth kernel's share)
+        dpr.flops = e->step_attn_flops;
+        dpr.kind = 5;
+        prof_begin(e, dpr);
+      }
       CS_CUDA_TRY(cs::attn_decode(dp, mk, mv, e->d, sp.n_dec, st));
+      if (e->profiling) prof_end(e, dpr);
     }
     CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
     if (e->profiling && bw_attn) prof_end(e, apr);
