@@ -298,6 +298,17 @@ def offline_profile(eng, ft_len: int, n_layers: int = 32, max_window: int = 8192
     pf_tok = max((t_pf - t0) / 512.0, 1e-6)
     fwd, bwd, layer0 = [], [], []
     ft_pass(min(1024, max_window), fwd, bwd)
+    # forward-only windows of other sizes (state reset, no backward) to separate the fixed
+    # per-window cost from the per-token slope
+    for win in sorted({min(2048, max_window), min(512, max_window)} - {min(1024, max_window)}):
+        eng.reset_ft()
+        for l in range(0, ft_len, win):
+            s_ = min(win, ft_len - l)
+            out = eng.step(decs() + [Seg(SEG_FT_FWD, toks[l:l + s_], l, ft_pages, adapter=True)],
+                           ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": s_,
+                               "targets": toks[l + 1:l + s_ + 1] + ([-1] if l + s_ == ft_len else [])})
+            fwd.append((s_, l, out["ms"]))
+    eng.reset_ft()
     def linfit(xs, ys):
         mx, my = statistics.mean(xs), statistics.mean(ys)
         vx = sum((x - mx) ** 2 for x in xs)
@@ -305,8 +316,15 @@ def offline_profile(eng, ft_len: int, n_layers: int = 32, max_window: int = 8192
         a = max(a, 0.0)
         return my - a * mx, a
 
-    # forward window: (ms - t0)/s = b + a_f (l + s/2);  backward: = w_b b + a_b (l_j - s/2)
-    b, a_f = linfit([l + s / 2.0 for s, l, _ in fwd], [(ms - t0) / s for s, _, ms in fwd])
+    # forward window: ms - t0 = c_w + b s + a_f s (l + s/2) (least squares over windows of
+    # 512 / 1024 / 2048 tokens); backward: (ms - t0)/s = w_b b + a_b (l_j - s/2)
+    import numpy as np
+    X = np.array([[1.0, s, s * (l + s / 2.0)] for s, l, _ in fwd])
+    y = np.array([ms - t0 for s, l, ms in fwd])
+    c_w, b, a_f = np.linalg.lstsq(X, y, rcond=None)[0].tolist()
+    if c_w < 0 or a_f < 0:  # degenerate fit: fall back to the slope-only form
+        c_w = 0.0
+        b, a_f = linfit([l + s / 2.0 for s, l, _ in fwd], [(ms - t0) / s for s, _, ms in fwd])
     wb, a_b = linfit([lj - s / 2.0 for s, lj, _ in bwd], [(ms - t0) / s for s, _, ms in bwd])
     b = max(b, 1e-6)
     w0 = 1.0
@@ -317,7 +335,7 @@ def offline_profile(eng, ft_len: int, n_layers: int = 32, max_window: int = 8192
     return {"t0_ms": t_fixed, "decode_ms_per_row": d_row, "prefill_ms_per_token": pf_tok,
             "slope_ms_per_token": b, "bwd_token_weight": max(wb, 1e-6) / b,
             "attn_fwd_ms_per_token_ctx": a_f, "attn_bwd_ms_per_token_ctx": a_b,
-            "bwd_layer0_weight": w0,
+            "bwd_layer0_weight": w0, "fwd_window_ms": max(0.0, c_w),
             "fwd_samples": fwd, "bwd_samples": bwd[:8]}
 
 
@@ -340,7 +358,8 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False,
     c.profile = profile_struct(prof["t0_ms"], prof["slope_ms_per_token"], 0.0,
                                prof["bwd_token_weight"], prof["attn_fwd_ms_per_token_ctx"],
                                prof["attn_bwd_ms_per_token_ctx"], prof["bwd_layer0_weight"],
-                               prof["decode_ms_per_row"], prof["prefill_ms_per_token"])
+                               prof["decode_ms_per_row"], prof["prefill_ms_per_token"],
+                               prof.get("fwd_window_ms", 0.0))
     c.multi_layer_bwd = 1
     c.ft_seq_len = ft_len
     c.growth_tokens = 128
@@ -546,7 +565,8 @@ def run_ours(a):
         "profile": {k: (float(f"{v:.4g}") if isinstance(v, float) else v) for k, v in prof.items()
                     if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",
                              "attn_fwd_ms_per_token_ctx", "attn_bwd_ms_per_token_ctx",
-                             "bwd_layer0_weight", "decode_ms_per_row", "prefill_ms_per_token")},
+                             "bwd_layer0_weight", "decode_ms_per_row", "prefill_ms_per_token",
+                             "fwd_window_ms")},
         "context": ({"paper_8b_a100x4_ft_tokens_per_s_at_20rps": 7200}
                     if a.model == "llama-3.1-8b" else None),
         "setup_s": round(setup_s, 1),

@@ -32,6 +32,10 @@ struct LatencyProfile {
   // profile charges decode rows and prefill tokens their own slopes (0 = the common slope).
   double decode_ms_per_row = 0.0;
   double prefill_ms_per_token = 0.0;
+  // Fixed cost of a finetuning forward window (its loss head / CE / saved-activation launches,
+  // independent of s); 0 = none.  Without it the per-token slope absorbs it and small windows
+  // (the tail of a sequence, at long context) are under-predicted.
+  double fwd_window_ms = 0.0;
   bool has_ctx_terms() const { return attn_fwd_ms_per_token_ctx > 0 || attn_bwd_ms_per_token_ctx > 0; }
   bool has_row_terms() const { return decode_ms_per_row > 0 || prefill_ms_per_token > 0; }
 };
@@ -75,7 +79,7 @@ inline double inference_cost(const LatencyProfile& p, int64_t n_dec, int64_t n_p
 
 // Marginal cost of finetuning windows on top of latency(c, 0) (profile with context terms).
 inline double ft_fwd_cost(const LatencyProfile& p, int64_t l, int64_t s) {
-  return p.slope_ms_per_token * (double)s +
+  return (s > 0 ? p.fwd_window_ms : 0.0) + p.slope_ms_per_token * (double)s +
          p.attn_fwd_ms_per_token_ctx * (double)s * ((double)l + 0.5 * (double)s);
 }
 inline double ft_bwd_cost(const LatencyProfile& p, int64_t lj, int64_t s, int layer = 1) {

@@ -203,6 +203,7 @@ typedef struct cs_latency_profile {
   double bwd_layer0_weight;  /* layer-0 (pruned) backward window cost factor; <= 0 -> 1     */
   double decode_ms_per_row;    /* inference decode row slope; <= 0 -> slope_ms_per_token     */
   double prefill_ms_per_token; /* inference prefill token slope; <= 0 -> slope_ms_per_token  */
+  double fwd_window_ms;        /* fixed cost of a finetuning forward window; <= 0 -> none     */
 } cs_latency_profile;
 
 double cs_sched_latency(const cs_latency_profile* p, int64_t c, int64_t s);

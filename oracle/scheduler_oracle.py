@@ -34,6 +34,7 @@ class Profile:
     layer0: float = 1.0     # cost factor of a (pruned) layer-0 backward window
     decode: float = 0.0     # per-decode-row slope of the inference rows (0 = slope)
     prefill: float = 0.0    # per-prefill-token slope (0 = slope)
+    fwd_window: float = 0.0  # fixed cost of a finetuning forward window (0 = none)
 
     def has_ctx(self):
         return self.attn_fwd > 0 or self.attn_bwd > 0
@@ -52,7 +53,8 @@ def inference_cost(p: "Profile", n_dec: int, n_pre: int) -> float:
 
 
 def ft_fwd_cost(p: Profile, l: int, s: int) -> float:
-    return p.slope * float(s) + p.attn_fwd * float(s) * (float(l) + 0.5 * float(s))
+    return ((p.fwd_window if s > 0 else 0.0) + p.slope * float(s)
+            + p.attn_fwd * float(s) * (float(l) + 0.5 * float(s)))
 
 
 def ft_bwd_cost(p: Profile, lj: int, s: int, layer: int = 1) -> float:

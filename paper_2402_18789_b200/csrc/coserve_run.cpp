@@ -140,6 +140,7 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.prof.bwd_layer0_weight = c->profile.bwd_layer0_weight > 0 ? c->profile.bwd_layer0_weight : 1.0;
   L.prof.decode_ms_per_row = c->profile.decode_ms_per_row > 0 ? c->profile.decode_ms_per_row : 0.0;
   L.prof.prefill_ms_per_token = c->profile.prefill_ms_per_token > 0 ? c->profile.prefill_ms_per_token : 0.0;
+  L.prof.fwd_window_ms = c->profile.fwd_window_ms > 0 ? c->profile.fwd_window_ms : 0.0;
   L.sched.multi_layer_bwd = c->multi_layer_bwd != 0;
   L.budget_ms = c->budget_ms > 0 ? c->budget_ms : c->tpot_slo_ms;
   L.growth_tokens = c->growth_tokens;

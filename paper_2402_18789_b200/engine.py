@@ -54,7 +54,8 @@ class LatencyProfileC(ctypes.Structure):
     _fields_ = [("t0_ms", f64), ("slope_ms_per_token", f64), ("knee_tokens", f64),
                 ("bwd_token_weight", f64), ("attn_fwd_ms_per_token_ctx", f64),
                 ("attn_bwd_ms_per_token_ctx", f64), ("bwd_layer0_weight", f64),
-                ("decode_ms_per_row", f64), ("prefill_ms_per_token", f64)]
+                ("decode_ms_per_row", f64), ("prefill_ms_per_token", f64),
+                ("fwd_window_ms", f64)]
 
 
 class CoserveConfig(ctypes.Structure):
@@ -480,8 +481,10 @@ def coserve_run(engine: Optional["Engine"], cfg: CoserveConfig, log_cap: int = 1
 
 
 def profile_struct(t0_ms, slope, knee=0.0, bwd_weight=1.0, attn_fwd=0.0, attn_bwd=0.0,
-                   layer0_weight=1.0, decode_row=0.0, prefill_token=0.0) -> LatencyProfileC:
+                   layer0_weight=1.0, decode_row=0.0, prefill_token=0.0,
+                   fwd_window=0.0) -> LatencyProfileC:
     p = LatencyProfileC()
+    p.fwd_window_ms = fwd_window
     p.t0_ms, p.slope_ms_per_token, p.knee_tokens, p.bwd_token_weight = t0_ms, slope, knee, bwd_weight
     p.attn_fwd_ms_per_token_ctx, p.attn_bwd_ms_per_token_ctx = attn_fwd, attn_bwd
     p.bwd_layer0_weight = layer0_weight

@@ -21,7 +21,8 @@ def _cfg(rate, prof, iters, ft_len, n_layers, seed, prepop=0, pages=4096, growth
     c.max_tokens = 8192
     c.max_ft_window = window
     c.profile = E.profile_struct(prof.t0_ms, prof.slope, 0.0 if prof.knee == S.INF else prof.knee,
-                                 prof.bwd_weight, prof.attn_fwd, prof.attn_bwd, prof.layer0)
+                                 prof.bwd_weight, prof.attn_fwd, prof.attn_bwd, prof.layer0,
+                                 prof.decode, prof.prefill, prof.fwd_window)
     c.multi_layer_bwd = 1 if multi_layer else 0
     c.ft_seq_len = ft_len
     c.growth_tokens = growth
@@ -49,6 +50,9 @@ CASES = [
 CASES_EXT = [
     (20.0, S.Profile(7.3, 0.018, S.INF, 0.06, 1.1e-6, 8e-8, 0.4), 400, 8192, 32, 4, 48, 8192, 128, 45.0, 0.0),
     (10.0, S.Profile(5.0, 0.02, S.INF, 0.1, 2e-6, 1e-7), 300, 2048, 6, 5, 8, 4096, 64, 40.0, 0.5),
+    # measured-profile form: per-kind inference rows + a fixed forward-window cost
+    (20.0, S.Profile(4.5, 0.02, S.INF, 0.023, 5.6e-7, 8e-8, 0.19, 0.016, 0.011, 1.7), 400, 8192, 32,
+     6, 100, 8192, 128, 45.0, 0.0),
 ]
 
 
