@@ -165,7 +165,11 @@ __global__ void __launch_bounds__(384, 1)
   const int kvh = blockIdx.y;
   const int nrows = p.b - p.a;
   const int n_qt = (nrows + rpt - 1) / rpt;
-  const int qt0 = k0 > p.a ? (k0 - p.a) / rpt : 0;  // first tile whose last position >= k0
+  // first tile whose last position >= k0; with dS stored for the dQ GEMM, from the first tile of
+  // the (128 / grp)-position dQ tile containing position k0, so every dS entry that GEMM reads
+  // for these keys is written (zeros where masked)
+  const int qt0 = p.ds_out ? (k0 > p.a ? ((k0 - p.a) / (128 / grp)) * (128 / grp) / rpt : 0)
+                           : (k0 > p.a ? (k0 - p.a) / rpt : 0);
   const int n = n_qt - qt0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -343,6 +347,13 @@ __global__ void __launch_bounds__(384, 1)
           const float2 ds = fmul2(pv, dd);
           pp[cc >> 1] = pack_bf16(pv.x, pv.y);
           pd[cc >> 1] = pack_bf16(ds.x, ds.y);
+          if (p.ds_out && key < p.ds_ld) {  // dS[row][q head][key] for the dQ GEMM (lanes: keys)
+            const int q0r = qbase + c / grp, q1r = qbase + (c + 1) / grp;
+            if (c < ROWS && q0r < nrows)
+              p.ds_out[((long)q0r * p.ds_heads + kvh * grp + c % grp) * p.ds_ld + key] = __float2bfloat16(ds.x);
+            if (c + 1 < ROWS && q1r < nrows)
+              p.ds_out[((long)q1r * p.ds_heads + kvh * grp + (c + 1) % grp) * p.ds_ld + key] = __float2bfloat16(ds.y);
+          }
         }
         tst_x16(tmem + lane_base + b * QB + h * 16, pp);
         tst_x16(tmem + lane_base + 128 + b * QB + h * 16, pd);
@@ -669,13 +680,18 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
   const int kvh = n_heads / p.grp;
   dim3 gq((rows + 128 / p.grp - 1) / (128 / p.grp), kvh);
   dim3 gk((p.b + 127) / 128, kvh);
-  g_launches.fetch_add(2, std::memory_order_relaxed);
+  g_launches.fetch_add(p.ds_out ? 1 : 2, std::memory_order_relaxed);
   static const int mask = [] {
     const char* v = std::getenv("CS_BWD2_MASK");  // debugging: 1 = dq v2 only, 2 = dkdv v2 only
     return v ? std::atoi(v) : 3;
   }();
-  if (mask & 1) attn_bwd_dq2_kernel<<<gq, 384, dq2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, p);
-  else attn_bwd_dq_v1(p, tmK, tmV, tmK128, tmV128, gq, st);
+  if (p.ds_out) {
+    // dQ comes from attn_dq_gemm over the stored dS (launched by the caller after this)
+  } else if (mask & 1) {
+    attn_bwd_dq2_kernel<<<gq, 384, dq2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, p);
+  } else {
+    attn_bwd_dq_v1(p, tmK, tmV, tmK128, tmV128, gq, st);
+  }
   if ((mask & 2) || (64 % p.grp) != 0)
     kDkdv2[p.grp - 1]<<<gk, 384, kv2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
   else attn_bwd_dkdv_v1(p, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, gk, st);

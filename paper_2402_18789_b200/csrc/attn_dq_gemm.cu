@@ -1,0 +1,148 @@
+// attn_dq_gemm.cu -- dQ of a token-level backward window as a masked GEMM over the dS the
+// dK/dV kernel already computed (CS_BWD_DSQ=1): dQ[p, h, :] = scale * sum_k dS[p, h, k] K[k, :]
+// (tiny_model.hpp:294-315, Alg. 2 line 19).  The dK/dV kernel holds dS^T in TMEM for
+// its own dK product; it stores it (bf16) to an HBM buffer laid out [window row][q head][key],
+// and this kernel streams it back as the K-major A operand (3-D TMA boxes of 64 keys x group
+// heads x positions = GQA-packed rows) against the paged K tile as an MN-major B operand.  It
+// replaces the dQ kernel that recomputed S and dP and was bounded by reading both back out of
+// TMEM (128 KB per 128x128 tile at 64 B/clk).
+//   warp 0: TMA producer (A: 3-D dS box, B: paged K rows, contiguous pages in one 64-row box)
+//   warp 1: single-thread tcgen05.mma M=128 N=128 (A K-major, B MN-major), fp32 in TMEM
+//   warps 4-7: epilogue (tcgen05.ld, scale, fp32 dQ rows of the window)
+#include "common.cuh"
+#include "engine_kernels.h"
+#include "kernels.h"
+
+namespace cs {
+
+namespace {
+constexpr int DQG_STAGES = 6;
+constexpr int DQG_A = 128 * 128;      // 128 packed rows x 64 keys x bf16
+constexpr int DQG_B = 64 * 128 * 2;   // 64 keys x 128 dims x bf16 (two 64-dim chunks, 8 KB apart)
+constexpr int DQG_STAGE = DQG_A + DQG_B;
+constexpr int DQG_SMEM = DQG_STAGES * DQG_STAGE + 1024 + 256;
+}  // namespace
+
+__global__ void __launch_bounds__(256, 1)
+    attn_dq_gemm_kernel(const __grid_constant__ CUtensorMap tmDS, const __grid_constant__ CUtensorMap tmK16,
+                        const __grid_constant__ CUtensorMap tmK64, AttnBwdParams p, int Hq) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DQG_STAGES * DQG_STAGE);
+  uint64_t* empty = full + DQG_STAGES;
+  uint64_t* acc_full = empty + DQG_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int grp = p.grp;
+  const int rpt = 128 / grp;  // positions per tile (rpt * grp <= 128 packed rows)
+  const int q0 = blockIdx.x * rpt;
+  const int kvh = blockIdx.y;
+  const int nq = min(rpt, p.b - p.a - q0);
+  const int last_key = p.a + q0 + nq - 1;  // causal: keys [0, last position of the tile]
+  const int nkb = (last_key + 64) / 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmDS);
+    tma_prefetch_desc(&tmK16);
+    tma_prefetch_desc(&tmK64);
+    for (int s = 0; s < DQG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int a_bytes = rpt * grp * 128;
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % DQG_STAGES;
+      mbar_wait(&empty[s], ((kb / DQG_STAGES) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], a_bytes + DQG_B);
+      uint8_t* sa = smem + s * DQG_STAGE;
+      uint8_t* sb = sa + DQG_A;
+      tma_load_3d(&tmDS, &full[s], sa, kb * 64, kvh * grp, q0);
+      // K rows [kb*64, kb*64+64) of the sequence: one 64-row box per 64-dim half when the four
+      // 16-key pages are consecutive in the pool, else one 16-row box per page
+      const int k0 = kb * 64, P = p.page_size;
+      const int pg0 = __ldg(p.page_table + p.page_off + k0 / P);
+      bool contig = (P % 16) == 0;
+      for (int key = (k0 / P + 1) * P; contig && key < k0 + 64; key += P)
+        contig = __ldg(p.page_table + p.page_off + key / P) == pg0 + (key / P - k0 / P);
+      for (int c = 0; c < 2; ++c) {
+        const int col = kvh * 128 + c * 64;
+        if (contig) {
+          tma_load_2d(&tmK64, &full[s], sb + c * 8192, col, pg0 * P + (k0 % P));
+        } else {
+          for (int j = 0; j < 4; ++j) {
+            const int key = k0 + 16 * j;
+            const int row = __ldg(p.page_table + p.page_off + key / P) * P + (key % P);
+            tma_load_2d(&tmK16, &full[s], sb + c * 8192 + j * 2048, col, row);
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = idesc_bf16_f32_major(128, 128, 0, 1);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % DQG_STAGES;
+      mbar_wait(&full[s], (kb / DQG_STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * DQG_STAGE), sb = sa + DQG_A;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_bf16(tmem, umma_desc_sw128(sa) + (uint64_t)(k * 2), umma_desc_sw128_mn(sb + k * 2048, 8192, 1024),
+                 idesc, (kb > 0 || k > 0) ? 1u : 0u);
+      mma_commit(&empty[s]);
+    }
+    mma_commit(acc_full);
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int r = ew * 32 + lane;  // packed row = TMEM lane
+    const int qr = r / grp, g = r - qr * grp;
+    const bool valid = qr < nq && r < rpt * grp;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16);
+    float* dst = p.dq + (long)(q0 + (valid ? qr : 0)) * p.dq_ld + (long)(kvh * grp + g) * 128;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c0, v);
+      tmem_ld_wait();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + c0 + i) =
+              make_float4(__uint_as_float(v[i]) * p.scale, __uint_as_float(v[i + 1]) * p.scale,
+                          __uint_as_float(v[i + 2]) * p.scale, __uint_as_float(v[i + 3]) * p.scale);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const CUtensorMap& tmK16,
+                         const CUtensorMap& tmK64, int n_heads, cudaStream_t st) {
+  const int rows = p.b - p.a;
+  if (rows <= 0) return cudaSuccess;
+  static bool once = (cudaFuncSetAttribute(attn_dq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           DQG_SMEM),
+                      true);
+  (void)once;
+  const int rpt = 128 / p.grp;
+  dim3 grid((rows + rpt - 1) / rpt, n_heads / p.grp);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  attn_dq_gemm_kernel<<<grid, 256, DQG_SMEM, st>>>(tmDS, tmK16, tmK64, p, n_heads);
+  return cudaGetLastError();
+}
+
+}  // namespace cs

@@ -60,6 +60,9 @@ struct cs_engine {
   // QKV / O / gate||up / unembedding weights (CS_BWD_MN=0 keeps the reference-layout copies)
   bool bwd_mn = true;
   int down_rows = 0;  // per-layer rows of down_cat: h (+ 64 LoRA-A^T rows when bwd_mn)
+  // CS_BWD_DSQ=1: dQ as a GEMM over the dS the dK/dV kernel stores ([window row][q head][key])
+  bool bwd_dsq = false;
+  bf16* ds_buf = nullptr;
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
     const char* name;
@@ -278,6 +281,7 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
   AL(tp_sync, 64);
   AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
+  AL(ds_buf, e->bwd_dsq ? S * e->Hq * Lm : 1);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
 #undef AL
@@ -370,6 +374,8 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
   e->down_rows = e->h + (e->bwd_mn ? 64 : 0);
+  if (const char* v = std::getenv("CS_BWD_DSQ"))
+    e->bwd_dsq = std::atoi(v) != 0 && c.head_dim == 128 && (c.max_ft_len % 8) == 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -1560,7 +1566,18 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
           cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
                           qbox) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
-      if (v2)
+      if (v2 && e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
+        CUtensorMap mds, mk64;
+        bp.ds_out = e->ds_buf;
+        bp.ds_ld = e->L_max;
+        bp.ds_heads = e->Hq;
+        if (cs::make_map_3d(&mds, e->ds_buf, e->L_max, e->Hq, e->S_max, (long)e->L_max * 2,
+                            (long)e->Hq * e->L_max * 2, e->grp, 128 / e->grp) != 0 ||
+            cs::make_map(&mk64, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 64) != 0)
+          return cs::set_error(CS_ERR_CUDA, "attention backward: dS TMA map creation failed");
+        CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
+        CS_CUDA_TRY(cs::attn_dq_gemm(bp, mds, mk, mk64, e->Hq, st));
+      } else if (v2)
         CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
       else
         CS_CUDA_TRY(cs::attn_bwd_tc(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));

@@ -77,6 +77,12 @@ struct AttnBwdParams {
   long acc_ld;
   int grp;
   float scale, scale_log2;
+  // CS_BWD_DSQ: the dK/dV kernel also stores dS (bf16) as [window row][q head][key] with key
+  // stride ds_ld (zeros where masked, from the first dQ-GEMM tile touching each key block) for
+  // attn_dq_gemm; nullptr = the dQ kernel recomputes S and dP
+  bf16* ds_out = nullptr;
+  long ds_ld = 0;
+  int ds_heads = 0;
 };
 
 // decode rows (q_len * group <= 16): HBM-bound paged kernel (attn_decode.cu); run before
@@ -92,6 +98,9 @@ cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cu
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
+// dQ = scale * dS . K over the dS the dK/dV kernel stored (attn_dq_gemm.cu)
+cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const CUtensorMap& tmK16,
+                         const CUtensorMap& tmK64, int n_heads, cudaStream_t st);
 void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st);
 // tcgen05 backward (dQ and dK/dV kernels); head_dim 128, 64 % grp == 0
 void attn_bwd_dq_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,

@@ -230,12 +230,13 @@ ARCH_D128 = O.Arch(n_layers=2, hidden=512, n_heads=4, n_kv_heads=2, head_dim=128
                    rope_theta=10000.0)
 
 
-@pytest.mark.parametrize("tc", ["1", "0"])
-def test_d128_tcgen05_attention_parity(tc, monkeypatch):
+@pytest.mark.parametrize("tc,dsq", [("1", "0"), ("0", "0"), ("1", "1")])
+def test_d128_tcgen05_attention_parity(tc, dsq, monkeypatch):
     """head_dim 128: prefill / FT-window rows run on the tcgen05 attention kernel (CS_ATTN_TC=1)
     or the mma.sync kernel (0); contexts span several 128-key tiles and a window boundary that
-    is not tile aligned."""
+    is not tile aligned.  dsq=1: dQ as a GEMM over the dS the dK/dV kernel stores."""
     monkeypatch.setenv("CS_ATTN_TC", tc)
+    monkeypatch.setenv("CS_BWD_DSQ", dsq)
     arch = ARCH_D128
     W = O.init_general(arch, 7)
     toks = list(np.random.default_rng(9).integers(0, arch.vocab, 300))
