@@ -347,13 +347,12 @@ __global__ void __launch_bounds__(384, 1)
           const float2 ds = fmul2(pv, dd);
           pp[cc >> 1] = pack_bf16(pv.x, pv.y);
           pd[cc >> 1] = pack_bf16(ds.x, ds.y);
-          if (p.ds_out && key < p.ds_ld) {  // dS[row][q head][key] for the dQ GEMM (lanes: keys)
-            const int q0r = qbase + c / grp, q1r = qbase + (c + 1) / grp;
-            if (c < ROWS && q0r < nrows)
-              p.ds_out[((long)q0r * p.ds_heads + kvh * grp + c % grp) * p.ds_ld + key] = __float2bfloat16(ds.x);
-            if (c + 1 < ROWS && q1r < nrows)
-              p.ds_out[((long)q1r * p.ds_heads + kvh * grp + (c + 1) % grp) * p.ds_ld + key] = __float2bfloat16(ds.y);
-          }
+        }
+        if (p.ds_out && key < p.ds_ld) {  // dS^T row of this key, tile-major [kvh][tile][key][64]
+          uint4* dst = reinterpret_cast<uint4*>(
+              p.ds_out + (((long)kvh * p.ds_heads + qt) * p.ds_ld + key) * QB + h * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pd[4 * v], pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
         }
         tst_x16(tmem + lane_base + b * QB + h * 16, pp);
         tst_x16(tmem + lane_base + 128 + b * QB + h * 16, pd);

@@ -1,9 +1,10 @@
 // attn_dq_gemm.cu -- dQ of a token-level backward window as a masked GEMM over the dS the
 // dK/dV kernel already computed (CS_BWD_DSQ=1): dQ[p, h, :] = scale * sum_k dS[p, h, k] K[k, :]
 // (tiny_model.hpp:294-315, Alg. 2 line 19).  The dK/dV kernel holds dS^T in TMEM for
-// its own dK product; it stores it (bf16) to an HBM buffer laid out [window row][q head][key],
-// and this kernel streams it back as the K-major A operand (3-D TMA boxes of 64 keys x group
-// heads x positions = GQA-packed rows) against the paged K tile as an MN-major B operand.  It
+// its own dK product; it also stores it (bf16) tile-major -- [kv head][64-row query tile][key]
+// [64 packed rows], each thread one 128-byte key row -- and this kernel streams it back as an
+// MN-major A operand (two 64-row tiles per 128-row dQ tile, {64 rows, 64 keys} TMA boxes)
+// against the paged K tile as an MN-major B operand.  It
 // replaces the dQ kernel that recomputed S and dP and was bounded by reading both back out of
 // TMEM (128 KB per 128x128 tile at 64 B/clk).
 //   warp 0: TMA producer (A: 3-D dS box, B: paged K rows, contiguous pages in one 64-row box)
@@ -17,7 +18,7 @@ namespace cs {
 
 namespace {
 constexpr int DQG_STAGES = 6;
-constexpr int DQG_A = 128 * 128;      // 128 packed rows x 64 keys x bf16
+constexpr int DQG_A = 128 * 128;      // 64 keys x 128 packed rows x bf16 (two 64-row chunks)
 constexpr int DQG_B = 64 * 128 * 2;   // 64 keys x 128 dims x bf16 (two 64-dim chunks, 8 KB apart)
 constexpr int DQG_STAGE = DQG_A + DQG_B;
 constexpr int DQG_SMEM = DQG_STAGES * DQG_STAGE + 1024 + 256;
@@ -56,15 +57,16 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int a_bytes = rpt * grp * 128;
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % DQG_STAGES;
       mbar_wait(&empty[s], ((kb / DQG_STAGES) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], a_bytes + DQG_B);
+      mbar_arrive_expect_tx(&full[s], DQG_A + DQG_B);
       uint8_t* sa = smem + s * DQG_STAGE;
       uint8_t* sb = sa + DQG_A;
-      tma_load_3d(&tmDS, &full[s], sa, kb * 64, kvh * grp, q0);
+      for (int m = 0; m < 2; ++m)  // the dQ tile's two 64-row dK/dV tiles, 64 keys each
+        tma_load_2d(&tmDS, &full[s], sa + m * 8192, 0,
+                    (int)(((long)kvh * p.ds_heads + 2 * blockIdx.x + m) * p.ds_ld + kb * 64));
       // K rows [kb*64, kb*64+64) of the sequence: one 64-row box per 64-dim half when the four
       // 16-key pages are consecutive in the pool, else one 16-row box per page
       const int k0 = kb * 64, P = p.page_size;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc = idesc_bf16_f32_major(128, 128, 0, 1);
+    constexpr uint32_t idesc = idesc_bf16_f32_major(128, 128, 1, 1);  // A and B MN-major
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % DQG_STAGES;
       mbar_wait(&full[s], (kb / DQG_STAGES) & 1);
@@ -94,8 +96,8 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t sa = smem_u32(smem + s * DQG_STAGE), sb = sa + DQG_A;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        mma_bf16(tmem, umma_desc_sw128(sa) + (uint64_t)(k * 2), umma_desc_sw128_mn(sb + k * 2048, 8192, 1024),
-                 idesc, (kb > 0 || k > 0) ? 1u : 0u);
+        mma_bf16(tmem, umma_desc_sw128_mn(sa + k * 2048, 8192, 1024),
+                 umma_desc_sw128_mn(sb + k * 2048, 8192, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
       mma_commit(&empty[s]);
     }
     mma_commit(acc_full);

@@ -281,7 +281,8 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
   AL(tp_sync, 64);
   AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
-  AL(ds_buf, e->bwd_dsq ? S * e->Hq * Lm : 1);
+  // dS^T tiles: [kv heads][64-row query tiles of a window][keys (L_max rounded to 128)][64]
+  AL(ds_buf, e->bwd_dsq ? (size_t)e->Hkv * (S * e->grp / 64 + 2) * ((Lm + 127) / 128 * 128) * 64 : 1);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
 #undef AL
@@ -375,7 +376,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
   e->down_rows = e->h + (e->bwd_mn ? 64 : 0);
   if (const char* v = std::getenv("CS_BWD_DSQ"))
-    e->bwd_dsq = std::atoi(v) != 0 && c.head_dim == 128 && (c.max_ft_len % 8) == 0;
+    e->bwd_dsq = std::atoi(v) != 0 && c.head_dim == 128 && 64 % (c.n_heads / c.n_kv_heads) == 0;
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -1568,11 +1569,12 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
       if (v2 && e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
         CUtensorMap mds, mk64;
+        const long keys = ((long)e->L_max + 127) / 128 * 128;
+        const long ntiles = (long)e->S_max * e->grp / 64 + 2;
         bp.ds_out = e->ds_buf;
-        bp.ds_ld = e->L_max;
-        bp.ds_heads = e->Hq;
-        if (cs::make_map_3d(&mds, e->ds_buf, e->L_max, e->Hq, e->S_max, (long)e->L_max * 2,
-                            (long)e->Hq * e->L_max * 2, e->grp, 128 / e->grp) != 0 ||
+        bp.ds_ld = keys;
+        bp.ds_heads = (int)ntiles;
+        if (cs::make_map(&mds, e->ds_buf, (long)e->Hkv * ntiles * keys, 64, 64, 64) != 0 ||
             cs::make_map(&mk64, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 64) != 0)
           return cs::set_error(CS_ERR_CUDA, "attention backward: dS TMA map creation failed");
         CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));

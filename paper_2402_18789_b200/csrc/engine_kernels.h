@@ -77,9 +77,10 @@ struct AttnBwdParams {
   long acc_ld;
   int grp;
   float scale, scale_log2;
-  // CS_BWD_DSQ: the dK/dV kernel also stores dS (bf16) as [window row][q head][key] with key
-  // stride ds_ld (zeros where masked, from the first dQ-GEMM tile touching each key block) for
-  // attn_dq_gemm; nullptr = the dQ kernel recomputes S and dP
+  // CS_BWD_DSQ: the dK/dV kernel also stores dS^T (bf16) tile-major as
+  // [kv head][64-row query tile (ds_heads of them)][key (ds_ld)][64 packed rows] -- each thread
+  // writes its key's 128-byte row (zeros where masked, from the first dQ-GEMM tile touching
+  // each key block) for attn_dq_gemm; nullptr = the dQ kernel recomputes S and dP
   bf16* ds_out = nullptr;
   long ds_ld = 0;
   int ds_heads = 0;
