@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 1
+#define CS_ABI_VERSION 2  /* 2: policy / VTC / tail-control / sim-clock config fields, per-tenant stats, fwd_window_ms */
 
 #define CS_OK 0
 #define CS_ERR_INVALID_ARGUMENT (-1)
