@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(384, 1)
                           const __grid_constant__ CUtensorMap tmQ3,
                           const __grid_constant__ CUtensorMap tmO3, AttnBwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   using namespace kv2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(384, 1)
                         const __grid_constant__ CUtensorMap tmK128,
                         const __grid_constant__ CUtensorMap tmV128, AttnBwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   using namespace dq2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -687,12 +689,12 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
   if (p.ds_out) {
     // dQ comes from attn_dq_gemm over the stored dS (launched by the caller after this)
   } else if (mask & 1) {
-    attn_bwd_dq2_kernel<<<gq, 384, dq2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, p);
+    launch_pdl(attn_bwd_dq2_kernel, dim3(gq), dim3(384), dq2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, p);
   } else {
     attn_bwd_dq_v1(p, tmK, tmV, tmK128, tmV128, gq, st);
   }
   if ((mask & 2) || (64 % p.grp) != 0)
-    kDkdv2[p.grp - 1]<<<gk, 384, kv2::SMEM_TOTAL, st>>>(tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
+    launch_pdl(kDkdv2[p.grp - 1], dim3(gk), dim3(384), kv2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
   else attn_bwd_dkdv_v1(p, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, gk, st);
   return cudaGetLastError();
 }

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        AttnFwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   constexpr int NH = D / 64;                       // 64-column halves
   constexpr int HALF = KT * 128;                   // one half of a K (or V) tile
   constexpr int TILE = NH * HALF;                  // K (or V) tile bytes
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     attn_decode_stream_kernel(const __grid_constant__ CUtensorMap tmK,
                               const __grid_constant__ CUtensorMap tmV, AttnFwdParams p, int n_items) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   constexpr int NH = D / 64;
   constexpr int HALF = KT * 128;
   constexpr int TILE = NH * HALF;
@@ -545,6 +547,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     attn_decode_swap_kernel(const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, AttnFwdParams p, int n_items) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   constexpr int NH = D / 64;
   constexpr int HALF = KT * 128;
   constexpr int TILE = NH * HALF;
@@ -791,7 +794,7 @@ cudaError_t launch_dec_swap(const AttnFwdParams& p, const CUtensorMap& tmK, cons
   const int cps = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
   const int grid = std::max(1, std::min((n_work + NW - 1) / NW, 148 * cps));
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_decode_swap_kernel<D, KT, NW, ST><<<grid, NW * 32, smem, st>>>(tmK, tmV, p, n_work);
+  launch_pdl(attn_decode_swap_kernel<D, KT, NW, ST>, dim3(grid), dim3(NW * 32), smem, st, tmK, tmV, p, n_work);
   return cudaGetLastError();
 }
 
@@ -806,7 +809,7 @@ cudaError_t launch_dec_stream(const AttnFwdParams& p, const CUtensorMap& tmK, co
   const int cps = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
   const int grid = std::max(1, std::min((n_work + NW - 1) / NW, 148 * cps));
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_decode_stream_kernel<D, KT, NW, ST><<<grid, NW * 32, smem, st>>>(tmK, tmV, p, n_work);
+  launch_pdl(attn_decode_stream_kernel<D, KT, NW, ST>, dim3(grid), dim3(NW * 32), smem, st, tmK, tmV, p, n_work);
   return cudaGetLastError();
 }
 
@@ -819,7 +822,7 @@ cudaError_t launch_dec(const AttnFwdParams& p, const CUtensorMap& tmK, const CUt
                       true);
   (void)once;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_decode_kernel<D, KT, NW, ST><<<n_work, NW * 32, smem, st>>>(tmK, tmV, p);
+  launch_pdl(attn_decode_kernel<D, KT, NW, ST>, dim3(n_work), dim3(NW * 32), smem, st, tmK, tmV, p);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,8 @@ constexpr int DQG_SMEM = DQG_STAGES * DQG_STAGE + 1024 + 256;
 __global__ void __launch_bounds__(256, 1)
     attn_dq_gemm_kernel(const __grid_constant__ CUtensorMap tmDS, const __grid_constant__ CUtensorMap tmK16,
                         const __grid_constant__ CUtensorMap tmK64, AttnBwdParams p, int Hq) {
+  griddep_launch();
+  griddep_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DQG_STAGES * DQG_STAGE);
@@ -143,8 +145,7 @@ cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const 
   const int rpt = 128 / p.grp;
   dim3 grid((rows + rpt - 1) / rpt, n_heads / p.grp);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_dq_gemm_kernel<<<grid, 256, DQG_SMEM, st>>>(tmDS, tmK16, tmK64, p, n_heads);
-  return cudaGetLastError();
+  return launch_pdl(attn_dq_gemm_kernel, grid, dim3(256), DQG_SMEM, st, tmDS, tmK16, tmK64, p, n_heads);
 }
 
 }  // namespace cs

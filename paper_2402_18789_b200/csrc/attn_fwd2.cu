@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(384, 1)
                         const __grid_constant__ CUtensorMap tmK128,
                         const __grid_constant__ CUtensorMap tmV128, AttnFwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -394,7 +395,7 @@ cudaError_t attn_fwd_tc2(const AttnFwdParams& p, const CUtensorMap& tmK, const C
                       true);
   (void)once;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_fwd_tc2_kernel<<<n_work, 384, SM_TOTAL2, st>>>(tmK, tmV, tmK128, tmV128, p);
+  launch_pdl(attn_fwd_tc2_kernel, dim3(n_work), dim3(384), SM_TOTAL2, st, tmK, tmV, tmK128, tmV128, p);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
                                                       float* __restrict__ rstd_out, int h, float eps,
                                                       int use_norm) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ float red[4];
   const long src_row = idx ? idx[blockIdx.x] : blockIdx.x;
   const float* xr = x + src_row * ldx;
@@ -128,19 +129,20 @@ void rmsnorm_cast(const float* x, long ldx, const float* g, bf16* out, long ldo,
                   int rows, int h, float eps, int use_norm, cudaStream_t st) {
   if (rows <= 0) return;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  rmsnorm_kernel<<<rows, 128, 0, st>>>(x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
+  launch_pdl(rmsnorm_kernel, dim3(rows), dim3(128), 0, st, x, ldx, nullptr, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 void rmsnorm_cast_gather(const float* x, long ldx, const int* idx, const float* g, bf16* out,
                          long ldo, float* rstd_out, int rows, int h, float eps, int use_norm,
                          cudaStream_t st) {
   if (rows <= 0) return;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  rmsnorm_kernel<<<rows, 128, 0, st>>>(x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
+  launch_pdl(rmsnorm_kernel, dim3(rows), dim3(128), 0, st, x, ldx, idx, g, out, ldo, rstd_out, h, eps, use_norm);
 }
 
 // ---------------------------------------------------------------- RoPE + KV append
 __global__ void rope_append_kernel(RopeAppendParams p, const float2* __restrict__ cs_tab) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   const int row = blockIdx.x;
   const int pos = p.row_pos[row];
   const AttnSeg sg = p.segs[p.row_seg[row]];
@@ -198,7 +200,7 @@ static const float2* s_rope_tab = nullptr;
 void set_rope_table(const float2* tab) { s_rope_tab = tab; }
 void rope_append(const RopeAppendParams& p, cudaStream_t st) {
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (p.T > 0) rope_append_kernel<<<p.T, 128, 0, st>>>(p, s_rope_tab);
+  if (p.T > 0) launch_pdl(rope_append_kernel, dim3(p.T), dim3(128), 0, st, p, s_rope_tab);
 }
 
 // ---------------------------------------------------------------- activations
@@ -209,6 +211,7 @@ constexpr int ACT_CH = 4;
 __global__ void __launch_bounds__(128) act_kernel(const bf16* __restrict__ gu, long ld_gu,
                                                   bf16* __restrict__ m, long ldm, int f, int swiglu) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   const long row = blockIdx.y;
   const int c0 = (blockIdx.x * ACT_CH * 128 + threadIdx.x) * 8;
   uint4 gv[ACT_CH], uv[ACT_CH];
@@ -246,12 +249,13 @@ void act_fwd(const bf16* gu, long ld_gu, bf16* m, long ldm, int rows, int f, int
   if (rows <= 0) return;
   dim3 grid((unsigned)((ldm / 8 + 128 * ACT_CH - 1) / (128 * ACT_CH)), rows);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  act_kernel<<<grid, 128, 0, st>>>(gu, ld_gu, m, ldm, f, swiglu);
+  launch_pdl(act_kernel, dim3(grid), dim3(128), 0, st, gu, ld_gu, m, ldm, f, swiglu);
 }
 
 __global__ void lora_pack_kernel(const float* __restrict__ lu, int r, bf16* __restrict__ m,
                                  long ldm, int f, int rows) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= rows * r) return;
   const int row = t / r, j = t % r;
@@ -259,7 +263,7 @@ __global__ void lora_pack_kernel(const float* __restrict__ lu, int r, bf16* __re
 }
 void lora_pack(const float* lu, int r, bf16* m, long ldm, int f, int rows, cudaStream_t st) {
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (rows > 0) lora_pack_kernel<<<(rows * r + 255) / 256, 256, 0, st>>>(lu, r, m, ldm, f, rows);
+  if (rows > 0) launch_pdl(lora_pack_kernel, dim3((rows * r + 255) / 256), dim3(256), 0, st, lu, r, m, ldm, f, rows);
 }
 
 // ---------------------------------------------------------------- sampling / CE
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
                                                  float* __restrict__ loss, bf16* __restrict__ dlog,
                                                  long ldd) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ float red_m[16], red_s[16];
   const int row = blockIdx.x;
   const float* x = logits + (long)row * ld;
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
 void ce_fwd_bwd(const float* logits, long ld, const int* targets, int rows, int V,
                 float inv_norm, float* loss, bf16* dlogits, long ldd, cudaStream_t st) {
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (rows > 0) ce_kernel<<<rows, 512, 0, st>>>(logits, ld, targets, V, inv_norm, loss, dlogits, ldd);
+  if (rows > 0) launch_pdl(ce_kernel, dim3(rows), dim3(512), 0, st, logits, ld, targets, V, inv_norm, loss, dlogits, ldd);
 }
 
 // ---------------------------------------------------------------- backward helpers
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(256) rms_bwd_kernel(const float* __restrict__ 
                                long ldh, float* __restrict__ out, long ldo, bf16* __restrict__ ob,
                                long ldob, int h, int use_norm) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ float red[32];
   const long row = blockIdx.x;
   const float* dr = dh + row * ldh;
@@ -462,7 +468,7 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
   if (rows <= 0) return;
   if (h > RMSB_V * 1024 || (h % 4) != 0) return;  // engine_create bounds h (multiple of 64)
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  rms_bwd_kernel<<<rows, 256, 0, st>>>(resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
+  launch_pdl(rms_bwd_kernel, dim3(rows), dim3(256), 0, st, resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
                                        ldob, h, use_norm);
 }
 
@@ -485,6 +491,7 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const float* __res
                                                               float* __restrict__ dA, int rows, int f,
                                                               int swiglu) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ __align__(16) float sl[MLP_ROWS * 16];
   const int col = 4 * (blockIdx.x * MLP_THREADS + threadIdx.x);
   const int r0 = blockIdx.y * MLP_ROWS;
@@ -588,7 +595,7 @@ void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const fl
   if (rows <= 0) return;
   dim3 grid((f / 4 + MLP_THREADS - 1) / MLP_THREADS, (rows + MLP_ROWS - 1) / MLP_ROWS);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  mlp_bwd_kernel<<<grid, MLP_THREADS, 0, st>>>(dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
+  launch_pdl(mlp_bwd_kernel, dim3(grid), dim3(MLP_THREADS), 0, st, dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
                                                swiglu);
 }
 
@@ -596,6 +603,7 @@ void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const fl
 __global__ void dycat_cast_kernel(const float* __restrict__ dY, long ldy, int h,
                                   bf16* __restrict__ dycat, long ldc) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   const long row = blockIdx.x;
   const float* y = dY + row * ldy;
   bf16* o = dycat + row * ldc;
@@ -616,6 +624,7 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
                                                       const float* __restrict__ lu, int r,
                                                       int rows, int h, float* __restrict__ dB) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ __align__(16) float sl[LDB_ROWS * 16];
   const int col = 4 * (blockIdx.x * 128 + threadIdx.x);
   const int r0 = blockIdx.y * LDB_ROWS;
@@ -665,14 +674,14 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
 void dycat_cast(const float* dY, long ldy, int rows, int h, bf16* dycat, long ldc, cudaStream_t st) {
   if (rows <= 0) return;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  dycat_cast_kernel<<<rows, 128, 0, st>>>(dY, ldy, h, dycat, ldc);
+  launch_pdl(dycat_cast_kernel, dim3(rows), dim3(128), 0, st, dY, ldy, h, dycat, ldc);
 }
 void lora_db(const float* dY, long ldy, const float* lu, int r, int rows, int h, float* dB,
              cudaStream_t st) {
   if (rows <= 0) return;
   dim3 grid((h / 4 + 127) / 128, (rows + LDB_ROWS - 1) / LDB_ROWS);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  lora_db_kernel<<<grid, 128, 0, st>>>(dY, ldy, lu, r, rows, h, dB);
+  launch_pdl(lora_db_kernel, dim3(grid), dim3(128), 0, st, dY, ldy, lu, r, rows, h, dB);
 }
 
 // inverse (transposed) rotate-half RoPE + pack [dq | dk | dv] as bf16
@@ -682,6 +691,7 @@ __global__ void rope_bwd_pack_kernel(const float* __restrict__ dq, long ldq,
                                      int use_rope, const float2* __restrict__ tab,
                                      bf16* __restrict__ out, long ldo) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
+  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   const int i = blockIdx.x;  // window-local row
   const int pos = a + i;
   const int half = d / 2;
@@ -714,7 +724,7 @@ void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, 
   (void)theta;
   if (rows > 0)
     cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    rope_bwd_pack_kernel<<<rows, 128, 0, st>>>(dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
+    launch_pdl(rope_bwd_pack_kernel, dim3(rows), dim3(128), 0, st, dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
                                                head_dim, use_rope, s_rope_tab, out, ldo);
 }
 
