@@ -232,8 +232,9 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnFwdParams p) {
 }
 
 // Merge split-KV partials: o = sum_s o_s * exp(lse_s - lse), lse = log sum_s exp(lse_s).
-// One warp per packed row (lanes over d, 4 columns each); the part LSEs are warp-broadcast
-// loads, independent across parts.
+// One warp per packed row (lanes over d, 4 columns each), one pass with a running max: the
+// part loads are independent of the merge arithmetic, so a row costs one memory round trip
+// (the two-pass max-then-sum form was two dependent round trips per row).
 template <int D>
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
@@ -249,21 +250,28 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   // item left the merge latency-bound)
   const int r_end = min(c.nq * grp, (int)(blockIdx.y + 1) * 16);
   for (int r = blockIdx.y * 16 + warp; r < r_end; r += 4) {
-    float mx = -INFINITY;
-    for (int s = 0; s < c.n_parts; ++s) mx = fmaxf(mx, __ldg(p.part_lse + (long)(c.part0 + s) * p.part_rows + r));
-    float den = 0.f;
+    float mx = -INFINITY, den = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (mx > -INFINITY) {
-      for (int s = 0; s < c.n_parts; ++s) {
-        const long pr = (long)(c.part0 + s) * p.part_rows + r;
-        const float wgt = __expf(__ldg(p.part_lse + pr) - mx);
-        den += wgt;
-        if (d < D) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(p.part_o + pr * D + d));
-          acc.x += wgt * v.x;
-          acc.y += wgt * v.y;
-          acc.z += wgt * v.z;
-          acc.w += wgt * v.w;
+    for (int s0 = 0; s0 < c.n_parts; s0 += 4) {
+      float l[4];
+      float4 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // issue the group's loads before any arithmetic
+        const long pr = (long)(c.part0 + min(s0 + i, c.n_parts - 1)) * p.part_rows + r;
+        l[i] = s0 + i < c.n_parts ? __ldg(p.part_lse + pr) : -INFINITY;
+        v[i] = __ldg(reinterpret_cast<const float4*>(p.part_o + pr * D + (d & (D - 1))));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (l[i] > -INFINITY) {  // an empty part (no unmasked key) contributes nothing
+          const float nm = fmaxf(mx, l[i]);
+          const float a = __expf(mx - nm), b = __expf(l[i] - nm);
+          den = den * a + b;
+          acc.x = acc.x * a + b * v[i].x;
+          acc.y = acc.y * a + b * v[i].y;
+          acc.z = acc.z * a + b * v[i].z;
+          acc.w = acc.w * a + b * v[i].w;
+          mx = nm;
         }
       }
     }
@@ -662,7 +670,7 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      const cudaError_t e = launch_pdl(attn_combine_kernel<128>, dim3(n_combine, 4), dim3(128), 0, st, p);
+      const cudaError_t e = launch_pdl(attn_combine_kernel<128>, dim3(n_combine, p.comb_slices), dim3(128), 0, st, p);
       if (e != cudaSuccess) return e;
     }
   } else if (head_dim == 64) {
@@ -675,7 +683,7 @@ cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_com
     }
     if (n_combine > 0) {
       cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-      const cudaError_t e = launch_pdl(attn_combine_kernel<64>, dim3(n_combine, 4), dim3(128), 0, st, p);
+      const cudaError_t e = launch_pdl(attn_combine_kernel<64>, dim3(n_combine, p.comb_slices), dim3(128), 0, st, p);
       if (e != cudaSuccess) return e;
     }
   } else {

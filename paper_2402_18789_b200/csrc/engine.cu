@@ -807,6 +807,7 @@ struct StepPlan {
   cs::AttnWork* work_tc;
   cs::AttnDecWork* work_dec;
   int dec_max_rows = 0;
+  int comb_slices = 4;  // 16-row slices of the largest decode / legacy combine item
   cs::AttnCombine* comb;
   cs::AttnCombine* comb_tc;  // split-KV parts of the tcgen05 kernel (256-row parts)
   std::vector<int> samp_seg;  // segment of each sampled row
@@ -1187,6 +1188,11 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.n_dec = (int)work_dec.size();
   sp.dec_max_rows = 0;
   for (const auto& w : work_dec) sp.dec_max_rows = std::max(sp.dec_max_rows, w.nq * e->grp);
+  {
+    int mr = 1;
+    for (const auto& c : comb) mr = std::max(mr, c.nq * e->grp);
+    sp.comb_slices = (mr + 15) / 16;
+  }
   sp.n_comb = (int)comb.size();
   sp.n_comb_tc = (int)comb_tc.size();
   if (sp.n_work + sp.n_tc + sp.n_dec > 65536 || sp.n_comb + sp.n_comb_tc > 8192)
@@ -1321,6 +1327,7 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     ap.part_o = e->part_o;
     ap.part_lse = e->part_lse;
     ap.grp = e->grp;
+    ap.comb_slices = sp.comb_slices;
     ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
     cs_engine::ProfRec apr{};
     const bool bw_attn = sp.n_work + sp.n_dec > 0;

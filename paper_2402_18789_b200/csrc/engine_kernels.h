@@ -50,6 +50,7 @@ struct AttnFwdParams {
   int grp;
   float scale_log2;
   int part_rows = 64;  // rows per split-KV part in part_o / part_lse (combine)
+  int comb_slices = 4;  // attn_fwd's combine grid.y: 16-row slices of the largest item
   int max_dec_rows = 16;  // attn_decode: max packed rows (q_len x group) over the work items
 };
 
