@@ -549,6 +549,9 @@ def run_ours(a):
         "cpu_baseline": cpu,
         "gpu_launches": int(st["gpu_launches"]),
         "clocks": clocks,
+        # per iteration: wall clock of the loop vs device time (first to last kernel of the
+        # step, CUDA events): the difference is the host's share (planning, launch, sync)
+        "host_gap_ms_per_step": round((st["timed_ms"] - st["timed_device_ms"]) / max(1, a.steps), 3),
         "inference": {"iter_p50_ms": round(st["iter_p50_ms"], 2),
                       "iter_p99_ms": round(st["iter_p99_ms"], 2),
                       "iter_max_ms": round(st["iter_max_ms"], 2),

@@ -9,6 +9,7 @@
 // the StepExecutor interface (implemented over the C ABI in csrc/coserve_run.cpp).
 #pragma once
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <deque>
@@ -38,12 +39,16 @@ struct StepInput {
   std::vector<int32_t> ft_targets;
   const std::vector<int32_t>* ft_pages = nullptr;
   std::vector<BwdWindow> extra_bwd;  // further backward windows after (ft_layer, ft_l, ft_s)
+  // wall clock at the end of the previous step: an executor's clock advance covers the whole
+  // cycle -- the loop's own admission / planning / bookkeeping and the Adam step included
+  std::chrono::steady_clock::time_point cycle_begin{};
 };
 
 struct StepOutput {
   std::vector<int32_t> next_tokens;  // per segment (-1 unsampled)
   double ms = 0.0;                   // clock advance
   double device_ms = 0.0;            // device time of the step
+  std::chrono::steady_clock::time_point t_end{};  // wall clock when the step returned
 };
 
 class StepExecutor {
@@ -185,6 +190,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
   size_t resid_pos = 0;
   double budget = cfg.budget_ms;
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
+  auto cycle_t = std::chrono::steady_clock::now();
   for (int it = 0; it < total_iters; ++it) {
     const bool timed = it >= cfg.warmup_iters;
     int64_t arrived = 0;
@@ -299,10 +305,12 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
     StepOutput out;
     if (exec) {
+      in.cycle_begin = cycle_t;
       if (!exec->run(in, out)) {
         st.ok = false;
         return st;
       }
+      cycle_t = out.t_end.time_since_epoch().count() ? out.t_end : std::chrono::steady_clock::now();
     } else {
       out.ms = plan.predicted_ms;
       out.device_ms = plan.predicted_ms;

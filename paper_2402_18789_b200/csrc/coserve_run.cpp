@@ -87,7 +87,11 @@ class GpuExecutor : public coserve::StepExecutor {
       d2h += (int64_t)ns * 4 + (w.phase == CS_FT_FORWARD ? (int64_t)in.ft_s * 4 : 0);
     }
     out.next_tokens.assign(next_.begin(), next_.begin() + in.segs.size());
-    out.ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    // the clock advances by the whole cycle since the previous step returned (the loop's
+    // planning and bookkeeping, the Adam step, this step's enqueue, execution and sync)
+    const auto tb = in.cycle_begin.time_since_epoch().count() ? in.cycle_begin : t0;
+    out.ms = std::chrono::duration<double, std::milli>(t1 - tb).count();
+    out.t_end = t1;
     out.device_ms = r.iteration_ms;
     // TP group: one loop per rank -> the clock must be rank-invariant (max over ranks), so
     // every rank admits, plans and corrects identically
