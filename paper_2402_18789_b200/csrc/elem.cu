@@ -476,7 +476,7 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
 //   swiglu: g=saved[:, :f], u=saved[:, f:]; dgu = [dm*u*dsilu(g), dm*silu(g)]; m = silu(g)*u
 //   relu  : m=saved;  dgu = dm * (m > 0)            (tiny_model.hpp:285-286)
 //   dA[col, :] += sum_rows m[row, col] * dlu[row, :] (tiny_model.hpp:282)
-// HBM-bound (12 B per (row, col): dm fp32 in, g / u bf16 in, dgu bf16 out).  Thread = 4
+// HBM-bound (10 B per (row, col): dm bf16 in, g / u bf16 in, dgu bf16 out).  Thread = 4
 // adjacent columns (16-B / 8-B accesses), block = 128 threads x 512 columns x 256 rows; rows
 // are processed in pairs with both rows' loads issued before either is used (memory-level
 // parallelism), sigmoid on the SFU (ex2 + rcp), the dA partial sums on FFMA2 (column pairs),
@@ -484,7 +484,7 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
 // 2-column variant at full occupancy measured 360 us).
 constexpr int MLP_ROWS = 256;
 constexpr int MLP_THREADS = 128;
-__global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const float* __restrict__ dm, long ld_dm,
+__global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const bf16* __restrict__ dm, long ld_dm,
                                                               const bf16* __restrict__ saved, long ld_s,
                                                               const float* __restrict__ dlu, int r,
                                                               bf16* __restrict__ dgu, long ld_dgu,
@@ -551,7 +551,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const float* __res
   };
   auto ld = [&](int i, float4& d, uint2& gv, uint2& uv) {
     const long row = r0 + i;
-    d = __ldg(reinterpret_cast<const float4*>(dm + row * ld_dm + col));
+    const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + row * ld_dm + col));
+    const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+    d = make_float4(__low2float(d2[0]), __high2float(d2[0]), __low2float(d2[1]), __high2float(d2[1]));
     gv = __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + col));
     uv = swiglu ? __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + f + col)) : make_uint2(0u, 0u);
   };
@@ -590,7 +592,7 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const float* __res
 #pragma unroll
   for (int q = 0; q < 4; ++q) flush(q, dA + (long)(col + q) * r);
 }
-void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
+void mlp_bwd(const bf16* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st) {
   if (rows <= 0) return;
   dim3 grid((f / 4 + MLP_THREADS - 1) / MLP_THREADS, (rows + MLP_ROWS - 1) / MLP_ROWS);

@@ -103,8 +103,8 @@ struct cs_engine {
   float* stage_tab[8] = {};
   std::vector<std::pair<void*, std::vector<float*>>> dst_tabs;
   // backward scratch
-  bf16 *dycat, *dgu, *dr1b, *dO, *dqkv;
-  float *dlu, *dm, *dh2, *dr1, *delta, *dq, *dh1;
+  bf16 *dycat, *dgu, *dr1b, *dO, *dqkv, *dm;  // dm: dLoss/d(MLP activation), bf16 like dgu
+  float *dlu, *dh2, *dr1, *delta, *dq, *dh1;
   float2* rope_tab;
   // per-step upload
   uint8_t* d_meta = nullptr;
@@ -1496,10 +1496,10 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   cs::lora_db(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, r, s, h, e->gB + (size_t)n * r * h, st);
   if (e->bwd_mn)  // dm = [dY | dU] . [W_down^T ; A^T]: down_cat's [h + 64, f] block, MN-major
     TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->down_cat + (size_t)n * e->down_rows * e->f_cat,
-             e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_F32, nullptr, nullptr, 1));
+             e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_BF16, nullptr, nullptr, 1));
   else
     TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
-             e->dm, f, s, f, e->h_cat, cs::EPI_F32));
+             e->dm, f, s, f, e->h_cat, cs::EPI_BF16));
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
               e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
   if (n > 0) {

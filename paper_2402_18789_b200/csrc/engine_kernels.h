@@ -181,7 +181,7 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
                  bf16* out_b, long ldob, int rows, int h, int use_norm, cudaStream_t st);
 
 // MLP + LoRA-A backward: dgu (bf16) from dm, saved gu/m; dA[f,r] += m^T dlu
-void mlp_bwd(const float* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
+void mlp_bwd(const bf16* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st);
 
 // dycat = [bf16(dY) | 0...]; dlu = dY B^T is a tcgen05 GEMM (B_t), packed by lora_pack
