@@ -601,30 +601,17 @@ void mlp_bwd(const bf16* dm, long ld_dm, const bf16* saved, long ld_s, const flo
                                                swiglu);
 }
 
-// dycat = [bf16(dY) | 0 (LoRA columns, filled by lora_pack after the dlu GEMM)]
-__global__ void dycat_cast_kernel(const float* __restrict__ dY, long ldy, int h,
-                                  bf16* __restrict__ dycat, long ldc) {
-  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
-  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
-  const long row = blockIdx.x;
-  const float* y = dY + row * ldy;
-  bf16* o = dycat + row * ldc;
-  for (int c = threadIdx.x * 4; c < ldc; c += blockDim.x * 4) {
-    uint2 p = make_uint2(0u, 0u);
-    if (c < h) {
-      const float4 v = *reinterpret_cast<const float4*>(y + c);
-      p = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-    }
-    *reinterpret_cast<uint2*>(o + c) = p;
-  }
-}
 // dB[j, c] += sum_rows lu[row, j] * dY[row, c]  (tiny_model.hpp:280); 4 columns per thread
 // (one float4 of dY per row), 128 threads x 512 columns x 64 rows per block (8 x s/64 blocks:
-// enough CTAs to fill the SMs at every window size), FFMA2 on column pairs, float4 atomics
+// enough CTAs to fill the SMs at every window size), FFMA2 on column pairs, float4 atomics.
+// The same pass writes dycat[:, :h] = bf16(dY), the A operand of the dlu and dm GEMMs (its
+// LoRA columns are filled by lora_pack, its pad columns stay zero from engine creation):
+// one read of the fp32 dY instead of two
 constexpr int LDB_ROWS = 64;
 __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ dY, long ldy,
                                                       const float* __restrict__ lu, int r,
-                                                      int rows, int h, float* __restrict__ dB) {
+                                                      int rows, int h, float* __restrict__ dB,
+                                                      bf16* __restrict__ dycat, long ldc) {
   griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
   griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ __align__(16) float sl[LDB_ROWS * 16];
@@ -641,6 +628,8 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
 #pragma unroll
   for (int j = 0; j < 16; ++j) a01[j] = a23[j] = make_float2(0.f, 0.f);
   auto row = [&](int i, const float4& v) {
+    *reinterpret_cast<uint2*>(dycat + (long)(r0 + i) * ldc + col) =
+        make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
     const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
     const float4* l4 = reinterpret_cast<const float4*>(sl + i * 16);
 #pragma unroll
@@ -673,17 +662,12 @@ __global__ void __launch_bounds__(128) lora_db_kernel(const float* __restrict__ 
       atomicAdd(reinterpret_cast<float4*>(dB + (long)j * h + col),
                 make_float4(a01[j].x, a01[j].y, a23[j].x, a23[j].y));
 }
-void dycat_cast(const float* dY, long ldy, int rows, int h, bf16* dycat, long ldc, cudaStream_t st) {
-  if (rows <= 0) return;
-  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  launch_pdl(dycat_cast_kernel, dim3(rows), dim3(128), 0, st, dY, ldy, h, dycat, ldc);
-}
 void lora_db(const float* dY, long ldy, const float* lu, int r, int rows, int h, float* dB,
-             cudaStream_t st) {
+             bf16* dycat, long ldc, cudaStream_t st) {
   if (rows <= 0) return;
   dim3 grid((h / 4 + 127) / 128, (rows + LDB_ROWS - 1) / LDB_ROWS);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  launch_pdl(lora_db_kernel, dim3(grid), dim3(128), 0, st, dY, ldy, lu, r, rows, h, dB);
+  launch_pdl(lora_db_kernel, dim3(grid), dim3(128), 0, st, dY, ldy, lu, r, rows, h, dB, dycat, ldc);
 }
 
 // inverse (transposed) rotate-half RoPE + pack [dq | dk | dv] as bf16

@@ -1489,11 +1489,11 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // ---- MLP + LoRA (tiny_model.hpp:276-287)
   // dycat = [bf16(dY) | bf16(dY B^T)] (tiny_model.hpp:281): dlu on the tensor cores (N = r),
   // dB += u^T dY (:280) on the CUDA cores
-  cs::dycat_cast(Y, h, s, h, e->dycat, e->h_cat, st);
+  cs::lora_db(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, r, s, h, e->gB + (size_t)n * r * h,
+              e->dycat, e->h_cat, st);
   TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->B_t + (size_t)n * 16 * h, h, 16, e->dlu, r, s, r, h,
            cs::EPI_F32));
   cs::lora_pack(e->dlu, r, e->dycat, e->h_cat, h, s, st);
-  cs::lora_db(Y, h, e->ft_lu + ((size_t)n * Lm + a) * r, r, s, h, e->gB + (size_t)n * r * h, st);
   if (e->bwd_mn)  // dm = [dY | dU] . [W_down^T ; A^T]: down_cat's [h + 64, f] block, MN-major
     TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->down_cat + (size_t)n * e->down_rows * e->f_cat,
              e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_BF16, nullptr, nullptr, 1));

@@ -184,11 +184,10 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
 void mlp_bwd(const bf16* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st);
 
-// dycat = [bf16(dY) | 0...]; dlu = dY B^T is a tcgen05 GEMM (B_t), packed by lora_pack
-void dycat_cast(const float* dY, long ldy, int rows, int h, bf16* dycat, long ldc, cudaStream_t st);
-// dB += lu^T dY
+// dB += lu^T dY, and dycat[:, :h] = bf16(dY) in the same pass (dlu = dY B^T is then a tcgen05
+// GEMM over dycat, packed into its LoRA columns by lora_pack)
 void lora_db(const float* dY, long ldy, const float* lu, int r, int rows, int h, float* dB,
-             cudaStream_t st);
+             bf16* dycat, long ldc, cudaStream_t st);
 
 // dqkv = [rope^-1(dq) | rope^-1(dk_acc[a:b]) | dv_acc[a:b]] (bf16)
 void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, long ld_acc,
