@@ -43,6 +43,11 @@ struct GemmArgs {
                 // stages may be fetched before griddepcontrol.wait
   GemmScatter sc;  // EPI_F32_SCATTER destination (peer staging slots)
   int b_mn;        // 1: B stored [K rows][N cols] (N contiguous): MN-major B operand
+  // tail split (CTA-pair kernel, accumulating epilogues): work units [0, full_units) are whole
+  // tiles, the tiles after them are split `splits` ways along K -- only the last, partial wave
+  // is split, so it is spread over all pairs instead of idling most of them.  0: uniform splits
+  int full_units = 0;
+  int units = 0;  // total work units
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -66,6 +71,20 @@ struct GemmCfg {
 
 __device__ __forceinline__ void decode_work(int w, const GemmArgs& a, int& m_blk, int& n_blk,
                                             int& kb0, int& kb1) {
+  if (a.full_units > 0) {
+    int t = w, ks = 0, sp = 1;
+    if (w >= a.full_units) {
+      const int u = w - a.full_units;
+      t = a.full_units + u / a.splits;
+      ks = u % a.splits;
+      sp = a.splits;
+    }
+    m_blk = t % a.num_m;
+    n_blk = t / a.num_m;
+    kb0 = (int)(((long)ks * a.kb_total) / sp);
+    kb1 = (int)(((long)(ks + 1) * a.kb_total) / sp);
+    return;
+  }
   int m = w % a.num_m;
   int rest = w / a.num_m;
   int ks = rest % a.splits;
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int total = args.num_m * args.num_n * args.splits;
+  const int total = args.units;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -411,7 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int total = args.num_m * args.num_n * args.splits;
+  const int total = args.units;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -692,6 +711,31 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.sc = d.scatter;
   a.splits = 1;
   a.b_mn = d.b_mn;
+  const long tiles2 = (long)a.num_m * a.num_n;
+  a.units = (int)tiles2;
+  // accumulating epilogues (C += acc): split the last, partial wave of tiles along K when the
+  // modelled time -- waves x (K blocks per unit + ~14 blocks of fill / epilogue) -- drops
+  // (down projection M=1728: 112 tiles = 1.51 waves on 74 pairs)
+  static const bool tail_on = [] {
+    const char* v = std::getenv("CS_GEMM_TAIL");
+    return !(v && std::atoi(v) == 0);
+  }();
+  const long np = kNumSMs / 2;
+  if (tail_on && (d.epi == EPI_F32_ADD || d.epi == EPI_F32_ATOMIC) && tiles2 > np && tiles2 % np) {
+    const long full = tiles2 / np * np, rem = tiles2 - full;
+    const double kb = a.kb_total;
+    double best = (double)(full / np + 1) * (kb + 14.0);
+    int best_s = 1;
+    for (int sp = 2; sp <= 8 && kb / sp >= 8; ++sp) {
+      const double c = (double)(full / np) * (kb + 14.0) + (double)((rem * sp + np - 1) / np) * (kb / sp + 14.0);
+      if (c < best - 1e-9) best = c, best_s = sp;
+    }
+    if (best_s > 1) {
+      a.full_units = (int)full;
+      a.splits = best_s;
+      a.units = (int)(full + rem * best_s);
+    }
+  }
   CUtensorMap ma, mb;
   const long a_rows = d.a_rows > 0 ? d.a_rows : d.M;
   const long b_rows = d.b_rows > 0 ? d.b_rows : d.N;
@@ -699,7 +743,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   if (d.b_mn ? make_map(&mb, d.B, d.K, d.N, d.ldb, 64) != 0
              : make_map(&mb, d.B, b_rows, d.K, d.ldb, BN / 2) != 0)
     return cudaErrorInvalidValue;
-  const long work = (long)a.num_m * a.num_n;
+  const long work = a.units;
   const int pairs = (int)std::min<long>(work, kNumSMs / 2);
   static bool attr_set = false;
   if (!attr_set) {
@@ -808,6 +852,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   if (d.epi == EPI_BF16) splits = 1;
   splits = std::max(1, std::min(splits, a.kb_total));
   a.splits = splits;
+  a.units = (int)((long)a.num_m * a.num_n * splits);
   if (d.epi == EPI_F32 && splits > 1) {
     cudaError_t e = cudaMemset2DAsync(d.C, d.ldc * sizeof(float), 0, d.N * sizeof(float), d.M, st);
     if (e != cudaSuccess) return e;

@@ -43,7 +43,8 @@ def test_gemm_bf16_out(cuda, M, N, K, bn):
 @pytest.mark.parametrize("M,N,K,splits", [(128, 256, 1024, 1), (64, 4096, 4096, 0), (256, 512, 2048, 4),
                                           (16, 4096, 14400, 0), (2048, 4096, 4096, 0),
                                           (1500, 4104, 512, 0), (64, 4096, 14400, 0),
-                                          (33, 4096, 4096, 0)])
+                                          (33, 4096, 4096, 0),
+                                          (1728, 4096, 14400, 0)])  # CTA pair, tail wave split
 def test_gemm_f32_add_splitk(cuda, M, N, K, splits):
     g = torch.Generator(device="cuda").manual_seed(3)
     A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
@@ -90,6 +91,7 @@ def _gemm_mn(A, Bkn, C, epi, bn=0, splits=0):
     (3000, 4096, 1024, 0, 0, 0),          # CTA pair
     (8192, 4096, 28672 // 8, 1, 0, 0),    # dX of gate|up at a full window (K scaled down)
     (640, 4096, 4096, 2, 0, 0),           # mid-M split-K fp32 add
+    (1728, 4096, 7168, 2, 0, 0),          # CTA pair, last partial wave split along K
     (64, 6144, 4096, 0, 0, 0), (17, 4096, 4096, 1, 0, 0),   # small M (half-height A)
     (200, 136, 256, 1, 0, 2),             # N tail, forced split
 ])
