@@ -349,11 +349,15 @@ __global__ void __launch_bounds__(384, 1)
           pp[cc >> 1] = pack_bf16(pv.x, pv.y);
           pd[cc >> 1] = pack_bf16(ds.x, ds.y);
         }
-        if (p.ds_out && key < p.ds_ld) {  // dS^T row of this key, tile-major [kvh][tile][key][64]
-          uint4* dst = reinterpret_cast<uint4*>(
-              p.ds_out + (((long)kvh * p.ds_heads + qt) * p.ds_ld + key) * QB + h * 32);
+        if (p.ds_out && key < p.ds_ld) {
+          // dS^T of this key, [kvh][tile][8-row chunk][key][8 rows]: for each chunk the warp's
+          // 32 keys store 512 contiguous bytes (one coalesced store instruction), and the dQ
+          // GEMM loads the chunks as no-swizzle MN-major core matrices
+          bf16* dst = p.ds_out + ((((long)kvh * p.ds_heads + qt) * (QB / 8) + h * 4) * p.ds_ld + key) * 8;
 #pragma unroll
-          for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pd[4 * v], pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
+          for (int v = 0; v < 4; ++v)
+            *reinterpret_cast<uint4*>(dst + (long)v * p.ds_ld * 8) =
+                make_uint4(pd[4 * v], pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
         }
         tst_x16(tmem + lane_base + b * QB + h * 16, pp);
         tst_x16(tmem + lane_base + 128 + b * QB + h * 16, pd);

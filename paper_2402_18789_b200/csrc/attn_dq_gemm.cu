@@ -1,10 +1,10 @@
 // attn_dq_gemm.cu -- dQ of a token-level backward window as a masked GEMM over the dS the
 // dK/dV kernel already computed (CS_BWD_DSQ=1): dQ[p, h, :] = scale * sum_k dS[p, h, k] K[k, :]
 // (tiny_model.hpp:294-315, Alg. 2 line 19).  The dK/dV kernel holds dS^T in TMEM for
-// its own dK product; it also stores it (bf16) tile-major -- [kv head][64-row query tile][key]
-// [64 packed rows], each thread one 128-byte key row -- and this kernel streams it back as an
-// MN-major A operand (two 64-row tiles per 128-row dQ tile, {64 rows, 64 keys} TMA boxes)
-// against the paged K tile as an MN-major B operand.  It
+// its own dK product; it also stores it (bf16) as [kv head][64-row query tile][8-row chunk]
+// [key][8 rows] -- a warp's 32 keys write 512 contiguous bytes per chunk -- and this kernel
+// streams it back as a no-swizzle MN-major A operand (two 64-row tiles per 128-row dQ tile,
+// {8 rows, 64 keys, 8 chunks} TMA boxes) against the paged K tile as an MN-major B operand.  It
 // replaces the dQ kernel that recomputed S and dP and was bounded by reading both back out of
 // TMEM (128 KB per 128x128 tile at 64 B/clk).
 //   warp 0: TMA producer (A: 3-D dS box, B: paged K rows, contiguous pages in one 64-row box)
@@ -22,6 +22,12 @@ constexpr int DQG_A = 128 * 128;      // 64 keys x 128 packed rows x bf16 (two 6
 constexpr int DQG_B = 64 * 128 * 2;   // 64 keys x 128 dims x bf16 (two 64-dim chunks, 8 KB apart)
 constexpr int DQG_STAGE = DQG_A + DQG_B;
 constexpr int DQG_SMEM = DQG_STAGES * DQG_STAGE + 1024 + 256;
+// no-swizzle MN-major A (dS^T): core matrices of 8 keys x 8 rows; K-adjacent ones 128 B apart,
+// MN-adjacent ones (next 8 rows) 1 KB apart
+// (LBO = the K-direction stride, SBO = the MN-direction stride for no-swizzle MN-major
+// operands -- the opposite of the SW128 MN-major convention; the swapped assignment fails the
+// dS-GEMM parity test)
+constexpr uint32_t kDsLbo = 128, kDsSbo = 1024;
 }  // namespace
 
 __global__ void __launch_bounds__(256, 1)
@@ -66,9 +72,11 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive_expect_tx(&full[s], DQG_A + DQG_B);
       uint8_t* sa = smem + s * DQG_STAGE;
       uint8_t* sb = sa + DQG_A;
-      for (int m = 0; m < 2; ++m)  // the dQ tile's two 64-row dK/dV tiles, 64 keys each
-        tma_load_2d(&tmDS, &full[s], sa + m * 8192, 0,
-                    (int)(((long)kvh * p.ds_heads + 2 * blockIdx.x + m) * p.ds_ld + kb * 64));
+      // the dQ tile's two 64-row dK/dV tiles: {8 rows, 64 keys, 8 chunks} boxes, 8 KB each,
+      // land as [16 chunks][64 keys][8 rows] -- uniform core-matrix strides over both
+      for (int m = 0; m < 2; ++m)
+        tma_load_3d(&tmDS, &full[s], sa + m * 8192, 0, kb * 64,
+                    (int)(((long)kvh * p.ds_heads + 2 * blockIdx.x + m) * 8));
       // K rows [kb*64, kb*64+64) of the sequence: one 64-row box per 64-dim half when the four
       // 16-key pages are consecutive in the pool, else one 16-row box per page
       const int k0 = kb * 64, P = p.page_size;
@@ -97,8 +105,8 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * DQG_STAGE), sb = sa + DQG_A;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        mma_bf16(tmem, umma_desc_sw128_mn(sa + k * 2048, 8192, 1024),
+      for (int k = 0; k < 4; ++k)  // A: 16 keys = two 128-byte core matrices along K
+        mma_bf16(tmem, umma_desc_plain(sa + k * 256, kDsLbo, kDsSbo),
                  umma_desc_sw128_mn(sb + k * 2048, 8192, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
       mma_commit(&empty[s]);
     }

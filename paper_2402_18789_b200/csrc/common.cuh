@@ -160,6 +160,18 @@ CS_DEV uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sb
   return d;
 }
 
+// SMEM descriptor, no swizzle (canonical core matrices of 8 rows x 16 bytes, 128 contiguous
+// bytes each): lbo / sbo are the byte strides between core matrices (see the caller for which
+// dimension each one steps)
+CS_DEV uint64_t umma_desc_plain(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
 // Instruction descriptor with explicit operand majors (0 = K-major, 1 = MN-major).
 __host__ __device__ constexpr uint32_t idesc_bf16_f32_major(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

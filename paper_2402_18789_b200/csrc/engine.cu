@@ -375,8 +375,11 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
   e->down_rows = e->h + (e->bwd_mn ? 64 : 0);
-  if (const char* v = std::getenv("CS_BWD_DSQ"))
-    e->bwd_dsq = std::atoi(v) != 0 && c.head_dim == 128 && 64 % (c.n_heads / c.n_kv_heads) == 0;
+  {  // dQ as a GEMM over the dS^T the dK/dV kernel exports (default; CS_BWD_DSQ=0: the
+     // recomputing dQ kernel) -- d = 128 and GQA groups dividing the 64-row dK/dV query tile
+    const char* v = std::getenv("CS_BWD_DSQ");
+    e->bwd_dsq = (!v || std::atoi(v) != 0) && c.head_dim == 128 && 64 % (c.n_heads / c.n_kv_heads) == 0;
+  }
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -1549,9 +1552,10 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     bp.scale_log2 = bp.scale * 1.4426950408889634f;
     cs_engine::ProfRec bpr{};
     if (e->profiling) {
-      // QK^T recompute twice (dq, dkdv kernels), dP twice, dV, dK, dQ: 7 x 2*d per (q,k,head)
+      // algorithmic work (2.5x the forward): S = QK^T recompute, dP, dV, dK,
+      // dQ -- 5 x 2*d per (q, k, head); the recomputing dQ kernel (CS_BWD_DSQ=0) does 7
       const double pairs = (double)s * ((double)a + (s + 1) / 2.0);
-      bpr.flops = 7.0 * 2.0 * e->d * e->Hq * pairs;
+      bpr.flops = 5.0 * 2.0 * e->d * e->Hq * pairs;
       bpr.bytes = 0;
       bpr.kind = 2;
       prof_begin(e, bpr);
@@ -1581,7 +1585,9 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
         bp.ds_out = e->ds_buf;
         bp.ds_ld = keys;
         bp.ds_heads = (int)ntiles;
-        if (cs::make_map(&mds, e->ds_buf, (long)e->Hkv * ntiles * keys, 64, 64, 64) != 0 ||
+        // dS^T as [kv head][tile][8-row chunk][key][8 rows] (attn_dq_gemm.cu)
+        if (cs::make_map_3d_plain(&mds, e->ds_buf, 8, keys, (long)e->Hkv * ntiles * 8, 16, keys * 16, 8, 64,
+                                  8) != 0 ||
             cs::make_map(&mk64, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 64) != 0)
           return cs::set_error(CS_ERR_CUDA, "attention backward: dS TMA map creation failed");
         CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));

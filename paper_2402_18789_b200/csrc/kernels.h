@@ -76,6 +76,8 @@ int make_map(CUtensorMap* out, const void* ptr, long rows, long cols, long ld, i
 // 3D bf16 map {d0 (contiguous), d1, d2}, SWIZZLE_128B, box {64, box1, box2}
 int make_map_3d(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
                 long stride2_bytes, int box1, int box2);
+int make_map_3d_plain(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
+                      long stride2_bytes, int box0, int box1, int box2);
 int gemm_pick_bn(long M, long N);
 
 }  // namespace cs
