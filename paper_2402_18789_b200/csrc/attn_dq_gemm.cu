@@ -17,7 +17,7 @@
 namespace cs {
 
 namespace {
-constexpr int DQG_STAGES = 6;
+constexpr int DQG_STAGES = 7;
 constexpr int DQG_A = 128 * 128;      // 64 keys x 128 packed rows x bf16 (two 64-row chunks)
 constexpr int DQG_B = 64 * 128 * 2;   // 64 keys x 128 dims x bf16 (two 64-dim chunks, 8 KB apart)
 constexpr int DQG_STAGE = DQG_A + DQG_B;
@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int grp = p.grp;
   const int rpt = 128 / grp;  // positions per tile (rpt * grp <= 128 packed rows)
-  const int q0 = blockIdx.x * rpt;
+  // longest tiles first (causal: a tile's key range grows with its position), so the last wave
+  // holds the short ones
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int q0 = qt * rpt;
   const int kvh = blockIdx.y;
   const int nq = min(rpt, p.b - p.a - q0);
   const int last_key = p.a + q0 + nq - 1;  // causal: keys [0, last position of the tile]
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(256, 1)
       // land as [16 chunks][64 keys][8 rows] -- uniform core-matrix strides over both
       for (int m = 0; m < 2; ++m)
         tma_load_3d(&tmDS, &full[s], sa + m * 8192, 0, kb * 64,
-                    (int)(((long)kvh * p.ds_heads + 2 * blockIdx.x + m) * 8));
+                    (int)(((long)kvh * p.ds_heads + 2 * qt + m) * 8));
       // K rows [kb*64, kb*64+64) of the sequence: one 64-row box per 64-dim half when the four
       // 16-key pages are consecutive in the pool, else one 16-row box per page
       const int k0 = kb * 64, P = p.page_size;
