@@ -17,8 +17,12 @@
 namespace cs {
 
 namespace {
-constexpr int DQG_STAGES = 7;
-constexpr int DQG_A = 128 * 128;      // 64 keys x 128 packed rows x bf16 (two 64-row chunks)
+// two 128-row dQ tiles per CTA share every K stage (M = 256 in two TMEM accumulators): half the
+// K-tile traffic and half the CTAs of one tile per CTA
+constexpr int DQG_TPC = 2;
+constexpr int DQG_STAGES = 4;
+constexpr int DQG_A1 = 128 * 128;     // one dQ tile: 64 keys x 128 packed rows x bf16 (two 8 KB boxes)
+constexpr int DQG_A = DQG_TPC * DQG_A1;
 constexpr int DQG_B = 64 * 128 * 2;   // 64 keys x 128 dims x bf16 (two 64-dim chunks, 8 KB apart)
 constexpr int DQG_STAGE = DQG_A + DQG_B;
 constexpr int DQG_SMEM = DQG_STAGES * DQG_STAGE + 1024 + 256;
@@ -43,14 +47,19 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int grp = p.grp;
   const int rpt = 128 / grp;  // positions per tile (rpt * grp <= 128 packed rows)
+  const int rows = p.b - p.a;
   // longest tiles first (causal: a tile's key range grows with its position), so the last wave
   // holds the short ones
-  const int qt = gridDim.x - 1 - blockIdx.x;
-  const int q0 = qt * rpt;
+  const int qt0 = (gridDim.x - 1 - blockIdx.x) * DQG_TPC;
   const int kvh = blockIdx.y;
-  const int nq = min(rpt, p.b - p.a - q0);
-  const int last_key = p.a + q0 + nq - 1;  // causal: keys [0, last position of the tile]
-  const int nkb = (last_key + 64) / 64;
+  int nq[DQG_TPC], nkb[DQG_TPC];
+  int nkb_max = 0;
+#pragma unroll
+  for (int t = 0; t < DQG_TPC; ++t) {
+    nq[t] = min(rpt, rows - (qt0 + t) * rpt);  // <= 0: no such tile (the window's end)
+    nkb[t] = nq[t] > 0 ? (p.a + (qt0 + t) * rpt + nq[t] - 1 + 64) / 64 : 0;  // causal key blocks
+    nkb_max = max(nkb_max, nkb[t]);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmDS);
@@ -63,23 +72,30 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 128);
+  if (warp == 2) tmem_alloc(tmem_slot, 128 * DQG_TPC);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp == 0 && lane == 0) {
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < nkb_max; ++kb) {
       const int s = kb % DQG_STAGES;
       mbar_wait(&empty[s], ((kb / DQG_STAGES) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], DQG_A + DQG_B);
+      int act = 0;
+#pragma unroll
+      for (int t = 0; t < DQG_TPC; ++t) act += kb < nkb[t];
+      mbar_arrive_expect_tx(&full[s], act * DQG_A1 + DQG_B);
       uint8_t* sa = smem + s * DQG_STAGE;
       uint8_t* sb = sa + DQG_A;
-      // the dQ tile's two 64-row dK/dV tiles: {8 rows, 64 keys, 8 chunks} boxes, 8 KB each,
-      // land as [16 chunks][64 keys][8 rows] -- uniform core-matrix strides over both
-      for (int m = 0; m < 2; ++m)
-        tma_load_3d(&tmDS, &full[s], sa + m * 8192, 0, kb * 64,
-                    (int)(((long)kvh * p.ds_heads + 2 * qt + m) * 8));
+      // each dQ tile's two 64-row dK/dV tiles: {8 rows, 64 keys, 8 chunks} boxes, 8 KB each,
+      // land as [16 chunks][64 keys][8 rows] -- uniform core-matrix strides over both.  A tile
+      // past its causal key range is not loaded (its dS there was never written)
+#pragma unroll
+      for (int t = 0; t < DQG_TPC; ++t)
+        if (kb < nkb[t])
+          for (int m = 0; m < 2; ++m)
+            tma_load_3d(&tmDS, &full[s], sa + t * DQG_A1 + m * 8192, 0, kb * 64,
+                        (int)(((long)kvh * p.ds_heads + 2 * (qt0 + t) + m) * 8));
       // K rows [kb*64, kb*64+64) of the sequence: one 64-row box per 64-dim half when the four
       // 16-key pages are consecutive in the pool, else one 16-row box per page
       const int k0 = kb * 64, P = p.page_size;
@@ -102,15 +118,19 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = idesc_bf16_f32_major(128, 128, 1, 1);  // A and B MN-major
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < nkb_max; ++kb) {
       const int s = kb % DQG_STAGES;
       mbar_wait(&full[s], (kb / DQG_STAGES) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * DQG_STAGE), sb = sa + DQG_A;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)  // A: 16 keys = two 128-byte core matrices along K
-        mma_bf16(tmem, umma_desc_plain(sa + k * 256, kDsLbo, kDsSbo),
-                 umma_desc_sw128_mn(sb + k * 2048, 8192, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+      for (int t = 0; t < DQG_TPC; ++t) {
+        if (kb >= nkb[t]) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // A: 16 keys = two 128-byte core matrices along K
+          mma_bf16(tmem + t * 128, umma_desc_plain(sa + t * DQG_A1 + k * 256, kDsLbo, kDsSbo),
+                   umma_desc_sw128_mn(sb + k * 2048, 8192, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+      }
       mma_commit(&empty[s]);
     }
     mma_commit(acc_full);
@@ -118,22 +138,26 @@ __global__ void __launch_bounds__(256, 1)
     const int ew = warp - 4;
     const int r = ew * 32 + lane;  // packed row = TMEM lane
     const int qr = r / grp, g = r - qr * grp;
-    const bool valid = qr < nq && r < rpt * grp;
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16);
-    float* dst = p.dq + (long)(q0 + (valid ? qr : 0)) * p.dq_ld + (long)(kvh * grp + g) * 128;
 #pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tb + c0, v);
-      tmem_ld_wait();
-      if (valid) {
+    for (int t = 0; t < DQG_TPC; ++t) {
+      const bool valid = qr < nq[t] && r < rpt * grp;
+      const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + t * 128;
+      float* dst = p.dq + (long)((qt0 + t) * rpt + (valid ? qr : 0)) * p.dq_ld + (long)(kvh * grp + g) * 128;
+      if (nq[t] <= 0) continue;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tb + c0, v);
+        tmem_ld_wait();
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + c0 + i) =
-              make_float4(__uint_as_float(v[i]) * p.scale, __uint_as_float(v[i + 1]) * p.scale,
-                          __uint_as_float(v[i + 2]) * p.scale, __uint_as_float(v[i + 3]) * p.scale);
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c0 + i) =
+                make_float4(__uint_as_float(v[i]) * p.scale, __uint_as_float(v[i + 1]) * p.scale,
+                            __uint_as_float(v[i + 2]) * p.scale, __uint_as_float(v[i + 3]) * p.scale);
+        }
       }
     }
     tc_fence_before();
@@ -141,7 +165,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, 128 * DQG_TPC);
   }
 }
 
@@ -154,7 +178,8 @@ cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const 
                       true);
   (void)once;
   const int rpt = 128 / p.grp;
-  dim3 grid((rows + rpt - 1) / rpt, n_heads / p.grp);
+  const int tiles = (rows + rpt - 1) / rpt;
+  dim3 grid((tiles + DQG_TPC - 1) / DQG_TPC, n_heads / p.grp);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return launch_pdl(attn_dq_gemm_kernel, grid, dim3(256), DQG_SMEM, st, tmDS, tmK16, tmK64, p, n_heads);
 }
