@@ -62,7 +62,7 @@ def main():
     torch.cuda.nvtx.range_push("coserve")
     st, log = coserve_run(eng, c)
     torch.cuda.nvtx.range_pop()
-    print({k: st[k] for k in ("ft_fwd_tokens", "ft_bwd_tokens", "gpu_launches")})
+    print({k: st[k] for k in ("ft_fwd_tokens", "ft_bwd_tokens", "gpu_launches", "timed_ms", "timed_device_ms")})
 
 
 if __name__ == "__main__":
