@@ -708,9 +708,9 @@ void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, 
                    int a, int rows, int n_heads, int n_kv_heads, int head_dim, int use_rope,
                    float theta, bf16* out, long ldo, cudaStream_t st) {
   (void)theta;
-  if (rows > 0)
-    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    launch_pdl(rope_bwd_pack_kernel, dim3(rows), dim3(128), 0, st, dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
+  if (rows <= 0) return;
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_pdl(rope_bwd_pack_kernel, dim3(rows), dim3(128), 0, st, dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
                                                head_dim, use_rope, s_rope_tab, out, ldo);
 }
 
