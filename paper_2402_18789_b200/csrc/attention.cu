@@ -288,23 +288,33 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnFwdParams p) {
   }
 }
 
+// delta[r, h] = sum_d dO[r, h, d] * O[r, h, d]: an 8-lane group per (row, head) pair, 16-byte
+// loads (8 bf16) per lane, 3-shuffle group reduction
 __global__ void attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ dO, long do_ld,
                                       const __nv_bfloat16* __restrict__ O, long o_ld, int rows,
                                       int heads, int D, float* __restrict__ delta) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows * heads) return;
-  const int r = warp / heads, h = warp % heads;
+  const long pair = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool ok = pair < (long)rows * heads;  // (no early exit: the group shuffles use all lanes)
+  const int r = ok ? (int)(pair / heads) : 0, h = ok ? (int)(pair % heads) : 0;
   const __nv_bfloat16* a = dO + (long)r * do_ld + (long)h * D;
   const __nv_bfloat16* b = O + (long)r * o_ld + (long)h * D;
   float acc = 0.f;
-  for (int d = lane * 2; d < D; d += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + d));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + d));
-    acc += x.x * y.x + x.y * y.y;
+  for (int d = sub * 8; ok && d < D; d += 64) {
+    const uint4 x = *reinterpret_cast<const uint4*>(a + d);
+    const uint4 y = *reinterpret_cast<const uint4*>(b + d);
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 u = __bfloat1622float2(x2[q]), v = __bfloat1622float2(y2[q]);
+      acc += u.x * v.x + u.y * v.y;
+    }
   }
-  acc = warp_sum(acc);
-  if (lane == 0) delta[(long)r * heads + h] = acc;
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (ok && sub == 0) delta[(long)r * heads + h] = acc;
 }
 
 // dQ for query tiles of the window: CTA = (64 packed rows, kv head); loop over key tiles [0, b)
@@ -703,18 +713,18 @@ cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cu
 }
 
 void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st) {
-  const int warps = rows * n_heads;
-  attn_bwd_delta_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(p.dO, p.do_ld, p.O, p.o_ld, rows,
-                                                                n_heads, p.q_ld / n_heads, p.delta);
+  const long threads = (long)rows * n_heads * 8;  // 8 lanes per (row, head)
+  attn_bwd_delta_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(p.dO, p.do_ld, p.O, p.o_ld, rows,
+                                                                     n_heads, p.q_ld / n_heads, p.delta);
 }
 
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st) {
   const int rows = p.b - p.a;
   if (rows <= 0) return cudaSuccess;
   {
-    const int warps = rows * n_heads;
+    const long threads = (long)rows * n_heads * 8;  // 8 lanes per (row, head)
     cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    attn_bwd_delta_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(
+    attn_bwd_delta_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(
         p.dO, p.do_ld, p.O, p.o_ld, rows, n_heads, head_dim, p.delta);
   }
   const int rows_per_tile = 64 / p.grp;
