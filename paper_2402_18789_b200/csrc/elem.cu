@@ -683,26 +683,37 @@ __global__ void rope_bwd_pack_kernel(const float* __restrict__ dq, long ldq,
   const int half = d / 2;
   const int q_dim = n_heads * d, kv_dim = n_kv * d;
   bf16* o = out + (long)i * ldo;
-  const int nqp = n_heads * half, nkp = n_kv * half;
+  // 4 consecutive rotation pairs per thread (d / 2 is a multiple of 4): 16-byte loads of both
+  // halves and of the table, 8-byte bf16 stores
+  const int nqp = n_heads * half / 4, nkp = n_kv * half / 4;
   for (int t = threadIdx.x; t < nqp + nkp; t += blockDim.x) {
     const bool isq = t < nqp;
-    const int tt = isq ? t : t - nqp;
+    const int tt = (isq ? t : t - nqp) * 4;
     const int hd = tt / half, j = tt % half;
     const float* src = isq ? dq + (long)i * ldq + hd * d : dk + (long)pos * ld_acc + hd * d;
-    float y1 = src[j], y2 = src[j + half];
+    const float4 a1 = *reinterpret_cast<const float4*>(src + j);
+    const float4 a2 = *reinterpret_cast<const float4*>(src + j + half);
+    float y1[4] = {a1.x, a1.y, a1.z, a1.w}, y2[4] = {a2.x, a2.y, a2.z, a2.w};
     if (use_rope) {
-      const float2 cs = tab[(long)pos * half + j];
-      const float x1 = y1 * cs.x + y2 * cs.y;
-      const float x2 = y2 * cs.x - y1 * cs.y;
-      y1 = x1;
-      y2 = x2;
+      const float4* tp = reinterpret_cast<const float4*>(tab + (long)pos * half + j);
+      const float4 c01 = tp[0], c23 = tp[1];
+      const float cx[4] = {c01.x, c01.z, c23.x, c23.z}, cy[4] = {c01.y, c01.w, c23.y, c23.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float x1 = y1[q] * cx[q] + y2[q] * cy[q];
+        const float x2 = y2[q] * cx[q] - y1[q] * cy[q];
+        y1[q] = x1;
+        y2[q] = x2;
+      }
     }
     bf16* dst = o + (isq ? 0 : q_dim) + hd * d;
-    dst[j] = __float2bfloat16(y1);
-    dst[j + half] = __float2bfloat16(y2);
+    *reinterpret_cast<uint2*>(dst + j) = make_uint2(pack_bf16(y1[0], y1[1]), pack_bf16(y1[2], y1[3]));
+    *reinterpret_cast<uint2*>(dst + j + half) = make_uint2(pack_bf16(y2[0], y2[1]), pack_bf16(y2[2], y2[3]));
   }
-  for (int c = threadIdx.x; c < kv_dim; c += blockDim.x)
-    o[q_dim + kv_dim + c] = __float2bfloat16(dv[(long)pos * ld_acc + c]);
+  for (int c = threadIdx.x * 4; c < kv_dim; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(dv + (long)pos * ld_acc + c);
+    *reinterpret_cast<uint2*>(o + q_dim + kv_dim + c) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  }
 }
 void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, long ld_acc,
                    int a, int rows, int n_heads, int n_kv_heads, int head_dim, int use_rope,
@@ -711,7 +722,7 @@ void rope_bwd_pack(const float* dq, long ldq, const float* dk, const float* dv, 
   if (rows <= 0) return;
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   launch_pdl(rope_bwd_pack_kernel, dim3(rows), dim3(128), 0, st, dq, ldq, dk, dv, ld_acc, a, n_heads, n_kv_heads,
-                                               head_dim, use_rope, s_rope_tab, out, ldo);
+             head_dim, use_rope, s_rope_tab, out, ldo);
 }
 
 // ---------------------------------------------------------------- Adam (fp32 master)
