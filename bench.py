@@ -78,9 +78,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rate", type=float, default=20.0)
-    # side rates (other_rates in the JSON line) are opt-in, e.g. --rates 4,10,20: the headline is
-    # the 20 req/s run, and the FT-heavy low-rate runs are where the open stall showed
-    ap.add_argument("--rates", default="20")
+    # side rates (other_rates in the JSON line): the headline is the --rate run
+    ap.add_argument("--rates", default="4,10,20")
     ap.add_argument("--ft-len", type=int, default=8192)
     ap.add_argument("--model", default="llama-3.1-8b", choices=sorted(MODELS))
     ap.add_argument("--tp", type=int, default=1,

@@ -206,34 +206,38 @@ __global__ void __launch_bounds__(256, 1)
     }
     fence_barrier_init();
   }
+  __syncthreads();  // barriers initialised
+  // PDL: barrier init / descriptor prefetch above overlap the previous kernel; the successor
+  // may start its own prologue (it takes TMEM only after its griddepcontrol.wait, i.e. after
+  // this grid has completed)
+  griddep_launch();
+  // weights do not depend on the previous kernel: the first tile's B stages are in flight
+  // before griddepcontrol.wait (the weight-stream fill overlaps the predecessor's tail)
+  int pre = 0;
+  if (warp == 0 && lane == 0 && args.b_const && (int)blockIdx.x < total) {
+    int mb, nb, kb0, kb1;
+    decode_work(blockIdx.x, args, mb, nb, kb0, kb1);
+    pre = min(Cfg::STAGES, kb1 - kb0);
+    for (int i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
+      load_b<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i, nb * BN,
+                 args.b_mn);
+    }
+  }
+  griddep_wait();
+  // TMEM only after griddepcontrol.wait: TMEM is an SM-wide resource, and a grid that held it
+  // while waiting on an unfinished predecessor could starve that predecessor's not-yet-allocated
+  // CTAs on the same SM (a timing-dependent deadlock)
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // PDL: barrier init / TMEM alloc / descriptor prefetch above overlapped the previous kernel;
-  // all CTAs of this persistent grid are resident, so the successor may start its prologue
-  griddep_launch();
-  if (warp != 0 || lane != 0) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      // weights do not depend on the previous kernel: the first tile's B stages are in flight
-      // before griddepcontrol.wait (the weight-stream fill overlaps the predecessor's tail)
-      int pre = 0;
-      if (args.b_const && (int)blockIdx.x < total) {
-        int mb, nb, kb0, kb1;
-        decode_work(blockIdx.x, args, mb, nb, kb0, kb1);
-        pre = min(Cfg::STAGES, kb1 - kb0);
-        for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full_bar[i], Cfg::STAGE_BYTES);
-          load_b<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i, nb * BN,
-                     args.b_mn);
-        }
-      }
-      griddep_wait();
       bool first = true;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         int mb, nb, kb0, kb1;
@@ -445,34 +449,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     fence_barrier_init();
   }
+  cluster_sync_all();  // barriers initialised in both CTAs (the peer's TMA signals the leader's)
+  griddep_launch();
+  int pre = 0;  // first tile's B (weight) stages issued before griddepcontrol.wait
+  if (warp == 0 && lane == 0 && args.b_const && pair < total) {
+    int mb, nb, kb0, kb1;
+    decode_work(pair, args, mb, nb, kb0, kb1);
+    pre = min(Cfg::STAGES, kb1 - kb0);
+    for (int i = 0; i < pre; ++i) {
+      if (leader) mbar_arrive_expect_tx(&full_bar[i], 2 * Cfg::STAGE_BYTES);
+      load_b_2sm<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i,
+                     nb * BN + (int)rank * (BN / 2), args.b_mn);
+    }
+  }
+  griddep_wait();
+  // TMEM only after griddepcontrol.wait (see gemm_tn_kernel)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"((uint32_t)Cfg::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  cluster_sync_all();  // TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_launch();
-  if (warp != 0 || lane != 0) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int pre = 0;  // first tile's B (weight) stages issued before griddepcontrol.wait
-      if (args.b_const && pair < total) {
-        int mb, nb, kb0, kb1;
-        decode_work(pair, args, mb, nb, kb0, kb1);
-        pre = min(Cfg::STAGES, kb1 - kb0);
-        for (int i = 0; i < pre; ++i) {
-          if (leader) mbar_arrive_expect_tx(&full_bar[i], 2 * Cfg::STAGE_BYTES);
-          load_b_2sm<BN>(&tmB, &full_bar[i], smem + i * Cfg::STAGE_BYTES + Cfg::A_BYTES, kb0 + i,
-                         nb * BN + (int)rank * (BN / 2), args.b_mn);
-        }
-      }
-      griddep_wait();
       bool first = true;
       for (int w = pair; w < total; w += n_pairs) {
         int mb, nb, kb0, kb1;
