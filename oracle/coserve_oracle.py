@@ -18,6 +18,15 @@ arch.norm == 'none', arch.act == 'relu', no RoPE, Hkv == Hq and no bias the
 general code path reduces to the reference's exact op sequence, which the tests
 pin against the reference itself (oracle/_ref) and SURVEY.md Appendix A.
 
+bf16 rounding-point emulation (emu=True on forward_full / backward_full / forward_window /
+backward_window): the same op sequence with every value rounded to bf16 where the GPU path
+stores or feeds bf16 -- frozen weights and the LoRA A/B copies as GEMM operands, normed
+activations, Q/K/V (after RoPE), P and dS inside attention, attention output, gate/up and the
+MLP activation, bf16(u) in the K-concatenated down GEMM, dlogits, dY / dU / dm / dgu / dr1 / dO /
+dqkv in the backward -- and fp32-like accumulation everywhere else (f64 here).  It isolates
+the GPU's kernel arithmetic from the bf16 storage floor: tests gate the GPU against it at
+rel <= 1e-2 (north_star) and report the f64 comparison as the floor.
+
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import this.
 """
 from __future__ import annotations
@@ -32,6 +41,19 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _RNG_LIB = None
+
+
+def bf16(x):
+    """Round to bf16 (round-to-nearest-even on the fp32 bit pattern, as __float2bfloat16_rn)
+    and return float64 -- the GPU's bf16 storage points in the emu oracle."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _rd(emu):
+    return bf16 if emu else (lambda v: v)
 
 
 def _rng_lib():
@@ -272,6 +294,7 @@ class LayerSaved:
     lu: np.ndarray   # LoRA u = m @ A
     rstd1: np.ndarray
     rstd2: np.ndarray
+    o: Optional[np.ndarray] = None  # attention output (emu: the bf16 O the GPU saves for Delta)
 
 
 class QkvCache:
@@ -291,7 +314,8 @@ class QkvCache:
                                  up=np.zeros((max_len, arch.ffn)),
                                  m=np.zeros((max_len, arch.ffn)),
                                  lu=np.zeros((max_len, arch.lora_rank)),
-                                 rstd1=np.zeros((max_len, 1)), rstd2=np.zeros((max_len, 1)))
+                                 rstd1=np.zeros((max_len, 1)), rstd2=np.zeros((max_len, 1)),
+                                 o=np.zeros((max_len, arch.q_dim)))
                       for _ in range(n)]
         del z
 
@@ -316,9 +340,10 @@ class OrderingViolation(RuntimeError):
 # Forward over a window of rows (attention_rows generalised; tiny_model.hpp:118-151)
 # ---------------------------------------------------------------------------
 
-def _attention_rows(arch: Arch, q, K, V, row_begin):
+def _attention_rows(arch: Arch, q, K, V, row_begin, emu: bool = False):
     """q: [s, Hq*d] rows at positions row_begin.., K/V: [row_begin+s, Hkv*d].
-    Returns out [s, Hq*d] and lse [s, Hq] (the GPU saves LSE instead of probs)."""
+    Returns out [s, Hq*d] and lse [s, Hq] (the GPU saves LSE instead of probs).
+    emu: unnormalised P rounded to bf16 for the PV product, fp32-style row sum, bf16 output."""
     s = q.shape[0]
     d, Hq, Hkv = arch.head_dim, arch.n_heads, arch.n_kv_heads
     grp = Hq // Hkv
@@ -337,16 +362,21 @@ def _attention_rows(arch: Arch, q, K, V, row_begin):
         mx = sc.max(axis=1, keepdims=True)
         p = np.exp(sc - mx)
         den = p.sum(axis=1, keepdims=True)
-        p /= den
-        out[:, hq * d:(hq + 1) * d] = p @ vh
+        if emu:
+            out[:, hq * d:(hq + 1) * d] = (bf16(p) @ vh) / den
+        else:
+            p /= den
+            out[:, hq * d:(hq + 1) * d] = p @ vh
         lse[:, hq] = (mx + np.log(den))[:, 0]
-    return out, lse
+    return (bf16(out) if emu else out), lse
 
 
 def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool = True,
-                   ar=None):
+                   ar=None, emu: bool = False):
     """ar: tensor-parallel all-reduce of the row-parallel partial sums (oracle/tp_oracle.py);
-    None = one rank, reference op order."""
+    None = one rank, reference op order.  emu: bf16 rounding points of the GPU path."""
+    if emu:
+        return _layer_forward_emu(arch, w, x, pos0, sv, lora)
     s = x.shape[0]
     rows = slice(pos0, pos0 + s)
     positions = np.arange(pos0, pos0 + s)
@@ -400,11 +430,64 @@ def _layer_forward(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool
     return y
 
 
-def _head(arch: Arch, W: Dict, x):
+def _layer_forward_emu(arch: Arch, w: Dict, x, pos0: int, sv: LayerSaved, lora: bool):
+    """_layer_forward with the GPU path's bf16 storage points (engine.cu:forward): residual x
+    fp32, GEMM operands bf16, fp32 accumulation; QKV (+bias) rounded in the GEMM epilogue,
+    RoPE applied to the bf16 values and rounded again (rope_append_kernel)."""
+    s = x.shape[0]
+    rows = slice(pos0, pos0 + s)
+    positions = np.arange(pos0, pos0 + s)
+    sv.x_in[rows] = x
+    if arch.norm == "rms":
+        h1, r = rms_fwd(x, w["g1"], arch.rms_eps)
+        sv.rstd1[rows] = r
+    else:
+        h1 = x
+    h1 = bf16(h1)
+    q, k, v = h1 @ bf16(w["wq"]), h1 @ bf16(w["wk"]), h1 @ bf16(w["wv"])
+    if arch.qkv_bias:
+        q, k, v = q + w["bq"], k + w["bk"], v + w["bv"]
+    q, k, v = bf16(q), bf16(k), bf16(v)
+    if arch.rope:
+        q = bf16(rope_apply(q, positions, arch.n_heads, arch.head_dim, arch.rope_theta))
+        k = bf16(rope_apply(k, positions, arch.n_kv_heads, arch.head_dim, arch.rope_theta))
+    sv.q[rows], sv.k[rows], sv.v[rows] = q, k, v
+    attn, _ = _attention_rows(arch, q, sv.k, sv.v, pos0, emu=True)
+    sv.o[rows] = attn
+    r1 = x + attn @ bf16(w["wo"])
+    sv.r1[rows] = r1
+    if arch.norm == "rms":
+        h2, r = rms_fwd(r1, w["g2"], arch.rms_eps)
+        sv.rstd2[rows] = r
+    else:
+        h2 = r1
+    h2 = bf16(h2)
+    if arch.act == "relu":
+        up = bf16(h2 @ bf16(w["w_up"]))
+        m = np.where(up > 0.0, up, 0.0)
+        sv.pre[rows] = up
+    else:
+        g = bf16(h2 @ bf16(w["w_gate"]))
+        u = bf16(h2 @ bf16(w["w_up"]))
+        m = bf16(silu(g) * u)
+        sv.pre[rows], sv.up[rows] = g, u
+    sv.m[rows] = m
+    y = r1 + m @ bf16(w["w_down"])
+    if lora:
+        lu = m @ bf16(w["lora_a"])           # fp32 u (saved for dB)
+        sv.lu[rows] = lu
+        y = y + bf16(lu) @ bf16(w["lora_b"])  # [m | bf16(u)] . [W_down ; B]
+    return y
+
+
+def _head(arch: Arch, W: Dict, x, emu: bool = False):
     if arch.norm == "rms":
         hf, rstd = rms_fwd(x, W["gf"], arch.rms_eps)
     else:
         hf, rstd = x, None
+    if emu:
+        hf = bf16(hf)
+        return hf @ bf16(W["unembed"]), hf, rstd
     return hf @ W["unembed"], hf, rstd                        # :215
 
 
@@ -426,7 +509,7 @@ def generative_loss(logits, targets) -> float:
 
 
 def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache,
-                   lora: bool = True, ar=None):
+                   lora: bool = True, ar=None, emu: bool = False):
     """SPEC.md:283-291 / Alg. 2 lines 3-11: positions [l_i, l_i+s) through all layers,
     attending to cached K,V [0, l_i) plus the causal window; appends Q,K,V.
     Returns (logits [s,V], final hidden [s,h])."""
@@ -434,18 +517,20 @@ def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache
         raise CacheDesync(f"cache length {cache.length} != l_i {l_i}")
     toks = np.asarray(tokens_window, dtype=np.int64)
     x = W["embed"][toks].copy()                              # tiny_model.hpp:189-190
+    if emu:
+        x = bf16(x)
     for n in range(arch.n_layers):
-        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora, ar)
+        x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora, ar, emu)
     cache.length = l_i + len(toks)
-    logits, _, _ = _head(arch, W, x)
+    logits, _, _ = _head(arch, W, x, emu)
     return logits, x
 
 
-def head_grad_rows(arch: Arch, W: Dict, final_hidden, targets, L: int):
+def head_grad_rows(arch: Arch, W: Dict, final_hidden, targets, L: int, emu: bool = False):
     """loss_head_grad restricted to window rows (tiny_model.hpp:223-246):
     dlogits = (softmax - onehot)/(L-1) on predicting rows, 0 otherwise; -> dX through the
     (optional) final norm."""
-    logits, hf, rstd = _head(arch, W, final_hidden)
+    logits, hf, rstd = _head(arch, W, final_hidden, emu)
     dlog = np.zeros_like(logits)
     for i in range(logits.shape[0]):
         t = int(targets[i])
@@ -456,7 +541,10 @@ def head_grad_rows(arch: Arch, W: Dict, final_hidden, targets, L: int):
         e = np.exp(row - mx)
         dlog[i] = e / e.sum() / float(L - 1)
         dlog[i, t] -= 1.0 / float(L - 1)
-    dh = dlog @ W["unembed"].T                                # matmul_nt :245
+    if emu:  # ce_kernel writes bf16 dlogits; dH = dlogits . U^T on the bf16 unembedding
+        dh = bf16(dlog) @ bf16(W["unembed"]).T
+    else:
+        dh = dlog @ W["unembed"].T                            # matmul_nt :245
     if arch.norm == "rms":
         dh = rms_bwd(final_hidden, W["gf"], rstd, dh)
     return dh
@@ -464,7 +552,7 @@ def head_grad_rows(arch: Arch, W: Dict, final_hidden, targets, L: int):
 
 def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
                     cache: QkvCache, accum: KvGradAccumulator, grads: Dict,
-                    state: Optional[Dict] = None, ar=None):
+                    state: Optional[Dict] = None, ar=None, emu: bool = False):
     """SPEC.md:292-300 / Alg. 2 lines 14-21 at layer n for rows [l_j - s_j, l_j)
     (Slice interpretation SPEC.md:333).  dY_slice is dLoss/d(layer-n output) for those rows.
     Accumulates this window's dK/dV contributions over [0, l_j) into accum (ΔKVAccum);
@@ -484,6 +572,8 @@ def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
     scale = 1.0 / math.sqrt(float(d))
     rows = slice(a, b)
     dY = np.asarray(dY_slice, dtype=np.float64)
+    if emu:
+        return _backward_window_emu(arch, w, sv, dY, a, b, accum, grads, n)
     # --- MLP + adapter (tiny_model.hpp:276-287)
     grads["b"][n] += sv.lu[rows].T @ dY                       # :280
     d_lu = dY @ w["lora_b"].T                                 # :281
@@ -541,6 +631,73 @@ def backward_window(arch: Arch, W: Dict, n: int, dY_slice, l_j: int, s_j: int,
     return dx, dq, dk_c, dv_c
 
 
+def _backward_window_emu(arch: Arch, w: Dict, sv: LayerSaved, dY, a: int, b: int,
+                         accum: KvGradAccumulator, grads: Dict, n: int):
+    """backward_window with the GPU path's bf16 points (engine.cu:backward_window):
+    dycat = [bf16(dY) | bf16(dY B^T)], dm / dgu / dr1 / dO / dqkv stored bf16, P and dS bf16 as
+    MMA operands inside the attention backward, fp32 dQ / dK / dV accumulation."""
+    d, Hq, Hkv = arch.head_dim, arch.n_heads, arch.n_kv_heads
+    grp = Hq // Hkv
+    scale = 1.0 / math.sqrt(float(d))
+    rows = slice(a, b)
+    s_j = b - a
+    Yb = bf16(dY)
+    grads["b"][n] += sv.lu[rows].T @ dY                       # lora_db: fp32 u, fp32 dY
+    d_lu = Yb @ bf16(w["lora_b"]).T                           # dlu GEMM (fp32 out)
+    if arch.act == "relu":
+        m32 = sv.m[rows]
+    else:
+        m32 = silu(sv.pre[rows]) * sv.up[rows]                # mlp_bwd recomputes m in fp32
+    grads["a"][n] += m32.T @ d_lu
+    d_m = bf16(Yb @ bf16(w["w_down"]).T + bf16(d_lu) @ bf16(w["lora_a"]).T)
+    if arch.act == "relu":
+        d_up = np.where(sv.m[rows] <= 0.0, 0.0, d_m)
+        dh2 = d_up @ bf16(w["w_up"]).T
+    else:
+        g, u = sv.pre[rows], sv.up[rows]
+        d_g = bf16(d_m * u * dsilu(g))
+        d_u = bf16(d_m * silu(g))
+        dh2 = d_g @ bf16(w["w_gate"]).T + d_u @ bf16(w["w_up"]).T
+    if arch.norm == "rms":
+        dh2 = rms_bwd(sv.r1[rows], w["g2"], sv.rstd2[rows], dh2)
+    d_r1 = dY + dh2
+    d_attn = bf16(bf16(d_r1) @ bf16(w["wo"]).T)
+    dq = np.zeros((s_j, Hq * d))
+    dk_c = np.zeros((b, Hkv * d))
+    dv_c = np.zeros((b, Hkv * d))
+    mask = np.arange(b)[None, :] <= np.arange(a, b)[:, None]
+    for hq in range(Hq):
+        hk = hq // grp
+        qh = sv.q[rows, hq * d:(hq + 1) * d]
+        kh = sv.k[:b, hk * d:(hk + 1) * d]
+        vh = sv.v[:b, hk * d:(hk + 1) * d]
+        sc = np.where(mask, (qh @ kh.T) * scale, -np.inf)
+        mx = sc.max(axis=1, keepdims=True)
+        lse = mx + np.log(np.exp(sc - mx).sum(axis=1, keepdims=True))
+        p = np.exp(sc - lse)
+        do = d_attn[:, hq * d:(hq + 1) * d]
+        dp = do @ vh.T
+        delta = np.sum(do * sv.o[rows, hq * d:(hq + 1) * d], axis=1, keepdims=True)
+        dsb = bf16((dp - delta) * p)
+        dq[:, hq * d:(hq + 1) * d] = (dsb @ kh) * scale
+        dk_c[:, hk * d:(hk + 1) * d] += (dsb.T @ qh) * scale
+        dv_c[:, hk * d:(hk + 1) * d] += bf16(p).T @ do
+    accum.dk[n][:b] += dk_c
+    accum.dv[n][:b] += dv_c
+    dk_fin = accum.dk[n][rows]
+    dv_fin = accum.dv[n][rows]
+    positions = np.arange(a, b)
+    dq_pre, dk_pre = dq, dk_fin
+    if arch.rope:
+        dq_pre = rope_apply(dq, positions, Hq, d, arch.rope_theta, inverse=True)
+        dk_pre = rope_apply(dk_fin, positions, Hkv, d, arch.rope_theta, inverse=True)
+    dh1 = bf16(dq_pre) @ bf16(w["wq"]).T + bf16(dk_pre) @ bf16(w["wk"]).T + bf16(dv_fin) @ bf16(w["wv"]).T
+    if arch.norm == "rms":
+        dh1 = rms_bwd(sv.x_in[rows], w["g1"], sv.rstd1[rows], dh1)
+    dx = d_r1 + dh1
+    return dx, dq, dk_c, dv_c
+
+
 def lora_grads_zeros(arch: Arch) -> Dict:
     """LoraGrads::zeros, tiny_model.hpp:75-82."""
     return {"a": [np.zeros((arch.ffn, arch.lora_rank)) for _ in range(arch.n_layers)],
@@ -551,17 +708,17 @@ def lora_grads_zeros(arch: Arch) -> Dict:
 # Full-sequence oracle = a single window (SPEC.md:289,299 degenerate partitions)
 # ---------------------------------------------------------------------------
 
-def forward_full(arch: Arch, W: Dict, tokens, ar=None):
+def forward_full(arch: Arch, W: Dict, tokens, ar=None, emu: bool = False):
     """tiny_model.hpp:181-221."""
     L = len(tokens)
     if L < 1:
         raise ValueError("forward_full: empty sequence")     # :183
     cache = QkvCache(arch, L)
-    logits, final = forward_window(arch, W, tokens, 0, cache, ar=ar)
+    logits, final = forward_window(arch, W, tokens, 0, cache, ar=ar, emu=emu)
     targets = np.concatenate([np.asarray(tokens[1:], dtype=np.int64), [-1]])
     loss = generative_loss(logits, targets) / float(L - 1) if L > 1 else 0.0
     return {"tokens": np.asarray(tokens), "cache": cache, "logits": logits,
-            "final_hidden": final, "loss": loss}
+            "final_hidden": final, "loss": loss, "emu": emu}
 
 
 def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None, ar=None):
@@ -570,7 +727,8 @@ def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None, 
     tokens = tr["tokens"]
     L = len(tokens)
     targets = np.concatenate([tokens[1:], [-1]])
-    dy = head_grad_rows(arch, W, tr["final_hidden"], targets, L) if L > 1 else \
+    emu = tr.get("emu", False)
+    dy = head_grad_rows(arch, W, tr["final_hidden"], targets, L, emu) if L > 1 else \
         np.zeros((L, arch.hidden))
     grads = lora_grads_zeros(arch)
     accum = KvGradAccumulator(arch, L)
@@ -584,7 +742,7 @@ def backward_full(arch: Arch, W: Dict, tr, windows: Optional[List[int]] = None, 
             if s <= 0:
                 break
             dxs, dq, _, _ = backward_window(arch, W, n, dy[lj - s:lj], lj, s, tr["cache"],
-                                            accum, grads, ar=ar)
+                                            accum, grads, ar=ar, emu=emu)
             dx[lj - s:lj] = dxs
             dq_all[lj - s:lj] = dq
             lj -= s

@@ -19,6 +19,43 @@ _PATH = os.path.join(_HERE, "_ref", "libcoserve_ref.so")
 _LIB = None
 
 
+def _cpu_flags() -> set:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def march() -> str:
+    """Highest x86-64 micro-architecture level of the prebuilt reference this host can run."""
+    fl = _cpu_flags()
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= fl and \
+            os.path.exists(_PATH.replace(".so", "_v4.so")):
+        return "x86-64-v4"
+    if {"avx2", "fma", "bmi2"} <= fl and os.path.exists(_PATH.replace(".so", "_v3.so")):
+        return "x86-64-v3"
+    return "x86-64-v2"
+
+
+def path() -> str:
+    lvl = march()
+    return {"x86-64-v4": _PATH.replace(".so", "_v4.so"),
+            "x86-64-v3": _PATH.replace(".so", "_v3.so")}.get(lvl, _PATH)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def available() -> bool:
     return os.path.exists(_PATH)
 
@@ -28,7 +65,7 @@ def lib():
     if _LIB is None:
         if not available():
             raise FileNotFoundError(f"{_PATH} not built (reference tree absent?)")
-        L = ctypes.CDLL(_PATH)
+        L = ctypes.CDLL(path())
         vp, i, l, u64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_long, ctypes.c_uint64, ctypes.c_double
         L.ref_last_error.restype = ctypes.c_char_p
         L.ref_model_init.restype = vp

@@ -37,18 +37,6 @@ CS_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-CS_DEV uint32_t mbar_try_wait(uint32_t bar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(bar), "r"(phase)
-      : "memory");
-  return ok;
-}
-
 CS_DEV uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -56,26 +44,50 @@ CS_DEV uint64_t globaltimer_ns() {
 }
 
 // Bounded wait: no barrier of these kernels legitimately stays unreleased for seconds, so a
-// wait that has spun for CS_MBAR_TIMEOUT_NS reports where it is stuck and traps (the launch
-// fails with an error the host sees) instead of spinning the SM forever.
+// wait that has spun for CS_MBAR_TIMEOUT_NS traps (the launch fails with an error the host
+// sees -- cudaErrorLaunchFailure at the next sync) instead of spinning the SM forever.  All in
+// one PTX block: no call, so the wait adds no register pressure to the hot loops (a printf
+// diagnostic path costs the attention kernels ~1.5 KB of spills; build with -DCS_HANG_DEBUG for it).
 #ifndef CS_MBAR_TIMEOUT_NS
 #define CS_MBAR_TIMEOUT_NS 20000000000ull
 #endif
-static __device__ __noinline__ void mbar_timeout_trap(uint32_t bar, uint32_t phase, int line) {
-  printf("cs: mbarrier wait timed out (common.cuh caller line %d) block (%d,%d) thread %d bar 0x%x phase %u\n",
+#ifdef CS_HANG_DEBUG
+static __device__ __noinline__ void mbar_timeout_report(uint32_t bar, uint32_t phase, int line) {
+  printf("cs: mbarrier wait timed out (caller line %d) block (%d,%d) thread %d bar 0x%x phase %u\n",
          line, (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x, bar, phase);
   __trap();
 }
-
 CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase, int line = __builtin_LINE()) {
   const uint32_t b = smem_u32(bar);
-  if (mbar_try_wait(b, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (!mbar_try_wait(b, phase)) {
-    if ((++n & 0x3FFu) == 0 && globaltimer_ns() - t0 > CS_MBAR_TIMEOUT_NS) mbar_timeout_trap(b, phase, line);
+  while (true) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(b), "r"(phase) : "memory");
+    if (ok) return;
+    if (globaltimer_ns() - t0 > CS_MBAR_TIMEOUT_NS) mbar_timeout_report(b, phase, line);
   }
 }
+#else
+CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .u64 t0, t1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t0, %%globaltimer;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t1, %%globaltimer;\n\t"
+      "sub.u64 t1, t1, t0;\n\t"
+      "setp.gt.u64 q, t1, %2;\n\t"
+      "@q trap;\n\t"
+      "bra.uni WAIT_%=;\n"
+      "DONE_%=:\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "l"((uint64_t)CS_MBAR_TIMEOUT_NS)
+      : "memory");
+}
+#endif
 
 // ---------------------------------------------------------------- TMA
 CS_DEV void tma_prefetch_desc(const CUtensorMap* m) {
