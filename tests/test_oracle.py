@@ -233,3 +233,49 @@ def test_adam_oracle():
     m, v = np.zeros(2), np.zeros(2)
     O.adam_step(p, g, m, v, 1, O.AdamConfig(lr=0.1))
     assert np.allclose(p, [0.9, -1.9], atol=1e-6)                             # step 1: -lr*sign(g)
+
+
+def test_bf16_rounding_matches_torch():
+    """O.bf16 is round-to-nearest-even, as torch's (and CUDA's __float2bfloat16_rn) cast."""
+    import torch
+    x = np.random.default_rng(0).standard_normal(4096) * np.logspace(-6, 6, 4096)
+    x[:4] = [1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -1.0 - 2 ** -8, 0.0]      # ties to even
+    ref = torch.from_numpy(x.astype(np.float32)).bfloat16().double().numpy()
+    assert np.array_equal(O.bf16(x), ref)
+
+
+def test_emu_oracle_floor_and_windows():
+    """The bf16 rounding-point oracle sits at the bf16 storage floor of the f64 reference
+    arithmetic (SURVEY cfg B: ~0.5% top-layer grads, ~3% layer-0 grads / dX), and is itself
+    window-partition invariant up to fp accumulation order (Alg. 2)."""
+    arch = O.Arch.reference(depth=2, hidden=256, heads=4, vocab=64, rank=8)
+    W = O.init_tiny(arch, 1)
+    toks = list(O.Rng(42).uniform_int(0, 63, 64))
+    tr, bw = _full(arch, W, toks)
+    te = O.forward_full(arch, W, toks, emu=True)
+    be = O.backward_full(arch, W, te)
+    assert abs(te["loss"] - tr["loss"]) < 1e-4
+    assert O.scaled_err(be["grads"]["a"][1], bw["grads"]["a"][1]) < 0.01
+    assert 0.005 < O.scaled_err(be["layers"][1]["dx"], bw["layers"][1]["dx"]) < 0.08
+    bew = O.backward_full(arch, W, te, windows=[20, 30, 14])
+    for l in range(2):
+        assert O.scaled_err(bew["grads"]["a"][l], be["grads"]["a"][l]) < 1e-9
+        assert O.scaled_err(bew["grads"]["b"][l], be["grads"]["b"][l]) < 1e-9
+
+
+def test_emu_sensitivity_relu_vs_swiglu():
+    """Why the GPU gates use the oracle's self-drift for some reference-arch quantities: with
+    only fp32-level (3e-7) noise on the activations before each bf16 rounding, the reference
+    arch's ReLU backward mask (tiny_model.hpp:285-286) flips on units with up ~ 0 and the
+    layer-1 dX drifts by more than 1e-2, while the smooth SwiGLU arch stays near 1e-2 and the
+    top-layer LoRA grads of both stay well under it."""
+    arch = O.Arch.reference(depth=2, hidden=256, heads=4, vocab=64, rank=8)
+    W = O.init_tiny(arch, 1)
+    toks = list(O.Rng(42).uniform_int(0, 63, 64))
+    s = O.emu_sensitivity(arch, W, toks)
+    assert s["dX1"] > 0.01 and s["dA1"] < 0.005 and s["dB1"] < 0.005
+    sw = O.Arch(n_layers=2, hidden=256, n_heads=4, n_kv_heads=2, head_dim=64, ffn=512, vocab=128,
+                lora_rank=16, norm="rms", act="swiglu", rope=True, qkv_bias=True)
+    Wsw = O.init_general(sw, 3)
+    ssw = O.emu_sensitivity(sw, Wsw, list(np.random.default_rng(5).integers(0, 128, 64)))
+    assert ssw["dX1"] < 0.015 and ssw["dA1"] < 0.01
