@@ -49,7 +49,9 @@ _BFW_CACHE: Dict[int, tuple] = {}
 def bfw(x):
     """Round to bf16 (round-to-nearest-even on the fp32 bit pattern, as __float2bfloat16_rn)
     and return float64: a weight operand of the emu oracle.  Large weight arrays are rounded
-    once and memoised (by identity; the cache holds the array so the id stays unique)."""
+    once and memoised (by identity; the cache holds the array so the id stays unique) -- only
+    persistent weight arrays may go through here, never temporaries, and they must not be
+    mutated in place while cached (clear_weight_cache)."""
     if isinstance(x, np.ndarray) and x.size >= (1 << 20):
         hit = _BFW_CACHE.get(id(x))
         if hit is not None and hit[0] is x:
@@ -84,7 +86,7 @@ def bf16(x):
         rng, amp = _NOISE
         x = np.asarray(x, dtype=np.float64)
         x = x * (1.0 + amp * rng.standard_normal(x.shape))
-    return bfw(x)
+    return _bfw(x)
 
 
 def emu_sensitivity(arch, W, tokens, amp: float = 3e-7, trials: int = 3, seed: int = 0):
@@ -579,7 +581,7 @@ def forward_window(arch: Arch, W: Dict, tokens_window, l_i: int, cache: QkvCache
     toks = np.asarray(tokens_window, dtype=np.int64)
     x = W["embed"][toks].copy()                              # tiny_model.hpp:189-190
     if emu:
-        x = bfw(x)
+        x = _bfw(x)  # rows of the bf16 embedding table (not memoised: a fresh gather)
     for n in range(arch.n_layers):
         x = _layer_forward(arch, W["layers"][n], x, l_i, cache.saved[n], lora, ar, emu)
     cache.length = l_i + len(toks)

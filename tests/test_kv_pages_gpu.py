@@ -150,7 +150,9 @@ def test_kv_pages_llama_arch_within_one_ulp():
                 # oracle's only in fp32-vs-f64 accumulation: <= 1 ulp of the row's scale
                 tol = np.abs(exp).max(axis=1, keepdims=True) * 2.0 ** -7
                 assert np.all(np.abs(got - exp) <= tol), (nm, layer, np.abs(got - exp).max())
-                # each stored row is its own position's row (no slot permutation)
+                # each stored row is (one of) the closest oracle row(s) to its own position's
+                # (no slot permutation; equal tokens give equal layer-0 V rows, hence "one of")
                 dist = ((got[:, None, :] - exp[None, :, :]) ** 2).sum(-1)
-                assert np.array_equal(dist.argmin(1), np.arange(n)), (nm, layer)
+                own = dist[np.arange(n), np.arange(n)]
+                assert np.all(own <= dist.min(1)), (nm, layer, np.flatnonzero(own > dist.min(1)))
     eng.close()
