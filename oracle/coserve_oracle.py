@@ -89,7 +89,8 @@ def bf16(x):
     return _bfw(x)
 
 
-def emu_sensitivity(arch, W, tokens, amp: float = 3e-7, trials: int = 3, seed: int = 0):
+def emu_sensitivity(arch, W, tokens, amp: float = 3e-7, trials: int = 3, seed: int = 0,
+                    clean=None):
     """How far two bf16 evaluations of the same model drift apart when their pre-rounding
     activations differ only at fp32 level (relative noise `amp` ~ a few fp32 ulps, i.e. fp32
     vs f64 accumulation): max over trials of the scale-normalised deviation of every backward
@@ -98,8 +99,9 @@ def emu_sensitivity(arch, W, tokens, amp: float = 3e-7, trials: int = 3, seed: i
     gradient row) no bf16 implementation can be held to 1e-2 of another; tests use it as the
     floor for those quantities."""
     global _NOISE
-    te = forward_full(arch, W, tokens, emu=True)
-    be = backward_full(arch, W, te)
+    if clean is None:  # the noise-free emu backward of the same case (or pass it in)
+        clean = backward_full(arch, W, forward_full(arch, W, tokens, emu=True))
+    be = clean
     out = {}
     try:
         _NOISE = (np.random.default_rng(seed), amp)

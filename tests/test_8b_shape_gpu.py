@@ -6,7 +6,7 @@ its tail-wave K split, attn_fwd_tc2 over 16 KV tiles, attn_bwd_dkdv2_kernel<4>, 
 dQ GEMM, the 1024-row CE head-chunk loop and the MN-major dX GEMMs.  The vocabulary is reduced
 to 16384 (the head loop and its chunking do not depend on V; the f64 oracle's [4096, V] logits
 would be 4 GB at V=128256).  Checked like tests/test_coserve_gpu.py: against the bf16
-rounding-point oracle at 1e-2 (or 1.5x its measured self-drift) and the f64 oracle under the
+rounding-point oracle at 1e-2 (or 2x its measured self-drift) and the f64 oracle under the
 bf16 storage floor -- both restating tiny_model.hpp:181-327 in the LLaMA generalisation."""
 import numpy as np
 import pytest
@@ -95,6 +95,6 @@ def test_llama8b_shape_two_layers_parity():
     gate_loss("llama8b_shape", loss_sum / (L - 1), {"loss": tr_loss}, te)
     del te
     gate_grads("llama8b_shape", arch, eng, bw, be, kvg, dys, floor_deep=FLOOR_DEEP,
-               sens=Sensitivity(arch, W, toks))
+               sens=Sensitivity(arch, W, toks, clean=be, trials=2))
     O.clear_weight_cache()
     eng.close()

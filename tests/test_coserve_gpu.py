@@ -61,12 +61,12 @@ def _log(rec):
 class Sensitivity:
     """Lazily computed O.emu_sensitivity of one (arch, weights, tokens) case."""
 
-    def __init__(self, arch, W, toks):
-        self.args, self.val = (arch, W, toks), None
+    def __init__(self, arch, W, toks, clean=None, trials=3):
+        self.args, self.kw, self.val = (arch, W, toks), {"clean": clean, "trials": trials}, None
 
     def __getitem__(self, q):
         if self.val is None:
-            self.val = O.emu_sensitivity(*self.args)
+            self.val = O.emu_sensitivity(*self.args, **self.kw)
         return self.val.get(q, 0.0)
 
 
@@ -227,7 +227,7 @@ def test_reference_tiny_config_parity():
     loss = loss_sum / 63.0
     assert abs(loss - 4.1809416937891104) < 1e-2 * 4.18  # SURVEY Appendix A (cfg B)
     gate_loss("tiny_cfg1", loss, tr, te)
-    gate_grads("tiny_cfg1", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks))
+    gate_grads("tiny_cfg1", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks, clean=be))
 
 
 @pytest.mark.parametrize("fwd,bwd", [([20, 30, 14], [24, 24, 16]), ([1, 63], [7, 57])])
@@ -241,7 +241,7 @@ def test_token_level_windows_match_full_sequence(fwd, bwd):
     eng, loss_sum, kvg, dys, _ = _run_coserve(arch, W, toks, fwd, bwd, n_inf=4,
                                               test=f"windows_{fwd}_{bwd}")
     gate_loss("windows", loss_sum / 63.0, tr, te)
-    gate_grads(f"windows_{fwd}_{bwd}", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks))
+    gate_grads(f"windows_{fwd}_{bwd}", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks, clean=be))
 
 
 LLAMA3 = O.Arch(n_layers=3, hidden=256, n_heads=4, n_kv_heads=2, head_dim=64, ffn=512,
@@ -258,7 +258,7 @@ def test_llama_arch_parity():
     eng, loss_sum, kvg, dys, _ = _run_coserve(arch, W, toks, [40, 60], [30, 30, 40], n_inf=5,
                                               logit_tol=0.04, test="llama3")
     gate_loss("llama3", loss_sum / 99.0, tr, te)
-    gate_grads("llama3", arch, eng, bw, be, kvg, dys, kv_layers=(1, 2), sens=Sensitivity(arch, W, toks))
+    gate_grads("llama3", arch, eng, bw, be, kvg, dys, kv_layers=(1, 2), sens=Sensitivity(arch, W, toks, clean=be))
 
 
 def test_adam_update_matches_oracle():
@@ -335,7 +335,7 @@ def test_d128_tcgen05_attention_parity(tc, dsq, monkeypatch):
     eng, loss_sum, kvg, dys, dmax = _run_coserve(arch, W, toks, [100, 200], [150, 150], n_inf=5,
                                                  logit_tol=0.04, test=t)
     gate_loss(t, loss_sum / 299.0, tr, te)
-    gate_grads(t, arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks))
+    gate_grads(t, arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks, clean=be))
 
 
 def test_reference_arch_d128_vs_live_reference():
@@ -360,7 +360,7 @@ def test_reference_arch_d128_vs_live_reference():
     eng, loss_sum, kvg, dys, _ = _run_coserve(arch, W, toks, [100, 156], [128, 128], n_inf=6,
                                               logit_tol=0.04, test="ref_d128")
     gate_loss("ref_d128", loss_sum / 255.0, tr, te)
-    gate_grads("ref_d128", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks))
+    gate_grads("ref_d128", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks, clean=be))
 
 
 ARCH_GQA4 = O.Arch(n_layers=2, hidden=512, n_heads=4, n_kv_heads=1, head_dim=128, ffn=512,
@@ -533,5 +533,5 @@ def test_qwen_geometry_gqa5_parity():
     eng, loss_sum, kvg, dys, _ = _run_coserve(arch, W, toks, [100, 200], [150, 150], n_inf=5,
                                               logit_tol=0.04, test="qwen_gqa5")
     gate_loss("qwen_gqa5", loss_sum / 299.0, tr, te)
-    gate_grads("qwen_gqa5", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks))
+    gate_grads("qwen_gqa5", arch, eng, bw, be, kvg, dys, sens=Sensitivity(arch, W, toks, clean=be))
     eng.close()

@@ -10,7 +10,7 @@ slot by slot with what the oracle says each position's K/V row is:
   difference.  Ragged prompts on non-monotone pages, chunked prefill continuing mid-page, decode
   rows crossing page boundaries and a finetuning window in its own pages all write in one
   engine; pages nobody owns must be untouched.
-* LLaMA arch (RMSNorm, RoPE, GQA): every slot within one bf16 ulp (of the row's scale) of the
+* LLaMA arch (RMSNorm, RoPE, GQA): every slot within two bf16 ulps (of the row's scale) of the
   bf16-emulated oracle's K/V, and each stored row closest to its own position's oracle row.
 """
 import numpy as np
@@ -146,9 +146,10 @@ def test_kv_pages_llama_arch_within_one_ulp():
             k, v = eng.read_kv(layer, r["pages"], n)
             ek, ev = r["cache"].saved[layer].k[:n], r["cache"].saved[layer].v[:n]
             for got, exp, nm in ((k, ek, "K"), (v, ev, "V")):
-                # two bf16 roundings (GEMM epilogue, RoPE) of values that differ from the
-                # oracle's only in fp32-vs-f64 accumulation: <= 1 ulp of the row's scale
-                tol = np.abs(exp).max(axis=1, keepdims=True) * 2.0 ** -7
+                # two bf16 roundings (GEMM epilogue, then RoPE of the rounded value) of numbers
+                # that differ from the oracle's only in fp32-vs-f64 accumulation: a 1-ulp flip
+                # at the first can carry through the rotation, so <= 2 ulps of the row's scale
+                tol = np.abs(exp).max(axis=1, keepdims=True) * 2.0 ** -6
                 assert np.all(np.abs(got - exp) <= tol), (nm, layer, np.abs(got - exp).max())
                 # each stored row is (one of) the closest oracle row(s) to its own position's
                 # (no slot permutation; equal tokens give equal layer-0 V rows, hence "one of")
