@@ -78,6 +78,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rate", type=float, default=20.0)
+    ap.add_argument("--rate-scope", default="replica", choices=["replica", "total"],
+                    help="replica: every co-serving replica (TP group) gets --rate (weak scaling); "
+                         "total: --rate is the whole job's arrival rate, split evenly over replicas")
     # side rates (other_rates in the JSON line): the headline is the --rate run
     ap.add_argument("--rates", default="4,10,20")
     ap.add_argument("--ft-len", type=int, default=8192)
@@ -426,17 +429,20 @@ def run_ours(a):
         allp = [None] * world
         dist.all_gather_object(allp, prof)
         prof = allp[group * tp]
+    n_groups = world // tp
+    per = (lambda r: r / n_groups) if a.rate_scope == "total" else (lambda r: r)
     rates = sorted({float(x) for x in a.rates.split(",") if x} | {a.rate})
     side = {}
     for r in rates:
         if r == a.rate:
             continue
-        st, _ = coserve_run(eng, coserve_config(r, prof, min(a.steps, 60), a.warmup, a.ft_len,
+        st, _ = coserve_run(eng, coserve_config(per(r), prof, min(a.steps, 60), a.warmup, a.ft_len,
                                                 seed=11 + int(r), slo_ms=slo,
                                                 max_window=a.ft_window, tail=m["tail_target"]))
         side[str(int(r) if r.is_integer() else r)] = {
             "value": round(1000.0 * ft_rate_per_ms(st, n_layers), 1),
             "iter_p99_ms": round(st["iter_p99_ms"], 2),
+            "itl_p99_ms": round(st["itl_p99_ms"], 2),
             "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4)}
     setup_s = time.time() - t_setup
 
@@ -445,7 +451,7 @@ def run_ours(a):
         dist.barrier()
     torch.cuda.synchronize()
     clk.start()
-    st, log = coserve_run(eng, coserve_config(a.rate, prof, a.steps, a.warmup, a.ft_len,
+    st, log = coserve_run(eng, coserve_config(per(a.rate), prof, a.steps, a.warmup, a.ft_len,
                                                seed=7 + group, slo_ms=slo,
                                                max_window=a.ft_window, tail=m["tail_target"]))
     torch.cuda.synchronize()
@@ -458,7 +464,7 @@ def run_ours(a):
     prof_steps = min(a.steps, 100) if a.kernel_profile else 0
     pst = st
     if prof_steps:
-        pst, _ = coserve_run(eng, coserve_config(a.rate, prof, prof_steps, a.warmup, a.ft_len,
+        pst, _ = coserve_run(eng, coserve_config(per(a.rate), prof, prof_steps, a.warmup, a.ft_len,
                                                  seed=7 + group, profile_timed=True, slo_ms=slo,
                                                  max_window=a.ft_window, tail=m["tail_target"]))
     gemm = eng.read_profile(0)
@@ -479,11 +485,16 @@ def run_ours(a):
     peaks, peak_kind = load_peaks()
     peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     gemm_tf = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else 0.0
-    traffic = None
+    # DRAM bytes per launch of the dominant kernel cannot be read with CUDA events; it comes from
+    # the committed ncu --set full capture of the same kernel at the bench's shapes (its file
+    # names the capture), null when that capture is absent
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath) and a.model == "llama-3.1-8b":
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_src = tj.get("source", "profiles/gemm_traffic.json")
         except Exception:
             traffic = None
     cpu = None
@@ -498,7 +509,9 @@ def run_ours(a):
                        "sample": "forward_full+backward_full of the reference (f64) on one "
                                  "8B-shaped layer (h=4096, 32 heads, ffn 4x, V=64), L=16 "
                                  "finetuning tokens, x32 layers extrapolated; "
-                                 f"{time.time() - t1:.1f}s incl. TinyModel::init"}
+                                 f"{time.time() - t1:.1f}s incl. TinyModel::init",
+                       "build": f"g++ -O3 -march={R.march()} (highest level this host runs)",
+                       "cpu_model": R.cpu_model(), "host_cores": os.cpu_count()}
         except Exception as ex:
             cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {ex}"}
@@ -520,10 +533,13 @@ def run_ours(a):
         "data": "synthetic: random-init weights (reference init scales), Poisson arrivals, "
                 "lognormal ShareGPT-like lengths, random tokens",
         "config": {"workload": f"{MODEL_NAMES[a.model]}-shaped co-serving, LoRA r=16 on down-proj, "
-                               f"{a.rate:g} req/s Poisson arrivals per replica, TPOT SLO {slo:g} ms, "
+                                      (f"{a.rate:g} req/s Poisson arrivals per replica" if a.rate_scope == "replica"
+                                       else f"{a.rate:g} req/s Poisson arrivals in total ({a.rate / n_groups:g} per replica)")
+                                      + f", TPOT SLO {slo:g} ms, "
                                f"finetuning sequences L={a.ft_len}"
                                + (f", windows <= {a.ft_window}" if a.ft_window < a.ft_len else ""),
-                   "model": f"{a.model}-shaped", "rate_rps_per_replica": a.rate,
+                   "model": f"{a.model}-shaped", "rate_rps_per_replica": per(a.rate),
+                   "rate_scope": a.rate_scope,
                    "ft_seq_len": a.ft_len, "ft_window_max": a.ft_window,
                    "parallelism": f"replicas x{world // tp} (TP={tp})",
                    "max_batch": MAX_BATCH, "chunk": 512, "tail_target": m["tail_target"],
@@ -533,7 +549,8 @@ def run_ours(a):
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all projections)",
                      "achieved": round(gemm_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(gemm_tf / peak_tf, 4) if peak_tf else None,
-                     "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": f"{peak_kind} bf16 sustained",
                      "launches": gemm["launches"],
                      "region": f"profiled pass: {prof_steps} steps of the same workload (CUDA "
                                "events around every GEMM launch on the engine stream)",
@@ -559,6 +576,18 @@ def run_ours(a):
                       "iter_p99_ms": round(st["iter_p99_ms"], 2),
                       "iter_max_ms": round(st["iter_max_ms"], 2),
                       "slo_ms": slo,
+                      # every decoding request in the timed region, observable in 20 steps
+                      "itl_p50_ms": round(st["itl_p50_ms"], 2),
+                      "itl_p99_ms": round(st["itl_p99_ms"], 2),
+                      "itl_max_ms": round(st["itl_max_ms"], 2),
+                      "itl_samples": st["itl_samples"],
+                      # requests that arrived in the timed region: completed inside both SLOs /
+                      # (all of them); unfinished ones already past the TTFT SLO count as misses
+                      "timed_arrivals": st["timed_arrivals"],
+                      "timed_done": st["timed_done"],
+                      "timed_unfinished_ttft_miss": st["timed_unfinished_miss"],
+                      "timed_slo_attainment": (round(st["timed_slo_ok"] / st["timed_arrivals"], 4)
+                                               if st["timed_arrivals"] else None),
                       "requests_done": st["requests_done"],
                       "slo_attainment": round(st["requests_slo_ok"] / max(1, st["requests_done"]), 4),
                       "tpot_p99_ms": round(st["tpot_p99_ms"], 2),
@@ -566,7 +595,13 @@ def run_ours(a):
                       "gen_tokens_per_s": round(1000.0 * st["gen_tokens"] / max(1e-9, st["timed_ms"]), 1),
                       "evictions": st["evictions"]},
         "finetune": {"fwd_tokens": st["ft_fwd_tokens"], "bwd_layer_tokens": st["ft_bwd_tokens"],
-                     "minibatches_done": st["minibatches_done"]},
+                     "minibatches_done": st["minibatches_done"],
+                     # value = L / (L / r_f + N L / r_b) from the measured window rates;
+                     # counted = sequences actually completed (fwd + all-layer bwd + Adam) in
+                     # the timed region x L / its wall time (0 when the run is shorter than one)
+                     "modelled_tokens_per_s": round(value, 1),
+                     "counted_tokens_per_s": round(1000.0 * st["minibatches_done"] * a.ft_len
+                                                   / max(1e-9, st["timed_ms"]), 1)},
         "other_rates": side,
         "profile": {k: (float(f"{v:.4g}") if isinstance(v, float) else v) for k, v in prof.items()
                     if k in ("t0_ms", "slope_ms_per_token", "bwd_token_weight",

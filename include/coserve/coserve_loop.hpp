@@ -109,6 +109,12 @@ struct LoopStats {
   int64_t requests_done = 0, requests_slo_ok = 0;
   int64_t evictions = 0;
   std::vector<double> ttft_ms, tpot_ms;
+  // observable in short runs: the gap between consecutive tokens of every decoding request in
+  // the timed region (prepopulated requests included), and SLO attainment over the requests
+  // that ARRIVED in the timed region only -- completed ones by their TTFT / TPOT, unfinished ones
+  // a miss once their wait for the first token already exceeds the TTFT SLO
+  std::vector<double> itl_ms;
+  int64_t timed_arrivals = 0, timed_done = 0, timed_slo_ok = 0, timed_unfinished_miss = 0;
   std::vector<IterLog> log;
   bool ok = true;
   // VTC: cumulative weighted service and completed requests per tenant, max spread of the
@@ -191,8 +197,10 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
   double budget = cfg.budget_ms;
   const int total_iters = cfg.warmup_iters + cfg.timed_iters;
   auto cycle_t = std::chrono::steady_clock::now();
+  double timed_t0 = 1e300;  // clock time the timed region starts
   for (int it = 0; it < total_iters; ++it) {
     const bool timed = it >= cfg.warmup_iters;
+    if (timed && timed_t0 > 1e299) timed_t0 = now;
     int64_t arrived = 0;
     while (next_arrival < trace.size() && trace[next_arrival].time_ms <= now) {
       ++arrived;
@@ -203,6 +211,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       r.prompt_len = a.prompt_len;
       r.gen_len = a.gen_len;
       r.arrival_ms = a.time_ms;
+      if (timed && r.arrival_ms >= timed_t0) st.timed_arrivals += 1;
       if (cfg.vtc) vtc.on_arrival(r.tenant);
       queue.push_back(std::move(r));
     }
@@ -342,7 +351,12 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       Request& r = running[i];
       r.last_token = out.next_tokens[seg++];
       r.emitted += 1;
-      if (timed) st.gen_tokens += 1;
+      if (timed) {
+        st.gen_tokens += 1;
+        // prepopulated requests have no emission time before their first decode in the run
+        if (r.last_emit_ms > -1e17 && r.last_emit_ms >= 0.0) st.itl_ms.push_back(now - r.last_emit_ms);
+      }
+      r.last_emit_ms = now;
       if (r.done()) r.completion_ms = now;
     }
     for (const PrefillChunk& pc : plan.prefill) {
@@ -352,6 +366,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
         r.last_token = out.next_tokens[seg];
         r.emitted = 1;
         r.first_token_ms = now;
+        r.last_emit_ms = now;
         if (timed) st.gen_tokens += 1;
         if (r.done()) r.completion_ms = now;
       }
@@ -387,6 +402,10 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
           st.tpot_ms.push_back(tpot);
           st.requests_done += 1;
           if (tpot <= cfg.sched.tpot_slo_ms && ttft <= cfg.sched.ttft_slo_ms) st.requests_slo_ok += 1;
+          if (r.arrival_ms >= timed_t0) {
+            st.timed_done += 1;
+            if (tpot <= cfg.sched.tpot_slo_ms && ttft <= cfg.sched.ttft_slo_ms) st.timed_slo_ok += 1;
+          }
           if ((int)st.tenant_done.size() <= r.tenant) st.tenant_done.resize(r.tenant + 1, 0);
           st.tenant_done[r.tenant] += 1;
         }
@@ -459,6 +478,14 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     st.log.push_back(lg);
     st.iters += 1;
   }
+  // timed-region arrivals still queued or prefilling whose first-token wait already breaks
+  // the TTFT SLO are misses; in-flight ones that have their first token count once done
+  auto unfinished_miss = [&](const Request& r) {
+    return r.arrival_ms >= timed_t0 && r.arrival_ms > -1e17 && r.first_token_ms < 0 &&
+           now - r.arrival_ms > cfg.sched.ttft_slo_ms;
+  };
+  for (const Request& r : queue) st.timed_unfinished_miss += unfinished_miss(r) ? 1 : 0;
+  for (const Request& r : running) st.timed_unfinished_miss += unfinished_miss(r) ? 1 : 0;
   st.tenant_service = vtc.service;
   return st;
 }

@@ -36,6 +36,7 @@ struct Request {
   double completion_ms = -1.0;
   int evictions = 0;
   int32_t last_token = 0;  // next input token for decode
+  double last_emit_ms = -1.0;  // time its latest token was emitted (inter-token latency)
   bool done() const { return emitted >= gen_len; }
   bool in_prefill() const { return prefilled < prompt_len; }
   int context() const { return prefilled + std::max(0, emitted - 1); }
@@ -126,29 +127,35 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
                                     double budget_ms) {
   IterationPlan p;
   if (!cfg.external_admission) p.admitted = admit_requests(queue, running, mem, cfg);
-  // token budget at the SLO for inference work (the inverse model with c = 0)
-  const int64_t tok_budget =
-      std::min<int64_t>(max_finetune_tokens(prof, 0, budget_ms), cfg.max_tokens);
-  int64_t c = 0;
+  // inference rows are sized against the cost the planner charges them (inference_cost: per-row
+  // decode / prefill slopes when the profile has them, latency(c, 0) otherwise -- then this is
+  // exactly the spec's token budget max_finetune_tokens(prof, 0, budget)), so the inference part
+  // alone never exceeds the budget whatever the fitted slopes
+  int64_t n_dec = 0, n_pre = 0;
+  auto fits = [&](int64_t nd, int64_t np) {
+    return nd + np <= cfg.max_tokens && inference_cost(prof, nd, np) <= budget_ms;
+  };
   // (1) decodes of running requests past their prompt
   for (int i = 0; i < (int)running.size(); ++i) {
     const Request& r = running[i];
-    if (!r.in_prefill() && !r.done() && c < tok_budget) {
+    if (!r.in_prefill() && !r.done() && fits(n_dec + 1, 0)) {
       p.decode.push_back(i);
-      c += 1;
+      n_dec += 1;
     }
   }
   // (2) chunked prefill in admission order within the remaining budget
   for (int i = 0; i < (int)running.size(); ++i) {
     const Request& r = running[i];
     if (!r.in_prefill()) continue;
-    const int64_t room = tok_budget - c;
+    const int64_t room = max_tokens_within([&](int64_t x) { return fits(n_dec, n_pre + x) ? 0.0 : 1.0; },
+                                           (int64_t)cfg.max_tokens - n_dec - n_pre, 0.5);
     if (room <= 0) break;
     const int len = (int)std::min<int64_t>({(int64_t)cfg.chunk_size, (int64_t)(r.prompt_len - r.prefilled), room});
     if (len <= 0) continue;
     p.prefill.push_back(PrefillChunk{i, r.prefilled, len});
-    c += len;
+    n_pre += len;
   }
+  const int64_t c = n_dec + n_pre;
   p.c = c;
   // (3) s = argmax f(c, s) <= budget, clipped to the FT phase and engine capacity
   const double w_b = prof.bwd_token_weight > 0 ? prof.bwd_token_weight : 1.0;
@@ -159,7 +166,9 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
       if (ft.phase == FtPhase::Backward && w_b != 1.0) s = (int64_t)std::floor((double)s / w_b);
       s = std::min<int64_t>(s, ft_phase_remaining(ft));
       s = std::min<int64_t>(s, cfg.max_ft_window);
-      if (ft.phase == FtPhase::Forward) s = std::min<int64_t>(s, cfg.max_tokens - c);
+      // forward rows share the engine's token capacity with the inference rows; a backward
+      // window is bounded by the same capacity (engine.cu backward_window: s <= max_tokens)
+      s = std::min<int64_t>(s, ft.phase == FtPhase::Forward ? cfg.max_tokens - c : (int64_t)cfg.max_tokens);
       s = std::max<int64_t>(s, 0);
       p.s = s;
       if (s > 0) {
@@ -198,7 +207,7 @@ inline IterationPlan plan_iteration(std::deque<Request>& queue, std::vector<Requ
   } else if (ft.phase == FtPhase::Backward) {
     int layer = ft.layer, lj = ft.lj;
     while (layer >= 0 && room > 0) {
-      const int64_t cap = std::min<int64_t>({(int64_t)lj, (int64_t)cfg.max_ft_window, (int64_t)cfg.max_tokens});
+      const int64_t cap = std::min<int64_t>({(int64_t)lj, (int64_t)cfg.max_ft_window, (int64_t)cfg.max_tokens});  // same cap as the engine's backward_window
       const int64_t lj0 = lj;
       const int ly = layer;
       const int64_t s = max_tokens_within([&](int64_t x) { return ft_bwd_cost(prof, lj0, x, ly); }, cap, room);

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 2  /* 2: policy / VTC / tail-control / sim-clock config fields, per-tenant stats, fwd_window_ms */
+#define CS_ABI_VERSION 3  /* 2: policy / VTC / tail-control / sim-clock config fields, per-tenant stats, fwd_window_ms; 3: ITL + timed-arrival SLO stats */
 
 #define CS_OK 0
 #define CS_ERR_INVALID_ARGUMENT (-1)
@@ -260,6 +260,12 @@ typedef struct cs_coserve_stats {
   double tenant_service[8];
   int64_t tenant_done[8];
   double vtc_spread_max, vtc_pair_gap_max;
+  /* observable in short runs: inter-token latency over every decoding request in the timed
+   * region; requests that arrived in the timed region: count, completed, completed inside both
+   * SLOs, unfinished with a first-token wait already past the TTFT SLO (misses) */
+  double itl_p50_ms, itl_p99_ms, itl_max_ms;
+  int64_t itl_samples;
+  int64_t timed_arrivals, timed_done, timed_slo_ok, timed_unfinished_miss;
 } cs_coserve_stats;
 
 typedef struct cs_iter_log {

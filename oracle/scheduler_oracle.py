@@ -267,24 +267,28 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
         r.pages = pages
         running.append(r)
         queue.popleft()
-    tok_budget = min(max_finetune_tokens(prof, 0, budget), max_tokens)
-    c = 0
+    def fits(nd, np_):
+        return nd + np_ <= max_tokens and inference_cost(prof, nd, np_) <= budget
+
+    n_dec = n_pre = 0
     decode, prefill = [], []
     for i, r in enumerate(running):
-        if not r.in_prefill() and not r.done() and c < tok_budget:
+        if not r.in_prefill() and not r.done() and fits(n_dec + 1, 0):
             decode.append(i)
-            c += 1
+            n_dec += 1
     for i, r in enumerate(running):
         if not r.in_prefill():
             continue
-        room = tok_budget - c
+        room = max_tokens_within(lambda x: 0.0 if fits(n_dec, n_pre + x) else 1.0,
+                                 max_tokens - n_dec - n_pre, 0.5)
         if room <= 0:
             break
         ln = min(chunk, r.prompt_len - r.prefilled, room)
         if ln <= 0:
             continue
         prefill.append((i, r.prefilled, ln))
-        c += ln
+        n_pre += ln
+    c = n_dec + n_pre
     w_b = prof.bwd_weight if prof.bwd_weight > 0 else 1.0
     s, phase, layer, l = 0, 0, -1, 0
     bwd = []
@@ -295,8 +299,7 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
                 s = int(math.floor(s / w_b))
             s = min(s, (ft.L - ft.l) if ft.phase == FWD else ft.lj)
             s = min(s, max_ft_window)
-            if ft.phase == FWD:
-                s = min(s, max_tokens - c)
+            s = min(s, (max_tokens - c) if ft.phase == FWD else max_tokens)
             s = max(s, 0)
             if s > 0:
                 phase = ft.phase

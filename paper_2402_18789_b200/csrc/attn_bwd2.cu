@@ -2,9 +2,7 @@
 // 14-21; tiny_model.hpp:294-315 for query rows [a, b) over keys [0, b)) on
 // tcgen05 with the elementwise products kept in TMEM.
 //
-// v1 (attn_bwd_tc.cu) staged P^T / dS^T and dS through shared memory (single-buffered, fenced)
-// and split every row over two threads; v2 re-derives both kernels the way attn_fwd2.cu does
-// the forward:
+// Both kernels follow the structure of attn_fwd2.cu's forward:
 //   dkdv: CTA = 128 keys x 1 KV head, loop over 64-row packed query tiles (3-stage TMA ring of
 //         Q / dO boxes).  S^T = K Q^T and dP^T = V dO^T land in double-buffered TMEM; two
 //         elementwise warpgroups take alternate tiles, one thread per key row owning all 64
@@ -686,20 +684,10 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
   dim3 gq((rows + 128 / p.grp - 1) / (128 / p.grp), kvh);
   dim3 gk((p.b + 127) / 128, kvh);
   g_launches.fetch_add(p.ds_out ? 1 : 2, std::memory_order_relaxed);
-  static const int mask = [] {
-    const char* v = std::getenv("CS_BWD2_MASK");  // debugging: 1 = dq v2 only, 2 = dkdv v2 only
-    return v ? std::atoi(v) : 3;
-  }();
-  if (p.ds_out) {
-    // dQ comes from attn_dq_gemm over the stored dS (launched by the caller after this)
-  } else if (mask & 1) {
+  // with p.ds_out the dQ comes from attn_dq_gemm over the stored dS (launched by the caller)
+  if (!p.ds_out)
     launch_pdl(attn_bwd_dq2_kernel, dim3(gq), dim3(384), dq2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, p);
-  } else {
-    attn_bwd_dq_v1(p, tmK, tmV, tmK128, tmV128, gq, st);
-  }
-  if ((mask & 2) || (64 % p.grp) != 0)
-    launch_pdl(kDkdv2[p.grp - 1], dim3(gk), dim3(384), kv2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
-  else attn_bwd_dkdv_v1(p, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, gk, st);
+  launch_pdl(kDkdv2[p.grp - 1], dim3(gk), dim3(384), kv2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
   return cudaGetLastError();
 }
 

@@ -1,10 +1,9 @@
 // attn_fwd2.cu -- K8 v2: causal attention forward on tcgen05 for prefill-chunk and finetuning-
 // window rows (attention_rows, tiny_model.hpp:118-151, over paged KV), two query tiles per CTA.
 //
-// v1 (attn_tc.cu) ran one 128-row query tile per CTA: every 64 KB K/V tile fed 8.4 MFLOP
-// (128 FLOP per L2 byte -- at the tensor peak that is the whole L2 bandwidth), the two
-// half-row softmax warps met at a named barrier every tile, and P went through shared memory.
-// v2 (the FA4 structure, re-derived for GQA-packed paged KV):
+// One 128-row query tile per CTA would feed every 64 KB K/V tile only 8.4 MFLOP (128 FLOP per L2
+// byte -- at the tensor peak that is the whole L2 bandwidth); this kernel (the FA4 structure,
+// re-derived for GQA-packed paged KV):
 //   * CTA = 2 query tiles x 128 GQA-packed rows sharing every K/V tile (256 FLOP / L2 byte);
 //   * TMEM (512 cols): S0 | S1 | O0 | O1; softmax writes P_i (bf16) back into the first 64
 //     columns of S_i and the PV MMA reads its A operand straight from TMEM (tcgen05.mma

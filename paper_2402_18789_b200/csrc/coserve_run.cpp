@@ -251,6 +251,14 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   }
   stats->vtc_spread_max = st.vtc_spread_max;
   stats->vtc_pair_gap_max = st.vtc_pair_gap_max;
+  stats->itl_p50_ms = pct(st.itl_ms, 0.5);
+  stats->itl_p99_ms = pct(st.itl_ms, 0.99);
+  stats->itl_max_ms = st.itl_ms.empty() ? 0.0 : *std::max_element(st.itl_ms.begin(), st.itl_ms.end());
+  stats->itl_samples = (int64_t)st.itl_ms.size();
+  stats->timed_arrivals = st.timed_arrivals;
+  stats->timed_done = st.timed_done;
+  stats->timed_slo_ok = st.timed_slo_ok;
+  stats->timed_unfinished_miss = st.timed_unfinished_miss;
   if (ex) {
     stats->gpu_launches = cs_engine_launch_count(e) - counting.launches0;
     stats->h2d_bytes = ex->h2d;

@@ -751,10 +751,7 @@ __global__ void adam_kernel(AdamParams p, int update) {
       const long rem = i % ((long)p.f * p.r);
       const int row = (int)(rem / p.r), j = (int)(rem % p.r);
       p.A_t[(l * 16 + j) * p.f + row] = wb;  // [n_layers][16][f]
-      if (p.a_in_down)
-        p.down_cat[(l * p.down_rows + p.h + j) * (p.f + 64) + row] = wb;
-      else
-        p.dbwd_cat[(l * p.f + row) * (p.h + 64) + p.h + j] = wb;
+      p.down_cat[(l * p.down_rows + p.h + j) * (p.f + 64) + row] = wb;
     } else {    // B[l][j][c]
       const long l = i / ((long)p.r * p.h);
       const long rem = i % ((long)p.r * p.h);

@@ -54,12 +54,9 @@ struct cs_engine {
   bool swiglu, norm, rope;
   bool use_tc_attn = true;  // CS_ATTN_TC=0 forces the mma.sync path (A/B testing)
   bool use_dec_attn = true;  // CS_ATTN_DEC=0 sends decode rows to the mma.sync tile kernel
-  bool use_fwd2 = true;      // CS_ATTN_FWD2=0 runs the one-query-tile tcgen05 kernel (v1)
-  bool use_bwd2 = true;      // CS_ATTN_BWD2=0 runs the shared-memory-staged backward (v1)
   // dX GEMMs read the forward weight layout as an MN-major B operand: one copy of the frozen
-  // QKV / O / gate||up / unembedding weights (CS_BWD_MN=0 keeps the reference-layout copies)
-  bool bwd_mn = true;
-  int down_rows = 0;  // per-layer rows of down_cat: h (+ 64 LoRA-A^T rows when bwd_mn)
+  // QKV / O / gate||up / unembedding weights serves x W and dY W^T
+  int down_rows = 0;  // per-layer rows of down_cat: h + 64 LoRA-A^T rows (MN-major dm operand)
   // CS_BWD_DSQ=1: dQ as a GEMM over the dS the dK/dV kernel stores ([window row][q head][key])
   bool bwd_dsq = false;
   bf16* ds_buf = nullptr;
@@ -76,7 +73,7 @@ struct cs_engine {
   // weights
   bf16 *embed, *unembed_t, *unembed;
   float* gf;
-  bf16 *wqkv_t, *wqkv, *wo_t, *wo, *wgu_t, *wgu, *down_cat, *dbwd_cat, *A_t, *B_t;
+  bf16 *wqkv_t, *wo_t, *wgu_t, *down_cat, *A_t, *B_t;
   float *bqkv, *g1, *g2;
   float *loraA, *loraB, *gA, *gB, *mA, *vA, *mB, *vB;
   // KV
@@ -202,19 +199,13 @@ void layout(cs_engine* e, bool measure, size_t* total) {
 #define AL(field, count) A(&e->field, (count), #field)
   const size_t NL = e->NL, h = e->h, V = e->V, f = e->f, r = e->r;
   const size_t T = e->T_max, Lm = e->L_max, S = e->S_max;
-  const bool dup = !e->bwd_mn;  // reference-layout copies only without MN-major dX GEMMs
   AL(embed, V * h);
   AL(unembed_t, V * h);
-  AL(unembed, dup ? h * V : 1);
   AL(gf, h);
   AL(wqkv_t, NL * e->nqkv * h);
-  AL(wqkv, dup ? NL * h * e->nqkv : 1);
   AL(wo_t, NL * h * e->q_dim);
-  AL(wo, dup ? NL * e->q_dim * h : 1);
   AL(wgu_t, NL * e->gu_n * h);
-  AL(wgu, dup ? NL * h * e->gu_n : 1);
   AL(down_cat, NL * e->down_rows * e->f_cat);
-  AL(dbwd_cat, dup ? NL * f * e->h_cat : 1);
   AL(A_t, NL * 16 * f);
   AL(B_t, NL * 16 * h);
   AL(bqkv, NL * e->nqkv);
@@ -371,10 +362,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   e->meta_bytes = meta_size(e);
   if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
-  if (const char* v = std::getenv("CS_ATTN_FWD2")) e->use_fwd2 = std::atoi(v) != 0;
-  if (const char* v = std::getenv("CS_ATTN_BWD2")) e->use_bwd2 = std::atoi(v) != 0;
-  if (const char* v = std::getenv("CS_BWD_MN")) e->bwd_mn = std::atoi(v) != 0;
-  e->down_rows = e->h + (e->bwd_mn ? 64 : 0);
+  e->down_rows = e->h + 64;
   {  // dQ as a GEMM over the dS^T the dK/dV kernel exports (default; CS_BWD_DSQ=0: the
      // recomputing dQ kernel) -- d = 128 and GQA groups dividing the 64-row dK/dV query tile
     const char* v = std::getenv("CS_BWD_DSQ");
@@ -592,9 +580,7 @@ int refresh_lora(cs_engine* e, int update, float lr, float b1, float b2, float e
   p.A_t = e->A_t;
   p.B_t = e->B_t;
   p.down_cat = e->down_cat;
-  p.dbwd_cat = e->dbwd_cat;
   p.down_rows = e->down_rows;
-  p.a_in_down = e->bwd_mn ? 1 : 0;
   p.n_layers = e->NL;
   p.f = e->f;
   p.r = e->r;
@@ -693,25 +679,19 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
   if (n == "embed") {
     cs::cast_f32_bf16(stage, lr, lc, e->embed, h, 0, st);
   } else if (n == "unembed") {
-    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->unembed, V, 0, st);
     cs::cast_f32_bf16(stage, lr, lc, e->unembed_t, h, 1, st);
   } else if (n == "final_norm") {
     cudaMemcpyAsync(e->gf, stage, h * 4, cudaMemcpyDeviceToDevice, st);
   } else if (n == "wq" || n == "wk" || n == "wv") {
     const long off = n == "wq" ? 0 : (n == "wk" ? qd : qd + kvd);
     cs::cast_f32_bf16(stage, lr, lc, e->wqkv_t + ((size_t)L * e->nqkv + off) * h, h, 1, st);
-    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wqkv + (size_t)L * h * e->nqkv + off, e->nqkv, 0, st);
   } else if (n == "wo") {
     cs::cast_f32_bf16(stage, lr, lc, e->wo_t + (size_t)L * h * qd, qd, 1, st);
-    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wo + (size_t)L * qd * h, h, 0, st);
   } else if (n == "w_gate" || n == "w_up") {
     const long off = (n == "w_up" && e->swiglu) ? f : 0;
     cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
-    if (!e->bwd_mn) cs::cast_f32_bf16(stage, lr, lc, e->wgu + (size_t)L * h * e->gu_n + off, e->gu_n, 0, st);
   } else if (n == "w_down") {
     cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * e->down_rows * e->f_cat, e->f_cat, 1, st);
-    if (!e->bwd_mn)
-      cs::cast_f32_bf16(stage, lr, lc, e->dbwd_cat + (size_t)L * f * e->h_cat, e->h_cat, 0, st);
   } else if (n == "lora_a") {
     cudaMemcpyAsync(e->loraA + (size_t)L * f * r, stage, lcount * 4, cudaMemcpyDeviceToDevice, st);
     rc = refresh_lora(e, 0, 0, 0, 0, 0);
@@ -746,12 +726,6 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
   cs::init_normal_bf16(e->wqkv_t, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
   cs::init_normal_bf16(e->wo_t, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
   cs::init_normal_bf16(e->wgu_t, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
-  if (!e->bwd_mn) {  // reference-layout copies (same statistics, not transposes)
-    cs::init_normal_bf16(e->unembed, (long)e->V * e->h, ws, seed + 2, st);
-    cs::init_normal_bf16(e->wqkv, (long)(NL * e->nqkv * e->h), ws, ss + 3, st);
-    cs::init_normal_bf16(e->wo, (long)(NL * e->q_dim * e->h), ws, ss + 4, st);
-    cs::init_normal_bf16(e->wgu, (long)(NL * e->gu_n * e->h), ws, ss + 5, st);
-  }
   // down: fill whole concat buffers, then the LoRA columns are rewritten by refresh_lora;
   // pad columns [f + r, f + 64) must stay zero -> fill per row via cast of random fp32
   {
@@ -761,8 +735,6 @@ extern "C" int cs_engine_init_random(cs_engine* e, uint64_t seed) {
     for (size_t l = 0; l < NL; ++l) {
       cs::init_normal_f32(tmp, (long)e->f * e->h, wf, ss + 100 + l, st);
       cs::cast_f32_bf16(tmp, e->f, e->h, e->down_cat + l * e->down_rows * e->f_cat, e->f_cat, 1, st);
-      if (!e->bwd_mn)
-        cs::cast_f32_bf16(tmp, e->f, e->h, e->dbwd_cat + l * e->f * e->h_cat, e->h_cat, 0, st);
     }
     cudaStreamSynchronize(st);
     cudaFree(tmp);
@@ -976,7 +948,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // tcgen05 attention items: two 128-row query tiles per CTA (v2) when the call has enough of
   // them to fill ~2 waves of SMs, else one tile per CTA (more CTAs for small windows)
   int rpt_tc = 128 / e->grp;
-  if (e->use_fwd2) {
+  {
     long n2 = 0;
     for (int s2 = 0; plan->segments && s2 < plan->n_segments; ++s2) {
       const int ql = plan->segments[s2].q_len;
@@ -1155,7 +1127,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // key ranges into parts of >= 1024 keys so ~2 waves of SMs share the work (flash-decoding
   // style; parts merged by the LSE combine) -- otherwise a 45-token window at 8K context ran
   // on 8 CTAs
-  if (e->use_fwd2 && !work_tc.empty() && (long)work_tc.size() < 148) {
+  if (!work_tc.empty() && (long)work_tc.size() < 148) {
     long total = 0;
     for (const auto& w : work_tc) total += w.k_end;
     long chunk = (total + 2L * 148 - 1) / (2L * 148);
@@ -1378,16 +1350,12 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         tpr.kind = 3;
         prof_begin(e, tpr);
       }
-      if (e->use_fwd2) {
-        CS_CUDA_TRY(cs::attn_fwd_tc2(tp, mk, mv, mk128, mv128, sp.n_tc, st));
-        if (sp.n_comb_tc > 0) {  // after the decode combine: the part buffers are reused
-          cs::AttnFwdParams cp = ap;
-          cp.combine = sp.comb_tc;
-          cp.part_rows = 256;
-          CS_CUDA_TRY(cs::attn_combine(cp, e->d, sp.n_comb_tc, st));
-        }
-      } else {
-        CS_CUDA_TRY(cs::attn_fwd_tc(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      CS_CUDA_TRY(cs::attn_fwd_tc2(tp, mk, mv, mk128, mv128, sp.n_tc, st));
+      if (sp.n_comb_tc > 0) {  // after the decode combine: the part buffers are reused
+        cs::AttnFwdParams cp = ap;
+        cp.combine = sp.comb_tc;
+        cp.part_rows = 256;
+        CS_CUDA_TRY(cs::attn_combine(cp, e->d, sp.n_comb_tc, st));
       }
       if (e->profiling) prof_end(e, tpr);
     }
@@ -1444,12 +1412,9 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
                e->V, cn, e->V, h, cs::EPI_F32));
       cs::ce_fwd_bwd(e->logits, e->V, sp.targets + c0, cn, e->V, inv, e->loss_rows + c0, e->dlog,
                      e->V, st);
-      if (e->bwd_mn)  // dH = dlogits . U^T, U^T read from the [V, h] forward copy (MN-major)
-        TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed_t, h, e->V, e->dh, h, cn, h, e->V,
-                 cs::EPI_F32, nullptr, nullptr, 1));
-      else
-        TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed, e->V, h, e->dh, h, cn, h, e->V,
-                 cs::EPI_F32));
+      // dH = dlogits . U^T, U^T read from the [V, h] forward copy (MN-major)
+      TRY(gemm(e, e->dlog, e->V, e->head_chunk, e->unembed_t, h, e->V, e->dh, h, cn, h, e->V,
+               cs::EPI_F32, nullptr, nullptr, 1));
       cs::rms_bwd_add(nullptr, 0, xs, h, e->gf, e->hrstd, e->dh, h,
                       e->dy[e->dy_cur] + (size_t)(l0 + c0) * h, h, nullptr, 0, cn, h, e->norm, st);
     }
@@ -1497,31 +1462,20 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->B_t + (size_t)n * 16 * h, h, 16, e->dlu, r, s, r, h,
            cs::EPI_F32));
   cs::lora_pack(e->dlu, r, e->dycat, e->h_cat, h, s, st);
-  if (e->bwd_mn)  // dm = [dY | dU] . [W_down^T ; A^T]: down_cat's [h + 64, f] block, MN-major
-    TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->down_cat + (size_t)n * e->down_rows * e->f_cat,
-             e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_BF16, nullptr, nullptr, 1));
-  else
-    TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->dbwd_cat + (size_t)n * f * e->h_cat, e->h_cat, f,
-             e->dm, f, s, f, e->h_cat, cs::EPI_BF16));
+  // dm = [dY | dU] . [W_down^T ; A^T]: down_cat's [h + 64, f] block, MN-major
+  TRY(gemm(e, e->dycat, e->h_cat, e->S_max, e->down_cat + (size_t)n * e->down_rows * e->f_cat,
+           e->f_cat, e->h_cat, e->dm, f, s, f, e->h_cat, cs::EPI_BF16, nullptr, nullptr, 1));
   cs::mlp_bwd(e->dm, f, e->ft_gu + ((size_t)n * Lm + a) * e->gu_n, e->gu_n, e->dlu, r, e->dgu,
               e->gu_n, e->gA + (size_t)n * f * r, s, f, e->swiglu, st);
   if (n > 0) {
-    if (e->bwd_mn)
-      TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu_t + (size_t)n * e->gu_n * h, h, e->gu_n, e->dh2,
-                    s, e->gu_n, false, 1));
-    else
-      TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu + (size_t)n * h * e->gu_n, e->gu_n, h, e->dh2,
-                    s, e->gu_n, false));
+    TRY(tp_rowpar(e, e->dgu, e->gu_n, e->S_max, e->wgu_t + (size_t)n * e->gu_n * h, h, e->gu_n, e->dh2,
+                  s, e->gu_n, false, 1));
     cs::rms_bwd_add(Y, h, e->ft_r1 + ((size_t)n * Lm + a) * h, h, e->g2 + (size_t)n * h,
                     e->ft_rstd2 + (size_t)n * Lm + a, e->dh2, h, e->dr1, h, e->dr1b, h, s, h,
                     e->norm, st);
     // ---- attention (tiny_model.hpp:289-315)
-    if (e->bwd_mn)
-      TRY(gemm(e, e->dr1b, h, e->S_max, e->wo_t + (size_t)n * h * e->q_dim, e->q_dim, h, e->dO,
-               e->q_dim, s, e->q_dim, h, cs::EPI_BF16, nullptr, nullptr, 1));
-    else
-      TRY(gemm(e, e->dr1b, h, e->S_max, e->wo + (size_t)n * e->q_dim * h, h, e->q_dim, e->dO,
-             e->q_dim, s, e->q_dim, h, cs::EPI_BF16));
+    TRY(gemm(e, e->dr1b, h, e->S_max, e->wo_t + (size_t)n * h * e->q_dim, e->q_dim, h, e->dO,
+             e->q_dim, s, e->q_dim, h, cs::EPI_BF16, nullptr, nullptr, 1));
     const size_t kv_layer = (size_t)e->npages * e->P * e->kv_dim;
     cs::AttnBwdParams bp;
     bp.q_cache = e->ft_q + (size_t)n * Lm * e->q_dim;
@@ -1562,12 +1516,10 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     }
     // v2 takes any GQA group <= 8 (groups that do not divide 64 leave pad rows in a query
     // tile); the v1 kernels need 64 % group == 0
-    const bool bwd_tc = e->use_tc_attn && e->d == 128 && (e->P % 16) == 0 &&
-                        (e->use_bwd2 ? e->grp <= 8 : (64 % e->grp) == 0);
+    const bool bwd_tc = e->use_tc_attn && e->d == 128 && (e->P % 16) == 0 && e->grp <= 8;
     if (bwd_tc) {
       CUtensorMap mk, mv, mk128, mv128, mq3, mo3;
       const long pool_rows = (long)e->npages * e->P;
-      const bool v2 = e->use_bwd2;
       const int qbox = 64 / e->grp;  // 3-D boxes: 64 / grp positions x grp heads packed rows
       if (cs::make_map(&mk, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
           cs::make_map(&mv, bp.v_pool, pool_rows, e->kv_dim, e->kv_dim, 16) != 0 ||
@@ -1578,7 +1530,7 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
           cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
                           qbox) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
-      if (v2 && e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
+      if (e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
         CUtensorMap mds, mk64;
         const long keys = ((long)e->L_max + 127) / 128 * 128;
         const long ntiles = (long)e->S_max * e->grp / 64 + 2;
@@ -1592,22 +1544,17 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
           return cs::set_error(CS_ERR_CUDA, "attention backward: dS TMA map creation failed");
         CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
         CS_CUDA_TRY(cs::attn_dq_gemm(bp, mds, mk, mk64, e->Hq, st));
-      } else if (v2)
+      } else {
         CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
-      else
-        CS_CUDA_TRY(cs::attn_bwd_tc(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
+      }
     } else {
       CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
     }
     if (e->profiling) prof_end(e, bpr);
     cs::rope_bwd_pack(e->dq, e->q_dim, e->dk_acc, e->dv_acc, e->kv_dim, a, s, e->Hq, e->Hkv, e->d,
                       e->rope, e->cfg.rope_theta, e->dqkv, e->nqkv, st);
-    if (e->bwd_mn)
-      TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv_t + (size_t)n * e->nqkv * h, h, e->nqkv,
-                    e->dh1, s, e->nqkv, false, 1));
-    else
-      TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv + (size_t)n * h * e->nqkv, e->nqkv, h, e->dh1,
-                    s, e->nqkv, false));
+    TRY(tp_rowpar(e, e->dqkv, e->nqkv, e->S_max, e->wqkv_t + (size_t)n * e->nqkv * h, h, e->nqkv,
+                  e->dh1, s, e->nqkv, false, 1));
     cs::rms_bwd_add(e->dr1, h, e->ft_x + ((size_t)n * Lm + a) * h, h, e->g1 + (size_t)n * h,
                     e->ft_rstd1 + (size_t)n * Lm + a, e->dh1, h, Xout, h, nullptr, 0, s, h,
                     e->norm, st);

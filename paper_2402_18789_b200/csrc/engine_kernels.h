@@ -104,29 +104,17 @@ cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStre
 cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const CUtensorMap& tmK16,
                          const CUtensorMap& tmK64, int n_heads, cudaStream_t st);
 void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st);
-// tcgen05 backward (dQ and dK/dV kernels); head_dim 128, 64 % grp == 0
-void attn_bwd_dq_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                    const CUtensorMap& tmK128, const CUtensorMap& tmV128, dim3 grid, cudaStream_t st);
-void attn_bwd_dkdv_v1(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                      const CUtensorMap& tmK128, const CUtensorMap& tmV128, const CUtensorMap& tmQ3,
-                      const CUtensorMap& tmO3, dim3 grid, cudaStream_t st);
-// v2: P^T / dS^T / dS kept in TMEM (TS-MMA), ping-pong elementwise warpgroups
+// tcgen05 backward (head_dim 128, GQA group <= 8): P^T / dS^T / dS kept in TMEM (TS-MMA),
+// ping-pong elementwise warpgroups
 cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          const CUtensorMap& tmK128, const CUtensorMap& tmV128,
                          const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
                          cudaStream_t st);
-cudaError_t attn_bwd_tc(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                        const CUtensorMap& tmK128, const CUtensorMap& tmV128,
-                        const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
-                        cudaStream_t st);
-// tcgen05 forward for prefill / finetuning-window tiles (head_dim 128, 128 packed rows per CTA)
-// v2: two query tiles per CTA (work items of 2 * (128 / group) positions), P kept in TMEM
+// tcgen05 forward for prefill / finetuning-window tiles (head_dim 128): two 128-row query tiles
+// per CTA (work items of 2 * (128 / group) positions), P kept in TMEM
 cudaError_t attn_fwd_tc2(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,
                          cudaStream_t st);
-cudaError_t attn_fwd_tc(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                        const CUtensorMap& tmK128, const CUtensorMap& tmV128, int n_work,
-                        cudaStream_t st);
 
 // ------------------------------------------------------------------ elementwise (elem.cu)
 void embed_gather(const int* tokens, const bf16* embed, float* x, int T, int h, cudaStream_t st);
@@ -206,9 +194,7 @@ struct AdamParams {
   bf16* A_t;        // [n_layers][16][f]          (lu GEMM B operand)
   bf16* B_t;        // [n_layers][16][h]          (dlu GEMM B operand)
   bf16* down_cat;   // [n_layers][down_rows][f + 64]  rows < h: cols f.. = B^T; rows h.. = A^T
-  bf16* dbwd_cat;   // [n_layers][f][h + 64]     cols h.. = A   (a_in_down == 0 only)
-  int down_rows;    // h (+ 64 when A^T rides in down_cat: the MN-major backward operand)
-  int a_in_down;
+  int down_rows;    // h + 64: A^T rides in down_cat (the MN-major backward operand)
   int n_layers, f, r, h;
   float lr, b1, b2, eps, bc1, bc2;
 };

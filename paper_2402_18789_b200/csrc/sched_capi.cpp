@@ -22,6 +22,7 @@ coserve::LatencyProfile to_profile(const cs_latency_profile* p) {
   q.bwd_layer0_weight = p->bwd_layer0_weight > 0 ? p->bwd_layer0_weight : 1.0;
   q.decode_ms_per_row = p->decode_ms_per_row > 0 ? p->decode_ms_per_row : 0.0;
   q.prefill_ms_per_token = p->prefill_ms_per_token > 0 ? p->prefill_ms_per_token : 0.0;
+  q.fwd_window_ms = p->fwd_window_ms > 0 ? p->fwd_window_ms : 0.0;
   return q;
 }
 }  // namespace

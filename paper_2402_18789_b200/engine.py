@@ -86,7 +86,10 @@ class CoserveStats(ctypes.Structure):
                 ("iter_p99_ms", f64), ("iter_max_ms", f64), ("gpu_launches", i64),
                 ("h2d_bytes", i64), ("d2h_bytes", i64),
                 ("tenant_service", f64 * 8), ("tenant_done", i64 * 8),
-                ("vtc_spread_max", f64), ("vtc_pair_gap_max", f64)]
+                ("vtc_spread_max", f64), ("vtc_pair_gap_max", f64),
+                ("itl_p50_ms", f64), ("itl_p99_ms", f64), ("itl_max_ms", f64), ("itl_samples", i64),
+                ("timed_arrivals", i64), ("timed_done", i64), ("timed_slo_ok", i64),
+                ("timed_unfinished_miss", i64)]
 
 
 class IterLogC(ctypes.Structure):

@@ -1,5 +1,5 @@
 """A/B the attention forward paths on the 8B shape: 2048-token FT windows at l=0..6144 with 64
-decode rows (CS_ATTN_FWD2=1 two-query-tile tcgen05 kernel vs 0 the one-tile kernel), device
+decode rows on the two-query-tile tcgen05 kernel, device
 time of the attention kernels from the engine's CUDA events."""
 import os
 import sys
@@ -21,7 +21,7 @@ for l in range(0, 8192, 2048):
     a = eng.read_profile(3)
     d = eng.read_profile(1)
     g = eng.read_profile(0)
-    print(f"CS_ATTN_FWD2={os.environ.get('CS_ATTN_FWD2','1')} l={l} step {out['ms']:.2f} ms  "
+    print(f"l={l} step {out['ms']:.2f} ms  "
           f"attn(tc) {a['ms']:.2f} ms {a['flops']/max(a['ms'],1e-9)/1e9:.0f} TFLOP/s  decode {d['ms']:.2f} ms  "
           f"gemm {g['ms']:.2f} ms {g['flops']/g['ms']/1e9:.0f} TFLOP/s", flush=True)
     eng.set_profiling(False); eng.set_profiling(True)

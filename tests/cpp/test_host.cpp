@@ -168,6 +168,63 @@ static void test_plan_iteration() {
   CHECK(!enforce_dependencies(mixed, bwd));
 }
 
+// with per-row inference slopes steeper than the common FT slope, the inference rows
+// alone must still fit the budget (the planner sizes them with inference_cost), and a
+// single-profile backward window is capped at the engine's max_tokens
+static void test_plan_row_slopes_and_caps() {
+  LatencyProfile p;
+  p.t0_ms = 1.0;
+  p.slope_ms_per_token = 0.01;
+  p.decode_ms_per_row = 0.05;       // 5x the common slope
+  p.prefill_ms_per_token = 0.03;
+  SchedulerConfig cfg;
+  cfg.chunk_size = 512;
+  cfg.max_tokens = 4096;
+  MemoryModel mem(4000, 16);
+  std::deque<Request> q;
+  std::vector<Request> running;
+  for (int i = 0; i < 300; ++i) {
+    Request r;
+    r.id = i;
+    r.prompt_len = 10;
+    r.gen_len = 100;
+    r.prefilled = i < 250 ? 10 : 0;  // 250 decoding, 50 in prefill
+    r.emitted = i < 250 ? 1 : 0;
+    running.push_back(r);
+  }
+  FtState ft;
+  ft.L = 8192;
+  ft.n_layers = 2;
+  ft.phase = FtPhase::Forward;
+  ft.minibatch = 0;
+  const double budget = 10.0;
+  IterationPlan pl = plan_iteration(q, running, ft, p, cfg, mem, budget);
+  int64_t n_pre = 0;
+  for (const auto& c : pl.prefill) n_pre += c.len;
+  CHECK(inference_cost(p, (int64_t)pl.decode.size(), n_pre) <= budget);
+  CHECK(pl.decode.size() == 180);   // (10 - 1) / 0.05
+  CHECK(pl.predicted_ms <= budget + 1e-9);
+  // single-profile backward window: capped by max_tokens even with a larger window cap
+  LatencyProfile flat;
+  flat.t0_ms = 0;
+  flat.slope_ms_per_token = 1e-4;
+  SchedulerConfig c2;
+  c2.max_tokens = 1024;
+  c2.max_ft_window = 8192;
+  FtState b;
+  b.L = 8192;
+  b.n_layers = 2;
+  b.l = b.L;
+  b.phase = FtPhase::Backward;
+  b.layer = 1;
+  b.lj = 8192;
+  b.minibatch = 0;
+  std::deque<Request> q2;
+  std::vector<Request> r2;
+  IterationPlan pb = plan_iteration(q2, r2, b, flat, c2, mem, 50.0);
+  CHECK(pb.s == 1024 && pb.bwd.size() == 1 && pb.bwd[0].s == 1024);
+}
+
 static void test_workload() {
   WorkloadConfig w;
   w.rate_rps = 0;
@@ -285,6 +342,7 @@ int main() {
   test_memory_model();
   test_advance_finetune();
   test_plan_iteration();
+  test_plan_row_slopes_and_caps();
   test_workload();
   test_sim_loop();
   test_vtc();

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     for n in declared_functions():
         assert hasattr(lib, n)
-    assert lib.cs_version() == 2
+    assert lib.cs_version() == 3
 
 
 def test_library_is_sm100a():
