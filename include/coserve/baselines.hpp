@@ -6,8 +6,16 @@
 //   * dynamic temporal sharing (DTS, PAPER.md:528-590 Algorithm "Dynamic Temporal Sharing"):
 //     the number of inference steps before the next finetuning iteration follows queue /
 //     spike / backlog pressure with hysteresis and a decision delay.
-// Spatial sharing is out of scope here (SPEC.md models it as a fractional split with an
-// interference coefficient, not as a GPU mechanism).
+//   * spatial sharing (§3 / Fig. 1(c)(d)): a fraction rho of the GPU
+//     serves inference and 1 - rho finetunes, concurrently, each side slowed by the
+//     interference coefficient gamma: an inference iteration takes gamma / rho of its
+//     dedicated-GPU time, and in that tick the finetuning side does (1 - rho) / gamma of the
+//     tick's length of dedicated-GPU finetuning work;
+//   * resource isolation ("two separate memory/cost models and a static request
+//     router"): the same split with no interference (gamma = 1) -- dedicated capacity for each
+//     workload, nothing shared.
+// The split is the spec's fractional abstraction ("no MPS/MIG modeling"): both
+// sides' kernels really run on the engine, the clock charges the modelled concurrency.
 #pragma once
 #include <algorithm>
 #include <cstdint>
@@ -18,7 +26,15 @@
 
 namespace coserve {
 
-enum class Policy : int { Coserve = 0, TemporalFixed = 1, Dts = 2 };
+enum class Policy : int { Coserve = 0, TemporalFixed = 1, Dts = 2, Spatial = 3, Isolate = 4 };
+
+// SpatialSplit: inference fraction rho in (0, 1), interference gamma >= 1
+struct SpatialSplit {
+  double rho = 0.5;
+  double gamma = 1.15;  // SPEC.md:529 default
+  double inf_factor() const { return gamma / rho; }          // inference latency multiplier
+  double ft_factor() const { return (1.0 - rho) / gamma; }   // finetuning throughput multiplier
+};
 
 // DtsState (f_p initial value 64 is SPEC.md's design decision, the paper
 // never initialises it)

@@ -82,6 +82,7 @@ struct LoopConfig {
   // iterations, after temporal_n inference iterations (fixed) or when DTS says so
   Policy policy = Policy::Coserve;
   int temporal_n = 128;
+  SpatialSplit split;           // Policy::Spatial / Isolate (Isolate forces gamma = 1)
   bool sim_clock = false;       // advance the clock by predicted latency even with an executor
   // Virtual Token Counter fair admission across tenants (coserve/vtc.hpp, App. C);
   // finetuning tokens are charged to ft_tenant (-1: to nobody)
@@ -180,7 +181,10 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
   }
   double corr[3] = {1.0, 1.0, 1.0};  // adaptive, per FT phase (none / forward / backward)
-  const bool temporal = cfg.policy != Policy::Coserve;
+  const bool spatial = cfg.policy == Policy::Spatial || cfg.policy == Policy::Isolate;
+  const bool temporal = cfg.policy == Policy::TemporalFixed || cfg.policy == Policy::Dts;
+  SpatialSplit split = cfg.split;
+  if (cfg.policy == Policy::Isolate) split.gamma = 1.0;
   DtsState dts;
   VtcLedger vtc;
   vtc.w_p = cfg.vtc_wp;
@@ -248,8 +252,13 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     std::vector<int64_t> vtc_admitted;
     if (cfg.vtc && !(temporal && ft_block))
       vtc_admitted = admit_requests_vtc(queue, running, mem, sched, vtc);
-    IterationPlan plan;
-    if (!temporal) {
+    IterationPlan plan, fplan;
+    if (spatial) {
+      // inference partition: sized so its slowed iteration (x gamma / rho) fits the budget
+      FtState idle = ft;
+      idle.phase = FtPhase::Idle;
+      plan = plan_iteration(queue, running, idle, prof, sched, mem, budget / split.inf_factor());
+    } else if (!temporal) {
       plan = plan_iteration(queue, running, ft, prof, sched, mem, budget);
     } else if (ft_block) {
       plan = plan_ft_block(ft, prof, cfg.sched);
@@ -260,6 +269,21 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       if (plan.c == 0 && ft.L > 0) {  // nothing to serve: the finetuning iteration runs now
         ft_block = true;
         plan = plan_ft_block(ft, prof, cfg.sched);
+      }
+    }
+    // spatial: the tick is the inference iteration slowed by gamma / rho (one budget period when
+    // there is no inference work); the finetuning partition gets (1 - rho) / gamma of it
+    double tick = 0.0;
+    if (spatial) {
+      tick = plan.c > 0 ? plan.predicted_ms * split.inf_factor() : budget;
+      std::deque<Request> no_q;
+      std::vector<Request> no_r;
+      SchedulerConfig fs = sched;
+      fs.external_admission = true;
+      fplan = plan_iteration(no_q, no_r, ft, prof, fs, mem, prof.t0_ms + tick * split.ft_factor());
+      if (!enforce_dependencies(fplan, ft)) {
+        st.ok = false;
+        return st;
       }
     }
     if (!enforce_dependencies(plan, ft)) {
@@ -288,7 +312,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       g.sample = pc.start + pc.len == r.prompt_len;
       in.segs.push_back(std::move(g));
     }
-    const int64_t s = plan.s;
+    int64_t s = plan.s;  // (spatial: the finetuning partition's, set after the steps)
     if (s > 0) {
       in.ft_phase = plan.ft_phase;
       in.ft_L = ft.L;
@@ -315,7 +339,7 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     StepOutput out;
     if (exec) {
       in.cycle_begin = cycle_t;
-      if (!exec->run(in, out)) {
+      if (!(spatial && in.segs.empty()) && !exec->run(in, out)) {
         st.ok = false;
         return st;
       }
@@ -325,7 +349,53 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
       out.device_ms = plan.predicted_ms;
       out.next_tokens.assign(in.segs.size(), 0);
     }
-    if (cfg.adaptive && plan.predicted_ms > 0 && out.device_ms > 0) {
+    if (spatial) {
+      // the finetuning partition's windows (their kernels run on the engine too; the clock
+      // charges the modelled concurrency, not their dedicated-GPU time)
+      if (exec && fplan.s > 0) {
+        StepInput fi;
+        fi.ft_phase = fplan.ft_phase;
+        fi.ft_L = ft.L;
+        fi.ft_pages = &ft_pages;
+        if (fplan.ft_phase == FtPhase::Forward) {
+          fi.ft_l = ft.l;
+          fi.ft_s = (int)fplan.s;
+          StepSegment g;
+          g.kind = 2;
+          g.tokens.assign(ft_tokens.begin() + ft.l, ft_tokens.begin() + ft.l + fplan.s);
+          g.ctx_start = ft.l;
+          g.pages = &ft_pages;
+          g.adapter = true;
+          fi.segs.push_back(std::move(g));
+          for (int64_t i = ft.l; i < ft.l + fplan.s; ++i) fi.ft_targets.push_back(i + 1 < ft.L ? ft_tokens[i + 1] : -1);
+        } else {
+          fi.ft_l = fplan.bwd[0].lj;
+          fi.ft_layer = fplan.bwd[0].layer;
+          fi.ft_s = fplan.bwd[0].s;
+          fi.extra_bwd.assign(fplan.bwd.begin() + 1, fplan.bwd.end());
+        }
+        StepOutput fo;
+        fi.cycle_begin = cycle_t;
+        if (!exec->run(fi, fo)) {
+          st.ok = false;
+          return st;
+        }
+        cycle_t = fo.t_end.time_since_epoch().count() ? fo.t_end : std::chrono::steady_clock::now();
+      }
+      // the tick replaces the inference step's own time on the clock (measured x gamma / rho
+      // with an executor, predicted otherwise)
+      const double t_inf = exec && !cfg.sim_clock && plan.c > 0 ? out.ms : plan.predicted_ms;
+      tick = plan.c > 0 ? t_inf * split.inf_factor() : budget;
+      out.ms = tick;
+      out.device_ms = tick;
+      plan.s = s = fplan.s;
+      plan.ft_phase = fplan.ft_phase;
+      plan.ft_layer = fplan.ft_layer;
+      plan.ft_l = fplan.ft_l;
+      plan.bwd = fplan.bwd;
+      plan.predicted_ms = tick;
+    }
+    if (cfg.adaptive && !spatial && plan.predicted_ms > 0 && out.device_ms > 0) {
       const int ph = plan.ft_phase == FtPhase::Forward ? 1 : (plan.ft_phase == FtPhase::Backward ? 2 : 0);
       // the step ran with corr[cph]; blend towards the measured ratio of its own phase
       const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));

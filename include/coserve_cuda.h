@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 3  /* 2: policy / VTC / tail-control / sim-clock config fields, per-tenant stats, fwd_window_ms; 3: ITL + timed-arrival SLO stats */
+#define CS_ABI_VERSION 3  /* 2: policy / VTC / tail-control / sim-clock config fields, per-tenant stats, fwd_window_ms; 3: ITL + timed-arrival SLO stats, spatial / isolation policies */
 
 #define CS_OK 0
 #define CS_ERR_INVALID_ARGUMENT (-1)
@@ -241,6 +241,9 @@ typedef struct cs_coserve_config {
   /* tail control (adaptive runs; 0 = off): planner budget = tail_target x TPOT SLO / q95 of
    * the recent measured/predicted iteration-time ratios */
   double tail_target;
+  /* policy 3 spatial sharing / 4 resource isolation: inference fraction
+   * spatial_rho in (0, 1), interference spatial_gamma >= 1 (< 1 -> 1.15; isolation: 1) */
+  double spatial_rho, spatial_gamma;
 } cs_coserve_config;
 
 typedef struct cs_coserve_stats {

@@ -354,7 +354,7 @@ def plan_iteration(queue: deque, running: List[Request], ft: FtState, prof: Prof
 
 # ---------------------------------------------------------------- baseline policies
 # PAPER.md §8.2 / SPEC.md:474-548 (include/coserve/baselines.hpp)
-COSERVE, TEMPORAL, DTS = 0, 1, 2
+COSERVE, TEMPORAL, DTS, SPATIAL, ISOLATE = 0, 1, 2, 3, 4
 
 
 class DtsState:
@@ -432,7 +432,7 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
         growth: int, ft_len: int, iters: int, prepopulate: int = 0, max_batch: int = 64,
         chunk: int = 512, max_tokens: int = 8192, max_ft_window: int = 8192,
         budget: Optional[float] = None, tpot_slo: float = 50.0, multi_layer: bool = False,
-        policy: int = COSERVE, temporal_n: int = 128):
+        policy: int = COSERVE, temporal_n: int = 128, rho: float = 0.5, gamma: float = 1.15):
     """coserve_loop.hpp run_coserve on the simulated clock.
     Returns the per-iteration log (list of dicts)."""
     budget = tpot_slo if budget is None else budget
@@ -465,7 +465,9 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
         r.pages = pages
         running.append(r)
     log = []
-    temporal = policy != COSERVE
+    temporal = policy in (TEMPORAL, DTS)
+    spatial = policy in (SPATIAL, ISOLATE)           # baselines.hpp SpatialSplit
+    g_int = 1.0 if policy == ISOLATE else gamma
     dts = DtsState()
     inf_since_ft, ft_block = 0, False
     for _ in range(iters):
@@ -489,7 +491,19 @@ def run(prof: Profile, w: Workload, seed: int, n_layers: int, page_size: int, to
                     running.pop(i)
                     continue
             i += 1
-        if not temporal:
+        if spatial:
+            idle = FtState(L=ft.L, n_layers=ft.n_layers, phase=0, minibatch=ft.minibatch,
+                           l=ft.l, layer=ft.layer, lj=ft.lj)
+            plan = plan_iteration(queue, running, idle, prof, max_batch, chunk, max_tokens,
+                                  max_ft_window, mem, budget / (g_int / rho), multi_layer)
+            tick = plan["pred"] * (g_int / rho) if plan["c"] > 0 else budget
+            fplan = plan_iteration(deque(), [], ft, prof, max_batch, chunk, max_tokens,
+                                   max_ft_window, mem, prof.t0_ms + tick * ((1.0 - rho) / g_int),
+                                   multi_layer)
+            for k in ("s", "phase", "layer", "l", "bwd"):
+                plan[k] = fplan[k]
+            plan["pred"] = tick
+        elif not temporal:
             plan = plan_iteration(queue, running, ft, prof, max_batch, chunk, max_tokens,
                                   max_ft_window, mem, budget, multi_layer)
         elif ft_block:

@@ -154,9 +154,15 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.prepopulate = c->prepopulate;
   L.adaptive = c->adaptive != 0;
   L.seed = c->seed;
-  if (c->policy < 0 || c->policy > 2)
-    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_coserve_run: policy must be 0, 1 or 2");
+  if (c->policy < 0 || c->policy > 4)
+    return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_coserve_run: policy must be in 0..4");
   L.policy = (coserve::Policy)c->policy;
+  if (L.policy == coserve::Policy::Spatial || L.policy == coserve::Policy::Isolate) {
+    if (!(c->spatial_rho > 0.0 && c->spatial_rho < 1.0))
+      return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_coserve_run: spatial_rho must be in (0, 1)");
+    L.split.rho = c->spatial_rho;
+    L.split.gamma = c->spatial_gamma >= 1.0 ? c->spatial_gamma : 1.15;
+  }
   L.temporal_n = c->temporal_n > 0 ? c->temporal_n : 128;
   L.sim_clock = c->sim_clock != 0;
   L.tail_target = c->tail_target > 0 && c->tail_target <= 1.0 ? c->tail_target : 0.0;

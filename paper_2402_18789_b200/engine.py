@@ -71,9 +71,9 @@ class CoserveConfig(ctypes.Structure):
                 ("policy", i32), ("temporal_n", i32), ("sim_clock", i32),
                 ("vtc", i32), ("n_tenants", i32), ("ft_tenant", i32),
                 ("tenant0_share", f64), ("vtc_wp", f64), ("vtc_wq", f64), ("vtc_wr", f64),
-                ("tail_target", f64)]
+                ("tail_target", f64), ("spatial_rho", f64), ("spatial_gamma", f64)]
 
-POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS = 0, 1, 2
+POLICY_COSERVE, POLICY_TEMPORAL, POLICY_DTS, POLICY_SPATIAL, POLICY_ISOLATE = 0, 1, 2, 3, 4
 
 
 class CoserveStats(ctypes.Structure):

@@ -250,3 +250,62 @@ def test_vtc_fairness_bounds_overloaded_tenants():
     # one; VTC admits the light tenant's requests first while its counter is lower
     done_v, done_f = st_v["tenant_done"], st_f["tenant_done"]
     assert done_v[1] / max(1, sum(done_v)) > done_f[1] / max(1, sum(done_f))
+
+
+# ---------------------------------------------------------------- spatial / isolation baselines
+@pytest.mark.parametrize("policy,rho,gamma", [(S.SPATIAL, 0.5, 1.15), (S.SPATIAL, 0.7, 1.3),
+                                              (S.ISOLATE, 0.4, 0.0)])
+def test_spatial_policies_bit_exact(policy, rho, gamma):
+    """Spatial sharing / resource isolation (coserve/baselines.hpp): the C++
+    loop and the Python restatement plan identical ticks on the simulated clock; every tick is
+    the inference iteration slowed by gamma / rho and carries the finetuning partition's
+    windows sized to (1 - rho) / gamma of it."""
+    prof = S.Profile(5.0, 0.01, S.INF, 0.3, 1e-6, 1e-7, 0.4)
+    c = _cfg(12.0, prof, 500, 1024, 4, 5, 16, 4096, 64, budget=45.0, multi_layer=True)
+    c.policy, c.spatial_rho, c.spatial_gamma = policy, rho, gamma
+    stats, log = E.coserve_run(None, c)
+    w = S.Workload(rate=12.0, duration_s=600.0, amplitude=0.0, period_s=20.0)
+    ref = S.run(prof, w, 5, 4, 16, 4096, 64, 1024, 500, prepopulate=16, budget=45.0,
+                multi_layer=True, policy=policy, rho=rho, gamma=gamma if gamma >= 1.0 else 1.15)
+    assert len(log) == len(ref) == 500
+    g = 1.0 if policy == S.ISOLATE else gamma
+    for i, (a, b) in enumerate(zip(log, ref)):
+        for k in ("c", "s", "phase", "layer", "l", "n_decode", "n_prefill", "n_running", "n_queue"):
+            assert a[k] == b[k], (i, k, a[k], b[k])
+        assert a["t_ms"] == b["t_ms"] and a["pred_ms"] == b["pred"], i
+        if a["c"] > 0:  # the inference side fits the budget only after its gamma / rho slowdown
+            assert a["pred_ms"] <= 45.0 + 1e-9
+    assert stats["minibatches_done"] >= 1
+    assert any(a["c"] > 0 and a["s"] > 0 for a in log)   # both partitions advance in one tick
+
+
+def _criterion7_cfg(seed, policy, n=0, rho=0.5):
+    # the measured 8B profile (BENCH_r01 "profile"): per-kind rows, context terms, window cost
+    prof = S.Profile(4.6, 0.0153, S.INF, 0.033, 7e-7, 7.5e-8, 0.18, 0.0149, 0.0109, 2.7)
+    c = _cfg(20.0, prof, 2500, 8192, 32, seed, 40, 24576, 128, max_batch=256, budget=45.0,
+             amplitude=0.5, multi_layer=True)
+    c.policy, c.temporal_n, c.spatial_rho, c.spatial_gamma = policy, n, rho, 1.15
+    return c
+
+
+def test_acceptance_criterion_7_slo_safety_and_policy_order():
+    """SPEC.md:780 (criterion 7): on 5 seeds of a 20 req/s burst trace, co-serving never plans
+    an iteration whose predicted latency exceeds the TPOT budget while inference is active, and
+    its inference SLO attainment is >= spatial(rho=0.5) and >= temporal(n=64) on the same
+    traces (§8.2, directional)."""
+    for seed in range(5):
+        att = {}
+        for name, pol, n in (("coserve", S.COSERVE, 0), ("spatial", S.SPATIAL, 0),
+                             ("temporal64", S.TEMPORAL, 64)):
+            c = _criterion7_cfg(seed, pol, n)
+            while True:  # the same simulated horizon (>= 100 s of the trace) for every policy
+                st, log = E.coserve_run(None, c)
+                if log[-1]["t_ms"] >= 100000.0:
+                    break
+                c.timed_iters *= 2
+            if name == "coserve":
+                assert all(a["pred_ms"] <= 50.0 for a in log if a["c"] > 0), seed
+            att[name] = st["requests_slo_ok"] / max(1, st["requests_done"])
+            assert st["requests_done"] > 50, (seed, name)
+        assert att["coserve"] >= att["spatial"], (seed, att)
+        assert att["coserve"] >= att["temporal64"], (seed, att)
