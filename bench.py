@@ -533,7 +533,7 @@ def run_ours(a):
         "data": "synthetic: random-init weights (reference init scales), Poisson arrivals, "
                 "lognormal ShareGPT-like lengths, random tokens",
         "config": {"workload": f"{MODEL_NAMES[a.model]}-shaped co-serving, LoRA r=16 on down-proj, "
-                                      (f"{a.rate:g} req/s Poisson arrivals per replica" if a.rate_scope == "replica"
+                               + (f"{a.rate:g} req/s Poisson arrivals per replica" if a.rate_scope == "replica"
                                        else f"{a.rate:g} req/s Poisson arrivals in total ({a.rate / n_groups:g} per replica)")
                                       + f", TPOT SLO {slo:g} ms, "
                                f"finetuning sequences L={a.ft_len}"
