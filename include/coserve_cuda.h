@@ -105,6 +105,18 @@ int cs_tp_group_create(int tp_size, cs_tp_group** out);
 int cs_tp_group_destroy(cs_tp_group* g); /* after every engine of the group is destroyed */
 int cs_engine_create_tp_local(const cs_model_config* cfg, int device, int tp_rank,
                               cs_tp_group* group, cs_engine** out);
+/* Cross-process peer-memory TP (one process per GPU, no NCCL): create every rank with
+ * cs_engine_create_ipc, export each rank's 64-byte CUDA IPC handle of its engine arena with
+ * cs_engine_ipc_handle, share them through any host channel (bench.py: torch.distributed),
+ * then cs_engine_ipc_attach on every rank with all ranks' handles and arena sizes in rank
+ * order ([tp_size][64] bytes, [tp_size] int64).  From then on the row-parallel GEMMs write
+ * their partial tiles straight into the owners' staging over NVLink (the fused GEMM +
+ * all-reduce of a single-process group) and the remaining all-reduces are one-shot peer
+ * kernels; cross-rank ordering is a device-side flag barrier.  Same plan on every rank. */
+int cs_engine_create_ipc(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                         cs_engine** out);
+int cs_engine_ipc_handle(cs_engine* e, void* out64, int64_t* arena_bytes);
+int cs_engine_ipc_attach(cs_engine* e, const void* handles, const int64_t* arena_bytes);
 int cs_engine_destroy(cs_engine* e);
 /* dtype: 0 = f64, 1 = f32.  name in {embed, unembed, final_norm, wq, wk, wv, wo, w_gate, w_up,
  * w_down, lora_a, lora_b, bq, bk, bv, norm1, norm2}; shapes in the reference layout. */

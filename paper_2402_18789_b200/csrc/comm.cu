@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "common.cuh"
 #include "kernels.h"
 
 namespace cs {
@@ -246,6 +247,154 @@ cudaError_t tp_reduce_bcast(float* stage, long ld, int nranks, int rank, int rpo
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   tp_reduce_bcast_kernel<<<blocks, 256, 0, st>>>(stage, ld, nranks, rank, rpo, M, h, pp, ldd, add_old);
   return cudaGetLastError();
+}
+
+// ============================================================================ IPC group
+// Device-side barrier across processes: thread j stores `epoch` into slot `rank` of rank j's
+// flag array (system-scope release: every earlier write of this rank -- the previous kernels on
+// this stream included -- is visible to rank j before the flag), then spins (acquire) until
+// rank j's store of the same epoch reached slot j of the local array.  20 s bound -> trap.
+struct IpcFlags {
+  unsigned* peer[kMaxRanks];  // peer[j] = rank j's flag array (mapped)
+  unsigned* local;
+};
+__global__ void ipc_barrier_kernel(IpcFlags f, int rank, int nranks, unsigned epoch) {
+  const int j = threadIdx.x;
+  if (j >= nranks) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.peer[j] + rank), "r"(epoch) : "memory");
+  const unsigned long long t0 = globaltimer_ns();
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f.local + j) : "memory");
+    if ((int)(v - epoch) >= 0) break;
+    if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+  }
+}
+
+namespace {
+struct IpcComm final : Comm {
+  int r = 0, n = 1, device = 0;
+  char* base = nullptr;
+  size_t bytes = 0;
+  unsigned* flags = nullptr;
+  char* peer_base[kMaxRanks] = {};
+  bool opened[kMaxRanks] = {};
+  bool attached = false;
+  unsigned epoch = 0;
+  ~IpcComm() override {
+    for (int j = 0; j < n; ++j)
+      if (opened[j]) cudaIpcCloseMemHandle(peer_base[j]);
+  }
+  int rank() const override { return r; }
+  int size() const override { return n; }
+  bool peer_capable() const override { return attached; }
+  void bind_arena(void* b, size_t nbytes, unsigned* f) override {
+    base = static_cast<char*>(b);
+    bytes = nbytes;
+    flags = f;
+  }
+  int ipc_handle(void* out64, std::string* err) override {
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, base);
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(out64, &h, 64);
+    return 0;
+  }
+  int ipc_attach(const void* handles, const int64_t* arena_bytes, std::string* err) override {
+    if (attached) return 0;
+    for (int j = 0; j < n; ++j) {
+      if (arena_bytes[j] != (int64_t)bytes) {
+        if (err) *err = "ipc_attach: ranks' engine arenas differ (different configs?)";
+        return -1;
+      }
+      if (j == r) {
+        peer_base[j] = base;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + 64 * j, 64);
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        if (err) *err = "cudaIpcOpenMemHandle(rank " + std::to_string(j) + "): " + cudaGetErrorString(e);
+        return -1;
+      }
+      peer_base[j] = static_cast<char*>(p);
+      opened[j] = true;
+    }
+    attached = true;
+    return 0;
+  }
+  int exchange_ptr(void* local, void** out, std::string* err) override {
+    // every rank's arena has the same layout: a buffer's peer address is the peer's arena
+    // base plus the local offset
+    const char* p = static_cast<const char*>(local);
+    if (!attached || p < base || p >= base + bytes) {
+      if (err) *err = attached ? "ipc exchange_ptr: pointer outside the engine arena" : "ipc group not attached";
+      return -1;
+    }
+    for (int j = 0; j < n; ++j) out[j] = peer_base[j] + (p - base);
+    return 0;
+  }
+  int stream_barrier(cudaStream_t st, std::string* err) override {
+    if (!attached) {
+      if (err) *err = "ipc group not attached (cs_engine_ipc_attach)";
+      return -1;
+    }
+    IpcFlags f{};
+    const size_t off = reinterpret_cast<char*>(flags) - base;
+    for (int j = 0; j < n; ++j) f.peer[j] = reinterpret_cast<unsigned*>(peer_base[j] + off);
+    f.local = flags;
+    ++epoch;
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+    ipc_barrier_kernel<<<1, 32, 0, st>>>(f, r, n, epoch);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("ipc_barrier_kernel: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return 0;
+  }
+  int allreduce_f32(float* buf, size_t count, cudaStream_t st, std::string* err) override {
+    if (count == 0) return 0;
+    void* out[kMaxRanks] = {};
+    if (exchange_ptr(buf, out, err) != 0) return -1;
+    if ((reinterpret_cast<uintptr_t>(buf) & 15) != 0) {
+      if (err) *err = "ipc all-reduce: buffer not 16-byte aligned";
+      return -1;
+    }
+    if (stream_barrier(st, err) != 0) return -1;  // every rank's buffer is final
+    PeerPtrs pp{};
+    for (int j = 0; j < n; ++j) pp.p[j] = static_cast<float*>(out[j]);
+    const size_t per4 = (count / 4 + n - 1) / n;
+    const int blocks = (int)std::max<size_t>(1, std::min<size_t>((per4 + 255) / 256, 148 * 4));
+    cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+    peer_allreduce_kernel<<<blocks, 256, 0, st>>>(pp, n, r, count);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("peer_allreduce_kernel: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return stream_barrier(st, err);  // every slice written before anyone reads its buffer
+  }
+};
+}  // namespace
+
+Comm* make_ipc_comm(int rank, int size, int device, std::string* err) {
+  if (size < 1 || size > kMaxRanks || rank < 0 || rank >= size) {
+    if (err) *err = "ipc tp comm: need 0 <= rank < size <= 8";
+    return nullptr;
+  }
+  auto* c = new IpcComm();
+  c->r = rank;
+  c->n = size;
+  c->device = device;
+  return c;
 }
 
 LocalGroup* local_group_create(int size, std::string* err) {

@@ -6,16 +6,24 @@
 //   forward : 2 all-reduces [T, h] per layer (after O, after down [+ the LoRA up, folded])
 //   backward: 2 all-reduces [s, h] per window and layer (dX of gate||up and of QKV)
 //   Adam    : 1 all-reduce of dB [layers, r, h] per mini-batch (the folded LoRA layout)
-// Two backends behind one interface:
+// Three backends behind one interface:
 //   * NCCL (one process per GPU, ncclCommInitRank from a unique id shared by the host),
 //   * local group (ranks are engines of one process, each driven by its own host thread):
 //     a one-shot peer all-reduce kernel -- every rank reduces its 1/tp slice of all ranks'
 //     buffers in a fixed order and writes the sum back into every buffer -- ordered by
 //     CUDA events exchanged at two host barriers.  Over NVSwitch the peer pointers are
 //     NVLink loads/stores (peer access enabled); on one device the same code runs with
-//     plain device pointers, which is how the TP math is tested on a single B200.
+//     plain device pointers, which is how the TP math is tested on a single B200;
+//   * IPC group (one process per GPU, no NCCL): every rank maps the other ranks' engine arenas
+//     with CUDA IPC handles the host exchanges (cs_engine_ipc_handle / cs_engine_ipc_attach);
+//     cross-rank ordering is a device-side flag barrier (system-scope release stores into each
+//     peer's flag slots, acquire spins on the local ones), so the fused row-parallel GEMM +
+//     all-reduce and the one-shot peer all-reduce run across processes over NVLink exactly as
+//     in a single-process group.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 #include <string>
 
@@ -42,6 +50,17 @@ struct Comm {
     if (err) *err = "stream_barrier: not a peer-memory group";
     return -1;
   }
+  // the engine's device arena (IPC groups map the peers' arenas; flags: 8 zeroed uint32 in it)
+  virtual void bind_arena(void* base, size_t bytes, unsigned* flags) {}
+  // IPC groups: export this rank's arena handle / map the other ranks' (handles[tp][64])
+  virtual int ipc_handle(void* out64, std::string* err) {
+    if (err) *err = "ipc_handle: not an IPC group";
+    return -1;
+  }
+  virtual int ipc_attach(const void* handles, const int64_t* arena_bytes, std::string* err) {
+    if (err) *err = "ipc_attach: not an IPC group";
+    return -1;
+  }
 };
 
 // Second half of the fused row-parallel GEMM + all-reduce: rank `rank` owns rows
@@ -62,5 +81,6 @@ LocalGroup* local_group_create(int size, std::string* err);
 void local_group_destroy(LocalGroup* g);
 int local_group_size(const LocalGroup* g);
 Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err);
+Comm* make_ipc_comm(int rank, int size, int device, std::string* err);
 
 }  // namespace cs

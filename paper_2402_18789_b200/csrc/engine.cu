@@ -97,6 +97,8 @@ struct cs_engine {
   // zero between uses; peer tables exchanged lazily (same call order on every rank)
   float* tp_stage = nullptr;
   bool tp_fused = false;
+  bool tp_fused_allowed = true;  // CS_TP_FUSED=0 -> GEMM + separate all-reduce (A/B)
+  unsigned* ipc_flags = nullptr;  // IPC groups: [8] barrier slots, one per peer rank
   float* stage_tab[8] = {};
   std::vector<std::pair<void*, std::vector<float*>>> dst_tabs;
   // backward scratch
@@ -271,6 +273,7 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(dh1, S * h);
   AL(rope_tab, (size_t)e->max_pos * (e->d / 2));
   AL(tp_sync, 64);
+  AL(ipc_flags, 64);
   AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
   // dS^T tiles: [kv heads][64-row query tiles of a window][keys (L_max rounded to 128)][64]
   AL(ds_buf, e->bwd_dsq ? (size_t)e->Hkv * (S * e->grp / 64 + 2) * ((Lm + 127) / 128 * 128) * 64 : 1);
@@ -382,7 +385,8 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
     }
     // CS_TP_FUSED=0 keeps GEMM + separate all-reduce on peer-memory groups (A/B)
     const char* v = std::getenv("CS_TP_FUSED");
-    e->tp_fused = e->comm->peer_capable() && !(v && std::atoi(v) == 0);
+    e->tp_fused_allowed = !(v && std::atoi(v) == 0);
+    e->tp_fused = e->comm->peer_capable() && e->tp_fused_allowed;  // IPC groups: after attach
   }
   size_t total = 0;
   layout(e, true, &total);
@@ -395,6 +399,7 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
                                          ") failed: " + cudaGetErrorString(err));
   }
   layout(e, false, nullptr);
+  if (e->comm) e->comm->bind_arena(e->arena, e->arena_bytes, e->ipc_flags);
   cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking);
   cudaEventCreate(&e->ev0);
   cudaEventCreate(&e->ev1);
@@ -475,6 +480,33 @@ extern "C" int cs_engine_create_tp_local(const cs_model_config* cfg, int device,
   return create_engine(cfg, device, tp_rank, n,
                        [&](std::string* err) { return cs::make_local_comm(group->g, tp_rank, device, err); },
                        out);
+}
+
+extern "C" int cs_engine_create_ipc(const cs_model_config* cfg, int device, int tp_rank, int tp_size,
+                                    cs_engine** out) {
+  return create_engine(cfg, device, tp_rank, tp_size,
+                       [&](std::string* err) { return cs::make_ipc_comm(tp_rank, tp_size, device, err); },
+                       out);
+}
+
+extern "C" int cs_engine_ipc_handle(cs_engine* e, void* out64, int64_t* arena_bytes) {
+  if (!e || !out64 || !arena_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "ipc_handle: null argument");
+  if (!e->comm) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "ipc_handle: not a tensor-parallel engine");
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  std::string err;
+  if (e->comm->ipc_handle(out64, &err) != 0) return cs::set_error(CS_ERR_INVALID_ARGUMENT, err);
+  *arena_bytes = (int64_t)e->arena_bytes;
+  return CS_OK;
+}
+
+extern "C" int cs_engine_ipc_attach(cs_engine* e, const void* handles, const int64_t* arena_bytes) {
+  if (!e || !handles || !arena_bytes) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "ipc_attach: null argument");
+  if (!e->comm) return cs::set_error(CS_ERR_INVALID_ARGUMENT, "ipc_attach: not a tensor-parallel engine");
+  CS_CUDA_TRY(cudaSetDevice(e->device));
+  std::string err;
+  if (e->comm->ipc_attach(handles, arena_bytes, &err) != 0) return cs::set_error(CS_ERR_RUNTIME, err);
+  e->tp_fused = e->comm->peer_capable() && e->tp_fused_allowed;
+  return CS_OK;
 }
 
 extern "C" int cs_engine_set_profiling(cs_engine* e, int on) {

@@ -129,8 +129,12 @@ def _declare_engine(L):
     L.cs_tp_group_create.argtypes = [ctypes.c_int, P(vp)]
     L.cs_tp_group_destroy.argtypes = [vp]
     L.cs_engine_create_tp_local.argtypes = [P(ModelConfig), ctypes.c_int, ctypes.c_int, vp, P(vp)]
+    L.cs_engine_create_ipc.argtypes = [P(ModelConfig), ctypes.c_int, ctypes.c_int, ctypes.c_int, P(vp)]
+    L.cs_engine_ipc_handle.argtypes = [vp, vp, P(i64)]
+    L.cs_engine_ipc_attach.argtypes = [vp, vp, vp]
     for name in ("cs_nccl_unique_id", "cs_tp_group_create", "cs_tp_group_destroy",
-                 "cs_engine_create_tp_local"):
+                 "cs_engine_create_tp_local", "cs_engine_create_ipc", "cs_engine_ipc_handle",
+                 "cs_engine_ipc_attach"):
         getattr(L, name).restype = ctypes.c_int
     L.cs_engine_alloc_audit.restype = ctypes.c_int
     L.cs_engine_alloc_audit.argtypes = [vp, vp, vp, P(i64)]
@@ -247,7 +251,10 @@ def tp_run(engines: Sequence["Engine"], fn):
 
 class Engine:
     def __init__(self, cfg: ModelConfig, device: int = 0, tp_rank: int = 0, tp_size: int = 1,
-                 group: Optional[TPGroup] = None, nccl_uid: Optional[bytes] = None):
+                 group: Optional[TPGroup] = None, nccl_uid: Optional[bytes] = None,
+                 ipc: bool = False):
+        """tp_size > 1: group -> single-process peer group; ipc -> cross-process CUDA-IPC peer
+        group (attach with tp_ipc.connect); else NCCL from nccl_uid."""
         self.cfg = cfg
         self._L = lib()
         self.tp_rank = tp_rank
@@ -257,6 +264,9 @@ class Engine:
             _lib.check(self._L.cs_engine_create_tp_local(ctypes.byref(cfg), device, tp_rank,
                                                          group._h, ctypes.byref(h)),
                        "cs_engine_create_tp_local")
+        elif ipc:
+            _lib.check(self._L.cs_engine_create_ipc(ctypes.byref(cfg), device, tp_rank, tp_size,
+                                                    ctypes.byref(h)), "cs_engine_create_ipc")
         else:
             uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
             _lib.check(self._L.cs_engine_create(ctypes.byref(cfg), device, tp_rank, tp_size, uid,
@@ -270,6 +280,22 @@ class Engine:
         if getattr(self, "_h", None):
             self._L.cs_engine_destroy(self._h)
             self._h = None
+
+    # -------------------------------------------------------------- IPC peer group
+    def ipc_handle(self):
+        """(64-byte CUDA IPC handle of this rank's engine arena, arena bytes)."""
+        buf = ctypes.create_string_buffer(64)
+        n = i64()
+        _lib.check(self._L.cs_engine_ipc_handle(self._h, buf, ctypes.byref(n)), "cs_engine_ipc_handle")
+        return buf.raw, n.value
+
+    def ipc_attach(self, handles: Sequence[bytes], arena_bytes: Sequence[int]):
+        """Map the other ranks' arenas (handles / sizes in tp-rank order)."""
+        if len(handles) != self.tp_size or any(len(h) != 64 for h in handles):
+            raise ValueError("ipc_attach: one 64-byte handle per tp rank")
+        hb = ctypes.create_string_buffer(b"".join(handles), 64 * self.tp_size)
+        sz = (i64 * self.tp_size)(*arena_bytes)
+        _lib.check(self._L.cs_engine_ipc_attach(self._h, hb, sz), "cs_engine_ipc_attach")
 
     def __del__(self):
         try:
