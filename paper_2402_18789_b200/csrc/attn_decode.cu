@@ -3,19 +3,21 @@
 // m16 tile: q_len * group <= 16).
 //
 // Work item = (segment, kv head, key range [k_begin, k_end)); the host balances the key
-// ranges over the SMs (flash-decoding split; partials merged by attn_combine_kernel).
-// Inside a CTA the 4 warps are independent streams over interleaved 32-key tiles:
-//   * each warp runs its own STAGES-deep TMA ring: lane 0 issues the tile as 16-row boxes
-//     (one page chunk each, SWIZZLE_128B) for K and V on one mbarrier -- 8 instructions per
-//     16 KB instead of a per-lane page-table walk (the cp.async version of this kernel spent
-//     most of its issue slots on that address arithmetic; ncu, profiles/),
-//   * the query tile is the GQA group packed into the M=16 rows of one mma.m16n8k16
-//     (4 useful rows for LLaMA-8B, 5 for Qwen) held in registers for the whole loop,
-//   * S = Q K^T and O += P V on mma.sync (16 FLOP per K/V byte: far below the HMMA roof),
-//     online softmax in the log2 domain with quad shuffles, O rescaled only when a row's
-//     running max moves,
-// then the warps' (m, l, O) are merged through shared memory.  Only K/V bytes touch HBM
-// in the loop: the algorithmic traffic is 2 * ctx * d * 2 B per (request, kv head).
+// ranges over the SMs (flash-decoding split).  Every warp is a persistent stream over items:
+//   * its own STAGES-deep TMA ring: lane 0 issues each 32-key tile as 16-row boxes (one page
+//     chunk each, SWIZZLE_128B) for K and V on one mbarrier -- 8 instructions per 16 KB
+//     instead of a per-lane page-table walk (the cp.async version spent most of its issue
+//     slots on that address arithmetic; profiles/r1_decode_ncu.txt), running across items;
+//   * attn_decode_swap_kernel (items of <= 8 GQA-packed rows, every decode row of LLaMA /
+//     Qwen): swapped operands, S^T = K Q^T and O^T = V^T P^T on mma.sync with the keys / head
+//     dims on M and the rows on N = 8;
+//   * attn_decode_stream_kernel (9-16 rows): the rows on M = 16.
+// Split items' partials are merged by attn_combine_kernel (PDL-launched).  Merging them in
+// the decode kernel instead -- the part that finishes last reads the group's partials --
+// measured slower at the 8B operating point (35.8 -> 52.6 us per launch: every part pays a
+// threadfence + atomic, and the merging warp's dependent loads stall its stream).
+// Online softmax in the log2 domain; only K/V bytes touch HBM in the loop: the algorithmic
+// traffic is 2 * ctx * d * 2 B per (request, kv head).
 #include <cfloat>
 
 #include <algorithm>
@@ -50,250 +52,6 @@ CS_DEV uint32_t tile_off(int r, int c) {
   return (uint32_t)((c >> 3) * (KT * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 }  // namespace
-
-// NWARP warps per CTA, each with a STAGES-deep ring; (NWARP, STAGES) set the CTAs per SM
-// (shared memory) and so how many items' prologues / epilogues overlap other items' streams
-template <int D, int KT, int NWARP, int STAGES>
-__global__ void __launch_bounds__(NWARP * 32, 1)
-    attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       AttnFwdParams p) {
-  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
-  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
-  constexpr int NH = D / 64;                       // 64-column halves
-  constexpr int HALF = KT * 128;                   // one half of a K (or V) tile
-  constexpr int TILE = NH * HALF;                  // K (or V) tile bytes
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-
-  const AttnDecWork* wp = p.dwork + blockIdx.x;
-  struct {
-    int q_row, pos0, page_off, kv_head, k_begin, k_end, part, nq;
-  } w;
-  {
-    const int4 a = __ldg(reinterpret_cast<const int4*>(wp));
-    const int4 b = __ldg(reinterpret_cast<const int4*>(wp) + 1);
-    w = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = p.grp;
-  const int nrows = w.nq * grp;  // <= 16
-  uint8_t* ws = smem + warp * (STAGES * 2 * TILE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NWARP * STAGES * 2 * TILE) + warp * STAGES;
-
-  const int kt0 = w.k_begin / KT, kt1 = (w.k_end + KT - 1) / KT;
-  const int n_my = max(0, (kt1 - kt0 - warp + NWARP - 1) / NWARP);
-  if (lane == 0) {
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-  }
-  __syncwarp();
-
-  // lane 0 issues the tile: 2 boxes (16 keys = one page chunk) x NH halves, for K and for V.
-  // Boxes past k_end re-load the last valid box (finite data under a -inf score mask).
-  const int last_box = (w.k_end - 1) & ~15;
-  auto issue = [&](int i) {
-    const int kt = kt0 + warp + i * NWARP, st = i % STAGES;
-    uint8_t* dk = ws + st * 2 * TILE;
-    uint8_t* dv = dk + TILE;
-    mbar_arrive_expect_tx(&full[st], 2 * TILE);
-#pragma unroll
-    for (int b = 0; b < KT / 16; ++b) {
-      const int jb = min(kt * KT + b * 16, last_box);
-      const int bi = (jb - w.k_begin) >> 4;  // host-resolved rows for the first 8 boxes
-      const int prow = bi < 8 ? __ldg(wp->prow + bi)
-                              : __ldg(p.page_table + w.page_off + jb / p.page_size) * p.page_size + jb % p.page_size;
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh) {
-        const int col = w.kv_head * D + hh * 64;
-        tma_load_2d(&tmK, &full[st], dk + hh * HALF + b * 2048, col, prow);
-        tma_load_2d(&tmV, &full[st], dv + hh * HALF + b * 2048, col, prow);
-      }
-    }
-  };
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < STAGES - 1; ++i)
-      if (i < n_my) issue(i);
-  }
-
-  // ---- Q fragment (A operand, rows = packed (query row, head-in-group)) from global
-  const int ra = lane >> 2, rb = ra + 8;
-  const __nv_bfloat16* qa = nullptr;
-  const __nv_bfloat16* qb = nullptr;
-  if (ra < nrows)
-    qa = p.q + (long)(w.q_row + ra / grp) * p.q_ld + (long)(w.kv_head * grp + ra % grp) * D;
-  if (rb < nrows)
-    qb = p.q + (long)(w.q_row + rb / grp) * p.q_ld + (long)(w.kv_head * grp + rb % grp) * D;
-  uint32_t qf[D / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < D / 16; ++kk) {
-    const int col = kk * 16 + 2 * (lane & 3);
-    qf[kk][0] = qa ? ld_u32(qa + col) : 0u;
-    qf[kk][1] = qb ? ld_u32(qb + col) : 0u;
-    qf[kk][2] = qa ? ld_u32(qa + col + 8) : 0u;
-    qf[kk][3] = qb ? ld_u32(qb + col + 8) : 0u;
-  }
-  const int pos_a = ra < nrows ? w.pos0 + ra / grp : -1;
-  const int pos_b = rb < nrows ? w.pos0 + rb / grp : -1;
-
-  float o[D / 8][4];
-#pragma unroll
-  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
-
-  for (int i = 0; i < n_my; ++i) {
-    if (lane == 0 && i + STAGES - 1 < n_my) issue(i + STAGES - 1);
-    const int st = i % STAGES;
-    mbar_wait(&full[st], (uint32_t)((i / STAGES) & 1));
-    const uint32_t kb = smem_u32(ws + st * 2 * TILE), vb = kb + TILE;
-    const int kt = kt0 + warp + i * NWARP;
-
-    float s[KT / 8][4];
-#pragma unroll
-    for (int n = 0; n < KT / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-#pragma unroll
-      for (int nbp = 0; nbp < KT / 16; ++nbp) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + tile_off<KT>(nbp * 16 + (lane & 7) + ((lane >> 4) << 3), kk * 2 + ((lane >> 3) & 1)),
-                b0, b1, b2, b3);
-        mma16816(s[2 * nbp], qf[kk], b0, b1);
-        mma16816(s[2 * nbp + 1], qf[kk], b2, b3);
-      }
-    }
-    float mx_a = -INFINITY, mx_b = -INFINITY;
-#pragma unroll
-    for (int nb = 0; nb < KT / 8; ++nb) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = kt * KT + nb * 8 + 2 * (lane & 3) + (e & 1);
-        const int pos = e < 2 ? pos_a : pos_b;
-        float v = s[nb][e] * p.scale_log2;
-        if (j > pos || j >= w.k_end) v = -INFINITY;
-        s[nb][e] = v;
-      }
-      mx_a = fmaxf(mx_a, fmaxf(s[nb][0], s[nb][1]));
-      mx_b = fmaxf(mx_b, fmaxf(s[nb][2], s[nb][3]));
-    }
-    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
-    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
-    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
-    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
-    const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
-    const float mu_a = mn_a == -INFINITY ? 0.f : mn_a;
-    const float mu_b = mn_b == -INFINITY ? 0.f : mn_b;
-    float rs_a = 0.f, rs_b = 0.f;
-#pragma unroll
-    for (int nb = 0; nb < KT / 8; ++nb) {
-      s[nb][0] = exp2f(s[nb][0] - mu_a);
-      s[nb][1] = exp2f(s[nb][1] - mu_a);
-      s[nb][2] = exp2f(s[nb][2] - mu_b);
-      s[nb][3] = exp2f(s[nb][3] - mu_b);
-      rs_a += s[nb][0] + s[nb][1];
-      rs_b += s[nb][2] + s[nb][3];
-    }
-    // rescale only when some row's running max moved (warp-uniform test)
-    if (__any_sync(0xffffffffu, mn_a != m_a || mn_b != m_b)) {
-      const float c_a = exp2f(m_a - mu_a), c_b = exp2f(m_b - mu_b);
-      l_a *= c_a;
-      l_b *= c_b;
-#pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o[n][0] *= c_a;
-        o[n][1] *= c_a;
-        o[n][2] *= c_b;
-        o[n][3] *= c_b;
-      }
-    }
-    m_a = mn_a;
-    m_b = mn_b;
-    l_a += rs_a;
-    l_b += rs_b;
-#pragma unroll
-    for (int kk = 0; kk < KT / 16; ++kk) {
-      uint32_t a[4];
-      a[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-      a[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-      a[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      a[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-#pragma unroll
-      for (int dp = 0; dp < D / 16; ++dp) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + tile_off<KT>(kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), dp * 2 + (lane >> 4)),
-                  b0, b1, b2, b3);
-        mma16816(o[2 * dp], a, b0, b1);
-        mma16816(o[2 * dp + 1], a, b2, b3);
-      }
-    }
-    __syncwarp();  // every lane is done reading this stage before lane 0 refills it
-  }
-  l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
-  l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
-  l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
-  l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
-  __syncthreads();  // all warps done with their rings (every issued tile was waited on)
-
-  // ---- merge the warps' partial softmax states
-  float* sm_o = reinterpret_cast<float*>(smem);       // [NWARP][16][D]
-  float* sm_m = sm_o + NWARP * 16 * D;                // [NWARP][16]
-  float* sm_l = sm_m + NWARP * 16;                    // [NWARP][16]
-  {
-    float* wo = sm_o + warp * 16 * D;
-#pragma unroll
-    for (int n = 0; n < D / 8; ++n) {
-      const int d = n * 8 + 2 * (lane & 3);
-      *reinterpret_cast<float2*>(wo + ra * D + d) = make_float2(o[n][0], o[n][1]);
-      *reinterpret_cast<float2*>(wo + rb * D + d) = make_float2(o[n][2], o[n][3]);
-    }
-    if ((lane & 3) == 0) {
-      sm_m[warp * 16 + ra] = m_a;
-      sm_m[warp * 16 + rb] = m_b;
-      sm_l[warp * 16 + ra] = l_a;
-      sm_l[warp * 16 + rb] = l_b;
-    }
-  }
-  __syncthreads();
-  // thread -> (row r, 4 consecutive columns); rows beyond nrows idle
-  for (int idx = threadIdx.x; idx < nrows * (D / 4); idx += NWARP * 32) {
-    const int r = idx / (D / 4), d = (idx % (D / 4)) * 4;
-    float M = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < NWARP; ++k) M = fmaxf(M, sm_m[k * 16 + r]);
-    float L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (M > -INFINITY) {
-#pragma unroll
-      for (int k = 0; k < NWARP; ++k) {
-        const float mk = sm_m[k * 16 + r];
-        const float wk = mk == -INFINITY ? 0.f : exp2f(mk - M);
-        L += sm_l[k * 16 + r] * wk;
-        const float4 v = *reinterpret_cast<const float4*>(sm_o + (k * 16 + r) * D + d);
-        acc.x += v.x * wk;
-        acc.y += v.y * wk;
-        acc.z += v.z * wk;
-        acc.w += v.w * wk;
-      }
-    }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    const float lse = L > 0.f ? (M + __log2f(L)) * kLn2 : -INFINITY;
-    const int qr = r / grp, g = r - qr * grp;
-    if (w.part < 0) {
-      const long row = w.q_row + qr;
-      const int qh = w.kv_head * grp + g;
-      __nv_bfloat16* dst = p.out + row * p.out_ld + (long)qh * D + d;
-      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc.x * inv, acc.y * inv);
-      *reinterpret_cast<uint32_t*>(dst + 2) = pack_bf16(acc.z * inv, acc.w * inv);
-      if (d == 0 && p.lse) p.lse[row * p.lse_ld + qh] = lse;
-    } else {
-      *reinterpret_cast<float4*>(p.part_o + ((long)w.part * 64 + r) * D + d) =
-          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-      if (d == 0) p.part_lse[(long)w.part * 64 + r] = lse;
-    }
-  }
-}
 
 // ---------------------------------------------------------------- persistent streams
 // Every warp is an independent, persistent stream over whole work items (items gw, gw + W,
@@ -763,26 +521,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 }
 
 namespace {
-struct DecVariant {
-  int stream, kt, nwarp, stages;
-};
-// CS_DEC_CFG=[k]<kt><nwarp><stages> (A/B testing): 3243 = per-item CTAs, 32-key tiles, 4 warps
-// x 3 stages; a leading 1 = persistent per-warp streams (attn_decode_stream_kernel), 2 = the
-// swapped-operand streams (attn_decode_swap_kernel)
-DecVariant dec_variant() {
-  static const DecVariant v = [] {
-    DecVariant d{2, 32, 2, 2};
-    if (const char* e = std::getenv("CS_DEC_CFG")) {
-      int x = std::atoi(e);
-      const int stream = x / 10000;  // 0 per-item CTAs, 1 streams, 2 swapped-operand streams
-      x %= 10000;
-      d = DecVariant{stream, x / 100, (x / 10) % 10, x % 10};
-    }
-    return d;
-  }();
-  return v;
-}
-
 template <int D, int KT, int NW, int ST>
 cudaError_t launch_dec_swap(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                             int n_work, cudaStream_t st) {
@@ -813,63 +551,26 @@ cudaError_t launch_dec_stream(const AttnFwdParams& p, const CUtensorMap& tmK, co
   return cudaGetLastError();
 }
 
-template <int D, int KT, int NW, int ST>
-cudaError_t launch_dec(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                       int n_work, cudaStream_t st) {
-  constexpr int smem = dec_smem<D, KT, NW, ST>();
-  static bool once = (cudaFuncSetAttribute(attn_decode_kernel<D, KT, NW, ST>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                      true);
-  (void)once;
-  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  launch_pdl(attn_decode_kernel<D, KT, NW, ST>, dim3(n_work), dim3(NW * 32), smem, st, tmK, tmV, p);
-  return cudaGetLastError();
-}
+// 32-key tiles, 2 warps x 2 stages per CTA, 3 CTAs per SM (scripts/decode_op.py: of the
+// {32, 16}-key x {2, 4}-warp x {2, 3, 4}-stage variants this is the fastest at the bench's
+// operating point, 100 rows x ~400 keys: 0.71 of measured HBM for the kernel)
+constexpr int kDecKT = 32, kDecNW = 2, kDecST = 2;
 
 template <int D>
 cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          int n_work, cudaStream_t st) {
-  const DecVariant v = dec_variant();
-  if (v.stream == 2) {  // swapped operands: every item's packed rows must fit N = 8
-    if (p.max_dec_rows <= 8) {
-      switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
-        case 3223: return launch_dec_swap<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
-        case 1624: return launch_dec_swap<D, 16, 2, 4>(p, tmK, tmV, n_work, st);
-        case 3242: return launch_dec_swap<D, 32, 4, 2>(p, tmK, tmV, n_work, st);
-        default: return launch_dec_swap<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
-      }
-    }
-    return launch_dec_stream<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
-  }
-  if (v.stream) {
-    switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
-      case 3222: return launch_dec_stream<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
-      case 3242: return launch_dec_stream<D, 32, 4, 2>(p, tmK, tmV, n_work, st);
-      case 1624: return launch_dec_stream<D, 16, 2, 4>(p, tmK, tmV, n_work, st);
-      case 1644: return launch_dec_stream<D, 16, 4, 4>(p, tmK, tmV, n_work, st);
-      default: return launch_dec_stream<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
-    }
-  }
-  switch (v.kt * 100 + v.nwarp * 10 + v.stages) {
-    case 3243: return launch_dec<D, 32, 4, 3>(p, tmK, tmV, n_work, st);
-    case 3223: return launch_dec<D, 32, 2, 3>(p, tmK, tmV, n_work, st);
-    case 1643: return launch_dec<D, 16, 4, 3>(p, tmK, tmV, n_work, st);
-    case 1623: return launch_dec<D, 16, 2, 3>(p, tmK, tmV, n_work, st);
-    case 1644: return launch_dec<D, 16, 4, 4>(p, tmK, tmV, n_work, st);
-    case 1614: return launch_dec<D, 16, 1, 4>(p, tmK, tmV, n_work, st);
-    default: return launch_dec<D, 32, 2, 2>(p, tmK, tmV, n_work, st);
-  }
+  if (p.max_dec_rows <= 8) return launch_dec_swap<D, kDecKT, kDecNW, kDecST>(p, tmK, tmV, n_work, st);
+  return launch_dec_stream<D, kDecKT, kDecNW, kDecST>(p, tmK, tmV, n_work, st);
 }
 }  // namespace
 
 void attn_decode_geometry(int head_dim, int* keys_per_tile, int* nwarp, int* ctas_per_sm,
                           int* streams) {
-  const DecVariant v = dec_variant();
-  const int smem = 1024 + v.nwarp * v.stages * 2 * v.kt * head_dim * 2 + v.nwarp * v.stages * 8;
-  *keys_per_tile = v.kt;
-  *nwarp = v.nwarp;
+  const int smem = 1024 + kDecNW * kDecST * 2 * kDecKT * head_dim * 2 + kDecNW * kDecST * 8;
+  *keys_per_tile = kDecKT;
+  *nwarp = kDecNW;
   *ctas_per_sm = std::max(1, std::min(16, (228 * 1024) / (smem + 1024)));
-  *streams = v.stream;
+  *streams = 2;
 }
 
 cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,

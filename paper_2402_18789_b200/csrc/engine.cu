@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <functional>
 #include <cstdlib>
@@ -1127,8 +1128,6 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     chunk = std::max<long>(4 * tile_round, (chunk + tile_round - 1) / tile_round * tile_round);
     int part = 0;
     for (const auto& c : comb) part = std::max(part, c.part0 + c.n_parts);
-    // (merging the split groups inside the decode kernel -- the last part merges -- measured
-    // slower than the separate, PDL-overlapped combine launch: one warp serialised the merge)
     std::vector<cs::AttnWork> w2;
     w2.reserve(work_dec.size());
     for (const auto& w : work_dec) {

@@ -18,7 +18,7 @@ struct AttnWork {  // one CTA of attn_fwd_kernel
   int seg, q0, nq, kv_head, k_begin, k_end, part, pad;
 };
 
-// one CTA of attn_decode_kernel: the segment fields and the KV-pool rows of the first 8
+// one decode work item (attn_decode_swap / _stream kernels): the segment fields and the KV-pool rows of the first 8
 // 16-key boxes are resolved on the host, so the kernel's prologue is one load deep (work item
 // -> TMA issue / Q loads) instead of three (work -> segment -> page table -> TMA)
 struct AttnDecWork {
@@ -39,7 +39,7 @@ struct AttnFwdParams {
   const int* page_table;
   const AttnSeg* segs;
   const AttnWork* work;
-  const AttnDecWork* dwork;  // attn_decode_kernel only
+  const AttnDecWork* dwork;  // decode kernels only
   const AttnCombine* combine;
   bf16* out;
   long out_ld;

@@ -1,0 +1,63 @@
+"""Decode attention at the bench's operating point: ~100 decoding requests of the 8B co-serving
+loop at 20 req/s (contexts = prompt lognormal(5.5, 0.8) clipped [16, 4096] + a uniform share of
+the lognormal(4.5, 0.7) generation), 8B-shaped layers.  Prints one JSON line:
+device time of the decode kernel alone (engine profile kind 5) and of the decode bracket incl.
+the split-KV combine (kind 1), their algorithmic K/V bytes and fraction of MEASURED_PEAKS hbm.
+
+  python scripts/decode_op.py [--B 100] [--layers 4] [--reps 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from scripts.kernel_sweep import make, P  # noqa: E402
+from paper_2402_18789_b200.engine import Seg, SEG_DECODE  # noqa: E402
+
+
+def contexts(B, seed=0):
+    rng = np.random.default_rng(seed)
+    prompt = np.clip(rng.lognormal(5.5, 0.8, B), 16, 4096).astype(int)
+    gen = np.clip(rng.lognormal(4.5, 0.7, B), 8, 1024).astype(int)
+    return [int(p + rng.integers(0, g)) for p, g in zip(prompt, gen)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--B", type=int, default=100)
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    ctxs = contexts(a.B)
+    pages = sum((c + P) // P + 1 for c in ctxs) + 16
+    eng = make(a.layers, pages, 256)
+    segs, base = [], 0
+    for i, c in enumerate(ctxs):
+        per = (c + P) // P + 1
+        segs.append(Seg(SEG_DECODE, [i % 1000], c, list(range(base, base + per)), sample=True))
+        base += per
+    for _ in range(3):
+        eng.step(segs)
+    eng.set_profiling(False)
+    eng.set_profiling(True)
+    for _ in range(a.reps):
+        eng.step(segs)
+    k1, k5 = eng.read_profile(1), eng.read_profile(5)
+    eng.set_profiling(False)
+    hbm = bench.load_peaks()[0]["hbm_gbs"]
+    out = {"B": a.B, "ctx_mean": float(np.mean(ctxs)), "ctx_max": max(ctxs),
+           "cfg": os.environ.get("CS_DEC_CFG", "default"), "target": os.environ.get("CS_DEC_TARGET", "default"),
+           "bytes_per_launch_MB": k5["bytes"] / max(1, k5["launches"]) / 1e6,
+           "kernel_us": 1e3 * k5["ms"] / max(1, k5["launches"]),
+           "kernel_hbm_frac": k5["bytes"] / (k5["ms"] * 1e-3) / 1e9 / hbm if k5["ms"] else None,
+           "bracket_us": 1e3 * k1["ms"] / max(1, k1["launches"]),
+           "bracket_hbm_frac": k1["bytes"] / (k1["ms"] * 1e-3) / 1e9 / hbm if k1["ms"] else None}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
