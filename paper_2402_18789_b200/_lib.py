@@ -8,7 +8,10 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcoserve_cuda.so")
+# CS_TRACE_LIB=1: the -DCS_TRACE build (in-kernel event timelines; scripts/trace_bwd.py only)
+# CS_LIB_PATH: an experiment variant built by scripts/build_variant.py
+LIB_PATH = os.environ.get("CS_LIB_PATH") or os.path.join(
+    _PKG, "libcoserve_cuda_trace.so" if os.environ.get("CS_TRACE_LIB") == "1" else "libcoserve_cuda.so")
 _LIB = None
 
 

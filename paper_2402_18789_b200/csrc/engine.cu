@@ -60,6 +60,7 @@ struct cs_engine {
   int down_rows = 0;  // per-layer rows of down_cat: h + 64 LoRA-A^T rows (MN-major dm operand)
   // CS_BWD_DSQ=1: dQ as a GEMM over the dS the dK/dV kernel stores ([window row][q head][key])
   bool bwd_dsq = false;
+  bool bwd_fused = true;  // fused dK/dV/dQ kernel (CS_BWD_FUSED=0: dK/dV + dS export + dQ GEMM)
   bf16* ds_buf = nullptr;
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
@@ -371,6 +372,9 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
      // recomputing dQ kernel) -- d = 128 and GQA groups dividing the 64-row dK/dV query tile
     const char* v = std::getenv("CS_BWD_DSQ");
     e->bwd_dsq = (!v || std::atoi(v) != 0) && c.head_dim == 128 && 64 % (c.n_heads / c.n_kv_heads) == 0;
+    const char* f = std::getenv("CS_BWD_FUSED");
+    e->bwd_fused = !f || std::atoi(f) != 0;
+    if (e->bwd_fused) e->bwd_dsq = false;
   }
 
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -1561,7 +1565,13 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
           cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
                           qbox) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
-      if (e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
+      if (e->bwd_fused) {  // dK/dV/dQ in one kernel; dQ reduce-added into fp32
+        CUtensorMap mdq;
+        if (cs::make_map_3d_f32(&mdq, bp.dq, e->d, e->Hq, s, (long)e->d * 4, bp.dq_ld * 4, 64, e->grp,
+                                64 / e->grp) != 0)
+          return cs::set_error(CS_ERR_CUDA, "attention backward: dQ TMA map creation failed");
+        CS_CUDA_TRY(cs::attn_bwd_fused(bp, mk, mv, mk128, mv128, mq3, mo3, mdq, e->Hq, st));
+      } else if (e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
         CUtensorMap mds, mk64;
         const long keys = ((long)e->L_max + 127) / 128 * 128;
         const long ntiles = (long)e->S_max * e->grp / 64 + 2;

@@ -110,6 +110,12 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
                          const CUtensorMap& tmK128, const CUtensorMap& tmV128,
                          const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
                          cudaStream_t st);
+// fused tcgen05 backward (head_dim 128, GQA group <= 8): dK / dV into ΔKVAccum and dQ (fp32,
+// zeroed here, then reduce-added per (key block, query tile) through tmDQ: {128 d, Hq, rows}
+// fp32, box {64, grp, 64 / grp})
+cudaError_t attn_bwd_fused(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                           const CUtensorMap& tmK128, const CUtensorMap& tmV128, const CUtensorMap& tmQ3,
+                           const CUtensorMap& tmO3, const CUtensorMap& tmDQ, int n_heads, cudaStream_t st);
 // tcgen05 forward for prefill / finetuning-window tiles (head_dim 128): two 128-row query tiles
 // per CTA (work items of 2 * (128 / group) positions), P kept in TMEM
 cudaError_t attn_fwd_tc2(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,

@@ -674,6 +674,20 @@ int make_map_3d_plain(CUtensorMap* out, const void* ptr, long d0, long d1, long 
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+int make_map_3d_f32(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
+                    long stride2_bytes, int box0, int box1, int box2) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)stride1_bytes, (cuuint64_t)stride2_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, (cuuint32_t)box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 namespace {
 
 template <int BN, bool SM = false>

@@ -78,6 +78,9 @@ int make_map_3d(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, lo
                 long stride2_bytes, int box1, int box2);
 int make_map_3d_plain(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
                       long stride2_bytes, int box0, int box1, int box2);
+// 3D fp32 map without swizzle (bulk tensor reduce-add targets), box = {box0, box1, box2}
+int make_map_3d_f32(CUtensorMap* out, const void* ptr, long d0, long d1, long d2, long stride1_bytes,
+                    long stride2_bytes, int box0, int box1, int box2);
 int gemm_pick_bn(long M, long N);
 
 }  // namespace cs

@@ -1,0 +1,78 @@
+// mma_rate.cu -- tcgen05.mma issue / execution rate per SM for M=128, N in {64,128,256}, K=16 bf16,
+// compile-time instruction descriptors, constant operand addresses, unrolled issue loop; NACC
+// accumulators used round-robin.  One CTA per SM on all 148 SMs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 mma_rate.cu -o mma_rate -lcuda
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../../paper_2402_18789_b200/csrc/common.cuh"
+using namespace cs;
+
+template <int N, int NACC, int TS>
+__global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 2) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0 && lane == 0) {
+    constexpr uint32_t id = idesc_bf16_f32(128, N);
+    const uint64_t da = umma_desc_sw128(smem_u32(smem)), db = umma_desc_sw128(smem_u32(smem + 32768));
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t d = tmem + (uint32_t)((j % NACC) * N);
+        if (TS)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+                       "r"(tmem + 384), "l"(db), "r"(id), "r"(1));
+        else
+          mma_bf16(d, da, db, id, 1);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+template <int N, int NACC, int TS>
+void run(const char* name) {
+  static unsigned long long* d_out = nullptr;
+  if (!d_out) cudaMalloc(&d_out, 148 * 8);
+  cudaFuncSetAttribute(k<N, NACC, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  std::vector<unsigned long long> h(148);
+  const int iters = 8192;
+  for (int rep = 0; rep < 2; ++rep) {
+    k<N, NACC, TS><<<148, 128, 65536 + 1024>>>(iters, d_out);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("%s failed\n", name); exit(1); }
+  }
+  cudaMemcpy(h.data(), d_out, 148 * 8, cudaMemcpyDeviceToHost);
+  double m = 0; for (auto v : h) m += v; m /= 148;
+  printf("%-22s %6.1f clk/mma  %6.0f MAC/clk/SM\n", name, m / iters, 128.0 * N * 16 * iters / m);
+}
+
+int main() {
+  run<64, 1, 0>("N=64  SS 1 acc");
+  run<64, 2, 0>("N=64  SS 2 acc");
+  run<64, 4, 0>("N=64  SS 4 acc");
+  run<128, 1, 0>("N=128 SS 1 acc");
+  run<128, 2, 0>("N=128 SS 2 acc");
+  run<256, 1, 0>("N=256 SS 1 acc");
+  run<64, 1, 1>("N=64  TS 1 acc");
+  run<128, 1, 1>("N=128 TS 1 acc");
+  run<256, 1, 1>("N=256 TS 1 acc");
+  return 0;
+}

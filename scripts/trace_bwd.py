@@ -5,6 +5,7 @@ import ctypes
 import json
 import os
 import sys
+os.environ["CS_TRACE_LIB"] = "1"  # the -DCS_TRACE build (python -m paper_2402_18789_b200.build --trace)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 import bench  # noqa: E402
