@@ -15,6 +15,7 @@
 // P is recomputed from Q, K and the saved LSE; exp2 on the SFU (ex2.approx), the rest on
 // FFMA2 / FADD2 / FMUL2.
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -28,8 +29,6 @@ namespace cs {
 // trace build (python -m paper_2402_18789_b200.build --trace -> libcoserve_cuda_trace.so): the
 // check reads a __device__ global, a load on the MMA issuer's critical path
 __device__ int g_trace_cta = -1;
-__device__ int g_trace_n = 0;
-__device__ int g_trace_cap = 0;
 __device__ unsigned long long* g_trace_buf = nullptr;
 __device__ __forceinline__ void trace_ev(int ev, int idx) {
 #if !defined(CS_TRACE) && !defined(CS_TRACE_CHECK)
@@ -38,10 +37,15 @@ __device__ __forceinline__ void trace_ev(int ev, int idx) {
   return;
 #endif
   if ((int)blockIdx.x != g_trace_cta || blockIdx.y != 0) return;
-  const int k = atomicAdd(&g_trace_n, 1);
-  if (k < g_trace_cap)
-    g_trace_buf[k] = ((unsigned long long)(ev & 0xFF) << 56) |
-                     ((unsigned long long)(idx & 0xFFFF) << 40) | (clock64() & 0xFFFFFFFFFFull);
+  // one slot per (event, index): a plain store, no atomic round trip on the traced path
+  if (idx < 4096 && ev < 64) {
+    unsigned long long* slot = g_trace_buf + ev * 4096 + idx;
+    if (ev == 35 || ev == 36) {  // "first seen" events: keep the earliest
+      if (*slot == 0) *slot = clock64();
+    } else {
+      *slot = clock64();
+    }
+  }
 }
 
 namespace {
@@ -808,38 +812,16 @@ __global__ void __launch_bounds__(512, 1)
         mbar_wait(kv_full, 0);
         tc_fence_after();
       }
-      for (int i = 0; i <= n; ++i) {
-        if (i < n) {  // S^T(i), dP^T(i) into the single S / dP buffer
-          const int st = i % QST;
-          mbar_wait(&q_full[st], (i / QST) & 1);
-          trace_ev(32, i);
-          if (i > 0) mbar_wait(sd_free, (i - 1) & 1);
-          tc_fence_after();
-          trace_ev(30, i);
-          const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
-          const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-              mma_bf16(tmem + TM_S, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-              mma_bf16(tmem + TM_DP, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
-            }
-            mma_commit(sd_full);
-          }
-          __syncwarp();
-        }
-        if (i > 0) {  // dV(j), dK(j), dQ^T(j) once P^T / dS^T of tile j are written
-          const int j = i - 1, st = j % QST;
-          mbar_wait(pds_full, j & 1);
-          trace_ev(33, j);
-          if (j > 0) mbar_wait(dq_free, (j - 1) & 1);
+      // two in-order streams, whichever is ready first: S^T / dP^T(i) (Q / dO of tile i landed,
+      // S / dP buffer released by the elementwise warps) and dV / dK / dQ^T(j) (P^T / dS^T of
+      // tile j written, dQ^T(j-1) read out), both probed without blocking (a try_wait with a
+      // suspend-time hint sleeps until the phase completes: S^T(i+1) then waited behind
+      // dV / dK / dQ^T(i), 1.76 -> 2.65 ms per 8K window) and a short nanosleep when neither is
+      // ready, so a late Q / dO tile never holds back the products of the previous one.
+      int si = 0, gj = 0;
+      while (gj < n) {
+        if (gj < si && mbar_test(pds_full, gj & 1) && (gj == 0 || mbar_test(dq_free, (gj - 1) & 1))) {
+          const int j = gj, st = j % QST;
           tc_fence_after();
           trace_ev(31, j);
           const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
@@ -862,6 +844,34 @@ __global__ void __launch_bounds__(512, 1)
             mma_commit(pds_free);
           }
           __syncwarp();
+          ++gj;
+          continue;
+        }
+        if (si < n && mbar_test(&q_full[si % QST], (si / QST) & 1) && (si == 0 || mbar_test(sd_free, (si - 1) & 1))) {
+          const int i = si, st = i % QST;
+          tc_fence_after();
+          trace_ev(30, i);
+          const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
+          const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
+              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
+              mma_bf16(tmem + TM_S, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
+              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
+              mma_bf16(tmem + TM_DP, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
+            }
+            mma_commit(sd_full);
+          }
+          __syncwarp();
+          ++si;
+        } else {
+          __nanosleep(32);  // neither stream is ready
         }
       }
       if (n > 0 && elect_one()) mma_commit(acc_done);
@@ -904,40 +914,32 @@ __global__ void __launch_bounds__(512, 1)
       mbar_arrive(sd_free);
       mbar_wait(&x_full[i % XST], (i / XST) & 1);
       if (lane == 0 && warp == 4) trace_ev(41, i);
-      float xl[32], xd[32];  // this half's 32 columns of -lse*log2(e) and -Delta (16-byte loads)
-      {
-        const float4* x4 = reinterpret_cast<const float4*>(xring + (i % XST) * 2 * QB + c * 32);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const float4 a = x4[t], d = x4[QB / 4 + t];
-          xl[4 * t] = a.x; xl[4 * t + 1] = a.y; xl[4 * t + 2] = a.z; xl[4 * t + 3] = a.w;
-          xd[4 * t] = d.x; xd[4 * t + 1] = d.y; xd[4 * t + 2] = d.z; xd[4 * t + 3] = d.w;
-        }
-      }
-      // full tile: every column is a real row whose position >= key, and the key is in range
-      const bool full = key < p.b && key <= p.a + qbase && qbase + rpt - 1 < nrows;
+      // valid columns of this half form one range [lo, hi): causal (row position >= key), rows
+      // inside the window and the tile, key inside [0, b)
+      const int lo = key < p.b ? max(0, grp * (key - p.a - qbase)) - c * 32 : 32;
+      const int hi = min(ROWS, grp * (nrows - qbase)) - c * 32;
+      const float4* x4 = reinterpret_cast<const float4*>(xring + (i % XST) * 2 * QB + c * 32);
       uint32_t pp[16], pd[16];
+      auto body = [&](auto masked) {
 #pragma unroll
-      for (int cc = 0; cc < 32; cc += 2) {
-        const int col = c * 32 + cc;
-        const float2 x = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2,
-                               make_float2(xl[cc], xl[cc + 1]));
-        float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-        if (!full) {
-          const int q0r = qbase + col / grp, q1r = qbase + (col + 1) / grp;
-          if (!(q0r < nrows && key <= p.a + q0r && key < p.b)) pv.x = 0.f;
-          if (!(q1r < nrows && key <= p.a + q1r && key < p.b)) pv.y = 0.f;
+        for (int cc = 0; cc < 32; cc += 2) {
+          const float4 xl4 = x4[cc >> 2], xd4 = x4[QB / 4 + (cc >> 2)];
+          const float2 xl = (cc & 2) ? make_float2(xl4.z, xl4.w) : make_float2(xl4.x, xl4.y);
+          const float2 xd = (cc & 2) ? make_float2(xd4.z, xd4.w) : make_float2(xd4.x, xd4.y);
+          const float2 x = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2, xl);
+          float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          if constexpr (decltype(masked)::value) {
+            if (cc < lo || cc >= hi) pv.x = 0.f;
+            if (cc + 1 < lo || cc + 1 >= hi) pv.y = 0.f;
+          }
+          const float2 dd = fadd2(make_float2(__uint_as_float(dv[cc]), __uint_as_float(dv[cc + 1])), xd);
+          const float2 ds = fmul2(pv, dd);
+          pp[cc >> 1] = pack_bf16(pv.x, pv.y);
+          pd[cc >> 1] = pack_bf16(ds.x, ds.y);
         }
-        if constexpr (ROWS < QB) {  // pad columns (q0r above may alias the next tile's rows)
-          if (col >= ROWS) pv.x = 0.f;
-          if (col + 1 >= ROWS) pv.y = 0.f;
-        }
-        const float2 dd = fadd2(make_float2(__uint_as_float(dv[cc]), __uint_as_float(dv[cc + 1])),
-                                make_float2(xd[cc], xd[cc + 1]));
-        const float2 ds = fmul2(pv, dd);
-        pp[cc >> 1] = pack_bf16(pv.x, pv.y);
-        pd[cc >> 1] = pack_bf16(ds.x, ds.y);
-      }
+      };
+      if (lo <= 0 && hi >= 32) body(std::false_type{});
+      else body(std::true_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&x_empty[i % XST]);
       if (i > 0) mbar_wait(pds_free, (i - 1) & 1);  // dV / dK / dQ^T of tile i-1 consumed the buffers
@@ -1107,13 +1109,11 @@ cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const C
 
 }  // namespace cs
 
+// trace build only: clock64() of event ev for tile idx of CTA (cta, 0) lands in
+// dev_buf[ev * 4096 + idx] (dev_buf: 64 x 4096 int64, zeroed by the caller); cta -1 stops
 extern "C" int64_t cs_debug_trace(int cta, void* dev_buf, int64_t capacity) {
-  int n = 0;
-  cudaMemcpyFromSymbol(&n, cs::g_trace_n, sizeof(int));
-  const int zero = 0, cap = (int)capacity;
-  cudaMemcpyToSymbol(cs::g_trace_n, &zero, sizeof(int));
-  cudaMemcpyToSymbol(cs::g_trace_cap, &cap, sizeof(int));
+  if (capacity < 64 * 4096) return -1;
   cudaMemcpyToSymbol(cs::g_trace_buf, &dev_buf, sizeof(void*));
   cudaMemcpyToSymbol(cs::g_trace_cta, &cta, sizeof(int));
-  return n;
+  return 0;
 }

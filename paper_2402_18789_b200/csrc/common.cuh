@@ -68,6 +68,46 @@ CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase, int line = __builtin_LINE()
     if (globaltimer_ns() - t0 > CS_MBAR_TIMEOUT_NS) mbar_timeout_report(b, phase, line);
   }
 }
+#elif defined(CS_MBAR_SPIN)
+// experiment: pure polling with the non-blocking test_wait (no suspension)
+CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .u64 t0, t1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t0, %%globaltimer;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t1, %%globaltimer;\n\t"
+      "sub.u64 t1, t1, t0;\n\t"
+      "setp.gt.u64 q, t1, %2;\n\t"
+      "@q trap;\n\t"
+      "bra.uni WAIT_%=;\n"
+      "DONE_%=:\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "l"((uint64_t)CS_MBAR_TIMEOUT_NS)
+      : "memory");
+}
+#elif defined(CS_MBAR_HINT)
+// experiment: try_wait with an explicit suspend-time hint (ns)
+CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .u64 t0, t1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %3;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t0, %%globaltimer;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %3;\n\t"
+      "@p bra.uni DONE_%=;\n\t"
+      "mov.u64 t1, %%globaltimer;\n\t"
+      "sub.u64 t1, t1, t0;\n\t"
+      "setp.gt.u64 q, t1, %2;\n\t"
+      "@q trap;\n\t"
+      "bra.uni WAIT_%=;\n"
+      "DONE_%=:\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "l"((uint64_t)CS_MBAR_TIMEOUT_NS), "r"(CS_MBAR_HINT)
+      : "memory");
+}
 #else
 CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -88,6 +128,23 @@ CS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 #endif
+
+// Non-blocking probe of an mbarrier phase (for schedulers that poll several barriers).
+CS_DEV bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+               "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+  return ok != 0;
+}
+
+// One try_wait with a suspend-time hint: the warp sleeps (no issue slots) until the phase
+// completes or ~ns elapse; false on timeout.
+CS_DEV bool mbar_try_wait_ns(uint64_t* bar, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+               "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase), "r"(ns) : "memory");
+  return ok != 0;
+}
 
 // ---------------------------------------------------------------- TMA
 CS_DEV void tma_prefetch_desc(const CUtensorMap* m) {

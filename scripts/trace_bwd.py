@@ -5,7 +5,7 @@ import ctypes
 import json
 import os
 import sys
-os.environ["CS_TRACE_LIB"] = "1"  # the -DCS_TRACE build (python -m paper_2402_18789_b200.build --trace)
+os.environ.setdefault("CS_TRACE_LIB", "1")  # the -DCS_TRACE build (python -m paper_2402_18789_b200.build --trace)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 import bench  # noqa: E402
@@ -15,7 +15,7 @@ from paper_2402_18789_b200.engine import Seg, SEG_FT_FWD, FT_FORWARD, FT_BACKWAR
 L = _lib.lib()
 L.cs_debug_trace.restype = ctypes.c_int64
 L.cs_debug_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64]
-buf = torch.zeros(1 << 16, dtype=torch.int64, device="cuda:0")
+buf = torch.zeros(64 * 4096, dtype=torch.int64, device="cuda:0")
 eng = bench.make_engine(0, 8192)
 ft_pages = list(range(0, 512))
 toks = [(7 * i) % 1000 for i in range(8192)]
@@ -28,8 +28,9 @@ L.cs_debug_trace(cta, buf.data_ptr(), buf.numel())
 eng.step([], ft={"phase": FT_BACKWARD, "seq_len": 8192, "l": 8192, "s": 8192, "layer": 31,
                  "pages": ft_pages})
 torch.cuda.synchronize()
-n = L.cs_debug_trace(-1, buf.data_ptr(), buf.numel())
-v = buf[:n].cpu().tolist()
-rec = sorted(((x >> 56) & 0xFF, (x >> 40) & 0xFFFF, x & 0xFFFFFFFFFF) for x in v)
+L.cs_debug_trace(-1, buf.data_ptr(), buf.numel())
+v = buf.view(64, 4096).cpu().numpy()
+evs, idxs = v.nonzero()
+rec = [(int(e), int(i), int(v[e, i])) for e, i in zip(evs, idxs)]
 json.dump(rec, open(os.path.join("gpurun_out", f"trace_{cta}.json"), "w"))
-print(n, "records")
+print(len(rec), "records")

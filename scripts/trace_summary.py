@@ -18,7 +18,7 @@ def med(x):
 
 
 for i in range(0, 8):
-    print(i, [f"{ev}:{by[ev][i]}" for ev in [34, 32, 30, 40, 41, 43, 42, 33, 31] if i in by.get(ev, {})])
+    print(i, [f"{ev}:{by[ev][i]}" for ev in [34, 37, 35, 36, 30, 40, 41, 43, 42, 31, 38, 50, 51] if i in by.get(ev, {})])
 ks = sorted(by[30])
 print("tiles", len(ks), "median S issue spacing", med([by[30][k + 1] - by[30][k] for k in ks[:-1]]))
 pairs = [("S issue -> E start", 30, 40, 0), ("E start -> E end", 40, 42, 0), ("E end -> dVdKdQ issue", 42, 31, 0),
