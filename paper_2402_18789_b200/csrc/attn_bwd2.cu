@@ -1,19 +1,8 @@
-// attn_bwd2.cu -- K9 v2: the attention part of a token-level backward window (Alg. 2 lines
-// 14-21; tiny_model.hpp:294-315 for query rows [a, b) over keys [0, b)) on
-// tcgen05 with the elementwise products kept in TMEM.
-//
-// Both kernels follow the structure of attn_fwd2.cu's forward:
-//   dkdv: CTA = 128 keys x 1 KV head, loop over 64-row packed query tiles (3-stage TMA ring of
-//         Q / dO boxes).  S^T = K Q^T and dP^T = V dO^T land in double-buffered TMEM; two
-//         elementwise warpgroups take alternate tiles, one thread per key row owning all 64
-//         columns, and write P^T, dS^T (bf16) back over the first 32 columns of S^T / dP^T;
-//         dV += P^T dO and dK += dS^T Q then read their A operand from TMEM (TS-MMA).
-//   dq  : CTA = 128 packed query rows x 1 KV head, loop over 128-key tiles.  S double-buffered
-//         in TMEM (dS aliases it: each half-row thread writes its 32 packed columns over its own
-//         S columns), dP single-buffered with an early release once it is in registers;
-//         dQ += dS K as a TS-MMA.  dQ of the window rows is final.
-// P is recomputed from Q, K and the saved LSE; exp2 on the SFU (ex2.approx), the rest on
-// FFMA2 / FADD2 / FMUL2.
+// attn_bwd2.cu -- K9: the attention part of a token-level backward window (Alg. 2 lines 14-21,
+// PAPER.md:353-364; tiny_model.hpp:294-315 for query rows [a, b) over keys [0, b)) as ONE tcgen05
+// kernel per window: dK / dV accumulate in TMEM per 128-key block, dQ is reduce-added into fp32
+// per (key block, query tile).  P is recomputed from Q, K and the saved LSE; exp2 on the SFU
+// (ex2.approx), the rest on FFMA2 / FADD2 / FMUL2.  Design and measurements: DESIGN.md §4 (K9).
 #include <atomic>
 #include <type_traits>
 #include <cstdlib>
@@ -54,9 +43,6 @@ constexpr int DB = 128;
 constexpr int HALFB = 128 * 128;  // [128 rows][128 B] = 16 KB
 constexpr int TILEB = 2 * HALFB;  // 32 KB
 
-CS_DEV uint32_t swzb(int r, int c) {  // chunk c (0..15) of row r, [2 halves][128 rows][128B]
-  return (uint32_t)((c >> 3) * HALFB + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4));
-}
 
 CS_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -78,24 +64,6 @@ CS_DEV void tst_x16(uint32_t taddr, const uint32_t* r) {
 
 CS_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// paged K (or V) tile of 128 keys -> two SW128 halves (contiguous-run fast path)
-CS_DEV void load_one(const CUtensorMap* t16, const CUtensorMap* t128, uint64_t* bar, uint8_t* dst,
-                     const int* pt, int page_off, int P, int k0, int k_end, int kvh) {
-  const int pg0 = __ldg(pt + page_off + k0 / P);
-  bool contig = true;
-  for (int key = (k0 / P + 1) * P; key < k0 + 128 && key < k_end; key += P)
-    contig &= __ldg(pt + page_off + key / P) == pg0 + (key / P - k0 / P);
-  if (contig) {
-    const int row = pg0 * P + (k0 % P);
-    for (int h = 0; h < 2; ++h) tma_load_2d(t128, bar, dst + h * HALFB, kvh * DB + h * 64, row);
-  } else {
-    for (int ch = 0; ch < 8; ++ch) {
-      const int key0 = k0 + ch * 16;
-      const int row = key0 < k_end ? __ldg(pt + page_off + key0 / P) * P + (key0 % P) : 0;
-      for (int h = 0; h < 2; ++h) tma_load_2d(t16, bar, dst + h * HALFB + ch * 2048, kvh * DB + h * 64, row);
-    }
-  }
-}
 
 // paged K and V tile of 128 keys -> two SW128 halves each (contiguous-run fast path)
 CS_DEV void load_kv2(const CUtensorMap* tK, const CUtensorMap* tV, const CUtensorMap* tK128,
@@ -123,549 +91,6 @@ CS_DEV void load_kv2(const CUtensorMap* tK, const CUtensorMap* tV, const CUtenso
   }
 }
 }  // namespace
-
-// ============================================================================ dK / dV
-namespace kv2 {
-constexpr int QB = 64;                 // packed query rows per tile
-constexpr int NB = 128 / QB;           // TMEM buffers (S^T / dP^T per tile): 2
-constexpr int LA = NB - 2;             // S^T issue lookahead beyond the next tile
-constexpr int HALFQ = QB * 128;        // 8 KB
-constexpr int QTILE = 2 * HALFQ;       // 16 KB
-constexpr int QST = 4;                 // Q / dO ring depth (tiles are held from S^T(i) to grad(i): 4 keeps ~2 in flight)
-constexpr int SMEM_K = 0;
-constexpr int SMEM_V = SMEM_K + TILEB;
-constexpr int SMEM_Q = SMEM_V + TILEB;
-constexpr int SMEM_O = SMEM_Q + QST * QTILE;
-constexpr int SMEM_X = SMEM_O + QST * QTILE;   // [2 WGs][2 slots][2 QB] floats: lse2 | delta
-constexpr int SMEM_BAR = SMEM_X + 2 * 2 * 2 * QB * 4;
-constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
-}  // namespace kv2
-
-// GRP: GQA group (query heads per KV head).  A 64-row packed query tile holds RPT = 64 / GRP
-// positions x GRP heads = ROWS rows; when GRP does not divide 64 (Qwen-2.5: 40 / 8 = 5 -> 60
-// rows) the last 64 - ROWS rows of every Q / dO stage are zeroed once and never written by
-// TMA (finite zeros: their P^T / dS^T columns are masked to 0, and 0 x stale NaN would not be)
-template <int GRP>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                          const __grid_constant__ CUtensorMap tmK128,
-                          const __grid_constant__ CUtensorMap tmV128,
-                          const __grid_constant__ CUtensorMap tmQ3,
-                          const __grid_constant__ CUtensorMap tmO3, AttnBwdParams p) {
-  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
-  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
-  using namespace kv2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;                 // [QST]
-  uint64_t* q_empty = q_full + QST;            // [QST]
-  uint64_t* st_full = q_empty + QST;           // [NB] S^T / dP^T of a tile ready
-  uint64_t* pds_full = st_full + NB;           // [NB] P^T / dS^T written (128 arrivals)
-  uint64_t* buf_free = pds_full + NB;          // [NB] dV/dK MMAs of a tile done
-  uint64_t* acc_done = buf_free + NB;          // all dV/dK MMAs done (completes once)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
-
-  constexpr int grp = GRP;
-  constexpr int rpt = QB / GRP;            // positions per query tile
-  constexpr int ROWS = rpt * GRP;          // real packed rows per tile (<= QB)
-  const int k0 = blockIdx.x * 128;
-  const int kvh = blockIdx.y;
-  const int nrows = p.b - p.a;
-  const int n_qt = (nrows + rpt - 1) / rpt;
-  // first tile whose last position >= k0; with dS stored for the dQ GEMM, from the first tile of
-  // the (128 / grp)-position dQ tile containing position k0, so every dS entry that GEMM reads
-  // for these keys is written (zeros where masked)
-  const int qt0 = p.ds_out ? (k0 > p.a ? ((k0 - p.a) / (128 / grp)) * (128 / grp) / rpt : 0)
-                           : (k0 > p.a ? (k0 - p.a) / rpt : 0);
-  const int n = n_qt - qt0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ3);
-    tma_prefetch_desc(&tmO3);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < QST; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-    }
-    for (int i = 0; i < NB; ++i) {
-      mbar_init(&st_full[i], 1);
-      mbar_init(&pds_full[i], 128);
-      mbar_init(&buf_free[i], 1);
-    }
-    mbar_init(acc_done, 1);
-    fence_barrier_init();
-  }
-  if constexpr (ROWS < QB) {  // pad rows [ROWS, QB) of every Q / dO stage, both 128-B halves
-    constexpr int PADB = (QB - ROWS) * 128;
-    for (int i = threadIdx.x; i < 2 * QST * 2 * (PADB / 16); i += blockDim.x) {
-      const int half = i / (PADB / 16), o = (i % (PADB / 16)) * 16;  // half: (Q|O, stage, h)
-      *reinterpret_cast<uint4*>(smem + SMEM_Q + half * HALFQ + ROWS * 128 + o) = make_uint4(0, 0, 0, 0);
-    }
-    fence_proxy_async_smem();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T[b] @QB*b (P^T over its first QB/2 cols) ; dP^T[b] @128+QB*b (dS^T likewise)
-  //       dV @256 ; dK @384
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    if (warp == 0 && lane == 0) {
-      if (n > 0) {
-        mbar_arrive_expect_tx(kv_full, 2 * TILEB);
-        load_kv2(&tmK, &tmV, &tmK128, &tmV128, kv_full, smem + SMEM_K, smem + SMEM_V, p.page_table,
-                 p.page_off, p.page_size, k0, p.b, kvh);
-      }
-      for (int i = 0; i < n; ++i) {
-        const int st = i % QST;
-        const int qt = qt0 + i;
-        mbar_wait(&q_empty[st], ((i / QST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[st], 2 * 2 * ROWS * 128);
-        for (int h = 0; h < 2; ++h) {
-          tma_load_3d(&tmQ3, &q_full[st], smem + SMEM_Q + st * QTILE + h * HALFQ, h * 64, kvh * grp,
-                      p.a + qt * rpt);
-          tma_load_3d(&tmO3, &q_full[st], smem + SMEM_O + st * QTILE + h * HALFQ, h * 64, kvh * grp,
-                      qt * rpt);
-        }
-      }
-    } else if (warp == 1 && lane == 0) {
-      constexpr uint32_t idS = idesc_bf16_f32_major(128, QB, 0, 0);
-      constexpr uint32_t idG = idesc_bf16_f32_major(128, 128, 0, 1);
-      const uint32_t sK = smem_u32(smem + SMEM_K), sV = smem_u32(smem + SMEM_V);
-      if (n > 0) {
-        mbar_wait(kv_full, 0);
-        tc_fence_after();
-      }
-      // S^T / dP^T run LA + 1 tiles ahead of the dV / dK products
-      auto issue_s = [&](int i) {
-        const int st = i % QST, b = i % NB;
-        mbar_wait(&q_full[st], (i / QST) & 1);
-        trace_ev(33, i);
-        if (i >= NB) mbar_wait(&buf_free[b], ((i / NB) - 1) & 1);
-        tc_fence_after();
-        trace_ev(30, i);
-        const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
-        const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-          const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-          mma_bf16(tmem + b * QB, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
-        }
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-          const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-          mma_bf16(tmem + 128 + b * QB, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
-        }
-        mma_commit(&st_full[b]);
-      };
-      for (int i = 0; i <= LA && i < n; ++i) issue_s(i);
-      for (int i = 0; i < n; ++i) {
-        if (i + LA + 1 < n) issue_s(i + LA + 1);
-        const int b = i % NB, st = i % QST;
-        mbar_wait(&pds_full[b], (i / NB) & 1);
-        tc_fence_after();
-        trace_ev(31, i);
-        const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
-        const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
-#pragma unroll
-        for (int kk = 0; kk < QB / 16; ++kk)  // dV += P^T dO   (A = P^T from TMEM)
-          mma_ts(tmem + 256, tmem + b * QB + kk * 8, umma_desc_sw128_mn(sO + kk * 2048, HALFQ, 1024),
-                 idG, (i > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < QB / 16; ++kk)  // dK += dS^T Q  (A = dS^T from TMEM)
-          mma_ts(tmem + 384, tmem + 128 + b * QB + kk * 8, umma_desc_sw128_mn(sQ + kk * 2048, HALFQ, 1024),
-                 idG, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&q_empty[st]);
-        mma_commit(&buf_free[b]);
-      }
-      // a dedicated one-shot barrier for the epilogue: a WG that finished its tiles early must
-      // not parity-wait on buf_free phases it never observed (parity aliasing)
-      if (n > 0) mma_commit(acc_done);
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    const int wg = (warp - 4) >> 2;  // elementwise warpgroup: tiles i with i % 2 == wg
-    const int ew = warp & 3;
-    const int tw = threadIdx.x - 128 - wg * 128;  // 0..127 within the WG
-    const int r = ew * 32 + lane;                  // key row == TMEM lane
-    const int key = k0 + r;
-    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    float* xw = reinterpret_cast<float*>(smem + SMEM_X) + wg * 4 * QB;
-    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    // per-column log2-LSE / Delta of this WG's tiles: loaded from global one tile ahead (the
-    // global latency hides behind the current tile), published through a double-buffered slot
-    auto fetch_x = [&](int i) -> float {
-      float v = 0.f;
-      if (i < n && tw < 2 * QB) {
-        const int col = tw & (QB - 1);
-        const int qr = (qt0 + i) * rpt + col / grp, g = col % grp;
-        if (qr < nrows) {
-          if (tw < QB) v = p.lse[(long)(p.a + qr) * p.lse_ld + kvh * grp + g] * kLog2eC;
-          else v = p.delta[(long)qr * p.delta_ld + kvh * grp + g];
-        }
-      }
-      return v;
-    };
-    float xnext = fetch_x(wg);
-    for (int i = wg; i < n; i += 2) {
-      const int b = i % NB, k = i / NB;
-      const int qt = qt0 + i, qbase = qt * rpt;
-      float* xs = xw + ((i >> 1) & 1) * 2 * QB;  // double-buffered per WG: one named barrier per tile
-      if (tw < 2 * QB) xs[tw] = xnext;
-      named_bar(1 + wg, 128);
-      xnext = fetch_x(i + 2);
-      mbar_wait(&st_full[b], k & 1);
-      tc_fence_after();
-      if (tw == 0) trace_ev(40 + wg, i);
-      // full tile: every column is a real row whose position >= key, and the key is in range
-      const bool full = key < p.b && key <= p.a + qbase && qbase + rpt - 1 < nrows;
-      // 32-column chunks (register budget); the packed P^T / dS^T of chunk h land on TMEM
-      // columns [16h, 16h+16), i.e. over S^T / dP^T columns this thread has already read
-#pragma unroll 1
-      for (int h = 0; h < QB / 32; ++h) {
-        uint32_t sv[32], dv[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + b * QB + h * 32, sv);
-        tmem_ld_32x32b_x32(tmem + lane_base + 128 + b * QB + h * 32, dv);
-        tmem_ld_wait();
-        uint32_t pp[16], pd[16];
-#pragma unroll
-        for (int cc = 0; cc < 32; cc += 2) {
-          const int c = h * 32 + cc;
-          float2 x = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2,
-                           make_float2(-xs[c], -xs[c + 1]));
-          float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-          if (!full) {
-            const int q0r = qbase + c / grp, q1r = qbase + (c + 1) / grp;
-            if (!(q0r < nrows && key <= p.a + q0r && key < p.b)) pv.x = 0.f;
-            if (!(q1r < nrows && key <= p.a + q1r && key < p.b)) pv.y = 0.f;
-          }
-          if constexpr (ROWS < QB) {  // pad columns (q0r above may alias the next tile's rows)
-            if (c >= ROWS) pv.x = 0.f;
-            if (c + 1 >= ROWS) pv.y = 0.f;
-          }
-          const float2 dd = fadd2(make_float2(__uint_as_float(dv[cc]), __uint_as_float(dv[cc + 1])),
-                                  make_float2(-xs[QB + c], -xs[QB + c + 1]));
-          const float2 ds = fmul2(pv, dd);
-          pp[cc >> 1] = pack_bf16(pv.x, pv.y);
-          pd[cc >> 1] = pack_bf16(ds.x, ds.y);
-        }
-        if (p.ds_out && key < p.ds_ld) {
-          // dS^T of this key, [kvh][tile][8-row chunk][key][8 rows]: for each chunk the warp's
-          // 32 keys store 512 contiguous bytes (one coalesced store instruction), and the dQ
-          // GEMM loads the chunks as no-swizzle MN-major core matrices
-          bf16* dst = p.ds_out + ((((long)kvh * p.ds_heads + qt) * (QB / 8) + h * 4) * p.ds_ld + key) * 8;
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            *reinterpret_cast<uint4*>(dst + (long)v * p.ds_ld * 8) =
-                make_uint4(pd[4 * v], pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
-        }
-        tst_x16(tmem + lane_base + b * QB + h * 16, pp);
-        tst_x16(tmem + lane_base + 128 + b * QB + h * 16, pd);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      if (tw == 0) trace_ev(42 + wg, i);
-      mbar_arrive(&pds_full[b]);
-    }
-    // ΔKVAccum rows [k0, k0+128) of this head: WG wg owns dV / dK columns [64 wg, 64 wg + 64)
-    if (n > 0) {
-      mbar_wait(acc_done, 0);
-      tc_fence_after();
-      uint32_t a0[32], a1[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + wg * 64, a0);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + wg * 64 + 32, a1);
-      tmem_ld_wait();
-      if (key < p.b) {
-        float* av = p.dv_acc + (long)key * p.acc_ld + kvh * DB + wg * 64;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 x = *reinterpret_cast<float4*>(av + i);
-          x.x += __uint_as_float(a0[i]); x.y += __uint_as_float(a0[i + 1]);
-          x.z += __uint_as_float(a0[i + 2]); x.w += __uint_as_float(a0[i + 3]);
-          *reinterpret_cast<float4*>(av + i) = x;
-          float4 y = *reinterpret_cast<float4*>(av + 32 + i);
-          y.x += __uint_as_float(a1[i]); y.y += __uint_as_float(a1[i + 1]);
-          y.z += __uint_as_float(a1[i + 2]); y.w += __uint_as_float(a1[i + 3]);
-          *reinterpret_cast<float4*>(av + 32 + i) = y;
-        }
-      }
-      tmem_ld_32x32b_x32(tmem + lane_base + 384 + wg * 64, a0);
-      tmem_ld_32x32b_x32(tmem + lane_base + 384 + wg * 64 + 32, a1);
-      tmem_ld_wait();
-      if (key < p.b) {
-        float* ak = p.dk_acc + (long)key * p.acc_ld + kvh * DB + wg * 64;
-        const float sc = p.scale;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 x = *reinterpret_cast<float4*>(ak + i);
-          x.x += __uint_as_float(a0[i]) * sc; x.y += __uint_as_float(a0[i + 1]) * sc;
-          x.z += __uint_as_float(a0[i + 2]) * sc; x.w += __uint_as_float(a0[i + 3]) * sc;
-          *reinterpret_cast<float4*>(ak + i) = x;
-          float4 y = *reinterpret_cast<float4*>(ak + 32 + i);
-          y.x += __uint_as_float(a1[i]) * sc; y.y += __uint_as_float(a1[i + 1]) * sc;
-          y.z += __uint_as_float(a1[i + 2]) * sc; y.w += __uint_as_float(a1[i + 3]) * sc;
-          *reinterpret_cast<float4*>(ak + 32 + i) = y;
-        }
-      }
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ============================================================================ dQ
-namespace dq2 {
-constexpr int KST = 3, VST = 2;             // K lives until dQ(j); V only until dP(j)
-constexpr int SMEM_Q = 0;
-constexpr int SMEM_O = SMEM_Q + TILEB;
-constexpr int SMEM_K = SMEM_O + TILEB;        // KST stages
-constexpr int SMEM_V = SMEM_K + KST * TILEB;  // VST stages
-constexpr int SMEM_BAR = SMEM_V + VST * TILEB;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
-}  // namespace dq2
-
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ CUtensorMap tmK128,
-                        const __grid_constant__ CUtensorMap tmV128, AttnBwdParams p) {
-  griddep_launch();  // PDL: a dependent GEMM may start its weight prefetch now
-  griddep_wait();    // launched with PDL: the producer's writes are visible from here on
-  using namespace dq2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* k_full = bars + 0;             // [KST]
-  uint64_t* k_empty = k_full + KST;        // [KST]
-  uint64_t* v_full = k_empty + KST;        // [VST]
-  uint64_t* v_empty = v_full + VST;        // [VST]
-  uint64_t* s_full = v_empty + VST;        // [2]
-  uint64_t* sbuf_free = s_full + 2;        // [2] dQ MMA consumed the dS aliasing S[b]
-  uint64_t* dp_full = sbuf_free + 2;
-  uint64_t* dp_free = dp_full + 1;         // 256 arrivals: dP in registers
-  uint64_t* ds_full = dp_free + 1;         // [2] 256 arrivals
-  uint64_t* q_full = ds_full + 2;
-  uint64_t* acc_done = q_full + 1;         // all dQ MMAs done (completes once)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
-
-  const int grp = p.grp;
-  const int rpt = 128 / grp;
-  const int q0 = blockIdx.x * rpt;
-  const int kvh = blockIdx.y;
-  const int nq = min(rpt, p.b - p.a - q0);
-  const int k_end = p.a + q0 + nq;
-  const int nt = (k_end + 127) / 128;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    tma_prefetch_desc(&tmK128);
-    tma_prefetch_desc(&tmV128);
-    for (int i = 0; i < KST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < VST; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&sbuf_free[i], 1);
-      mbar_init(&ds_full[i], 256);
-    }
-    mbar_init(dp_full, 1);
-    mbar_init(dp_free, 256);
-    mbar_init(q_full, 256);
-    mbar_init(acc_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S[2] @0,128 (dS bf16 over cols +0..31 and +64..95) ; dP @256 ; dQ @384
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    if (warp == 0 && lane == 0) {
-      for (int j = 0; j < nt; ++j) {
-        const int ks = j % KST, vs = j % VST;
-        mbar_wait(&k_empty[ks], ((j / KST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[ks], TILEB);
-        load_one(&tmK, &tmK128, &k_full[ks], smem + SMEM_K + ks * TILEB, p.page_table, p.page_off,
-                 p.page_size, j * 128, k_end, kvh);
-        mbar_wait(&v_empty[vs], ((j / VST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[vs], TILEB);
-        load_one(&tmV, &tmV128, &v_full[vs], smem + SMEM_V + vs * TILEB, p.page_table, p.page_off,
-                 p.page_size, j * 128, k_end, kvh);
-      }
-    } else if (warp == 1 && lane == 0) {
-      constexpr uint32_t idKK = idesc_bf16_f32_major(128, 128, 0, 0);
-      constexpr uint32_t idKM = idesc_bf16_f32_major(128, 128, 0, 1);
-      const uint32_t sQ = smem_u32(smem + SMEM_Q), sO = smem_u32(smem + SMEM_O);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j <= nt; ++j) {
-        if (j < nt) {
-          const int ks = j % KST, vs = j % VST, b = j & 1;
-          mbar_wait(&k_full[ks], (j / KST) & 1);
-          trace_ev(14, j);
-          if (j >= 2) mbar_wait(&sbuf_free[b], ((j >> 1) - 1) & 1);
-          tc_fence_after();
-          trace_ev(10, j);
-          const uint32_t sK = smem_u32(smem + SMEM_K + ks * TILEB);
-          const uint32_t sV = smem_u32(smem + SMEM_V + vs * TILEB);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * HALFB + (kk & 3) * 32;
-            mma_bf16(tmem + b * 128, umma_desc_sw128(sQ + off), umma_desc_sw128(sK + off), idKK, kk > 0);
-          }
-          mma_commit(&s_full[b]);
-          mbar_wait(&v_full[vs], (j / VST) & 1);
-          trace_ev(15, j);
-          if (j >= 1) mbar_wait(dp_free, (j - 1) & 1);
-          tc_fence_after();
-          trace_ev(11, j);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * HALFB + (kk & 3) * 32;
-            mma_bf16(tmem + 256, umma_desc_sw128(sO + off), umma_desc_sw128(sV + off), idKK, kk > 0);
-          }
-          mma_commit(dp_full);
-          mma_commit(&v_empty[vs]);
-        }
-        if (j >= 1) {  // dQ += dS(j-1) K(j-1)  (A = dS from TMEM, K read MN-major)
-          const int jj = j - 1, b = jj & 1, ks = jj % KST;
-          mbar_wait(&ds_full[b], (jj >> 1) & 1);
-          tc_fence_after();
-          trace_ev(12, jj);
-          const uint32_t sK = smem_u32(smem + SMEM_K + ks * TILEB);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t acol = b * 128 + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
-            mma_ts(tmem + 384, tmem + acol, umma_desc_sw128_mn(sK + kk * 2048, HALFB, 1024), idKM,
-                   (jj > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&sbuf_free[b]);
-          mma_commit(&k_empty[ks]);
-        }
-      }
-      if (nt > 0) mma_commit(acc_done);
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    const int ew = warp & 3, hh = (warp - 4) >> 2;  // hh: keys [64 hh, 64 hh + 64) of a tile
-    const int r = ew * 32 + lane;
-    const int qr = r / grp, g = r % grp;
-    const bool valid = qr < nq;
-    const int pos = valid ? p.a + q0 + qr : -1;
-    const int qh = kvh * grp + g;
-    float lse2 = 0.f, dlt = 0.f;
-    {  // Q and dO half rows -> SW128 smem; per-row LSE / Delta in registers
-      const bf16* qs = p.q_cache + (long)(valid ? pos : 0) * p.q_ld + (long)qh * DB;
-      const bf16* os = p.dO + (long)(q0 + (valid ? qr : 0)) * p.do_ld + (long)qh * DB;
-#pragma unroll
-      for (int c = hh * 8; c < hh * 8 + 8; ++c) {
-        uint4 vq = make_uint4(0, 0, 0, 0), vo = make_uint4(0, 0, 0, 0);
-        if (valid) {
-          vq = *reinterpret_cast<const uint4*>(qs + c * 8);
-          vo = *reinterpret_cast<const uint4*>(os + c * 8);
-        }
-        *reinterpret_cast<uint4*>(smem + SMEM_Q + swzb(r, c)) = vq;
-        *reinterpret_cast<uint4*>(smem + SMEM_O + swzb(r, c)) = vo;
-      }
-      if (valid) {
-        lse2 = p.lse[(long)pos * p.lse_ld + qh] * kLog2eC;
-        dlt = p.delta[(long)(q0 + qr) * p.delta_ld + qh];
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(q_full);
-    }
-    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
-    const float2 nd2 = make_float2(-dlt, -dlt);
-    for (int j = 0; j < nt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      mbar_wait(dp_full, j & 1);
-      tc_fence_after();
-      if (lane == 0 && ew == 0) trace_ev(20 + hh, j);
-      uint32_t sv[2][32], dv[2][32];
-      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + hh * 64, sv[0]);
-      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + hh * 64 + 32, sv[1]);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + hh * 64, dv[0]);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + hh * 64 + 32, dv[1]);
-      tmem_ld_wait();
-      tc_fence_before();
-      if (lane == 0 && ew == 0) trace_ev(22 + hh, j);
-      mbar_arrive(dp_free);  // the next dP may overwrite its TMEM columns
-      const int kb = j * 128 + hh * 64;
-      const bool full = kb + 63 <= pos && kb + 64 <= p.b;
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        const uint32_t* s2 = &sv[c >> 5][c & 31];
-        const uint32_t* d2 = &dv[c >> 5][c & 31];
-        float2 x = ffma2(make_float2(__uint_as_float(s2[0]), __uint_as_float(s2[1])), sc2, nl2);
-        float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-        if (!full) {
-          if (!(kb + c <= pos && kb + c < p.b)) pv.x = 0.f;
-          if (!(kb + c + 1 <= pos && kb + c + 1 < p.b)) pv.y = 0.f;
-        }
-        const float2 dd = fadd2(make_float2(__uint_as_float(d2[0]), __uint_as_float(d2[1])), nd2);
-        const float2 ds = fmul2(pv, dd);
-        pk[c >> 1] = pack_bf16(ds.x, ds.y);
-      }
-      // dS over this thread's own S columns: keys [64hh, 64hh+64) -> packed cols [64hh, 64hh+32)
-      tst_x16(tmem + lane_base + b * 128 + hh * 64, pk);
-      tst_x16(tmem + lane_base + b * 128 + hh * 64 + 16, pk + 16);
-      tmem_st_wait();
-      tc_fence_before();
-      if (lane == 0 && ew == 0) trace_ev(24 + hh, j);
-      mbar_arrive(&ds_full[b]);
-    }
-    if (nt > 0) {
-      mbar_wait(acc_done, 0);
-      tc_fence_after();
-    }
-    uint32_t o[2][32];
-    tmem_ld_32x32b_x32(tmem + lane_base + 384 + hh * 64, o[0]);
-    tmem_ld_32x32b_x32(tmem + lane_base + 384 + hh * 64 + 32, o[1]);
-    tmem_ld_wait();
-    if (valid) {
-      float* dst = p.dq + (long)(q0 + qr) * p.dq_ld + (long)qh * DB + hh * 64;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + c * 32 + i) =
-              make_float4(__uint_as_float(o[c][i]) * p.scale, __uint_as_float(o[c][i + 1]) * p.scale,
-                          __uint_as_float(o[c][i + 2]) * p.scale, __uint_as_float(o[c][i + 3]) * p.scale);
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
 
 // ============================================================================ fused dK / dV / dQ
 // One pass over (128-key block, 64-row packed query tile) pairs computes all five products:
@@ -1069,41 +494,6 @@ cudaError_t attn_bwd_fused(const AttnBwdParams& p, const CUtensorMap& tmK, const
   attn_bwd_delta_kernel_launch(p, rows, n_heads, st);
   dim3 grid((p.b + 127) / 128, n_heads / p.grp);
   launch_pdl(kFused[p.grp - 1], grid, dim3(512), kv3::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, tmDQ, p);
-  return cudaGetLastError();
-}
-
-using Dkdv2Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                         const CUtensorMap, const CUtensorMap, AttnBwdParams);
-static const Dkdv2Fn kDkdv2[8] = {attn_bwd_dkdv2_kernel<1>, attn_bwd_dkdv2_kernel<2>,
-                                  attn_bwd_dkdv2_kernel<3>, attn_bwd_dkdv2_kernel<4>,
-                                  attn_bwd_dkdv2_kernel<5>, attn_bwd_dkdv2_kernel<6>,
-                                  attn_bwd_dkdv2_kernel<7>, attn_bwd_dkdv2_kernel<8>};
-
-cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                         const CUtensorMap& tmK128, const CUtensorMap& tmV128,
-                         const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
-                         cudaStream_t st) {
-  const int rows = p.b - p.a;
-  if (rows <= 0) return cudaSuccess;
-  if (p.grp < 1 || p.grp > 8) return cudaErrorInvalidValue;
-  static bool once = [] {
-    cudaFuncSetAttribute(attn_bwd_dq2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         dq2::SMEM_TOTAL);
-    for (auto k : kDkdv2)
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kv2::SMEM_TOTAL);
-    return true;
-  }();
-  (void)once;
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  attn_bwd_delta_kernel_launch(p, rows, n_heads, st);
-  const int kvh = n_heads / p.grp;
-  dim3 gq((rows + 128 / p.grp - 1) / (128 / p.grp), kvh);
-  dim3 gk((p.b + 127) / 128, kvh);
-  g_launches.fetch_add(p.ds_out ? 1 : 2, std::memory_order_relaxed);
-  // with p.ds_out the dQ comes from attn_dq_gemm over the stored dS (launched by the caller)
-  if (!p.ds_out)
-    launch_pdl(attn_bwd_dq2_kernel, dim3(gq), dim3(384), dq2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, p);
-  launch_pdl(kDkdv2[p.grp - 1], dim3(gk), dim3(384), kv2::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, p);
   return cudaGetLastError();
 }
 

@@ -58,10 +58,6 @@ struct cs_engine {
   // dX GEMMs read the forward weight layout as an MN-major B operand: one copy of the frozen
   // QKV / O / gate||up / unembedding weights serves x W and dY W^T
   int down_rows = 0;  // per-layer rows of down_cat: h + 64 LoRA-A^T rows (MN-major dm operand)
-  // CS_BWD_DSQ=1: dQ as a GEMM over the dS the dK/dV kernel stores ([window row][q head][key])
-  bool bwd_dsq = false;
-  bool bwd_fused = true;  // fused dK/dV/dQ kernel (CS_BWD_FUSED=0: dK/dV + dS export + dQ GEMM)
-  bf16* ds_buf = nullptr;
   // arena (+ the allocation audit of every buffer carved from it, cf. Matrix::alloc_hook)
   struct AuditRec {
     const char* name;
@@ -278,7 +274,6 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   AL(ipc_flags, 64);
   AL(tp_stage, e->tp_size > 1 ? (std::max(T, S) + 8) * h : 1);
   // dS^T tiles: [kv heads][64-row query tiles of a window][keys (L_max rounded to 128)][64]
-  AL(ds_buf, e->bwd_dsq ? (size_t)e->Hkv * (S * e->grp / 64 + 2) * ((Lm + 127) / 128 * 128) * 64 : 1);
   AL(d_meta, e->meta_bytes);
   if (measure) *total = pl.used;
 #undef AL
@@ -368,14 +363,6 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("CS_ATTN_TC")) e->use_tc_attn = std::atoi(v) != 0;
   if (const char* v = std::getenv("CS_ATTN_DEC")) e->use_dec_attn = std::atoi(v) != 0;
   e->down_rows = e->h + 64;
-  {  // dQ as a GEMM over the dS^T the dK/dV kernel exports (default; CS_BWD_DSQ=0: the
-     // recomputing dQ kernel) -- d = 128 and GQA groups dividing the 64-row dK/dV query tile
-    const char* v = std::getenv("CS_BWD_DSQ");
-    e->bwd_dsq = (!v || std::atoi(v) != 0) && c.head_dim == 128 && 64 % (c.n_heads / c.n_kv_heads) == 0;
-    const char* f = std::getenv("CS_BWD_FUSED");
-    e->bwd_fused = !f || std::atoi(f) != 0;
-    if (e->bwd_fused) e->bwd_dsq = false;
-  }
 
   if (cudaSetDevice(device) != cudaSuccess) {
     delete e;
@@ -1542,7 +1529,7 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     cs_engine::ProfRec bpr{};
     if (e->profiling) {
       // algorithmic work (2.5x the forward): S = QK^T recompute, dP, dV, dK,
-      // dQ -- 5 x 2*d per (q, k, head); the recomputing dQ kernel (CS_BWD_DSQ=0) does 7
+      // dQ -- 5 x 2*d per (q, k, head)
       const double pairs = (double)s * ((double)a + (s + 1) / 2.0);
       bpr.flops = 5.0 * 2.0 * e->d * e->Hq * pairs;
       bpr.bytes = 0;
@@ -1565,29 +1552,11 @@ int backward_window(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
           cs::make_map_3d(&mo3, bp.dO, 128, e->Hq, e->S_max, 256, (long)e->q_dim * 2, e->grp,
                           qbox) != 0)
         return cs::set_error(CS_ERR_CUDA, "attention backward: TMA map creation failed");
-      if (e->bwd_fused) {  // dK/dV/dQ in one kernel; dQ reduce-added into fp32
-        CUtensorMap mdq;
-        if (cs::make_map_3d_f32(&mdq, bp.dq, e->d, e->Hq, s, (long)e->d * 4, bp.dq_ld * 4, 64, e->grp,
-                                64 / e->grp) != 0)
-          return cs::set_error(CS_ERR_CUDA, "attention backward: dQ TMA map creation failed");
-        CS_CUDA_TRY(cs::attn_bwd_fused(bp, mk, mv, mk128, mv128, mq3, mo3, mdq, e->Hq, st));
-      } else if (e->bwd_dsq) {  // dK/dV (+ dS to HBM), then dQ = dS . K as a GEMM
-        CUtensorMap mds, mk64;
-        const long keys = ((long)e->L_max + 127) / 128 * 128;
-        const long ntiles = (long)e->S_max * e->grp / 64 + 2;
-        bp.ds_out = e->ds_buf;
-        bp.ds_ld = keys;
-        bp.ds_heads = (int)ntiles;
-        // dS^T as [kv head][tile][8-row chunk][key][8 rows] (attn_dq_gemm.cu)
-        if (cs::make_map_3d_plain(&mds, e->ds_buf, 8, keys, (long)e->Hkv * ntiles * 8, 16, keys * 16, 8, 64,
-                                  8) != 0 ||
-            cs::make_map(&mk64, bp.k_pool, pool_rows, e->kv_dim, e->kv_dim, 64) != 0)
-          return cs::set_error(CS_ERR_CUDA, "attention backward: dS TMA map creation failed");
-        CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
-        CS_CUDA_TRY(cs::attn_dq_gemm(bp, mds, mk, mk64, e->Hq, st));
-      } else {
-        CS_CUDA_TRY(cs::attn_bwd_tc2(bp, mk, mv, mk128, mv128, mq3, mo3, e->Hq, st));
-      }
+      CUtensorMap mdq;  // dK/dV/dQ in one kernel; dQ reduce-added into fp32
+      if (cs::make_map_3d_f32(&mdq, bp.dq, e->d, e->Hq, s, (long)e->d * 4, bp.dq_ld * 4, 64, e->grp,
+                              64 / e->grp) != 0)
+        return cs::set_error(CS_ERR_CUDA, "attention backward: dQ TMA map creation failed");
+      CS_CUDA_TRY(cs::attn_bwd_fused(bp, mk, mv, mk128, mv128, mq3, mo3, mdq, e->Hq, st));
     } else {
       CS_CUDA_TRY(cs::attn_bwd(bp, e->d, e->Hq, st));
     }

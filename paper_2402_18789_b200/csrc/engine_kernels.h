@@ -78,13 +78,6 @@ struct AttnBwdParams {
   long acc_ld;
   int grp;
   float scale, scale_log2;
-  // CS_BWD_DSQ: the dK/dV kernel also stores dS^T (bf16) tile-major as
-  // [kv head][64-row query tile (ds_heads of them)][key (ds_ld)][64 packed rows] -- each thread
-  // writes its key's 128-byte row (zeros where masked, from the first dQ-GEMM tile touching
-  // each key block) for attn_dq_gemm; nullptr = the dQ kernel recomputes S and dP
-  bf16* ds_out = nullptr;
-  long ds_ld = 0;
-  int ds_heads = 0;
 };
 
 // decode rows (q_len * group <= 16): HBM-bound paged kernel (attn_decode.cu); run before
@@ -100,16 +93,7 @@ cudaError_t attn_combine(const AttnFwdParams& p, int head_dim, int n_combine, cu
 cudaError_t attn_fwd(const AttnFwdParams& p, int head_dim, int n_work, int n_combine,
                      cudaStream_t st);
 cudaError_t attn_bwd(const AttnBwdParams& p, int head_dim, int n_heads, cudaStream_t st);
-// dQ = scale * dS . K over the dS the dK/dV kernel stored (attn_dq_gemm.cu)
-cudaError_t attn_dq_gemm(const AttnBwdParams& p, const CUtensorMap& tmDS, const CUtensorMap& tmK16,
-                         const CUtensorMap& tmK64, int n_heads, cudaStream_t st);
 void attn_bwd_delta_kernel_launch(const AttnBwdParams& p, int rows, int n_heads, cudaStream_t st);
-// tcgen05 backward (head_dim 128, GQA group <= 8): P^T / dS^T / dS kept in TMEM (TS-MMA),
-// ping-pong elementwise warpgroups
-cudaError_t attn_bwd_tc2(const AttnBwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                         const CUtensorMap& tmK128, const CUtensorMap& tmV128,
-                         const CUtensorMap& tmQ3, const CUtensorMap& tmO3, int n_heads,
-                         cudaStream_t st);
 // fused tcgen05 backward (head_dim 128, GQA group <= 8): dK / dV into ΔKVAccum and dQ (fp32,
 // zeroed here, then reduce-added per (key block, query tile) through tmDQ: {128 d, Hq, rows}
 // fp32, box {64, grp, 64 / grp})

@@ -38,7 +38,7 @@ for rep in range(args.reps + 1):  # pass 0 is warm-up
                 res.setdefault((layer, lj, s), []).append((b["ms"], b["flops"], out["ms"]))
             lj -= s
     # the remaining layers' backward windows are not needed: the next pass resets the FT state
-tag = "fused" if os.environ.get("CS_BWD_FUSED", "1") != "0" else "dS-export + dQ GEMM"
+tag = "fused"
 for (layer, lj, s), v in res.items():
     ms = statistics.median(x[0] for x in v)
     fl = v[0][1]

@@ -2,8 +2,9 @@
 Hq 32 / Hkv 8, d=128, f=14336, r=16, RoPE theta 5e5) for 2 layers, a 4096-token finetuning
 sequence in two 2048-token windows (the second at 2K-4K context) fused with 64 decode rows,
 then two 2048-token backward windows per layer -- the shapes that run the CTA-pair GEMM with
-its tail-wave K split, attn_fwd_tc2 over 16 KV tiles, attn_bwd_dkdv2_kernel<4>, the two-tile
-dQ GEMM, the 1024-row CE head-chunk loop and the MN-major dX GEMMs.  The vocabulary is reduced
+its tail-wave K split, attn_fwd_tc2 over 16 KV tiles, the fused attention backward
+attn_bwd_fused_kernel<4> (dQ reduce-added across 32 key blocks), the 1024-row CE head-chunk
+loop and the MN-major dX GEMMs.  The vocabulary is reduced
 to 16384 (the head loop and its chunking do not depend on V; the f64 oracle's [4096, V] logits
 would be 4 GB at V=128256).  Checked like tests/test_coserve_gpu.py: against the bf16
 rounding-point oracle at 1e-2 (or 2x its measured self-drift) and the f64 oracle under the

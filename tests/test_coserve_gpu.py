@@ -320,18 +320,17 @@ ARCH_D128 = O.Arch(n_layers=2, hidden=512, n_heads=4, n_kv_heads=2, head_dim=128
                    rope_theta=10000.0)
 
 
-@pytest.mark.parametrize("tc,dsq", [("1", "0"), ("0", "0"), ("1", "1")])
-def test_d128_tcgen05_attention_parity(tc, dsq, monkeypatch):
-    """head_dim 128: prefill / FT-window rows run on the tcgen05 attention kernel (CS_ATTN_TC=1)
-    or the mma.sync kernel (0); contexts span several 128-key tiles and a window boundary that
-    is not tile aligned.  dsq=1: dQ as a GEMM over the dS the dK/dV kernel stores."""
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_d128_tcgen05_attention_parity(tc, monkeypatch):
+    """head_dim 128: prefill / FT-window rows run on the tcgen05 attention kernels (CS_ATTN_TC=1:
+    forward attn_fwd_tc2, backward the fused dK/dV/dQ kernel) or the mma.sync kernels (0);
+    contexts span several 128-key tiles and a window boundary that is not tile aligned."""
     monkeypatch.setenv("CS_ATTN_TC", tc)
-    monkeypatch.setenv("CS_BWD_DSQ", dsq)
     arch = ARCH_D128
     W = O.init_general(arch, 7)
     toks = list(np.random.default_rng(9).integers(0, arch.vocab, 300))
     tr, bw, te, be = oracles(arch, W, toks)
-    t = f"d128_tc{tc}_dsq{dsq}"
+    t = f"d128_tc{tc}"
     eng, loss_sum, kvg, dys, dmax = _run_coserve(arch, W, toks, [100, 200], [150, 150], n_inf=5,
                                                  logit_tol=0.04, test=t)
     gate_loss(t, loss_sum / 299.0, tr, te)
