@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(384, 1)
   const AttnSeg sg = p.segs[w.seg];
   const int grp = p.grp;
   const int rpt = BM2 / grp;  // query positions per tile
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;  // warp-uniform
   // keys [k_begin, k_end) of the item (k_begin a multiple of 128; > 0 for split-KV parts)
   const int j0 = w.k_begin / BN2;
   const int nt = (w.k_end + BN2 - 1) / BN2 - j0;
@@ -152,29 +152,41 @@ __global__ void __launch_bounds__(384, 1)
         load_tile2(&tmV, &tmV128, &v_full[st], smem + SM_V + st * TILE2, p.page_table, sg.page_off,
                    p.page_size, (j0 + j) * BN2, w.k_end, w.kv_head);
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
       // ------------------------------------------------------------ MMA issuer
+      // the whole warp walks the schedule (descriptors in uniform registers: no per-MMA
+      // R2UR / elect loop), one elected lane issues each group of MMAs and its commit
       constexpr uint32_t idS = idesc_bf16_f32_major(128, 128, 0, 0);
       constexpr uint32_t idO = idesc_bf16_f32_major(128, 128, 0, 1);
       mbar_wait(q_full, 0);
       tc_fence_after();
       auto qk = [&](int i, uint32_t sK) {
         const uint32_t sQ = smem_u32(smem + SM_Q + i * TILE2);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D2 / 16; ++kk) {
-          const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * HALF2 + (kk & 3) * 32);
-          const uint64_t b = umma_desc_sw128(sK + (kk >> 2) * HALF2 + (kk & 3) * 32);
-          mma_bf16(tmem + i * 128, a, b, idS, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D2 / 16; ++kk) {
+            const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * HALF2 + (kk & 3) * 32);
+            const uint64_t b = umma_desc_sw128(sK + (kk >> 2) * HALF2 + (kk & 3) * 32);
+            mma_bf16(tmem + i * 128, a, b, idS, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[i]);
         }
-        mma_commit(&s_full[i]);
+        __syncwarp();
       };
       auto pv = [&](int i, uint32_t sV, int j) {
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BN2 / 16; ++kk) {
-          const uint64_t b = umma_desc_sw128_mn(sV + kk * 2048, HALF2, 1024);
-          mma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, b, idO, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN2 / 16; ++kk) {
+            const uint64_t b = umma_desc_sw128_mn(sV + kk * 2048, HALF2, 1024);
+            mma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, b, idO, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&pv_done[i]);
         }
-        mma_commit(&pv_done[i]);
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) mma_commit(bar);
+        __syncwarp();
       };
       if (ntile == 2) {
         // ping-pong: while the softmax of query tile 0 runs on S_0(j), the tensor pipe does
@@ -190,12 +202,12 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(&p_full[1], (j - 1) & 1);
             tc_fence_after();
             pv(1, smem_u32(smem + SM_V + pst * TILE2), j - 1);
-            mma_commit(&v_empty[pst]);  // V(j-1) fully consumed
+            commit(&v_empty[pst]);  // V(j-1) fully consumed
             mbar_wait(&pv_done[1], (j - 1) & 1);
             tc_fence_after();
           }
           qk(1, sK);
-          mma_commit(&k_empty[st]);
+          commit(&k_empty[st]);
           mbar_wait(&v_full[st], (j >> 1) & 1);
           mbar_wait(&p_full[0], j & 1);
           tc_fence_after();
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(384, 1)
           mbar_wait(&p_full[1], (nt - 1) & 1);
           tc_fence_after();
           pv(1, smem_u32(smem + SM_V + lst * TILE2), nt - 1);
-          mma_commit(&v_empty[lst]);
+          commit(&v_empty[lst]);
         }
       } else {
         for (int j = 0; j < nt; ++j) {
@@ -215,12 +227,12 @@ __global__ void __launch_bounds__(384, 1)
           if (j > 0) mbar_wait(&pv_done[0], (j - 1) & 1);  // P_0(j-1) aliases S_0
           tc_fence_after();
           qk(0, smem_u32(smem + SM_K + st * TILE2));
-          mma_commit(&k_empty[st]);
+          commit(&k_empty[st]);
           mbar_wait(&v_full[st], (j >> 1) & 1);
           mbar_wait(&p_full[0], j & 1);
           tc_fence_after();
           pv(0, smem_u32(smem + SM_V + st * TILE2), j);
-          mma_commit(&v_empty[st]);
+          commit(&v_empty[st]);
         }
       }
     }

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);  // warp-uniform
   const int lane = threadIdx.x & 31;
   const int total = args.units;
 
@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp walks the schedule (descriptors stay in uniform registers: no per-MMA
+    // R2UR / elect loop), one elected lane issues
+    {
       const uint32_t idesc = args.b_mn ? idesc_bf16_f32_major(128, BN, 0, 1) : idesc_bf16_f32(128, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -281,21 +283,25 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t sb = sa + Cfg::A_BYTES;
           const uint64_t ad = umma_desc_sw128(sa);
           const uint64_t bd = umma_desc_sw128(sb);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < Cfg::BK / 16; ++k) {
-            // K-major: +32 bytes per K=16 step inside the 128B swizzle atom (16-byte units);
-            // MN-major: +16 rows x 128 B, 64-column chunks 8 KB apart (LBO), 8-row groups (SBO)
-            const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
-                                         : bd + (uint64_t)(k * 2);
-            mma_bf16(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < Cfg::BK / 16; ++k) {
+              // K-major: +32 bytes per K=16 step inside the 128B swizzle atom (16-byte units);
+              // MN-major: +16 rows x 128 B, 64-column chunks 8 KB apart (LBO), 8-row groups (SBO)
+              const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
+                                           : bd + (uint64_t)(k * 2);
+              mma_bf16(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty_bar[stage]);
           }
-          mma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        if (elect_one()) mma_commit(&tfull_bar[acc]);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -429,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);  // warp-uniform
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -502,7 +508,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    // leader CTA: the whole warp walks the schedule (uniform descriptors), one lane issues
+    if (leader) {
       const uint32_t idesc = args.b_mn ? idesc_bf16_f32_major(256, BN, 0, 1) : idesc_bf16_f32(256, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -521,19 +528,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint32_t sb = sa + Cfg::A_BYTES;
           const uint64_t ad = umma_desc_sw128(sa);
           const uint64_t bd = umma_desc_sw128(sb);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < Cfg::BK / 16; ++k) {
-            const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
-                                         : bd + (uint64_t)(k * 2);
-            mma_bf16_2sm(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < Cfg::BK / 16; ++k) {
+              const uint64_t b = args.b_mn ? umma_desc_sw128_mn(sb + k * 2048, 8192, 1024)
+                                           : bd + (uint64_t)(k * 2);
+              mma_bf16_2sm(d_tmem, ad + (uint64_t)(k * 2), b, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_2sm(&empty_bar[stage]);
           }
-          mma_commit_2sm(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_2sm(&tfull_bar[acc]);
+        if (elect_one()) mma_commit_2sm(&tfull_bar[acc]);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
