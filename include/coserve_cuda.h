@@ -55,7 +55,9 @@ int64_t cs_debug_trace(int cta, void* dev_buf, int64_t capacity);
 
 /* ---------------------------------------------------------------- primitives (device ptrs) */
 /* C[M,N] (op)= A[M,K] . B[N,K]^T, bf16 operands (K contiguous), fp32 accumulate on
- * tcgen05/TMEM.  epi: 0 bf16 store (+bias), 1 fp32 store, 2 fp32 +=, 3 fp32 atomic +=.
+ * tcgen05/TMEM.  epi: 0 bf16 store (+bias), 1 fp32 store, 2 fp32 +=, 3 fp32 atomic +=,
+ * 5 SwiGLU (B's rows interleaved in 64-row [gate | up] blocks, N % 128 == 0: C (bf16, ldc >= N/2)
+ * receives silu(bf16 gate) * bf16 up for N/2 columns and zeros in [N/2, ldc)).
  * bn in {0(auto),16,32,64,128,256}; splits 0 = auto (fp32 epilogues only). */
 int cs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, int epi, const float* bias, int bn, int splits,

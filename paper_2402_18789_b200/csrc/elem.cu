@@ -473,7 +473,9 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
 }
 
 // MLP backward fused with the LoRA-A gradient:
-//   swiglu: g=saved[:, :f], u=saved[:, f:]; dgu = [dm*u*dsilu(g), dm*silu(g)]; m = silu(g)*u
+//   swiglu: saved / dgu in the interleaved gate||up layout (kernels.h EPI_SWIGLU: column j's
+//           gate at (j/64)*128 + j%64, its up 64 further); dgu_gate = dm*u*dsilu(g),
+//           dgu_up = dm*silu(g); m = silu(g)*u
 //   relu  : m=saved;  dgu = dm * (m > 0)            (tiny_model.hpp:285-286)
 //   dA[col, :] += sum_rows m[row, col] * dlu[row, :] (tiny_model.hpp:282)
 // HBM-bound (10 B per (row, col): dm bf16 in, g / u bf16 in, dgu bf16 out).  Thread = 4
@@ -530,9 +532,10 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const bf16* __rest
       }
     }
     const long row = r0 + i;
-    *reinterpret_cast<uint2*>(dgu + row * ld_dgu + col) = make_uint2(pack_bf16(o0[0], o0[1]), pack_bf16(o0[2], o0[3]));
+    const int gc = swiglu ? (col >> 6) * 128 + (col & 63) : col;
+    *reinterpret_cast<uint2*>(dgu + row * ld_dgu + gc) = make_uint2(pack_bf16(o0[0], o0[1]), pack_bf16(o0[2], o0[3]));
     if (swiglu)
-      *reinterpret_cast<uint2*>(dgu + row * ld_dgu + f + col) =
+      *reinterpret_cast<uint2*>(dgu + row * ld_dgu + gc + 64) =
           make_uint2(pack_bf16(o1[0], o1[1]), pack_bf16(o1[2], o1[3]));
     const float2 m01 = make_float2(m[0], m[1]), m23 = make_float2(m[2], m[3]);
     const float4* l4 = reinterpret_cast<const float4*>(sl + i * 16);
@@ -554,8 +557,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const bf16* __rest
     const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + row * ld_dm + col));
     const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
     d = make_float4(__low2float(d2[0]), __high2float(d2[0]), __low2float(d2[1]), __high2float(d2[1]));
-    gv = __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + col));
-    uv = swiglu ? __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + f + col)) : make_uint2(0u, 0u);
+    const int gc = swiglu ? (col >> 6) * 128 + (col & 63) : col;
+    gv = __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + gc));
+    uv = swiglu ? __ldg(reinterpret_cast<const uint2*>(saved + row * ld_s + gc + 64)) : make_uint2(0u, 0u);
   };
   int i = 0;
   for (; i + 3 < nr; i += 4) {  // four rows' loads in flight before any is used
@@ -767,8 +771,10 @@ void adam_step(const AdamParams& p, int update, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- weight prep
+// transpose: dst row = c, mapped through 64-row blocks when blk_stride > 0 (the interleaved
+// gate||up layout: row (c / 64) * blk_stride + blk_off + c % 64)
 __global__ void cast_kernel(const float* __restrict__ src, int rows, int cols, bf16* dst,
-                            long ldd, int transpose) {
+                            long ldd, int transpose, int blk_stride, int blk_off) {
   __shared__ float tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -783,14 +789,21 @@ __global__ void cast_kernel(const float* __restrict__ src, int rows, int cols, b
   __syncthreads();
   for (int k = 0; k < 32; k += 8) {
     const int c = bx + ty + k, r = by + tx;  // dst row = c, dst col = r
-    if (r < rows && c < cols) dst[(long)c * ldd + r] = __float2bfloat16(tile[tx][ty + k]);
+    const long dr = blk_stride > 0 ? (long)(c >> 6) * blk_stride + blk_off + (c & 63) : c;
+    if (r < rows && c < cols) dst[dr * ldd + r] = __float2bfloat16(tile[tx][ty + k]);
   }
 }
 void cast_f32_bf16(const float* src, int rows, int cols, bf16* dst, long ldd, int transpose,
                    cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  cast_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, transpose);
+  cast_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, transpose, 0, 0);
+}
+void cast_f32_bf16_interleaved(const float* src, int rows, int cols, bf16* dst, long ldd, int blk_stride,
+                               int blk_off, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  cs::g_launches.fetch_add(1, std::memory_order_relaxed);
+  cast_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, 1, blk_stride, blk_off);
 }
 
 CS_DEV uint64_t splitmix(uint64_t x) {

@@ -712,8 +712,11 @@ extern "C" int cs_engine_set_weight(cs_engine* e, const char* name, int layer, c
   } else if (n == "wo") {
     cs::cast_f32_bf16(stage, lr, lc, e->wo_t + (size_t)L * h * qd, qd, 1, st);
   } else if (n == "w_gate" || n == "w_up") {
-    const long off = (n == "w_up" && e->swiglu) ? f : 0;
-    cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + ((size_t)L * e->gu_n + off) * h, h, 1, st);
+    if (e->swiglu)  // interleaved 64-row blocks [gate | up] (kernels.h EPI_SWIGLU)
+      cs::cast_f32_bf16_interleaved(stage, lr, lc, e->wgu_t + (size_t)L * e->gu_n * h, h, 128,
+                                    n == "w_up" ? 64 : 0, st);
+    else
+      cs::cast_f32_bf16(stage, lr, lc, e->wgu_t + (size_t)L * e->gu_n * h, h, 1, st);
   } else if (n == "w_down") {
     cs::cast_f32_bf16(stage, lr, lc, e->down_cat + (size_t)L * e->down_rows * e->f_cat, e->f_cat, 1, st);
   } else if (n == "lora_a") {
@@ -814,7 +817,8 @@ struct StepPlan {
 
 int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb, long b_rows,
          void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr,
-         const cs::GemmScatter* sc = nullptr, int b_mn = 0) {
+         const cs::GemmScatter* sc = nullptr, int b_mn = 0, void* C2 = nullptr, long ldc2 = 0,
+         int c2_row0 = 0) {
   cs::GemmDesc g;
   if (sc) g.scatter = *sc;
   g.b_mn = b_mn;
@@ -832,11 +836,18 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
   g.epi = epi;
   g.bias = bias;
   g.b_const = 1;  // every engine GEMM's B operand is a (frozen or LoRA) weight
+  if (epi == cs::EPI_SWIGLU) {  // m = silu(gate) * up into C, the FT rows' gate / up into C2
+    g.C2 = C2;
+    g.ldc2 = ldc2;
+    g.c2_row0 = c2_row0;
+    g.m_cols = (int)(N / 2);
+  }
   e->launches++;
   cs_engine::ProfRec pr{};
   if (e->profiling) {
     pr.flops = 2.0 * (double)M * (double)N * (double)K;
-    pr.bytes = 2.0 * ((double)M * K + (double)N * K) + (double)M * N * (epi == cs::EPI_BF16 ? 2 : 4);
+    pr.bytes = 2.0 * ((double)M * K + (double)N * K) +
+               (double)M * N * (epi == cs::EPI_SWIGLU ? 1 : epi == cs::EPI_BF16 ? 2 : 4);
     pr.kind = 0;
     prof_begin(e, pr);
   }
@@ -1395,12 +1406,21 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     cs::rmsnorm_cast(e->x, h, e->g2 + (size_t)l * h, e->xb, h, e->rstd, T, h, eps, e->norm, st);
     if (n_ft > 0 && e->norm)
       save_rows(e, e->ft_rstd2 + (size_t)l * e->L_max + l0, 1, e->rstd + sp.ft_row0, 1, n_ft, 1);
-    TRY(gemm(e, e->xb, h, e->T_max, e->wgu_t + (size_t)l * e->gu_n * h, h, e->gu_n, e->gu, e->gu_n,
-             T, e->gu_n, h, cs::EPI_BF16));
-    if (n_ft > 0)
-      save_rows(e, e->ft_gu + ((size_t)l * e->L_max + l0) * e->gu_n, e->gu_n,
-                e->gu + (size_t)sp.ft_row0 * e->gu_n, e->gu_n, n_ft, e->gu_n);
-    cs::act_fwd(e->gu, e->gu_n, e->m, e->f_cat, T, f, e->swiglu, st);
+    if (e->swiglu) {
+      // gate||up with the SwiGLU in the epilogue: m straight from the accumulators (pad
+      // columns zeroed), the FT rows' bf16 gate / up saved for the backward (tiny_model.hpp:205)
+      TRY(gemm(e, e->xb, h, e->T_max, e->wgu_t + (size_t)l * e->gu_n * h, h, e->gu_n, e->m, e->f_cat,
+               T, e->gu_n, h, cs::EPI_SWIGLU, nullptr, nullptr, 0,
+               n_ft > 0 ? e->ft_gu + ((size_t)l * e->L_max + l0) * e->gu_n : nullptr, e->gu_n,
+               n_ft > 0 ? sp.ft_row0 : T));
+    } else {
+      TRY(gemm(e, e->xb, h, e->T_max, e->wgu_t + (size_t)l * e->gu_n * h, h, e->gu_n, e->gu, e->gu_n,
+               T, e->gu_n, h, cs::EPI_BF16));
+      if (n_ft > 0)
+        save_rows(e, e->ft_gu + ((size_t)l * e->L_max + l0) * e->gu_n, e->gu_n,
+                  e->gu + (size_t)sp.ft_row0 * e->gu_n, e->gu_n, n_ft, e->gu_n);
+      cs::act_fwd(e->gu, e->gu_n, e->m, e->f_cat, T, f, e->swiglu, st);
+    }
     if (n_ad > 0) {
       // u = m A for adapter rows (segmented LoRA down, tiny_model.hpp:207)
       TRY(gemm(e, e->m + (size_t)sp.ad_row0 * e->f_cat, e->f_cat, e->T_max - sp.ad_row0,

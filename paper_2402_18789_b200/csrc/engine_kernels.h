@@ -193,6 +193,9 @@ void adam_step(const AdamParams& p, int update, cudaStream_t st);
 // weight prep: dst_bf16 (optionally transposed) from fp32 staging; dst[i*ldd + j]
 void cast_f32_bf16(const float* src, int rows, int cols, bf16* dst, long ldd, int transpose,
                    cudaStream_t st);
+// transposed cast into 64-row blocks: dst row (c / 64) * blk_stride + blk_off + c % 64
+void cast_f32_bf16_interleaved(const float* src, int rows, int cols, bf16* dst, long ldd, int blk_stride,
+                               int blk_off, cudaStream_t st);
 void init_normal_bf16(bf16* dst, long n, float scale, uint64_t seed, cudaStream_t st);
 void init_normal_f32(float* dst, long n, float scale, uint64_t seed, cudaStream_t st);
 void fill_f32(float* dst, long n, float v, cudaStream_t st);

@@ -48,6 +48,10 @@ struct GemmArgs {
   // is split, so it is spread over all pairs instead of idling most of them.  0: uniform splits
   int full_units = 0;
   int units = 0;  // total work units
+  void* C2 = nullptr;  // EPI_SWIGLU (kernels.h)
+  long ldc2 = 0;
+  int c2_row0 = 0;
+  int m_cols = 0;
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -158,6 +162,42 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int row, int c
         else if (a.epi == EPI_F32_ADD) C[i] += v;
         else C[i] = v;
       }
+    }
+  }
+}
+
+// EPI_SWIGLU: 32 gate columns (g, output columns col_g .. col_g+31, inside the gate half of a
+// 128-column group) and the matching 32 up columns (64 further).  Rounding points as the
+// unfused path (tiny_model.hpp:205 in the LLaMA generalisation): g and u rounded to bf16, then
+// m = bf16(silu(g) * u) in fp32.
+__device__ __forceinline__ void epilogue_swiglu(const GemmArgs& a, int row, int col_g, const uint32_t* g,
+                                                const uint32_t* u) {
+  if (row >= a.M || col_g >= a.N) return;
+  uint32_t gp[16], up[16], mp[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    gp[i] = pack_bf16(__uint_as_float(g[2 * i]), __uint_as_float(g[2 * i + 1]));
+    up[i] = pack_bf16(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));
+    const __nv_bfloat162 gb = *reinterpret_cast<const __nv_bfloat162*>(&gp[i]);
+    const __nv_bfloat162 ub = *reinterpret_cast<const __nv_bfloat162*>(&up[i]);
+    const float g0 = __low2float(gb), g1 = __high2float(gb);
+    const float s0 = g0 * __fdividef(1.f, 1.f + __expf(-g0)), s1 = g1 * __fdividef(1.f, 1.f + __expf(-g1));
+    mp[i] = pack_bf16(s0 * __low2float(ub), s1 * __high2float(ub));
+  }
+  const int f0 = (col_g >> 7) * 64 + (col_g & 127);
+  __nv_bfloat16* m = reinterpret_cast<__nv_bfloat16*>(a.C) + (long)row * a.ldc;
+#pragma unroll
+  for (int i = 0; i < 16; i += 4)
+    *reinterpret_cast<uint4*>(m + f0 + 2 * i) = make_uint4(mp[i], mp[i + 1], mp[i + 2], mp[i + 3]);
+  if (f0 + 32 == a.m_cols)  // the K-concatenation pad columns of m (LoRA-up inputs, lora_pack)
+    for (int c = a.m_cols; c < a.ldc; c += 8)
+      *reinterpret_cast<uint4*>(m + c) = make_uint4(0, 0, 0, 0);
+  if (a.C2 && row >= a.c2_row0) {
+    __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(a.C2) + (long)(row - a.c2_row0) * a.ldc2 + col_g;
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      *reinterpret_cast<uint4*>(s + 2 * i) = make_uint4(gp[i], gp[i + 1], gp[i + 2], gp[i + 3]);
+      *reinterpret_cast<uint4*>(s + 64 + 2 * i) = make_uint4(up[i], up[i + 1], up[i + 2], up[i + 3]);
     }
   }
 }
@@ -319,6 +359,27 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * Cfg::BM + ew * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if constexpr (BN >= 128) {
+        if (args.epi == EPI_SWIGLU) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 128)
+#pragma unroll 1
+            for (int h = 0; h < 64; h += 32) {
+              uint32_t g[32], u[32];
+              tmem_ld_32x32b_x32(tbase + c0 + h, g);
+              tmem_ld_32x32b_x32(tbase + c0 + 64 + h, u);
+              tmem_ld_wait();
+              epilogue_swiglu(args, row, nb * BN + c0 + h, g, u);
+            }
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += Cfg::CHUNK) {
         const int col0 = nb * BN + c0;
@@ -562,13 +623,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * 256 + (int)rank * 128 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (args.epi == EPI_SWIGLU) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int col0 = nb * BN + c0;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + c0, r);
-        tmem_ld_wait();
-        if (col0 < args.N) epilogue_store<BN>(args, row, col0, r, 32);
+        for (int c0 = 0; c0 < BN; c0 += 128)
+#pragma unroll 1
+          for (int h = 0; h < 64; h += 32) {
+            uint32_t g[32], u[32];
+            tmem_ld_32x32b_x32(tbase + c0 + h, g);
+            tmem_ld_32x32b_x32(tbase + c0 + 64 + h, u);
+            tmem_ld_wait();
+            epilogue_swiglu(args, row, nb * BN + c0 + h, g, u);
+          }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int col0 = nb * BN + c0;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + c0, r);
+          tmem_ld_wait();
+          if (col0 < args.N) epilogue_store<BN>(args, row, col0, r, 32);
+        }
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty_bar[acc]);
@@ -757,6 +831,10 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.sc = d.scatter;
   a.splits = 1;
   a.b_mn = d.b_mn;
+  a.C2 = d.C2;
+  a.ldc2 = d.ldc2;
+  a.c2_row0 = d.c2_row0;
+  a.m_cols = (int)(d.N / 2);
   const long tiles2 = (long)a.num_m * a.num_n;
   a.units = (int)tiles2;
   // accumulating epilogues (C += acc): split the last, partial wave of tiles along K when the
@@ -812,6 +890,11 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   if (glog) std::fprintf(glog, "%ld %ld %ld %d\n", d.M, d.N, d.K, d.epi);
   if (d.K <= 0 || (d.K % 8) != 0 || (d.lda % 8) != 0 || (d.ldb % 8) != 0)
     return cudaErrorInvalidValue;
+  if (d.epi == EPI_SWIGLU && (d.N % 128 != 0 || (d.m_cols != 0 && d.m_cols * 2 != d.N) || d.ldc < d.N / 2 ||
+                              (d.ldc % 8) != 0))
+    return cudaErrorInvalidValue;
+  // bf16-output epilogues: no K split (EPI_SWIGLU as EPI_BF16 below)
+  const bool bf16_out = d.epi == EPI_BF16 || d.epi == EPI_SWIGLU;
   // large GEMMs (at least one wave of 256 x BN tiles): CTA-pair kernel
   if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 256) {
     const long mt = (d.M + 255) / 256;
@@ -836,7 +919,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   }();
   const bool tiny_m = smallm_on && d.bn <= 0 && d.splits <= 0 && d.M <= 64 && d.N >= 1024;
   if (tiny_m) {
-    if (d.epi == EPI_BF16) {
+    if (bf16_out) {
       long best = -1;
       for (int c : {256, 128, 64}) {  // >= 64: the MMA's phantom A rows stay inside the stage
         const long waves = (((d.N + c - 1) / c) + kNumSMs - 1) / kNumSMs;
@@ -847,7 +930,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
       bn = 256;
     }
   }
-  const bool small_f32 = !tiny_m && d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.M <= 256 &&
+  const bool small_f32 = !tiny_m && d.bn <= 0 && d.splits <= 0 && !bf16_out && d.M <= 256 &&
                          d.N >= 1024;
   if (small_f32) bn = 128;
   // mid-M fp32 epilogues that missed the CTA-pair kernel (the O / down projections and dX
@@ -857,7 +940,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   // 256 one at ~85% of its per-FLOP rate.  M=640 N=4096 K=14400: 130 us (bn 128, 1 split,
   // 160 tiles = 1.08 waves) -> 80 us (bn 256 x 3 splits)
   int mid_splits = 0;
-  if (!tiny_m && !small_f32 && d.bn <= 0 && d.splits <= 0 && d.epi != EPI_BF16 && d.N >= 1024) {
+  if (!tiny_m && !small_f32 && d.bn <= 0 && d.splits <= 0 && !bf16_out && d.N >= 1024) {
     const long kb = (d.K + 63) / 64;
     double best = 0;
     for (int c : {256, 128}) {
@@ -870,6 +953,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
     }
   }
   if (d.b_mn && bn < 64) bn = 64;  // MN-major B stages are 64-column chunks
+  if (d.epi == EPI_SWIGLU && bn < 128) bn = 128;  // whole 128-column gate / up groups per tile
   GemmArgs a;
   a.M = (int)d.M;
   a.N = (int)d.N;
@@ -883,19 +967,23 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.bias = d.bias;
   a.b_const = d.b_const;
   a.sc = d.scatter;
+  a.C2 = d.C2;
+  a.ldc2 = d.ldc2;
+  a.c2_row0 = d.c2_row0;
+  a.m_cols = (int)(d.N / 2);
   int splits = d.splits > 0 ? d.splits : mid_splits;
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {
     splits = 1;
-    if (small_f32 || (tiny_m && d.epi != EPI_BF16)) {
+    if (small_f32 || (tiny_m && !bf16_out)) {
       splits = (int)((kNumSMs + tiles / 2) / tiles);
       splits = std::max(1, std::min(splits, a.kb_total / 8));
-    } else if (d.epi != EPI_BF16 && tiles < kNumSMs) {
+    } else if (!bf16_out && tiles < kNumSMs) {
       splits = (int)((kNumSMs + tiles - 1) / tiles);
       splits = std::min(splits, std::max(1, a.kb_total / 4));
     }
   }
-  if (d.epi == EPI_BF16) splits = 1;
+  if (bf16_out) splits = 1;
   splits = std::max(1, std::min(splits, a.kb_total));
   a.splits = splits;
   a.units = (int)((long)a.num_m * a.num_n * splits);

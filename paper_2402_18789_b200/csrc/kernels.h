@@ -38,6 +38,13 @@ enum GemmEpi : int {
   EPI_F32_ADD = 2,     // C_f32 += acc   (residual stream; split-K via atomics)
   EPI_F32_ATOMIC = 3,  // C_f32 += acc with atomics (caller-initialised C)
   EPI_F32_SCATTER = 4, // row-parallel TP partial -> the owning rank's staging slot (GemmScatter)
+  // gate||up projection with the SwiGLU fused into the epilogue: B's rows (the weights) are
+  // interleaved in 64-row blocks [gate 64b..64b+63 | up 64b..64b+63], so every 128-column group
+  // of the output holds matching gate / up columns.  C (bf16, ldc) receives
+  // m[:, j] = silu(bf16(g_j)) * bf16(u_j) for j < m_cols and zeros in [m_cols, ldc); rows >=
+  // c2_row0 also store the raw bf16 gate / up (interleaved layout) to C2 + (row - c2_row0) * ldc2
+  // (the finetuning rows' saved activations).  BN >= 128, no K split.
+  EPI_SWIGLU = 5,
 };
 
 // EPI_F32_SCATTER: output row `row` belongs to rank owner = row / rows_per_owner; the fp32
@@ -68,6 +75,10 @@ struct GemmDesc {
   int b_const = 0;              // B not produced by the preceding kernel (weights): PDL prefetch
   GemmScatter scatter;          // EPI_F32_SCATTER only
   int b_mn = 0;                 // 1: B stored [K rows][N cols] (ldb >= N): MN-major operand
+  void* C2 = nullptr;           // EPI_SWIGLU: saved gate / up rows (see above)
+  long ldc2 = 0;
+  int c2_row0 = 0;
+  int m_cols = 0;               // EPI_SWIGLU: width of m (the ffn size f)
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);

@@ -110,3 +110,26 @@ def test_gemm_mn_major_b(cuda, M, N, K, epi, bn, splits):
     torch.cuda.synchronize()
     err = (C.float() - ref).abs().max().item() / ref.abs().max().item()
     assert err < (1e-2 if epi == 0 else 1e-4), err
+
+
+@pytest.mark.parametrize("M,f,K", [(64, 1024, 512), (300, 2048, 1024), (2048, 14336, 512), (17, 512, 4096),
+                                   (1000, 1536, 512)])
+def test_gemm_swiglu_epilogue(cuda, M, f, K):
+    """EPI_SWIGLU (the gate||up projection with the SwiGLU fused into the epilogue): B's rows
+    interleaved in 64-row [gate | up] blocks; m = silu(bf16 gate) * bf16 up (the unfused path's
+    rounding points), the K-concatenation pad columns [f, ldc) zeroed."""
+    g = torch.Generator(device="cuda").manual_seed(M + f)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    Wg = torch.randn(f, K, device=cuda, generator=g).bfloat16() / 8
+    Wu = torch.randn(f, K, device=cuda, generator=g).bfloat16() / 8
+    B = torch.stack([Wg.view(f // 64, 64, K), Wu.view(f // 64, 64, K)], 1).reshape(2 * f, K).contiguous()
+    ldc = f + 64
+    C = torch.full((M, ldc), 7.0, device=cuda, dtype=torch.bfloat16)
+    _gemm(A, B, C, 5)
+    gate = (A.float() @ Wg.float().T).bfloat16().float()
+    up = (A.float() @ Wu.float().T).bfloat16().float()
+    ref = torch.nn.functional.silu(gate) * up
+    torch.cuda.synchronize()
+    err = (C[:, :f].float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+    assert C[:, f:].float().abs().max().item() == 0.0
