@@ -19,6 +19,7 @@
 #include <cmath>
 #include <functional>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -282,7 +283,7 @@ void layout(cs_engine* e, bool measure, size_t* total) {
 size_t meta_size(const cs_engine* e) {
   const size_t T = e->T_max, S = e->max_seg;
   size_t b = 0;
-  b += T * 4 * 3;                          // tokens, row_pos, row_seg
+  b += T * 4 * 4;                          // tokens, row_pos, row_seg, row_slot
   b += S * sizeof(cs::AttnSeg);
   b += (size_t)e->npages * 4 + 4096 * 4;   // page table (upper bound)
   b += 65536 * sizeof(cs::AttnWork) + 16384 * sizeof(cs::AttnDecWork);
@@ -803,7 +804,7 @@ struct StepPlan {
   int n_samp = 0;
   int n_work = 0, n_comb = 0, n_tc = 0, n_dec = 0, n_comb_tc = 0;
   // device pointers into d_meta
-  int *tokens, *row_pos, *row_seg, *page_table, *samp_idx, *targets;
+  int *tokens, *row_pos, *row_seg, *row_slot, *page_table, *samp_idx, *targets;
   cs::AttnSeg* segs;
   cs::AttnWork* work;
   cs::AttnWork* work_tc;
@@ -818,7 +819,7 @@ struct StepPlan {
 int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long ldb, long b_rows,
          void* C, long ldc, long M, long N, long K, int epi, const float* bias = nullptr,
          const cs::GemmScatter* sc = nullptr, int b_mn = 0, void* C2 = nullptr, long ldc2 = 0,
-         int c2_row0 = 0) {
+         int c2_row0 = 0, const cs::QkvEpi* qkv = nullptr) {
   cs::GemmDesc g;
   if (sc) g.scatter = *sc;
   g.b_mn = b_mn;
@@ -836,6 +837,7 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
   g.epi = epi;
   g.bias = bias;
   g.b_const = 1;  // every engine GEMM's B operand is a (frozen or LoRA) weight
+  if (qkv) g.qkv = *qkv;
   if (epi == cs::EPI_SWIGLU) {  // m = silu(gate) * up into C, the FT rows' gate / up into C2
     g.C2 = C2;
     g.ldc2 = ldc2;
@@ -964,11 +966,13 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     return o;
   };
   const size_t o_tok = take((size_t)T * 4), o_pos = take((size_t)T * 4), o_seg = take((size_t)T * 4);
+  const size_t o_slot = take((size_t)T * 4);  // KV-pool row of each token (QKV epilogue append)
   const size_t o_segs = take((size_t)sp.n_seg * sizeof(cs::AttnSeg));
   const size_t o_pt = take((size_t)ptl * 4);
   int* h_tok = reinterpret_cast<int*>(hb + o_tok);
   int* h_pos = reinterpret_cast<int*>(hb + o_pos);
   int* h_rseg = reinterpret_cast<int*>(hb + o_seg);
+  int* h_slot = reinterpret_cast<int*>(hb + o_slot);
   cs::AttnSeg* h_segs = reinterpret_cast<cs::AttnSeg*>(hb + o_segs);
   if (ptl) std::memcpy(hb + o_pt, plan->page_table, (size_t)ptl * 4);
   for (int i = 0; i < ptl; ++i)
@@ -1031,6 +1035,8 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       h_tok[row + i] = t;
       h_pos[row + i] = g.ctx_start + i;
       h_rseg[row + i] = s;
+      const int pos = g.ctx_start + i;
+      h_slot[row + i] = plan->page_table[g.page_off + pos / P] * P + pos % P;
     }
     if (g.sample) {
       samp_rows.push_back(row + g.q_len - 1);
@@ -1256,6 +1262,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   sp.tokens = reinterpret_cast<int*>(db + o_tok);
   sp.row_pos = reinterpret_cast<int*>(db + o_pos);
   sp.row_seg = reinterpret_cast<int*>(db + o_seg);
+  sp.row_slot = reinterpret_cast<int*>(db + o_slot);
   sp.segs = reinterpret_cast<cs::AttnSeg*>(db + o_segs);
   sp.page_table = reinterpret_cast<int*>(db + o_pt);
   sp.work = reinterpret_cast<cs::AttnWork*>(db + o_work);
@@ -1296,8 +1303,6 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         save_rows(e, e->ft_rstd1 + (size_t)l * e->L_max + l0, 1, e->rstd + sp.ft_row0, 1, n_ft, 1);
       }
     }
-    TRY(gemm(e, e->xb, h, e->T_max, e->wqkv_t + (size_t)l * e->nqkv * h, h, e->nqkv, e->qkv, e->nqkv,
-             T, e->nqkv, h, cs::EPI_BF16, e->cfg.qkv_bias ? e->bqkv + (size_t)l * e->nqkv : nullptr));
     cs::RopeAppendParams rp;
     rp.qkv = e->qkv;
     rp.ld = e->nqkv;
@@ -1316,7 +1321,27 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     rp.T = T;
     rp.ft_row0 = sp.ft_row0;
     rp.q_cache = (n_ft > 0 && keep_attn) ? e->ft_q + (size_t)l * e->L_max * e->q_dim : nullptr;
-    cs::rope_append(rp, st);
+    const float* qkv_bias = e->cfg.qkv_bias ? e->bqkv + (size_t)l * e->nqkv : nullptr;
+    if (e->d == 128) {
+      // RoPE and the KV append in the QKV GEMM's epilogue (kernels.h EPI_QKV_ROPE)
+      cs::QkvEpi qe;
+      qe.row_pos = rp.row_pos;
+      qe.row_slot = sp.row_slot;
+      qe.k_pool = rp.k_pool;
+      qe.v_pool = rp.v_pool;
+      qe.q_cache = rp.q_cache;
+      qe.rope_tab = e->rope_tab;
+      qe.q_dim = e->q_dim;
+      qe.kv_dim = e->kv_dim;
+      qe.ft_row0 = sp.ft_row0;
+      qe.use_rope = e->rope;
+      TRY(gemm(e, e->xb, h, e->T_max, e->wqkv_t + (size_t)l * e->nqkv * h, h, e->nqkv, e->qkv, e->nqkv,
+               T, e->nqkv, h, cs::EPI_QKV_ROPE, qkv_bias, nullptr, 0, nullptr, 0, 0, &qe));
+    } else {
+      TRY(gemm(e, e->xb, h, e->T_max, e->wqkv_t + (size_t)l * e->nqkv * h, h, e->nqkv, e->qkv, e->nqkv,
+               T, e->nqkv, h, cs::EPI_BF16, qkv_bias));
+      cs::rope_append(rp, st);
+    }
     cs::AttnFwdParams ap;
     ap.q = e->qkv;
     ap.q_ld = e->nqkv;

@@ -52,6 +52,7 @@ struct GemmArgs {
   long ldc2 = 0;
   int c2_row0 = 0;
   int m_cols = 0;
+  QkvEpi qkv;          // EPI_QKV_ROPE
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -200,6 +201,92 @@ __device__ __forceinline__ void epilogue_swiglu(const GemmArgs& a, int row, int 
       *reinterpret_cast<uint4*>(s + 64 + 2 * i) = make_uint4(up[i], up[i + 1], up[i + 2], up[i + 3]);
     }
   }
+}
+
+// EPI_QKV_ROPE: one 128-column head group (head-aligned, output columns col .. col+127) of `row`,
+// read from TMEM in 32-column chunks (tb = this row's lane, this group's first column).
+// q / k heads: rotate-half pairs (i, i+64) of RoPE; q stays in C (and the FT rows' q_cache),
+// k and v go to the row's page slot of the K / V pool (tiny_model.hpp:225-232 + paging).
+__device__ __forceinline__ void epilogue_qkv_rope(const GemmArgs& a, int row, int col, uint32_t tb, long prow,
+                                                  int pos) {
+  const QkvEpi& e = a.qkv;
+  const bool valid = row < a.M && col < a.N;
+  const bool isq = col < e.q_dim, isk = !isq && col < e.q_dim + e.kv_dim;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(a.C) + (long)row * a.ldc;
+  if (isq || isk) {
+#pragma unroll 1
+    for (int h = 0; h < 64; h += 32) {
+      uint32_t x1[32], x2[32];
+      tmem_ld_32x32b_x32(tb + h, x1);
+      tmem_ld_32x32b_x32(tb + 64 + h, x2);
+      tmem_ld_wait();
+      if (!valid) continue;
+      uint32_t o1[16], o2[16];
+      const float2* tab = e.rope_tab + (long)pos * 64 + h;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float v1[2], v2[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c = col + h + j + t;
+          v1[t] = __bfloat162float(__float2bfloat16(__uint_as_float(x1[j + t]) + (a.bias ? a.bias[c] : 0.f)));
+          v2[t] = __bfloat162float(__float2bfloat16(__uint_as_float(x2[j + t]) + (a.bias ? a.bias[c + 64] : 0.f)));
+          if (e.use_rope) {
+            const float2 cs = tab[j + t];
+            const float r1 = v1[t] * cs.x - v2[t] * cs.y, r2 = v2[t] * cs.x + v1[t] * cs.y;
+            v1[t] = r1;
+            v2[t] = r2;
+          }
+        }
+        o1[j >> 1] = pack_bf16(v1[0], v1[1]);
+        o2[j >> 1] = pack_bf16(v2[0], v2[1]);
+      }
+      __nv_bfloat16* d1;
+      if (isq) {
+        d1 = C + col + h;
+      } else {
+        d1 = e.k_pool + prow * e.kv_dim + (col - e.q_dim) + h;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        *reinterpret_cast<uint4*>(d1 + 2 * i) = make_uint4(o1[i], o1[i + 1], o1[i + 2], o1[i + 3]);
+        *reinterpret_cast<uint4*>(d1 + 64 + 2 * i) = make_uint4(o2[i], o2[i + 1], o2[i + 2], o2[i + 3]);
+      }
+      if (isq && e.q_cache && row >= e.ft_row0) {
+        __nv_bfloat16* qc = e.q_cache + (long)pos * e.q_dim + col + h;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          *reinterpret_cast<uint4*>(qc + 2 * i) = make_uint4(o1[i], o1[i + 1], o1[i + 2], o1[i + 3]);
+          *reinterpret_cast<uint4*>(qc + 64 + 2 * i) = make_uint4(o2[i], o2[i + 1], o2[i + 2], o2[i + 3]);
+        }
+      }
+    }
+  } else {  // v head -> the V page slot
+#pragma unroll 1
+    for (int h = 0; h < 128; h += 32) {
+      uint32_t x[32];
+      tmem_ld_32x32b_x32(tb + h, x);
+      tmem_ld_wait();
+      if (!valid) continue;
+      uint32_t o[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2)
+        o[j >> 1] = pack_bf16(__uint_as_float(x[j]) + (a.bias ? a.bias[col + h + j] : 0.f),
+                              __uint_as_float(x[j + 1]) + (a.bias ? a.bias[col + h + j + 1] : 0.f));
+      __nv_bfloat16* d = e.v_pool + prow * e.kv_dim + (col - e.q_dim - e.kv_dim) + h;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<uint4*>(d + 2 * i) = make_uint4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+    }
+  }
+}
+
+// the row's page slot and position for EPI_QKV_ROPE (one lookup per row and tile)
+__device__ __forceinline__ void qkv_row_slot(const GemmArgs& a, int row, long& prow, int& pos) {
+  prow = 0;
+  pos = 0;
+  if (row >= a.M) return;
+  pos = __ldg(a.qkv.row_pos + row);
+  prow = __ldg(a.qkv.row_slot + row);
 }
 
 // B stage of BN columns x 64 K: K-major = one box {64 K, BN rows}; MN-major (B stored
@@ -360,6 +447,20 @@ __global__ void __launch_bounds__(256, 1)
       const int row = mb * Cfg::BM + ew * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       if constexpr (BN >= 128) {
+        if (args.epi == EPI_QKV_ROPE) {
+          long prow;
+          int pos;
+          qkv_row_slot(args, row, prow, pos);
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 128) epilogue_qkv_rope(args, row, nb * BN + c0, tbase + c0, prow, pos);
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+          continue;
+        }
         if (args.epi == EPI_SWIGLU) {
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 128)
@@ -623,7 +724,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * 256 + (int)rank * 128 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-      if (args.epi == EPI_SWIGLU) {
+      if (args.epi == EPI_QKV_ROPE) {
+        long prow;
+        int pos;
+        qkv_row_slot(args, row, prow, pos);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 128) epilogue_qkv_rope(args, row, nb * BN + c0, tbase + c0, prow, pos);
+      } else if (args.epi == EPI_SWIGLU) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 128)
 #pragma unroll 1
@@ -835,6 +942,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.ldc2 = d.ldc2;
   a.c2_row0 = d.c2_row0;
   a.m_cols = (int)(d.N / 2);
+  a.qkv = d.qkv;
   const long tiles2 = (long)a.num_m * a.num_n;
   a.units = (int)tiles2;
   // accumulating epilogues (C += acc): split the last, partial wave of tiles along K when the
@@ -893,8 +1001,11 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   if (d.epi == EPI_SWIGLU && (d.N % 128 != 0 || (d.m_cols != 0 && d.m_cols * 2 != d.N) || d.ldc < d.N / 2 ||
                               (d.ldc % 8) != 0))
     return cudaErrorInvalidValue;
-  // bf16-output epilogues: no K split (EPI_SWIGLU as EPI_BF16 below)
-  const bool bf16_out = d.epi == EPI_BF16 || d.epi == EPI_SWIGLU;
+  if (d.epi == EPI_QKV_ROPE && (d.N % 128 != 0 || d.qkv.q_dim % 128 != 0 || d.qkv.kv_dim % 128 != 0 ||
+                                !d.qkv.row_pos || !d.qkv.row_slot || !d.qkv.k_pool || !d.qkv.v_pool || !d.qkv.rope_tab))
+    return cudaErrorInvalidValue;
+  // bf16-output epilogues: no K split (EPI_SWIGLU / EPI_QKV_ROPE as EPI_BF16 below)
+  const bool bf16_out = d.epi == EPI_BF16 || d.epi == EPI_SWIGLU || d.epi == EPI_QKV_ROPE;
   // large GEMMs (at least one wave of 256 x BN tiles): CTA-pair kernel
   if (d.bn <= 0 && d.splits <= 0 && use_2sm() && d.M >= 256) {
     const long mt = (d.M + 255) / 256;
@@ -953,7 +1064,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
     }
   }
   if (d.b_mn && bn < 64) bn = 64;  // MN-major B stages are 64-column chunks
-  if (d.epi == EPI_SWIGLU && bn < 128) bn = 128;  // whole 128-column gate / up groups per tile
+  if ((d.epi == EPI_SWIGLU || d.epi == EPI_QKV_ROPE) && bn < 128) bn = 128;  // whole 128-column groups per tile
   GemmArgs a;
   a.M = (int)d.M;
   a.N = (int)d.N;
@@ -971,6 +1082,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.ldc2 = d.ldc2;
   a.c2_row0 = d.c2_row0;
   a.m_cols = (int)(d.N / 2);
+  a.qkv = d.qkv;
   int splits = d.splits > 0 ? d.splits : mid_splits;
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {

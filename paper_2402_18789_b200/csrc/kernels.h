@@ -45,6 +45,21 @@ enum GemmEpi : int {
   // c2_row0 also store the raw bf16 gate / up (interleaved layout) to C2 + (row - c2_row0) * ldc2
   // (the finetuning rows' saved activations).  BN >= 128, no K split.
   EPI_SWIGLU = 5,
+  // QKV projection with RoPE and the KV-cache append fused into the epilogue (head_dim 128;
+  // QkvEpi): C (bf16 [T, q|k|v], +bias) receives the roped q heads (and the FT rows' copy in
+  // q_cache); the roped k and the v heads go straight to the row's paged K / V slot.  Rounding
+  // points as rope_append after a bf16 GEMM: bf16(acc + bias), rotation in fp32, bf16.
+  EPI_QKV_ROPE = 6,
+};
+
+struct QkvEpi {
+  const int* row_pos = nullptr;    // [T] absolute position
+  const int* row_slot = nullptr;   // [T] KV-pool row (page * page_size + pos % page_size)
+  __nv_bfloat16* k_pool = nullptr;
+  __nv_bfloat16* v_pool = nullptr;
+  __nv_bfloat16* q_cache = nullptr;  // [L][q_dim] (this layer) or null
+  const float2* rope_tab = nullptr;  // [max_pos][64] (cos, sin)
+  int q_dim = 0, kv_dim = 0, ft_row0 = 0, use_rope = 0;
 };
 
 // EPI_F32_SCATTER: output row `row` belongs to rank owner = row / rows_per_owner; the fp32
@@ -79,6 +94,7 @@ struct GemmDesc {
   long ldc2 = 0;
   int c2_row0 = 0;
   int m_cols = 0;               // EPI_SWIGLU: width of m (the ffn size f)
+  QkvEpi qkv;                   // EPI_QKV_ROPE
 };
 
 cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st);
