@@ -163,8 +163,12 @@ __global__ void __launch_bounds__(512, 1)
   const int kvh = blockIdx.y;
   const int nrows = p.b - p.a;
   const int n_qt = (nrows + rpt - 1) / rpt;
-  const int qt0 = k0 > p.a ? (k0 - p.a) / rpt : 0;  // first tile whose last position >= k0
-  const int n = n_qt - qt0;
+  // first tile whose last position >= k0; long key blocks are split over gridDim.z CTAs of at
+  // most p.tiles_per_cta query tiles each (their ΔKV partial sums then add atomically)
+  const int qt_first = k0 > p.a ? (k0 - p.a) / rpt : 0;
+  const int qt0 = qt_first + (int)blockIdx.z * p.tiles_per_cta;
+  const int n = max(0, min(n_qt - qt0, p.tiles_per_cta));
+  const bool split = gridDim.z > 1;
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);  // warp-uniform
   const int lane = threadIdx.x & 31;
 
@@ -392,37 +396,34 @@ __global__ void __launch_bounds__(512, 1)
       tmem_ld_32x32b_x32(tmem + lane_base + TM_DV + c * 64, a0);
       tmem_ld_32x32b_x32(tmem + lane_base + TM_DV + c * 64 + 32, a1);
       tmem_ld_wait();
-      if (key < p.b) {
-        float* av = p.dv_acc + (long)key * p.acc_ld + kvh * DB + c * 64;
+      // += into ΔKVAccum: plain read-modify-write, or float4 atomics when the key block is split
+      auto acc4 = [&](float* dst, const uint32_t* v, float sc) {
 #pragma unroll
         for (int t = 0; t < 32; t += 4) {
-          float4 x = *reinterpret_cast<float4*>(av + t);
-          x.x += __uint_as_float(a0[t]); x.y += __uint_as_float(a0[t + 1]);
-          x.z += __uint_as_float(a0[t + 2]); x.w += __uint_as_float(a0[t + 3]);
-          *reinterpret_cast<float4*>(av + t) = x;
-          float4 y = *reinterpret_cast<float4*>(av + 32 + t);
-          y.x += __uint_as_float(a1[t]); y.y += __uint_as_float(a1[t + 1]);
-          y.z += __uint_as_float(a1[t + 2]); y.w += __uint_as_float(a1[t + 3]);
-          *reinterpret_cast<float4*>(av + 32 + t) = y;
+          const float4 d = make_float4(__uint_as_float(v[t]) * sc, __uint_as_float(v[t + 1]) * sc,
+                                       __uint_as_float(v[t + 2]) * sc, __uint_as_float(v[t + 3]) * sc);
+          float4* q4 = reinterpret_cast<float4*>(dst + t);
+          if (split) {
+            atomicAdd(q4, d);
+          } else {
+            float4 x = *q4;
+            x.x += d.x; x.y += d.y; x.z += d.z; x.w += d.w;
+            *q4 = x;
+          }
         }
+      };
+      if (key < p.b) {
+        float* av = p.dv_acc + (long)key * p.acc_ld + kvh * DB + c * 64;
+        acc4(av, a0, 1.f);
+        acc4(av + 32, a1, 1.f);
       }
       tmem_ld_32x32b_x32(tmem + lane_base + TM_DK + c * 64, a0);
       tmem_ld_32x32b_x32(tmem + lane_base + TM_DK + c * 64 + 32, a1);
       tmem_ld_wait();
       if (key < p.b) {
         float* ak = p.dk_acc + (long)key * p.acc_ld + kvh * DB + c * 64;
-        const float sc = p.scale;
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          float4 x = *reinterpret_cast<float4*>(ak + t);
-          x.x += __uint_as_float(a0[t]) * sc; x.y += __uint_as_float(a0[t + 1]) * sc;
-          x.z += __uint_as_float(a0[t + 2]) * sc; x.w += __uint_as_float(a0[t + 3]) * sc;
-          *reinterpret_cast<float4*>(ak + t) = x;
-          float4 y = *reinterpret_cast<float4*>(ak + 32 + t);
-          y.x += __uint_as_float(a1[t]) * sc; y.y += __uint_as_float(a1[t + 1]) * sc;
-          y.z += __uint_as_float(a1[t + 2]) * sc; y.w += __uint_as_float(a1[t + 3]) * sc;
-          *reinterpret_cast<float4*>(ak + 32 + t) = y;
-        }
+        acc4(ak, a0, p.scale);
+        acc4(ak + 32, a1, p.scale);
       }
     }
     tc_fence_before();
@@ -492,8 +493,21 @@ cudaError_t attn_bwd_fused(const AttnBwdParams& p, const CUtensorMap& tmK, const
   if (err != cudaSuccess) return err;
   g_launches.fetch_add(2, std::memory_order_relaxed);
   attn_bwd_delta_kernel_launch(p, rows, n_heads, st);
-  dim3 grid((p.b + 127) / 128, n_heads / p.grp);
-  launch_pdl(kFused[p.grp - 1], grid, dim3(512), kv3::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, tmDQ, p);
+  // query tiles per key block: n(x) = n_qt - first tile at or after key block x.  A small causal
+  // window leaves fewer key-block CTAs than SMs with a 16x spread of lengths (s = 2048 at
+  // l_j = 2048: 128 CTAs of 8..128 tiles), so long blocks are split into CTAs of at most
+  // ~total / (2 x 148) tiles (>= 24: K / V load and ΔKV epilogue per CTA), spread over grid.z
+  const int rpt = 64 / p.grp, nkb = (p.b + 127) / 128, kvh = n_heads / p.grp;
+  const long n_qt = (rows + rpt - 1) / rpt;
+  long total = 0;
+  for (int x = 0; x < nkb; ++x) total += n_qt - (x * 128 > p.a ? (x * 128 - p.a) / rpt : 0);
+  total *= kvh;
+  AttnBwdParams q = p;
+  q.tiles_per_cta = (int)std::max<long>(24, (total + 2 * kNumSMs - 1) / (2 * kNumSMs));
+  const int nz = (int)std::min<long>(8, (n_qt + q.tiles_per_cta - 1) / q.tiles_per_cta);
+  if ((n_qt + q.tiles_per_cta - 1) / q.tiles_per_cta > 8) q.tiles_per_cta = (int)((n_qt + 7) / 8);
+  dim3 grid(nkb, kvh, nz);
+  launch_pdl(kFused[p.grp - 1], grid, dim3(512), kv3::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, tmDQ, q);
   return cudaGetLastError();
 }
 

@@ -78,6 +78,7 @@ struct AttnBwdParams {
   long acc_ld;
   int grp;
   float scale, scale_log2;
+  int tiles_per_cta = 1 << 30;  // fused kernel: query tiles per CTA (set by attn_bwd_fused)
 };
 
 // decode rows (q_len * group <= 16): HBM-bound paged kernel (attn_decode.cu); run before
