@@ -49,6 +49,10 @@ struct cs_engine {
   cs::Comm* comm = nullptr;  // tp_size > 1: all-reduce of the row-parallel partial sums
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // decode / small-segment attention on a side stream next to the tcgen05 FT-window attention
+  // (forward(): fork after the QKV projection, join before the O projection)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // dims (per rank: heads and ffn columns are this rank's shard; *_g = whole model)
   int Hq_g, Hkv_g, f_g;
   int h, Hq, Hkv, d, q_dim, kv_dim, nqkv, f, V, r, NL, P, npages, gu_n, f_cat, h_cat, grp;
@@ -91,6 +95,7 @@ struct cs_engine {
   int* next_tok;
   unsigned long long* amax_part;
   float *part_o, *part_lse;
+  float *part_o_tc, *part_lse_tc;  // split-KV parts of the tcgen05 forward (its own stream)
   float* tp_sync;  // [8 ranks][8 values]: cs_engine_tp_sync_max
   // fused row-parallel GEMM + all-reduce (peer-memory groups): staging [ranks][rpo][h] fp32,
   // zero between uses; peer tables exchanged lazily (same call order on every rank)
@@ -258,6 +263,8 @@ void layout(cs_engine* e, bool measure, size_t* total) {
   const size_t max_parts = 4096;
   AL(part_o, max_parts * 64 * e->d);
   AL(part_lse, max_parts * 64);
+  AL(part_o_tc, max_parts * 64 * e->d);
+  AL(part_lse_tc, max_parts * 64);
   AL(dycat, S * e->h_cat);
   AL(dgu, S * e->gu_n);
   AL(dr1b, S * h);
@@ -394,8 +401,11 @@ int create_engine(const cs_model_config* cfg, int device, int tp_rank, int tp_si
   layout(e, false, nullptr);
   if (e->comm) e->comm->bind_arena(e->arena, e->arena_bytes, e->ipc_flags);
   cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&e->st2, cudaStreamNonBlocking);
   cudaEventCreate(&e->ev0);
   cudaEventCreate(&e->ev1);
+  cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming);
   cudaMallocHost(&e->h_meta, e->meta_bytes);
   cudaMallocHost(&e->h_loss, (size_t)e->L_max * sizeof(float));
   // zero everything that has padding semantics (concat pad columns, LoRA state, norms)
@@ -584,6 +594,9 @@ extern "C" int cs_engine_destroy(cs_engine* e) {
   cudaFreeHost(e->h_loss);
   cudaEventDestroy(e->ev0);
   cudaEventDestroy(e->ev1);
+  cudaEventDestroy(e->ev_fork);
+  cudaEventDestroy(e->ev_join);
+  cudaStreamDestroy(e->st2);
   cudaStreamDestroy(e->st);
   delete e->comm;
   delete e;
@@ -1364,6 +1377,15 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
     ap.scale_log2 = (float)(1.0 / std::sqrt((double)e->d) * 1.4426950408889634);
     cs_engine::ProfRec apr{};
     const bool bw_attn = sp.n_work + sp.n_dec > 0;
+    // spatial sharing inside the step: the HBM-bound decode (and small-segment) attention runs
+    // on a side stream next to the tensor-bound FT-window attention, on the SMs the latter's
+    // grid leaves free (profiling runs keep one stream: its events serialise anyway)
+    const bool fork = bw_attn && sp.n_tc > 0 && !e->profiling;
+    cudaStream_t sa = fork ? e->st2 : st;
+    if (fork) {
+      CS_CUDA_TRY(cudaEventRecord(e->ev_fork, st));
+      CS_CUDA_TRY(cudaStreamWaitEvent(e->st2, e->ev_fork, 0));
+    }
     if (e->profiling && bw_attn) {
       apr.flops = e->step_attn_flops;
       apr.bytes = e->step_attn_bytes;
@@ -1386,11 +1408,12 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         dpr.kind = 5;
         prof_begin(e, dpr);
       }
-      CS_CUDA_TRY(cs::attn_decode(dp, mk, mv, e->d, sp.n_dec, st));
+      CS_CUDA_TRY(cs::attn_decode(dp, mk, mv, e->d, sp.n_dec, sa));
       if (e->profiling) prof_end(e, dpr);
     }
-    CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, st));
+    CS_CUDA_TRY(cs::attn_fwd(ap, e->d, sp.n_work, sp.n_comb, sa));
     if (e->profiling && bw_attn) prof_end(e, apr);
+    if (fork) CS_CUDA_TRY(cudaEventRecord(e->ev_join, sa));
     if (sp.n_tc > 0) {
       CUtensorMap mk, mv, mk128, mv128;
       const long pool_rows = (long)e->npages * e->P;
@@ -1401,6 +1424,8 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         return cs::set_error(CS_ERR_CUDA, "attention: TMA map creation failed");
       cs::AttnFwdParams tp = ap;
       tp.work = sp.work_tc;
+      tp.part_o = e->part_o_tc;
+      tp.part_lse = e->part_lse_tc;
       cs_engine::ProfRec tpr{};
       if (e->profiling) {
         tpr.flops = e->step_tc_flops;
@@ -1409,14 +1434,15 @@ int forward(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp, double* l
         prof_begin(e, tpr);
       }
       CS_CUDA_TRY(cs::attn_fwd_tc2(tp, mk, mv, mk128, mv128, sp.n_tc, st));
-      if (sp.n_comb_tc > 0) {  // after the decode combine: the part buffers are reused
-        cs::AttnFwdParams cp = ap;
+      if (sp.n_comb_tc > 0) {
+        cs::AttnFwdParams cp = tp;
         cp.combine = sp.comb_tc;
         cp.part_rows = 256;
         CS_CUDA_TRY(cs::attn_combine(cp, e->d, sp.n_comb_tc, st));
       }
       if (e->profiling) prof_end(e, tpr);
     }
+    if (fork) CS_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_join, 0));
     if (n_ft > 0 && keep_attn) {
       save_rows(e, e->ft_o + ((size_t)l * e->L_max + l0) * e->q_dim, e->q_dim,
                 e->attn + (size_t)sp.ft_row0 * e->q_dim, e->q_dim, n_ft, e->q_dim);

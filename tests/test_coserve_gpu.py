@@ -454,7 +454,7 @@ def test_alloc_audit_no_frozen_weight_gradients():
     size1 = {n: (el, b) for n, el, b in recs1}
     model_sized = {n for n, el, b in recs2 if b == 4 and size1.get(n) == (el, b)}
     allowed = {"gf", "bqkv", "g1", "g2", "loraA", "loraB", "gA", "gB", "mA", "vA", "mB", "vB",
-               "part_o", "part_lse", "tp_sync", "tp_stage", "ipc_flags"}
+               "part_o", "part_lse", "part_o_tc", "part_lse_tc", "tp_sync", "tp_stage", "ipc_flags"}
     assert model_sized <= allowed, model_sized - allowed
     NL, f, r, h = arch.n_layers, arch.ffn, arch.lora_rank, arch.hidden
     assert size1["gA"][0] == NL * f * r and size1["gB"][0] == NL * r * h
