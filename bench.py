@@ -17,8 +17,10 @@ the measured forward-window rate r_f (tokens/ms over forward-phase iterations) a
 rate r_b (layer-tokens/ms): t_mb = L/r_f + N_layers*L/r_b.
 
 Multi-GPU (--gpus N under torchrun): 8B runs as N independent replicas (TP=1 pipelines, as in
-PAPER.md:437-439 for the 8B model), each at the per-replica arrival rate: weak scaling, no
-data-path collective; value = sum of replica throughputs over the max-over-ranks time.
+PAPER.md:437-439 for the 8B model); the --rate arrivals are the whole job's (north_star: 8xB200 at
+20 req/s), split evenly over the replicas (--rate-scope replica: --rate each); every replica runs
+its own finetuning job (weak scaling of the finetuning work), no data-path collective; value =
+sum of replica throughputs over the max-over-ranks time.
 
 --impl reference: the reference's own CPU path (oracle/_ref: tiny_model.hpp forward_full +
 backward_full compiled unmodified) on an 8B-shaped single layer, all host cores.
@@ -78,9 +80,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rate", type=float, default=20.0)
-    ap.add_argument("--rate-scope", default="replica", choices=["replica", "total"],
-                    help="replica: every co-serving replica (TP group) gets --rate (weak scaling); "
-                         "total: --rate is the whole job's arrival rate, split evenly over replicas")
+    ap.add_argument("--rate-scope", default="total", choices=["replica", "total"],
+                    help="total (default, north_star: 8xB200 at 20 req/s): --rate is the whole job's "
+                         "arrival rate, split evenly over the replicas / TP groups; replica: every "
+                         "replica gets --rate")
     # side rates (other_rates in the JSON line): the headline is the --rate run
     ap.add_argument("--rates", default="4,10,20")
     ap.add_argument("--ft-len", type=int, default=8192)
