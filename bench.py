@@ -69,7 +69,7 @@ MODELS = {
     "qwen-2.5-32b": dict(shape=dict(n_layers=64, hidden=5120, n_heads=40, n_kv_heads=8,
                                     head_dim=128, ffn=27648, vocab=152064, lora_rank=16),
                          qkv_bias=1, rope_theta=1000000.0, rms_eps=1e-6, slo_ms=75.0,
-                         n_pages=8192, tail_target=0.92),
+                         n_pages=8192, tail_target=0.89),
 }
 
 
