@@ -445,7 +445,7 @@ def run_ours(a):
     for r in rates:
         if r == a.rate:
             continue
-        st, _ = coserve_run(eng, coserve_config(per(r), prof, min(a.steps, 60), a.warmup, a.ft_len,
+        st, _ = coserve_run(eng, coserve_config(per(r), prof, min(a.steps, 150), a.warmup, a.ft_len,
                                                 seed=11 + int(r), slo_ms=slo,
                                                 max_window=a.ft_window, tail=m["tail_target"]))
         side[str(int(r) if r.is_integer() else r)] = {
