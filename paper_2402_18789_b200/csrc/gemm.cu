@@ -53,6 +53,7 @@ struct GemmArgs {
   int c2_row0 = 0;
   int m_cols = 0;
   QkvEpi qkv;          // EPI_QKV_ROPE
+  int group_m = 1;     // m-blocks per raster run (tile_mn)
 };
 
 // SM (small M <= 64): only 64 rows of A are loaded per stage; the M=128 MMA reads the other 64
@@ -74,17 +75,23 @@ struct GemmCfg {
   static constexpr int CHUNK = BN >= 32 ? 32 : 16;
 };
 
-// tile index -> (m, n) block, grouped raster: runs of GROUP_M m-blocks sweep all n-blocks, so
+// tile index -> (m, n) block, grouped raster: runs of group_m m-blocks sweep all n-blocks, so
 // the tiles in flight at once (a wave of 74 pairs / 148 CTAs) share A rows and B columns in L2
 // (M = 8192 backward dX GEMMs: a plain m-fastest order kept all 32 m-blocks' A rows in flight,
-// 1394 vs cuBLAS 1612 TF/s at K = 28672); num_m <= GROUP_M keeps the plain m-fastest order
-constexpr int GROUP_M = 8;
+// 1394 vs cuBLAS 1612 TF/s at K = 28672), and every run streams B (the weights) once: the host
+// sizes the runs evenly (<= 12 m-blocks) -- a ragged last run of one m-block re-read all of B
+// (gate||up M = 1088 on 128-row tiles: 217 us vs 191 us)
 __device__ __forceinline__ void tile_mn(int t, const GemmArgs& a, int& m, int& n) {
-  const int per = GROUP_M * a.num_n;
+  const int G = a.group_m;
+  const int per = G * a.num_n;
   const int g = t / per, r = t - g * per;
-  const int gm = min(GROUP_M, a.num_m - g * GROUP_M);
-  m = g * GROUP_M + r % gm;
+  const int gm = min(G, a.num_m - g * G);
+  m = g * G + r % gm;
   n = r / gm;
+}
+inline int group_m_for(int num_m) {
+  const int ng = (num_m + 11) / 12;
+  return (num_m + ng - 1) / ng;
 }
 
 __device__ __forceinline__ void decode_work(int w, const GemmArgs& a, int& m_blk, int& n_blk,
@@ -939,6 +946,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.kb_total = (int)((d.K + 63) / 64);
   a.num_m = (int)((d.M + 255) / 256);
   a.num_n = (int)((d.N + BN - 1) / BN);
+  a.group_m = group_m_for(a.num_m);
   a.epi = d.epi;
   a.C = d.C;
   a.ldc = d.ldc;
@@ -1081,6 +1089,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   a.kb_total = (int)((d.K + 63) / 64);
   a.num_m = (int)((d.M + 127) / 128);
   a.num_n = (int)((d.N + bn - 1) / bn);
+  a.group_m = group_m_for(a.num_m);
   a.epi = d.epi;
   a.C = d.C;
   a.ldc = d.ldc;
