@@ -4,6 +4,7 @@
 // LoRA packing for the K-concatenated down projection (tiny_model.hpp:207-211), fused
 // cross-entropy forward+backward (row_cross_entropy :170-177, loss_head_grad :223-246),
 // token-level backward helpers (tiny_model.hpp:276-319), and the LoRA Adam update.
+#include <algorithm>
 #include <cfloat>
 
 #include <atomic>
@@ -406,8 +407,11 @@ void ce_fwd_bwd(const float* logits, long ld, const int* targets, int rows, int 
 // RMSNorm backward + residual add, one 256-thread block per row; the row's dY, x (and the
 // residual) are read once into registers (float4, <= 8 per thread: h <= 8192) and reused for
 // the dot product and the output.
+// (float4 registers sized for the row: h <= 4096 uses the V = 4 instance, 4 blocks per SM
+// resident instead of 2 -- a 2048-row window ran at 50% of HBM with 23% of warps active)
 constexpr int RMSB_V = 8;
-__global__ void __launch_bounds__(256) rms_bwd_kernel(const float* __restrict__ resid, long ldr,
+template <int V>
+__global__ void __launch_bounds__(256, V == 4 ? 4 : 2) rms_bwd_kernel(const float* __restrict__ resid, long ldr,
                                const float* __restrict__ x, long ldx, const float* __restrict__ g,
                                const float* __restrict__ rstd, const float* __restrict__ dh,
                                long ldh, float* __restrict__ out, long ldo, bf16* __restrict__ ob,
@@ -419,9 +423,9 @@ __global__ void __launch_bounds__(256) rms_bwd_kernel(const float* __restrict__ 
   const float* dr = dh + row * ldh;
   const float* rr = resid ? resid + row * ldr : nullptr;
   float* o = out + row * ldo;
-  float4 vd[RMSB_V], vx[RMSB_V], vr[RMSB_V];
+  float4 vd[V], vx[V], vr[V];
 #pragma unroll
-  for (int k = 0; k < RMSB_V; ++k) {
+  for (int k = 0; k < V; ++k) {
     const int c = (threadIdx.x + k * 256) * 4;
     vd[k] = vx[k] = vr[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < h) {
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(256) rms_bwd_kernel(const float* __restrict__ 
   if (use_norm) {
     rs = rstd[row];
 #pragma unroll
-    for (int k = 0; k < RMSB_V; ++k) {
+    for (int k = 0; k < V; ++k) {
       const int c = (threadIdx.x + k * 256) * 4;
       if (c < h) {
         const float4 gg = __ldg(reinterpret_cast<const float4*>(g + c));
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(256) rms_bwd_kernel(const float* __restrict__ 
     dot = block_sum(dot * rs, red) / (float)h;
   }
 #pragma unroll
-  for (int k = 0; k < RMSB_V; ++k) {
+  for (int k = 0; k < V; ++k) {
     const int c = (threadIdx.x + k * 256) * 4;
     if (c >= h) continue;
     float4 v;
@@ -468,7 +472,8 @@ void rms_bwd_add(const float* resid, long ldr, const float* x, long ldx, const f
   if (rows <= 0) return;
   if (h > RMSB_V * 1024 || (h % 4) != 0) return;  // engine_create bounds h (multiple of 64)
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
-  launch_pdl(rms_bwd_kernel, dim3(rows), dim3(256), 0, st, resid, ldr, x, ldx, g, rstd, dh, ldh, out, ldo, out_b,
+  launch_pdl(h <= 4096 ? rms_bwd_kernel<4> : rms_bwd_kernel<RMSB_V>, dim3(rows), dim3(256), 0, st, resid, ldr, x, ldx, g,
+             rstd, dh, ldh, out, ldo, out_b,
                                        ldob, h, use_norm);
 }
 
@@ -496,8 +501,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const bf16* __rest
   griddep_wait();    // launched with PDL: the producer's writes are visible from here on
   __shared__ __align__(16) float sl[MLP_ROWS * 16];
   const int col = 4 * (blockIdx.x * MLP_THREADS + threadIdx.x);
-  const int r0 = blockIdx.y * MLP_ROWS;
-  const int nr = min(MLP_ROWS, rows - r0);
+  const int rpb = (rows + gridDim.y - 1) / gridDim.y;  // rows per block (<= MLP_ROWS)
+  const int r0 = blockIdx.y * rpb;
+  const int nr = max(0, min(rpb, rows - r0));
   for (int i = threadIdx.x; i < nr * 16; i += MLP_THREADS) {
     const int rr = i >> 4, j = i & 15;
     sl[i] = j < r ? dlu[(long)(r0 + rr) * r + j] : 0.f;
@@ -599,7 +605,12 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_bwd_kernel(const bf16* __rest
 void mlp_bwd(const bf16* dm, long ld_dm, const bf16* saved, long ld_s, const float* dlu, int r,
              bf16* dgu, long ld_dgu, float* dA, int rows, int f, int swiglu, cudaStream_t st) {
   if (rows <= 0) return;
-  dim3 grid((f / 4 + MLP_THREADS - 1) / MLP_THREADS, (rows + MLP_ROWS - 1) / MLP_ROWS);
+  // enough blocks to keep ~6 per SM streaming (a 2048-row window on 256-row blocks ran 224
+  // blocks: 9% warps active, 30% of HBM; ncu profiles/r2_elem_bwd_ncu.txt), <= MLP_ROWS rows each
+  const int gx = (f / 4 + MLP_THREADS - 1) / MLP_THREADS;
+  const int gy = std::max((rows + MLP_ROWS - 1) / MLP_ROWS,
+                          std::min((rows + 31) / 32, (6 * 148 + gx - 1) / gx));
+  dim3 grid(gx, gy);
   cs::g_launches.fetch_add(1, std::memory_order_relaxed);
   launch_pdl(mlp_bwd_kernel, dim3(grid), dim3(MLP_THREADS), 0, st, dm, ld_dm, saved, ld_s, dlu, r, dgu, ld_dgu, dA, rows, f,
                                                swiglu);
