@@ -937,7 +937,7 @@ bool use_2sm() {
 
 // 256 x BN tiles on CTA pairs, persistent over the pairs (<= 74 pairs on 148 SMs)
 template <int BN>
-cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
+cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st, int k_splits = 1) {
   using Cfg = Gemm2Cfg<BN>;
   GemmArgs a;
   a.M = (int)d.M;
@@ -962,6 +962,12 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
   a.qkv = d.qkv;
   const long tiles2 = (long)a.num_m * a.num_n;
   a.units = (int)tiles2;
+  if (k_splits > 1) {  // fewer tiles than pairs (EPI_F32): uniform K split, atomics into zeroed C
+    cudaError_t e = cudaMemset2DAsync(d.C, d.ldc * sizeof(float), 0, d.N * sizeof(float), d.M, st);
+    if (e != cudaSuccess) return e;
+    a.splits = k_splits;
+    a.units = (int)(tiles2 * k_splits);
+  }
   // accumulating epilogues (C += acc): split the last, partial wave of tiles along K when the
   // modelled time -- waves x (K blocks per unit + ~14 blocks of fill / epilogue) -- drops
   // (down projection M=1728: 112 tiles = 1.51 waves on 74 pairs)
@@ -970,7 +976,7 @@ cudaError_t gemm_tn_2sm(const GemmDesc& d, cudaStream_t st) {
     return !(v && std::atoi(v) == 0);
   }();
   const long np = kNumSMs / 2;
-  if (tail_on && (d.epi == EPI_F32_ADD || d.epi == EPI_F32_ATOMIC) && tiles2 > np && tiles2 % np) {
+  if (k_splits <= 1 && tail_on && (d.epi == EPI_F32_ADD || d.epi == EPI_F32_ATOMIC) && tiles2 > np && tiles2 % np) {
     const long full = tiles2 / np * np, rem = tiles2 - full;
     const double kb = a.kb_total;
     double best = (double)(full / np + 1) * (kb + 14.0);
@@ -1029,6 +1035,19 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
     // (256 x 128 pair tiles measured slower even where they quantise better onto the 74
     // pairs: QKV M=1728 78 -> 108 us, scripts/gemm_cfg_sweep.py)
     if (d.M >= 512 && mt * ((d.N + 255) / 256) >= kNumSMs / 2) return gemm_tn_2sm<256>(d, st);
+    // fewer 256 x 256 tiles than pairs but a long K (the LM head's dH = dlogits U, K = V): split K
+    // uniformly so the units fill whole waves of pairs -- waves x (k-blocks / split + ~14)
+    const long t2 = mt * ((d.N + 255) / 256), kbt = (d.K + 63) / 64;
+    if (d.epi == EPI_F32 && d.M >= 512 && t2 >= 16 && kbt >= 512) {
+      const int np = kNumSMs / 2;
+      int best_s = 1;
+      double best = 1e30;
+      for (int sp = 2; sp <= 16 && kbt / sp >= 32; ++sp) {
+        const double c = (double)((t2 * sp + np - 1) / np) * ((double)kbt / sp + 14.0);
+        if (c < best - 1e-9) best = c, best_s = sp;
+      }
+      if (best_s > 1) return gemm_tn_2sm<256>(d, st, best_s);
+    }
     static const bool bn128 = [] {  // measured neutral-to-negative in the co-serving bench
       const char* v = std::getenv("CS_GEMM_2SM128");
       return v && std::atoi(v) != 0;

@@ -133,3 +133,18 @@ def test_gemm_swiglu_epilogue(cuda, M, f, K):
     err = (C[:, :f].float() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-2, err
     assert C[:, f:].float().abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 4096, 32768), (640, 4096, 40960)])
+def test_gemm_f32_pair_ksplit(cuda, M, N, K):
+    """EPI_F32 with fewer 256 x 256 tiles than CTA pairs and a long K (the LM head's dH): the
+    pair kernel with a uniform K split, fp32 atomics into the zeroed output."""
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    C = torch.full((M, N), 3.0, device=cuda)
+    _gemm(A, B, C, 1)
+    ref = A.float() @ B.float().T
+    torch.cuda.synchronize()
+    err = (C - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-4, err
