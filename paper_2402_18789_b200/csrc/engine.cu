@@ -1204,6 +1204,37 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
     }
     work_tc.swap(w2);
+  } else if ((long)work_tc.size() < 3L * 148 && work_tc.size() % 148 != 0) {
+    // a partial last wave (216 items = 1.46 waves: every SM of the 2nd wave ran one more whole
+    // item): split the longest items in two key halves until the count fills whole waves, so
+    // the 2nd wave runs halves (LPT over the sorted list); the halves merge in the LSE combine
+    std::stable_sort(work_tc.begin(), work_tc.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
+      return x.k_end - x.k_begin > y.k_end - y.k_begin;
+    });
+    const long target = ((long)work_tc.size() + 147) / 148 * 148;
+    long nsplit = target - (long)work_tc.size();
+    int part = 0;
+    std::vector<cs::AttnWork> w2;
+    for (const auto& w : work_tc) {
+      const int len = w.k_end - w.k_begin;
+      if (nsplit > 0 && w.part < 0 && len >= 4 * 128 && part + 2 <= 1024) {
+        const int mid = w.k_begin + (len / 2 + 127) / 128 * 128;
+        cs::AttnWork x = w;
+        x.k_end = mid;
+        x.part = part;
+        w2.push_back(x);
+        x = w;
+        x.k_begin = mid;
+        x.part = part + 1;
+        w2.push_back(x);
+        comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, part, 2, 0, 0});
+        part += 2;
+        --nsplit;
+      } else {
+        w2.push_back(w);
+      }
+    }
+    work_tc.swap(w2);
   }
   // longest key ranges first (causal tiles have very different lengths)
   std::stable_sort(work_tc.begin(), work_tc.end(),
