@@ -50,7 +50,7 @@ def main():
     eng.set_profiling(False)
     hbm = bench.load_peaks()[0]["hbm_gbs"]
     out = {"B": a.B, "ctx_mean": float(np.mean(ctxs)), "ctx_max": max(ctxs),
-           "cfg": os.environ.get("CS_DEC_CFG", "default"), "target": os.environ.get("CS_DEC_TARGET", "default"),
+           "target": os.environ.get("CS_DEC_TARGET", "default"),
            "bytes_per_launch_MB": k5["bytes"] / max(1, k5["launches"]) / 1e6,
            "kernel_us": 1e3 * k5["ms"] / max(1, k5["launches"]),
            "kernel_hbm_frac": k5["bytes"] / (k5["ms"] * 1e-3) / 1e9 / hbm if k5["ms"] else None,
