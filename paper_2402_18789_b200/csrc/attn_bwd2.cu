@@ -231,7 +231,14 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
       }
-    } else if (warp == 1) {  // MMA issuer: the whole warp walks the schedule, one lane issues
+    } else if (warp == 1 || warp == 2) {
+      // two MMA issuers, each blocking on its own stream's barriers (tcgen05.commit tracks the
+      // issuing thread's MMAs, so the streams stay independent): warp 1 issues S^T / dP^T(i)
+      // (Q / dO of tile i landed, S / dP buffer released by the elementwise warps), warp 2
+      // dV / dK / dQ^T(j) (P^T / dS^T of tile j written, dQ^T(j-1) read out).  One issuer
+      // polling both streams spent ~1.5 K clk per block on probes and MIO back-pressure, with
+      // the tensor pipe idle 43% of the time (scripts/micro/mma_rate.cu: the tile's MMAs alone
+      // take 1751 clk against ~3.1 K clk per tile in the kernel)
       constexpr uint32_t idS = idesc_bf16_f32_major(128, QB, 0, 0);
       constexpr uint32_t idG = idesc_bf16_f32_major(128, 128, 0, 1);
       constexpr uint32_t idQ = idesc_bf16_f32_major(128, QB, 1, 1);
@@ -241,16 +248,37 @@ __global__ void __launch_bounds__(512, 1)
         mbar_wait(kv_full, 0);
         tc_fence_after();
       }
-      // two in-order streams, whichever is ready first: S^T / dP^T(i) (Q / dO of tile i landed,
-      // S / dP buffer released by the elementwise warps) and dV / dK / dQ^T(j) (P^T / dS^T of
-      // tile j written, dQ^T(j-1) read out), both probed without blocking (a try_wait with a
-      // suspend-time hint sleeps until the phase completes: S^T(i+1) then waited behind
-      // dV / dK / dQ^T(i), 1.76 -> 2.65 ms per 8K window) and a short nanosleep when neither is
-      // ready, so a late Q / dO tile never holds back the products of the previous one.
-      int si = 0, gj = 0;
-      while (gj < n) {
-        if (gj < si && mbar_test(pds_full, gj & 1) && (gj == 0 || mbar_test(dq_free, (gj - 1) & 1))) {
-          const int j = gj, st = j % QST;
+      if (warp == 1) {
+        for (int i = 0; i < n; ++i) {
+          const int st = i % QST;
+          mbar_wait(&q_full[st], (i / QST) & 1);
+          if (i > 0) mbar_wait(sd_free, (i - 1) & 1);
+          tc_fence_after();
+          trace_ev(30, i);
+          const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
+          const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
+              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
+              mma_bf16(tmem + TM_S, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
+              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
+              mma_bf16(tmem + TM_DP, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
+            }
+            mma_commit(sd_full);
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int j = 0; j < n; ++j) {
+          const int st = j % QST;
+          mbar_wait(pds_full, j & 1);
+          if (j > 0) mbar_wait(dq_free, (j - 1) & 1);
           tc_fence_after();
           trace_ev(31, j);
           const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
@@ -273,37 +301,9 @@ __global__ void __launch_bounds__(512, 1)
             mma_commit(pds_free);
           }
           __syncwarp();
-          ++gj;
-          continue;
         }
-        if (si < n && mbar_test(&q_full[si % QST], (si / QST) & 1) && (si == 0 || mbar_test(sd_free, (si - 1) & 1))) {
-          const int i = si, st = i % QST;
-          tc_fence_after();
-          trace_ev(30, i);
-          const uint32_t sQ = smem_u32(smem + SMEM_Q + st * QTILE);
-          const uint32_t sO = smem_u32(smem + SMEM_O + st * QTILE);
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-              mma_bf16(tmem + TM_S, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t ak = (kk >> 2) * HALFB + (kk & 3) * 32;
-              const uint32_t bq = (kk >> 2) * HALFQ + (kk & 3) * 32;
-              mma_bf16(tmem + TM_DP, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
-            }
-            mma_commit(sd_full);
-          }
-          __syncwarp();
-          ++si;
-        } else {
-          __nanosleep(32);  // neither stream is ready
-        }
+        if (n > 0 && elect_one()) mma_commit(acc_done);
       }
-      if (n > 0 && elect_one()) mma_commit(acc_done);
     } else if (warp == 3) {  // per-column -lse*log2(e) and -Delta of each tile into the x ring
       for (int i = 0; i < n; ++i) {
         const int slot = i % XST;

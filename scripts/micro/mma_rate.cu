@@ -64,7 +64,93 @@ void run(const char* name) {
   printf("%-22s %6.1f clk/mma  %6.0f MAC/clk/SM\n", name, m / iters, 128.0 * N * 16 * iters / m);
 }
 
+
+// the fused attention backward's per-tile MMA mix (attn_bwd2.cu), issued back to back by one
+// thread with no waits: S^T, dP^T (8 + 8 SS, N=64, K-major), dV, dK (4 + 4 TS, N=128, B MN-major),
+// dQ^T (8 SS, N=64, both MN-major) and the kernel's 4 commits per tile -- the tensor pipe's own
+// floor for one (key block, query tile) pair
+__global__ void __launch_bounds__(128, 1) tile_mix(int tiles, unsigned long long* out, int mode) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[5];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 163840 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1); fence_barrier_init(); }
+  if (warp == 2) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0 && lane == 0) {
+    constexpr uint32_t idS = idesc_bf16_f32_major(128, 64, 0, 0);
+    constexpr uint32_t idG = idesc_bf16_f32_major(128, 128, 0, 1);
+    constexpr uint32_t idQ = idesc_bf16_f32_major(128, 64, 1, 1);
+    const uint32_t sK = smem_u32(smem), sV = sK + 32768, sQ = sK + 65536, sO = sK + 98304, sDS = sK + 131072;
+    unsigned long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      if (mode != 2) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ak = (kk >> 2) * 16384 + (kk & 3) * 32, bq = (kk >> 2) * 8192 + (kk & 3) * 32;
+          mma_bf16(tmem + 0, umma_desc_sw128(sK + ak), umma_desc_sw128(sQ + bq), idS, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ak = (kk >> 2) * 16384 + (kk & 3) * 32, bq = (kk >> 2) * 8192 + (kk & 3) * 32;
+          mma_bf16(tmem + 64, umma_desc_sw128(sV + ak), umma_desc_sw128(sO + bq), idS, kk > 0);
+        }
+        mma_commit(&bar[0]);
+      }
+      if (mode != 1) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem + 256),
+                       "r"(tmem + 128 + kk * 8), "l"(umma_desc_sw128_mn(sO + kk * 2048, 8192, 1024)), "r"(idG), "r"(1));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem + 384),
+                       "r"(tmem + 160 + kk * 8), "l"(umma_desc_sw128_mn(sQ + kk * 2048, 8192, 1024)), "r"(idG), "r"(1));
+        mma_commit(&bar[1]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_bf16(tmem + 192, umma_desc_sw128_mn(sK + kk * 2048, 16384, 1024),
+                   umma_desc_sw128_mn(sDS + kk * 2048, 16384, 1024), idQ, kk > 0);
+        mma_commit(&bar[2]);
+        mma_commit(&bar[3]);
+      }
+    }
+    mma_commit(&bar[4]);
+    mbar_wait(&bar[4], 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+void run_mix(int mode, const char* name) {
+  static unsigned long long* d_out = nullptr;
+  if (!d_out) cudaMalloc(&d_out, 148 * 8);
+  cudaFuncSetAttribute(tile_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, 163840 + 1024);
+  std::vector<unsigned long long> h(148);
+  const int tiles = 2048;
+  for (int rep = 0; rep < 2; ++rep) {
+    tile_mix<<<148, 128, 163840 + 1024>>>(tiles, d_out, mode);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("%s failed\n", name); exit(1); }
+  }
+  cudaMemcpy(h.data(), d_out, 148 * 8, cudaMemcpyDeviceToHost);
+  double m = 0; for (auto v : h) m += v; m /= 148;
+  printf("%-34s %7.1f clk/tile\n", name, m / tiles);
+}
+
 int main() {
+  run_mix(0, "bwd tile: S,dP + dV,dK,dQ^T");
+  run_mix(1, "bwd tile: S,dP only");
+  run_mix(2, "bwd tile: dV,dK,dQ^T only");
   run<64, 1, 0>("N=64  SS 1 acc");
   run<64, 2, 0>("N=64  SS 2 acc");
   run<64, 4, 0>("N=64  SS 4 acc");
