@@ -1,7 +1,8 @@
 """Summarise an attention-backward CTA trace (gpurun_out/trace_<cta>.json from trace_bwd.py):
 per-tile event times and median intervals.  Events: 30 S/dP issue, 31 dV/dK/dQ issue,
 40 elementwise start (warp 4), 41 its x ring wait done, 43 its P/dS buffer wait done, 42
-elementwise end (warp 4), 32 issuer's Q/dO wait done, 33 issuer's P/dS-ready wait done."""
+elementwise end (warp 4), 32 S issuer's Q/dO wait done, 33 G issuer's P/dS-ready wait done,
+50 dQ warps see dQ^T."""
 import json
 import sys
 
@@ -26,6 +27,9 @@ pairs = [("S issue -> E start", 30, 40, 0), ("E start -> E end", 40, 42, 0), ("E
          ("S issue -> next S issue", 30, 30, 1), ("E start -> x ready", 40, 41, 0),
          ("x ready -> P/dS buffer free", 41, 43, 0), ("buffer free -> E end", 43, 42, 0),
          ("prev S issue -> Q ready", 30, 32, 1), ("Q ready -> S issue", 32, 30, 0),
-         ("E end -> issuer sees pds", 42, 33, 0), ("Q/dO TMA issue -> issuer sees it", 34, 32, 0), ("issuer sees pds -> dVdKdQ issue", 33, 31, 0)]
+         ("E end -> issuer sees pds", 42, 33, 0), ("Q/dO TMA issue -> issuer sees it", 34, 32, 0), ("issuer sees pds -> dVdKdQ issue", 33, 31, 0),
+         ("S issue -> next sd_full seen (E start)", 30, 40, 0), ("dVdKdQ issue -> E sees buffer free (next tile)", 31, 43, 1),
+         ("dVdKdQ issue -> dQ warps see dQ", 31, 50, 0), ("dQ seen -> next dVdKdQ issue", 50, 31, 1),
+         ("Q ready(seen by S issuer) -> S issue", 32, 30, 0)]
 for name, a, b, off in pairs:
     print(f"{name:32s}", med([by[b][i + off] - by[a][i] for i in by.get(a, {}) if i + off in by.get(b, {})]))
