@@ -31,6 +31,17 @@
 
 namespace cs {
 
+#ifdef CS_DEC_TRACE
+// experiment build only: per-warp globaltimer stamps of the swap kernel (start, first tile
+// landed, end, tiles, SM) -- scripts/decode_trace.py
+__device__ unsigned long long* g_dec_trace = nullptr;
+CS_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 namespace {
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -325,6 +336,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     tma_prefetch_desc(&tmV);
   }
   __syncwarp();
+#ifdef CS_DEC_TRACE
+  const unsigned long long tr_t0 = gtimer();
+  unsigned long long tr_t1 = 0;
+#endif
   if (gw >= n_items) return;
   const int grp = p.grp;
   struct Item {
@@ -405,6 +420,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       if (lane == 0) top_up();
       const int st = (int)(g_cons % STAGES);
       mbar_wait(&full[st], (uint32_t)((g_cons / STAGES) & 1));
+#ifdef CS_DEC_TRACE
+      if (g_cons == 0) tr_t1 = gtimer();
+#endif
       const uint32_t kb = smem_u32(ws + st * 2 * TILE), vb = kb + TILE;
       const int kt = kt0 + tt;
       // ---- S^T = K Q^T
@@ -518,6 +536,14 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       }
     }
   }
+#ifdef CS_DEC_TRACE
+  if (lane == 0 && g_dec_trace) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* o = g_dec_trace + (long)gw * 5;
+    o[0] = tr_t0; o[1] = tr_t1; o[2] = gtimer(); o[3] = (unsigned long long)g_cons; o[4] = smid;
+  }
+#endif
 }
 
 namespace {
@@ -554,7 +580,13 @@ cudaError_t launch_dec_stream(const AttnFwdParams& p, const CUtensorMap& tmK, co
 // 32-key tiles, 2 warps x 2 stages per CTA, 3 CTAs per SM (scripts/decode_op.py: of the
 // {32, 16}-key x {2, 4}-warp x {2, 3, 4}-stage variants this is the fastest at the bench's
 // operating point, 100 rows x ~400 keys: 0.71 of measured HBM for the kernel)
-constexpr int kDecKT = 32, kDecNW = 2, kDecST = 2;
+#ifndef CS_DEC_NW
+#define CS_DEC_NW 2
+#endif
+#ifndef CS_DEC_ST
+#define CS_DEC_ST 2
+#endif
+constexpr int kDecKT = 32, kDecNW = CS_DEC_NW, kDecST = CS_DEC_ST;
 
 template <int D>
 cudaError_t launch_dec_d(const AttnFwdParams& p, const CUtensorMap& tmK, const CUtensorMap& tmV,
@@ -582,3 +614,9 @@ cudaError_t attn_decode(const AttnFwdParams& p, const CUtensorMap& tmK, const CU
 }
 
 }  // namespace cs
+
+#ifdef CS_DEC_TRACE
+extern "C" int cs_debug_dec_trace(void* dev_buf) {
+  return (int)cudaMemcpyToSymbol(cs::g_dec_trace, &dev_buf, sizeof(void*));
+}
+#endif
