@@ -384,7 +384,7 @@ def coserve_config(rate, prof, steps, warmup, ft_len, seed, profile_timed=False,
     # mid-generation at any moment (Little's law; 115 tokens x ~45 ms), so the timed region
     # does not start from an empty system
     c.prepopulate = int(min(MAX_BATCH, round(rate * 115 * 0.045)))
-    c.adaptive = 1
+    c.adaptive = int(os.environ.get("BENCH_ADAPTIVE", "1"))
     c.profile_timed = 1 if profile_timed else 0
     c.seed = seed
     return c
@@ -468,6 +468,10 @@ def run_ours(a):
                                                max_window=a.ft_window, tail=m["tail_target"]))
     torch.cuda.synchronize()
     clocks = clk.stop()
+    if os.environ.get("BENCH_ITERLOG") and rank == 0:  # per-iteration plan / latency log (JSONL)
+        with open(os.environ["BENCH_ITERLOG"], "w") as f:
+            for r in log:
+                f.write(json.dumps(r) + "\n")
     if dist:
         dist.barrier()
     # roofline pass: the same workload again with CUDA events around every GEMM / attention

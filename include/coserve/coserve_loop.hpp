@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "coserve/baselines.hpp"
+#include "coserve/calibrate.hpp"
 #include "coserve/vtc.hpp"
 #include "coserve/cost_model.hpp"
 #include "coserve/scheduler.hpp"
@@ -72,6 +73,9 @@ struct LoopConfig {
   int timed_iters = 100;
   int prepopulate = 0;          // requests already decoding at t=0 (steady-state start)
   bool adaptive = false;        // correct the profile with measured/predicted ratios
+  // adaptive + co-serving policy + a profile with row and context terms: calibrate each
+  // coefficient of f(c, s) online (coserve/calibrate.hpp) instead of one ratio per FT phase
+  bool calibrate = false;
   // tail control (adaptive only; 0 = off): the planner budget becomes
   // tail_target x TPOT SLO / q95(measured / predicted over the last 96 inference iterations),
   // so the iteration-latency tail -- not the mean -- sits at the SLO on any box
@@ -181,6 +185,9 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
   }
   double corr[3] = {1.0, 1.0, 1.0};  // adaptive, per FT phase (none / forward / backward)
+  const bool use_cal = cfg.adaptive && cfg.calibrate && cfg.policy == Policy::Coserve &&
+                       CostCalibrator::applicable(cfg.prof);
+  CostCalibrator cal(cfg.prof);
   const bool spatial = cfg.policy == Policy::Spatial || cfg.policy == Policy::Isolate;
   const bool temporal = cfg.policy == Policy::TemporalFixed || cfg.policy == Policy::Dts;
   SpatialSplit split = cfg.split;
@@ -241,7 +248,9 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     }
     LatencyProfile prof = cfg.prof;
     const int cph = ft.phase == FtPhase::Forward ? 1 : (ft.phase == FtPhase::Backward ? 2 : 0);
-    if (cfg.adaptive) {
+    if (use_cal) {
+      prof = cal.profile();
+    } else if (cfg.adaptive) {
       prof.t0_ms *= corr[cph];
       prof.slope_ms_per_token *= corr[cph];
       prof.attn_fwd_ms_per_token_ctx *= corr[cph];
@@ -398,8 +407,12 @@ inline LoopStats run_coserve(const LoopConfig& cfg, StepExecutor* exec) {
     if (cfg.adaptive && !spatial && plan.predicted_ms > 0 && out.device_ms > 0) {
       const int ph = plan.ft_phase == FtPhase::Forward ? 1 : (plan.ft_phase == FtPhase::Backward ? 2 : 0);
       // the step ran with corr[cph]; blend towards the measured ratio of its own phase
-      const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));
-      corr[ph] = std::max(0.5, std::min(2.0, 0.8 * corr[ph] + 0.2 * r));
+      if (use_cal) {
+        cal.update(cal.features(plan), out.device_ms);
+      } else {
+        const double r = corr[cph] * std::max(0.8, std::min(1.25, out.device_ms / plan.predicted_ms));
+        corr[ph] = std::max(0.5, std::min(2.0, 0.8 * corr[ph] + 0.2 * r));
+      }
       if (cfg.tail_target > 0 && plan.c > 0) {
         const double x = out.device_ms / plan.predicted_ms;
         if (resid.size() < 96) resid.push_back(x);

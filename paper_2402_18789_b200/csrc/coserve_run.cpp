@@ -153,6 +153,7 @@ extern "C" int cs_coserve_run(cs_engine* e, const cs_coserve_config* c, cs_coser
   L.timed_iters = c->timed_iters;
   L.prepopulate = c->prepopulate;
   L.adaptive = c->adaptive != 0;
+  L.calibrate = c->adaptive == 2;  // adaptive 2: per-coefficient online calibration
   L.seed = c->seed;
   if (c->policy < 0 || c->policy > 4)
     return cs::set_error(CS_ERR_INVALID_ARGUMENT, "cs_coserve_run: policy must be in 0..4");

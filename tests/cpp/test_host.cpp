@@ -337,6 +337,95 @@ static void test_vtc() {
   CHECK(near(c.counter[0], 142.0) && near(c.service[0], 142.0));
 }
 
+// online calibration (coserve/calibrate.hpp): a "true" box whose coefficients differ from the
+// profiled prior by up to +-20% each; after ~400 measured iterations of mixed plans the
+// calibrated model predicts fresh plans within 2% (the prior is off by up to ~15%), the
+// prediction equals the planner's own predicted_ms for ctx-term profiles, and coefficients
+// stay inside [1/2, 2] x prior under adversarial measurements
+static void test_calibrator() {
+  LatencyProfile prior;
+  prior.t0_ms = 4.8;
+  prior.slope_ms_per_token = 0.013;
+  prior.bwd_token_weight = 0.026;
+  prior.attn_fwd_ms_per_token_ctx = 7.1e-7;
+  prior.attn_bwd_ms_per_token_ctx = 5.5e-8;
+  prior.bwd_layer0_weight = 0.25;
+  prior.decode_ms_per_row = 0.007;
+  prior.prefill_ms_per_token = 0.0099;
+  prior.fwd_window_ms = 2.3;
+  CHECK(CostCalibrator::applicable(prior));
+  CHECK(!CostCalibrator::applicable(LatencyProfile{}));
+  LatencyProfile truth = prior;
+  truth.t0_ms *= 1.12;
+  truth.decode_ms_per_row *= 0.85;
+  truth.prefill_ms_per_token *= 1.1;
+  truth.fwd_window_ms *= 0.8;
+  truth.slope_ms_per_token *= 0.92;
+  truth.attn_fwd_ms_per_token_ctx *= 1.2;
+  truth.bwd_token_weight *= 1.15 / 0.92;  // backward token cost x 1.15
+  truth.attn_bwd_ms_per_token_ctx *= 0.85;
+  CostCalibrator cal(prior), truth_model(truth);
+  TraceRng rng(11);
+  auto random_plan = [&](int kind) {
+    IterationPlan p;
+    const int nd = 40 + (int)(rng.uniform() * 60), np = rng.uniform() < 0.5 ? 0 : 512;
+    p.decode.resize(nd);
+    p.c = nd + np;
+    if (kind == 1) {
+      p.ft_phase = FtPhase::Forward;
+      p.s = 200 + (int64_t)(rng.uniform() * 1800);
+      p.ft_l = (int)(rng.uniform() * 6000);
+    } else if (kind == 2) {
+      p.ft_phase = FtPhase::Backward;
+      int lj = 8192, layer = 31 - (int)(rng.uniform() * 31);
+      for (int w = 0; w < 4 && layer >= 0; ++w) {
+        const int s = std::min(lj, 1024 + (int)(rng.uniform() * 7168));
+        p.bwd.push_back(BwdWindow{layer, lj, s});
+        p.s += s;
+        lj -= s;
+        if (lj == 0) { layer -= 1; lj = 8192; }
+      }
+      p.ft_layer = p.bwd[0].layer;
+      p.ft_l = p.bwd[0].lj;
+    }
+    return p;
+  };
+  for (int it = 0; it < 400; ++it) {
+    const IterationPlan p = random_plan(it % 3);
+    const double y = truth_model.predict(truth_model.features(p)) * (1.0 + 0.02 * (rng.uniform() - 0.5));
+    cal.update(cal.features(p), y);
+  }
+  CostCalibrator prior_model(prior);
+  double worst = 0, worst_prior = 0;
+  for (int it = 0; it < 300; ++it) {
+    const IterationPlan p = random_plan(it % 3);
+    const double y = truth_model.predict(truth_model.features(p));
+    worst = std::max(worst, std::fabs(cal.predict(cal.features(p)) / y - 1.0));
+    worst_prior = std::max(worst_prior, std::fabs(prior_model.predict(prior_model.features(p)) / y - 1.0));
+  }
+  CHECK(worst < 0.02);
+  CHECK(worst_prior > 0.08);
+  // the calibrated profile drives the planner's cost functions to the same prediction
+  {
+    const LatencyProfile q = cal.profile();
+    const IterationPlan f = random_plan(1), b = random_plan(2);
+    const double pf = inference_cost(q, (int64_t)f.decode.size(), f.c - (int64_t)f.decode.size()) +
+                      ft_fwd_cost(q, f.ft_l, f.s);
+    double pb = inference_cost(q, (int64_t)b.decode.size(), b.c - (int64_t)b.decode.size());
+    for (const BwdWindow& w : b.bwd) pb += ft_bwd_cost(q, w.lj, w.s, w.layer);
+    CHECK(std::fabs(pf / cal.predict(cal.features(f)) - 1.0) < 1e-9);
+    CHECK(std::fabs(pb / cal.predict(cal.features(b)) - 1.0) < 1e-9);
+  }
+  // adversarial measurements (10x) cannot push a coefficient past 2x its prior
+  CostCalibrator bad(prior);
+  for (int it = 0; it < 200; ++it) {
+    const IterationPlan p = random_plan(it % 3);
+    bad.update(bad.features(p), 10.0 * prior_model.predict(prior_model.features(p)));
+  }
+  CostCalibrator ref(prior);
+  for (int i = 0; i < CostCalibrator::K; ++i) CHECK(bad.theta()[i] <= 2.0 * ref.theta()[i] + 1e-15);
+}
+
 int main() {
   test_cost_model();
   test_memory_model();
@@ -346,6 +435,7 @@ int main() {
   test_workload();
   test_sim_loop();
   test_vtc();
+  test_calibrator();
   if (failures) {
     std::printf("%d failure(s)\n", failures);
     return 1;
