@@ -161,9 +161,14 @@ void prof_end(cs_engine* e, cs_engine::ProfRec& r) {
   e->recs.push_back(r);
 }
 void prof_collect(cs_engine* e) {
+  static FILE* plog = [] {  // CS_PROF_LOG=<file>: one line per profiled launch (kind flops bytes ms)
+    const char* v = std::getenv("CS_PROF_LOG");
+    return v ? std::fopen(v, "w") : nullptr;
+  }();
   for (auto& r : e->recs) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    if (plog) std::fprintf(plog, "%d %.6g %.6g %.6f\n", r.kind, r.flops, r.bytes, ms);
     e->prof_ms[r.kind] += ms;
     e->prof_flops[r.kind] += r.flops;
     e->prof_bytes[r.kind] += r.bytes;
@@ -1175,11 +1180,89 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     });
     work_dec.swap(w2);
   }
-  // tcgen05 items: when a call has few of them (a short window at a long context), split the
-  // key ranges into parts of >= 1024 keys so ~2 waves of SMs share the work (flash-decoding
-  // style; parts merged by the LSE combine) -- otherwise a 45-token window at 8K context ran
-  // on 8 CTAs
-  if (!work_tc.empty() && (long)work_tc.size() < 148) {
+  // tcgen05 items: split key ranges (flash-decoding style; parts merged by the LSE combine) by
+  // a makespan model of the launch: a part of t 128-key tiles costs t + kFix tile-times (TMEM /
+  // barrier setup, the two Q tiles, first K/V latency, epilogue), parts go to the 148 SMs
+  // longest first (the block scheduler's greedy order = LPT), a split adds the combine launch
+  // (kComb) and each split part its fp32 partial round trip (kPer).  Constants fitted on 48
+  // launches of scripts/attn_mix_bench.py (8B, windows 512-2048 at context 0-7680, with and
+  // without a prefill chunk; 2.3% mean error): 1 tile = 2.6 us, kFix 4.5, kComb 4.3, kPer 0.01.  Candidates: no split, and parts
+  // capped at T / (148 m) tiles or at the longest item / k.  (The earlier fixed rules -- >= 1024-
+  // key parts over ~2 waves below 148 items, halves to fill the last wave below 444 -- split
+  // a 1024-token window at 4K context into 1.7 waves of halves: 145 us vs 121 us unsplit.)
+  static const int tc_split = [] {
+    const char* v = std::getenv("CS_TC_SPLIT");  // 0: the earlier fixed rules (A/B)
+    return v ? std::atoi(v) : 1;
+  }();
+  if (!work_tc.empty() && tc_split == 1) {
+    constexpr double kFix = 4.5, kComb = 4.3, kPer = 0.01;
+    constexpr int kSMs = 148;
+    std::vector<int> t(work_tc.size());
+    long T = 0;
+    int tmax = 0;
+    for (size_t i = 0; i < work_tc.size(); ++i) {
+      t[i] = (work_tc[i].k_end - work_tc[i].k_begin + 127) / 128;
+      T += t[i];
+      tmax = std::max(tmax, t[i]);
+    }
+    std::vector<double> cost, load(kSMs);
+    auto makespan = [&](int cap, int* n_parts) {
+      cost.clear();
+      int n_split = 0;
+      for (int x : t) {
+        const int ns = (x + cap - 1) / cap, per = (x + ns - 1) / ns;
+        if (ns > 1) n_split += ns;
+        for (int k = 0, left = x; k < ns; ++k, left -= per) cost.push_back(std::min(per, left) + kFix);
+      }
+      *n_parts = (int)cost.size();
+      std::sort(cost.begin(), cost.end(), std::greater<double>());
+      // greedy onto the least-loaded SM (min-heap of loads)
+      std::fill(load.begin(), load.end(), 0.0);
+      double mx = 0.0;
+      for (double c : cost) {
+        std::pop_heap(load.begin(), load.end(), std::greater<double>());
+        load.back() += c;
+        mx = std::max(mx, load.back());
+        std::push_heap(load.begin(), load.end(), std::greater<double>());
+      }
+      return mx + (n_split ? kComb + kPer * n_split : 0.0);
+    };
+    int best_cap = tmax, best_parts = 0;
+    double best = makespan(tmax, &best_parts);
+    std::vector<int> caps;
+    for (int m : {1, 2, 3, 4, 6, 8}) caps.push_back((int)((T + (long)kSMs * m - 1) / ((long)kSMs * m)));
+    for (int k : {2, 3, 4}) caps.push_back((tmax + k - 1) / k);
+    for (int cap : caps) {
+      if (cap < 2 || cap >= tmax) continue;
+      int np = 0;
+      const double ms = makespan(cap, &np);
+      if (np <= 1024 && ms < best - 1e-9) best = ms, best_cap = cap, best_parts = np;
+    }
+    if (best_cap < tmax) {
+      int part = 0;
+      std::vector<cs::AttnWork> w2;
+      for (size_t i = 0; i < work_tc.size(); ++i) {
+        const cs::AttnWork& w = work_tc[i];
+        const int ns = (t[i] + best_cap - 1) / best_cap;
+        if (ns <= 1) {
+          w2.push_back(w);
+          continue;
+        }
+        const int per = (t[i] + ns - 1) / ns;
+        const int p0 = part;
+        for (int k = 0; k < ns; ++k) {
+          cs::AttnWork x = w;
+          x.k_begin = w.k_begin + k * per * 128;
+          x.k_end = std::min(w.k_end, w.k_begin + (k + 1) * per * 128);
+          if (x.k_begin >= x.k_end) break;
+          x.part = part++;
+          w2.push_back(x);
+        }
+        comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
+      }
+      work_tc.swap(w2);
+    }
+  } else if (!work_tc.empty() && (long)work_tc.size() < 148) {
     long total = 0;
     for (const auto& w : work_tc) total += w.k_end;
     long chunk = (total + 2L * 148 - 1) / (2L * 148);
