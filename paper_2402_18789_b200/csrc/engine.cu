@@ -130,6 +130,8 @@ struct cs_engine {
     cudaEvent_t a, b;
     double flops, bytes;
     int kind;  // see prof_ms
+    long m = 0, n = 0, k = 0;  // GEMM shape (CS_PROF_LOG)
+    int epi = -1;
   };
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -168,7 +170,7 @@ void prof_collect(cs_engine* e) {
   for (auto& r : e->recs) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    if (plog) std::fprintf(plog, "%d %.6g %.6g %.6f\n", r.kind, r.flops, r.bytes, ms);
+    if (plog) std::fprintf(plog, "%d %.6g %.6g %.6f %ld %ld %ld %d\n", r.kind, r.flops, r.bytes, ms, r.m, r.n, r.k, r.epi);
     e->prof_ms[r.kind] += ms;
     e->prof_flops[r.kind] += r.flops;
     e->prof_bytes[r.kind] += r.bytes;
@@ -869,6 +871,7 @@ int gemm(cs_engine* e, const void* A, long lda, long a_rows, const void* B, long
     pr.bytes = 2.0 * ((double)M * K + (double)N * K) +
                (double)M * N * (epi == cs::EPI_SWIGLU ? 1 : epi == cs::EPI_BF16 ? 2 : 4);
     pr.kind = 0;
+    pr.m = M, pr.n = N, pr.k = K, pr.epi = (int)epi;
     prof_begin(e, pr);
   }
   cudaError_t err = cs::gemm_tn(g, e->st);
