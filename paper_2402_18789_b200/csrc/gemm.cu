@@ -1124,9 +1124,20 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
   const long tiles = (long)a.num_m * a.num_n;
   if (splits <= 0) {
     splits = 1;
-    if (small_f32 || (tiny_m && !bf16_out)) {
+    if (tiny_m && !bf16_out) {
+      // M <= 64 (half-height A stages, more weight bytes in flight per CTA): ~one unit per SM
       splits = (int)((kNumSMs + tiles / 2) / tiles);
       splits = std::max(1, std::min(splits, a.kb_total / 8));
+    } else if (small_f32) {
+      // 64 < M <= 256: whole waves, minimise waves x (k-blocks per unit + ~14 blocks of fill /
+      // epilogue) -- rounding 148 / tiles to the nearest count gave 5 splits x 32 tiles = 160
+      // units, 1.08 waves, for the M = 81 O / down projections: 20.5 / 43.8 -> 18.4 / 36.9 us,
+      // a decode-only 8B step with 81 rows 5.42 -> 5.03 ms (scripts/decode_step_bench.py)
+      double best = 0;
+      for (int sp = 1; sp <= 16 && (sp == 1 || a.kb_total / sp >= 8); ++sp) {
+        const double c = (double)((tiles * sp + kNumSMs - 1) / kNumSMs) * ((double)a.kb_total / sp + 14.0);
+        if (best == 0 || c < best - 1e-9) best = c, splits = sp;
+      }
     } else if (!bf16_out && tiles < kNumSMs) {
       splits = (int)((kNumSMs + tiles - 1) / tiles);
       splits = std::min(splits, std::max(1, a.kb_total / 4));
