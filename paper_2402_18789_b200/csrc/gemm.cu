@@ -1139,8 +1139,13 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
         if (best == 0 || c < best - 1e-9) best = c, splits = sp;
       }
     } else if (!bf16_out && tiles < kNumSMs) {
-      splits = (int)((kNumSMs + tiles - 1) / tiles);
-      splits = std::min(splits, std::max(1, a.kb_total / 4));
+      // fewer tiles than SMs (the LoRA products, N = r = 16): whole waves as above -- the ceil
+      // gave 10 splits x 16 tiles = 160 units for u = m A at 2K rows
+      double best = 0;
+      for (int sp = 1; sp <= 64 && (sp == 1 || a.kb_total / sp >= 4); ++sp) {
+        const double c = (double)((tiles * sp + kNumSMs - 1) / kNumSMs) * ((double)a.kb_total / sp + 14.0);
+        if (best == 0 || c < best - 1e-9) best = c, splits = sp;
+      }
     }
   }
   if (bf16_out) splits = 1;
