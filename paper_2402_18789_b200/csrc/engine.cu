@@ -1005,22 +1005,10 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   std::vector<cs::AttnWork> work, work_tc, work_dec;
   std::vector<cs::AttnCombine> comb, comb_tc;
   const int rpt = 64 / e->grp;
-  // tcgen05 attention items: two 128-row query tiles per CTA (v2) when the call has enough of
-  // them to fill ~2 waves of SMs, else one tile per CTA (more CTAs for small windows)
-  int rpt_tc = 128 / e->grp;
-  {
-    long n2 = 0;
-    for (int s2 = 0; plan->segments && s2 < plan->n_segments; ++s2) {
-      const int ql = plan->segments[s2].q_len;
-      if (e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn && ql >= 16)
-        n2 += (long)((ql + 2 * rpt_tc - 1) / (2 * rpt_tc)) * e->Hkv;
-    }
-    static const bool one_tile = [] {  // measured slightly negative in the bench: off
-      const char* v = std::getenv("CS_ATTN_FWD2_1T");
-      return v && std::atoi(v) != 0;
-    }();
-    if (n2 >= 2L * 148 || !one_tile) rpt_tc *= 2;
-  }
+  // tcgen05 attention items: two 128-row query tiles per CTA share every K/V tile (one tile per
+  // CTA for small calls measured slightly negative in the bench); the key-range split below
+  // spreads small calls over the SMs
+  const int rpt_tc = 2 * (128 / e->grp);
   const bool tc_ok = e->d == 128 && (e->P % 16) == 0 && e->use_tc_attn;
   double attn_flops = 0, attn_bytes = 0, tc_flops = 0, tc_bytes = 0;
   for (int s = 0; s < sp.n_seg; ++s) {
@@ -1193,11 +1181,7 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // capped at T / (148 m) tiles or at the longest item / k.  (The earlier fixed rules -- >= 1024-
   // key parts over ~2 waves below 148 items, halves to fill the last wave below 444 -- split
   // a 1024-token window at 4K context into 1.7 waves of halves: 145 us vs 121 us unsplit.)
-  static const int tc_split = [] {
-    const char* v = std::getenv("CS_TC_SPLIT");  // 0: the earlier fixed rules (A/B)
-    return v ? std::atoi(v) : 1;
-  }();
-  if (!work_tc.empty() && tc_split == 1) {
+  if (!work_tc.empty()) {
     constexpr double kFix = 4.5, kComb = 4.3, kPer = 0.01;
     constexpr int kSMs = 148;
     std::vector<int> t(work_tc.size());
@@ -1265,62 +1249,6 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
       }
       work_tc.swap(w2);
     }
-  } else if (!work_tc.empty() && (long)work_tc.size() < 148) {
-    long total = 0;
-    for (const auto& w : work_tc) total += w.k_end;
-    long chunk = (total + 2L * 148 - 1) / (2L * 148);
-    chunk = std::max<long>(1024, (chunk + 127) / 128 * 128);
-    int part = 0;
-    std::vector<cs::AttnWork> w2;
-    for (const auto& w : work_tc) {
-      const int ns = (int)std::max<long>(1, (w.k_end + chunk / 2) / chunk);
-      if (ns <= 1 || part + ns > 1024) {
-        w2.push_back(w);
-        continue;
-      }
-      const long per = ((w.k_end + ns - 1) / ns + 127) / 128 * 128;
-      const int p0 = part;
-      for (int t = 0; t < ns && t * per < w.k_end; ++t) {
-        cs::AttnWork x = w;
-        x.k_begin = (int)(t * per);
-        x.k_end = (int)std::min<long>(w.k_end, (t + 1) * per);
-        x.part = part++;
-        w2.push_back(x);
-      }
-      comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, p0, part - p0, 0, 0});
-    }
-    work_tc.swap(w2);
-  } else if ((long)work_tc.size() < 3L * 148 && work_tc.size() % 148 != 0) {
-    // a partial last wave (216 items = 1.46 waves: every SM of the 2nd wave ran one more whole
-    // item): split the longest items in two key halves until the count fills whole waves, so
-    // the 2nd wave runs halves (LPT over the sorted list); the halves merge in the LSE combine
-    std::stable_sort(work_tc.begin(), work_tc.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
-      return x.k_end - x.k_begin > y.k_end - y.k_begin;
-    });
-    const long target = ((long)work_tc.size() + 147) / 148 * 148;
-    long nsplit = target - (long)work_tc.size();
-    int part = 0;
-    std::vector<cs::AttnWork> w2;
-    for (const auto& w : work_tc) {
-      const int len = w.k_end - w.k_begin;
-      if (nsplit > 0 && w.part < 0 && len >= 4 * 128 && part + 2 <= 1024) {
-        const int mid = w.k_begin + (len / 2 + 127) / 128 * 128;
-        cs::AttnWork x = w;
-        x.k_end = mid;
-        x.part = part;
-        w2.push_back(x);
-        x = w;
-        x.k_begin = mid;
-        x.part = part + 1;
-        w2.push_back(x);
-        comb_tc.push_back(cs::AttnCombine{w.seg, w.q0, w.nq, w.kv_head, part, 2, 0, 0});
-        part += 2;
-        --nsplit;
-      } else {
-        w2.push_back(w);
-      }
-    }
-    work_tc.swap(w2);
   }
   // longest key ranges first (causal tiles have very different lengths)
   std::stable_sort(work_tc.begin(), work_tc.end(),

@@ -1048,11 +1048,7 @@ cudaError_t gemm_tn(const GemmDesc& d, cudaStream_t st) {
       }
       if (best_s > 1) return gemm_tn_2sm<256>(d, st, best_s);
     }
-    static const bool bn128 = [] {  // measured neutral-to-negative in the co-serving bench
-      const char* v = std::getenv("CS_GEMM_2SM128");
-      return v && std::atoi(v) != 0;
-    }();
-    if (bn128 && mt * ((d.N + 127) / 128) >= kNumSMs / 2) return gemm_tn_2sm<128>(d, st);
+    // (256 x 128 pair tiles measured neutral-to-negative in the co-serving bench: not used)
   }
   int bn = d.bn > 0 ? d.bn : gemm_pick_bn(d.M, d.N);
   // small-M fp32-epilogue GEMMs (the O / down projections of inference-only rows): weight
