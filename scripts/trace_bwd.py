@@ -1,6 +1,7 @@
-"""SM-clock timeline of one CTA of the attention-backward kernels (cs_debug_trace):
-8B shape, FT forward over L=8192, one backward window s=8192 at layer 31; traces the dq
-kernel CTA (x = last query tile) then the dkdv CTA (x = the middle key tile)."""
+"""SM-clock timeline of one CTA of the fused attention-backward kernel (cs_debug_trace; the
+-DCS_TRACE build, python -m paper_2402_18789_b200.build --trace): 8B shape, FT forward over
+L=8192, one backward window s=8192 at layer 31; traces CTA (x = argv[1] key block, kv head 0)
+into gpurun_out/trace_<x>.json (summary: scripts/trace_summary.py)."""
 import ctypes
 import json
 import os
