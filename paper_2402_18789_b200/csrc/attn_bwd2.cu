@@ -13,8 +13,8 @@
 
 namespace cs {
 
-// ---- in-kernel event trace (debugging): SM-clock timeline of one CTA (blockIdx.x == cta,
-// blockIdx.y == 0) of the backward kernels, set by cs_debug_trace(); compiled in only for the
+// ---- in-kernel event trace (debugging): SM-clock timeline of one CTA (key block == cta,
+// kv head 0) of the backward kernels, set by cs_debug_trace(); compiled in only for the
 // trace build (python -m paper_2402_18789_b200.build --trace -> libcoserve_cuda_trace.so): the
 // check reads a __device__ global, a load on the MMA issuer's critical path
 __device__ int g_trace_cta = -1;
@@ -25,7 +25,7 @@ __device__ __forceinline__ void trace_ev(int ev, int idx) {
   (void)idx;
   return;
 #endif
-  if ((int)blockIdx.x != g_trace_cta || blockIdx.y != 0) return;
+  if ((int)blockIdx.y != g_trace_cta || blockIdx.x != 0) return;
   // one slot per (event, index): a plain store, no atomic round trip on the traced path
   if (idx < 4096 && ev < 64) {
     unsigned long long* slot = g_trace_buf + ev * 4096 + idx;
@@ -165,8 +165,10 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int grp = GRP;
   constexpr int rpt = QB / GRP;            // positions per query tile
   constexpr int ROWS = rpt * GRP;          // real packed rows per tile (<= QB)
-  const int k0 = blockIdx.x * 128;
-  const int kvh = blockIdx.y;
+  // grid (kv heads, key blocks, splits): the block scheduler's linear order then starts the
+  // longest key blocks (the first, causal) of every head first -- LPT over the SMs
+  const int k0 = blockIdx.y * 128;
+  const int kvh = blockIdx.x;
   const int nrows = p.b - p.a;
   const int n_qt = (nrows + rpt - 1) / rpt;
   // first tile whose last position >= k0; long key blocks are split over gridDim.z CTAs of at
@@ -522,7 +524,7 @@ cudaError_t attn_bwd_fused(const AttnBwdParams& p, const CUtensorMap& tmK, const
   q.tiles_per_cta = (int)std::max<long>(24, (total + 2 * kNumSMs - 1) / (2 * kNumSMs));
   const int nz = (int)std::min<long>(8, (n_qt + q.tiles_per_cta - 1) / q.tiles_per_cta);
   if ((n_qt + q.tiles_per_cta - 1) / q.tiles_per_cta > 8) q.tiles_per_cta = (int)((n_qt + 7) / 8);
-  dim3 grid(nkb, kvh, nz);
+  dim3 grid(kvh, nkb, nz);
   launch_pdl(kFused[p.grp - 1], grid, dim3(512), kv3::SMEM_TOTAL, st, tmK, tmV, tmK128, tmV128, tmQ3, tmO3, tmDQ, q);
   return cudaGetLastError();
 }
