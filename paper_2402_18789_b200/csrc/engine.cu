@@ -1177,10 +1177,11 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
   // longest first (the block scheduler's greedy order = LPT), a split adds the combine launch
   // (kComb) and each split part its fp32 partial round trip (kPer).  Constants fitted on 48
   // launches of scripts/attn_mix_bench.py (8B, windows 512-2048 at context 0-7680, with and
-  // without a prefill chunk; 2.3% mean error): 1 tile = 2.6 us, kFix 4.5, kComb 4.3, kPer 0.01.  Candidates: no split, and parts
-  // capped at T / (148 m) tiles or at the longest item / k.  (The earlier fixed rules -- >= 1024-
-  // key parts over ~2 waves below 148 items, halves to fill the last wave below 444 -- split
-  // a 1024-token window at 4K context into 1.7 waves of halves: 145 us vs 121 us unsplit.)
+  // without a prefill chunk; 2.3% mean error): 1 tile = 2.6 us, kFix 4.5, kComb 4.3, kPer 0.01.
+  // Candidates: no split, and parts capped at T / (148 m) tiles or at the longest item / k.
+  // (The earlier fixed rules -- >= 1024-key parts over ~2 waves below 148 items, halves to fill
+  // the last wave below 444 -- split a 1024-token window at 4K context into 1.7 waves of
+  // halves: 145 us vs 121 us unsplit.)
   if (!work_tc.empty()) {
     constexpr double kFix = 4.5, kComb = 4.3, kPer = 0.01;
     constexpr int kSMs = 148;
