@@ -109,9 +109,13 @@ __device__ __forceinline__ void decode_work(int w, const GemmArgs& a, int& m_blk
     kb1 = (int)(((long)(ks + 1) * a.kb_total) / sp);
     return;
   }
-  // units: num_m tiles, then the next K split of the same tiles, then the next num_m tiles
-  const int ks = (w / a.num_m) % a.splits;
-  tile_mn(w % a.num_m + (w / (a.num_m * a.splits)) * a.num_m, a, m_blk, n_blk);
+  // uniform K split: every tile's split ks, then split ks + 1 -- the units of one split run
+  // together, so a wave shares each A slice across the n-blocks and each B slice across the
+  // m-blocks in L2 (the LM head's dH = dlogits U, K = V: with the splits of a tile adjacent a
+  // wave needed all of A's slices and re-read A once per ~2 n-blocks)
+  const long tiles = (long)a.num_m * a.num_n;
+  const int ks = (int)(w / tiles);
+  tile_mn((int)(w % tiles), a, m_blk, n_blk);
   kb0 = (int)(((long)ks * a.kb_total) / a.splits);
   kb1 = (int)(((long)(ks + 1) * a.kb_total) / a.splits);
 }
