@@ -15,7 +15,9 @@ from paper_2402_18789_b200.engine import Seg, SEG_FT_FWD, FT_FORWARD, FT_BACKWAR
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--window", type=int, default=0, help="layer 31 windows of this size over the whole sequence instead")
 args = ap.parse_args()
+a_w = args.window
 eng = bench.make_engine(0, 8192)
 ft_pages = list(range(64 * 40, 64 * 40 + 512))
 toks = [(7 * i) % 1000 for i in range(8192)]
@@ -26,7 +28,8 @@ for rep in range(args.reps + 1):  # pass 0 is warm-up
         eng.step([Seg(SEG_FT_FWD, toks[l:l + 2048], l, ft_pages, adapter=True)],
                  ft={"phase": FT_FORWARD, "seq_len": 8192, "l": l, "s": 2048,
                      "targets": toks[l + 1:l + 2049] + ([-1] if l + 2048 == 8192 else [])})
-    for layer, windows in [(31, [2048, 2048, 2048, 2048]), (30, [8192])]:
+    plan = [(31, [a_w] * (8192 // a_w))] if a_w else [(31, [2048, 2048, 2048, 2048]), (30, [8192])]
+    for layer, windows in plan:
         lj = 8192
         for s in windows:
             eng.set_profiling(True)
