@@ -99,6 +99,16 @@ def main():
     def rate(pr, peak):
         return (round(pr["flops"] / pr["ms"] / 1e9, 1), round(pr["flops"] / pr["ms"] / 1e9 / peak, 4)) \
             if pr["ms"] else (None, None)
+    # warm-up: one forward pass and one backward window untimed, so module loading / first-launch
+    # costs of the finetuning kernels stay out of the first timed window size (a cold first
+    # backward once measured 53 ms for the 1024-token windows instead of 9)
+    eng.reset_ft()
+    for l in range(0, ft_len, 2048):
+        eng.step([Seg(SEG_FT_FWD, toks[l:l + 2048], l, ft_pages, adapter=True)],
+                 ft={"phase": FT_FORWARD, "seq_len": ft_len, "l": l, "s": 2048,
+                     "targets": toks[l + 1:l + 2049] + ([-1] if l + 2048 == ft_len else [])})
+    eng.step([], ft={"phase": FT_BACKWARD, "seq_len": ft_len, "l": ft_len, "s": 2048,
+                     "layer": a.layers - 1, "pages": ft_pages})
     for s in ([1024, 2048, 4096] if not a.quick else [2048]):
         eng.reset_ft()
         eng.set_profiling(False)
