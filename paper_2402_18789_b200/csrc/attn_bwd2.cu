@@ -111,13 +111,7 @@ namespace kv3 {
 constexpr int QB = 64;                  // packed query rows per tile
 constexpr int HALFQ = QB * 128;         // 8 KB: one 64-column half of a Q / dO tile
 constexpr int QTILE = 2 * HALFQ;        // 16 KB
-#ifdef CS_BWD_Q4
-constexpr int QST = 4;
-constexpr int DQ_HALVES = 1;
-#else
 constexpr int QST = 3;                  // Q / dO ring depth (a stage is held from S^T(i) until dV / dK(i))
-constexpr int DQ_HALVES = 2;
-#endif
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + TILEB;
 constexpr int SMEM_Q = SMEM_V + TILEB;
@@ -125,7 +119,7 @@ constexpr int SMEM_O = SMEM_Q + QST * QTILE;
 constexpr int SMEM_DS = SMEM_O + QST * QTILE;  // dS^T [128 keys][64 rows] bf16, K-major SW128: 16 KB
 constexpr int XST = 2;                  // x ring depth
 constexpr int SMEM_DQ = SMEM_DS + 128 * 128;   // dQ staging: [2 head-dim halves][64 rows][64] f32
-constexpr int SMEM_X = SMEM_DQ + DQ_HALVES * QB * 64 * 4;  // [XST slots][2][QB] f32: -lse*log2e | -Delta
+constexpr int SMEM_X = SMEM_DQ + 2 * QB * 64 * 4;  // [XST slots][2][QB] f32: -lse*log2e | -Delta
 constexpr int SMEM_BAR = SMEM_X + XST * 2 * QB * 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
 // TMEM columns: S^T, dP^T (fp32, 64 rows), P^T, dS^T (bf16 pairs), dQ^T (fp32), dV, dK
@@ -456,20 +450,13 @@ __global__ void __launch_bounds__(512, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
-#ifdef CS_BWD_Q4
-      continue;
-#endif
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       named_bar(2 + half, 64);  // the previous reduce has read this half's staging buffer
 #pragma unroll
       for (int t = 0; t < ROWS; ++t) stage[t * 64 + dl] = __uint_as_float(v[t]) * p.scale;
       fence_proxy_async_smem();
       named_bar(2 + half, 64);
-#if defined(CS_BWD_NORED)
-      if (false) {
-#else
       if (issuer) {
-#endif
         asm volatile(
             "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                 reinterpret_cast<uint64_t>(&tmDQ)),
