@@ -1169,6 +1169,15 @@ int prepare(cs_engine* e, const cs_iteration_plan* plan, StepPlan& sp) {
     std::stable_sort(w2.begin(), w2.end(), [](const cs::AttnWork& x, const cs::AttnWork& y) {
       return x.k_end - x.k_begin > y.k_end - y.k_begin;
     });
+    if (dec_stream) {
+      // the stream warps take items w, w + W, w + 2W, ... (W = warps of the grid): reverse every
+      // second round of W so each warp pairs a long item with a short one (boustrophedon):
+      // 1-1.5% per launch at the bench's operating point (profiles/r2_decode_timeline.txt)
+      const long n = (long)w2.size();
+      const long grid = std::min<long>((n + dec_nw - 1) / dec_nw, 148L * dec_cps);
+      const long W = grid * dec_nw;
+      for (long r0 = W; r0 < n; r0 += 2 * W) std::reverse(w2.begin() + r0, w2.begin() + std::min(n, r0 + W));
+    }
     work_dec.swap(w2);
   }
   // tcgen05 items: split key ranges (flash-decoding style; parts merged by the LSE combine) by
